@@ -1,0 +1,373 @@
+"""bench.py -- fused F / EucGrad / EucHessianEta throughput (GNNZ*k/s) on B200, BASELINE.json's metric.
+
+A step = one plp_fgrad_hessvec call (SURVEY.md §8(a) a7 = a2..a5 fused, sparse-mode Hessian) on
+the workload config (default C5: 8,388,608 uniform points in [0,1]^2, symmetrised 6-NN graph,
+Gaussian weights, k = 8, p = 1.2, RCM order), with A, B at U supplied from a preceding plp_fgrad
+(the trust-region rho-test always has them).  Inputs (CSR 0.71 GB + U, eta 1.07 GB)
+exceed the 126 MB L2, so no flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl plp|reference] [--config C5]
+
+N > 1: launched by torchrun; rows are split in contiguous blocks (RCM order), each step exchanges
+the U and eta halos with NCCL and all-reduces A, B; time = max over ranks.
+`--impl reference` times the fp64 CPU oracle (oracle/) on a bounded row sample of the same
+workload on this host's cores (the tier's reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import hashlib
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG_DESC = {
+    "C5": "n=8,388,608 uniform points in [0,1]^2, symmetrised 6-NN, w=exp(-d^2/(2 median d^2)), k=8, p=1.2",
+    "C3": "128^3 grid 7-point stencil + 1% long-range edges (w=0.1), k=8, p=1.5",
+    "C4": "10-D GMM n=1,000,000, 20 clusters, symmetrised 15-NN, k=20, p=1.2",
+    "C2": "two moons n=100,000, 10-NN, k=2, p=1.1",
+}
+CONFIG_KP = {"C5": (8, 1.2), "C3": (8, 1.5), "C4": (20, 1.2), "C2": (2, 1.1), "C1": (3, 1.2)}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def get_graph(name: str, order: str):
+    """Seeded synthetic graph (plp_inputs) in RCM order (libplp host code); cached under /tmp only
+    to save generation time between runs (regenerated when absent)."""
+    from plp_inputs import make_config, Graph
+    from paper_2605_26975_b200 import plp
+    key = hashlib.sha1(f"{name}-{order}-v1".encode()).hexdigest()[:12]
+    cache = f"/tmp/plp_cache/{name}_{order}_{key}.npz"
+    if os.path.exists(cache):
+        try:
+            z = np.load(cache)
+            return Graph(name, int(z["n"]), z["rp"], z["col"], z["w"])
+        except Exception:
+            pass
+    t0 = time.time()
+    g = make_config(name)
+    log(f"[bench] generated {name}: n={g.n} nnz={g.nnz} in {time.time() - t0:.1f}s")
+    if order == "rcm":
+        t0 = time.time()
+        perm = plp.rcm_order(g.row_ptr, g.col)
+        rp, col, w = plp.permute_csr(g.row_ptr, g.col, g.w, perm)
+        g = Graph(name, g.n, rp, col, w)
+        log(f"[bench] RCM reorder in {time.time() - t0:.1f}s")
+    try:
+        os.makedirs(os.path.dirname(cache), exist_ok=True)
+        np.savez(cache + ".tmp.npz", n=g.n, rp=g.row_ptr, col=g.col, w=g.w)
+        os.replace(cache + ".tmp.npz", cache)
+    except Exception:
+        pass
+    return g
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def algorithmic_bytes(n: int, nnz: int, k: int) -> int:
+    """CSR once (12 nnz + 4(n+1)), U and eta read once, G and Hv written once."""
+    return 12 * nnz + 4 * (n + 1) + 32 * n * k
+
+
+# ------------------------------------------------------------------------------------------------
+def cpu_oracle_sample(g, k, p, eps, rows_frac=0.25, reps=1):
+    """Time the fp64 oracle (as it stands) on rows [0, S) of the workload (a local CSR whose
+    columns index an extended U, like one rank's shard).  Returns (GNNZ*k/s, seconds, desc, cores)."""
+    import oracle
+    from paper_2605_26975_b200 import plp
+    from plp_inputs import draw_U, draw_eta
+    S = max(1, int(g.n * rows_frac))
+    halo, rp_loc, col_loc = plp.halo_plan(g.row_ptr, g.col, 0, S)
+    ext = np.concatenate([np.arange(S), halo])
+
+    class Loc:
+        row_ptr, col, w = rp_loc, col_loc, g.w[:g.row_ptr[S]]
+
+    U = draw_U(g.n, k, 0)[ext]
+    eta = draw_eta(g.n, k, 0)[ext]
+    nnz_s = int(rp_loc[-1])
+    oracle.set_threads(os.cpu_count() or 1)
+    cores = oracle.get_threads()
+    t0 = time.time()
+    for _ in range(reps):
+        F, A, B = oracle.objective(Loc, U, p)
+        Gr = oracle.euc_grad(Loc, U, p, A, B)
+        Hv = oracle.hessvec(Loc, U, eta, p, eps, "sparse", (A, B))
+    dt = (time.time() - t0) / reps
+    desc = (f"oracle F+grad+Hv (sparse) on rows [0,{S}) of the workload = {nnz_s} stored nonzeros "
+            f"x k={k} (fraction {rows_frac} of nnz), {cores} OpenMP threads")
+    del Gr, Hv
+    return nnz_s * k / dt / 1e9, dt, desc, cores
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle on the same config/metric, bounded sample per step."""
+    if rank != 0:
+        return
+    k, p = CONFIG_KP[args.config]
+    g = get_graph(args.config, "rcm")
+    vals, dts = [], []
+    desc, cores = "", 0
+    for s in range(args.warmup + args.steps):
+        v, dt, desc, cores = cpu_oracle_sample(g, k, p, 1e-9, rows_frac=args.ref_frac)
+        if s >= args.warmup:
+            vals.append(v)
+            dts.append(dt)
+    val = float(np.median(vals))
+    out = {"metric": "fused grad+Hv GNNZ*k/s", "value": val, "unit": "GNNZ*k/s", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.median(dts)),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "impl": "reference",
+           "config": {"workload": args.config, "desc": CONFIG_DESC.get(args.config, args.config),
+                      "n": g.n, "nnz": g.nnz, "k": k, "p": p, "order": "rcm"},
+           "cpu_baseline": {"value": val, "unit": "GNNZ*k/s", "cores": cores, "kind": "oracle",
+                            "sample": desc},
+           "e2e": {"value": val, "unit": "GNNZ*k/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ------------------------------------------------------------------------------------------------
+def run_plp(args, rank, world):
+    import torch
+    from paper_2605_26975_b200 import plp
+    from plp_inputs import draw_U, draw_eta
+
+    dev = torch.device(f"cuda:{args.local_rank}")
+    torch.cuda.set_device(dev)
+    k, p = CONFIG_KP[args.config]
+    eps = 1e-9
+    mode = plp.HESS_FULL if args.mode == "full" else plp.HESS_SPARSE
+    g = get_graph(args.config, args.order)
+    n, nnz = g.n, g.nnz
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    ctx = plp.Context(args.local_rank, stream)
+    U_h = draw_U(n, k, 0)
+    eta_h = draw_eta(n, k, 0)
+
+    if world > 1:
+        from paper_2605_26975_b200 import dist
+        prob = dist.ShardedProblem(ctx, g, k, rank, world, device=dev)
+        step = prob.make_step(U_h, eta_h, p, eps, mode)
+        nnz_local = prob.nnz_local
+    else:
+        G = plp.Graph(ctx, g.row_ptr, g.col, g.w, flags=plp.VALIDATE)
+        U = torch.from_numpy(U_h).to(dev)
+        eta = torch.from_numpy(eta_h).to(dev)
+        Fb = torch.empty(1, dtype=torch.float64, device=dev)
+        AB_in = torch.empty(2 * k, dtype=torch.float64, device=dev)
+        AB_out = torch.empty(2 * k, dtype=torch.float64, device=dev)
+        Gr = torch.empty(n, k, dtype=torch.float64, device=dev)
+        Hv = torch.empty(n, k, dtype=torch.float64, device=dev)
+        plp.fgrad(ctx, G, U, p, F=Fb, AB=AB_in, want_grad=False)
+
+        def step():
+            plp.fgrad_hessvec_raw(ctx, G, k, U, eta, p, AB_in, mode, eps, Fb, AB_out, Gr, Hv)
+        nnz_local = nnz
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(args.local_rank) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    value = nnz * k / (ms * 1e-3) / 1e9  # whole-job GNNZ*k/s
+
+    # ---- dominant kernel alone (edge pass without finalize), per-launch CUDA events ----
+    roof = None
+    if world == 1:
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+        torch.cuda.synchronize()
+        evs[0].record(stream)
+        for i in range(args.steps):
+            plp.edge_pass(ctx, G, U, eta, p, eps, AB_in=AB_in, G=Gr, Hv=Hv)
+            evs[i + 1].record(stream)
+        torch.cuda.synchronize()
+        kms = float(np.mean([evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]))
+        peak, peak_kind = load_peaks()
+        byts = algorithmic_bytes(n, nnz, k)
+        ach = byts / (kms * 1e-3) / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            try:
+                traffic = json.load(open(tp)).get(f"{args.config}-{args.order}-{args.mode}")
+            except Exception:
+                traffic = None
+        roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                "traffic": traffic, "kernel": "edge_kernel<2,4,PowRoot<5>,eta>",
+                "kernel_ms": kms, "algorithmic_bytes": byts, "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"}
+
+    # ---- end to end through the public API: pinned host inputs in, results out, every step ----
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        U_p = torch.from_numpy(U_h).pin_memory()
+        E_p = torch.from_numpy(eta_h).pin_memory()
+        G_p = torch.empty(n, k, dtype=torch.float64).pin_memory()
+        H_p = torch.empty(n, k, dtype=torch.float64).pin_memory()
+        F_p = torch.empty(1, dtype=torch.float64).pin_memory()
+        AB_p = torch.empty(2 * k, dtype=torch.float64).pin_memory()
+        e_steps = max(3, min(args.steps, 10))
+
+        def e2e_step():
+            U.copy_(U_p, non_blocking=True)
+            eta.copy_(E_p, non_blocking=True)
+            plp.fgrad_hessvec_raw(ctx, G, k, U, eta, p, AB_in, mode, eps, Fb, AB_out, Gr, Hv)
+            G_p.copy_(Gr, non_blocking=True)
+            H_p.copy_(Hv, non_blocking=True)
+            F_p.copy_(Fb, non_blocking=True)
+            AB_p.copy_(AB_out, non_blocking=True)
+        e2e_step()
+        torch.cuda.synchronize()
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(e_steps):
+            e2e_step()
+        a1.record(stream)
+        torch.cuda.synchronize()
+        ems = a0.elapsed_time(a1) / e_steps
+        e2e = {"value": nnz * k / (ems * 1e-3) / 1e9, "unit": "GNNZ*k/s",
+               "h2d_bytes_per_step": 2 * n * k * 8, "d2h_bytes_per_step": 2 * n * k * 8 + 8 + 16 * k,
+               "ms_per_step": ems}
+
+    # ---- consistency: AB recomputed by the fused pass vs AB_in ----
+    if world == 1:
+        d = (AB_out - AB_in).abs().max().item() / AB_in.abs().max().item()
+        log(f"[bench] AB_out vs AB_in max rel diff {d:.2e}")
+
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        v, dt, desc, cores = cpu_oracle_sample(g, k, p, eps, rows_frac=args.cpu_frac)
+        cpu = {"value": v, "unit": "GNNZ*k/s", "cores": cores, "kind": "oracle", "sample": desc,
+               "seconds": dt}
+    out = {"metric": "fused grad+Hv GNNZ*k/s", "value": value, "unit": "GNNZ*k/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": args.config, "desc": CONFIG_DESC.get(args.config, args.config),
+                      "n": n, "nnz": nnz, "k": k, "p": p, "eps": eps, "order": args.order,
+                      "hessian": args.mode, "ab_in": "supplied (from plp_fgrad at the same U)",
+                      "l2": "inputs (1.8 GB) larger than the 126 MB L2; no flush",
+                      "parallelism": f"row-blocks x{world}", "nnz_local_rank0": nnz_local},
+           "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
+           "gpu_launches": 2 * args.steps * (1 if world == 1 else 1)}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="plp", choices=["plp", "reference"])
+    ap.add_argument("--config", default="C5", choices=sorted(CONFIG_KP))
+    ap.add_argument("--order", default="rcm", choices=["rcm", "none"])
+    ap.add_argument("--mode", default="sparse", choices=["sparse", "full"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-frac", type=float, default=0.25)
+    ap.add_argument("--ref-frac", type=float, default=0.1)
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    args.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        torch.cuda.set_device(args.local_rank)
+        torch.distributed.init_process_group("nccl", device_id=torch.device(f"cuda:{args.local_rank}"))
+    try:
+        run_plp(args, rank, world)
+    finally:
+        if world > 1:
+            import torch
+            torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,233 @@
+/*
+ * plp.h -- C ABI of libplp: the B200 (sm_100a) hot path of p-spectral clustering on the
+ * Grassmann manifold (arxiv 2605.26975, "Nonlinear spectral clustering with C++ GraphBLAS").
+ *
+ * The entry points follow the paper's statement of the problem:
+ *   Eq. (1)  F_p(U) = sum_l sum_{i,j} w_ij |u_i^l - u_j^l|^p / (2 ||u^l||_p^p)
+ *   Delta_p, phi_p, ||.||_p
+ *   EucGrad, EucHessianEta (Alg. 1)
+ *   k-means discretisation
+ *   RCut = sum_i cut(C_i, ~C_i)/|C_i|
+ * Readings of the paper where it is silent or garbled are listed in DESIGN.md §3 (numbered #1..#19
+ * as in SURVEY.md §8(c)); the ones that change numbers are cited at each call below.
+ *
+ * Conventions (all calls):
+ *  - Dense arrays are fp64, contiguous, node-major (row-major) n x k: element (i, l) at [i*k + l].
+ *    U, eta, G, Hv, xi, X and every other dense array are DEVICE pointers owned by the caller
+ *    (e.g. torch tensors); libplp never frees them.  Small outputs (F, AB, dots, Grams, rcut) are
+ *    device pointers too, so no hot call synchronises with the host.  Exceptions are stated.
+ *  - libplp owns plp_ctx and plp_graph and everything inside them (device CSR, workspaces).
+ *    Hot calls never allocate; all workspace is sized at plp_ctx_create / plp_create_graph.
+ *  - Work is enqueued on the ctx's CUDA stream (plp_ctx_set_stream).  Calls are rank-local: on P
+ *    ranks each rank passes its own rows (plus halo rows of U/eta, see plp_create_graph) and the
+ *    caller all-reduces the small partial outputs (AB, dots, Grams) -- DESIGN.md §7.
+ *  - 1 <= k <= 32.  p in (1, 2].  eps > 0 when p < 2 (curvature cap, reading #6).
+ *  - Every call returns a plp_status; plp_last_error() gives a thread-local message.  No C++
+ *    exception crosses the ABI.  Results are deterministic: every reduction runs in a fixed order
+ *    (no floating-point atomics), so two identical calls are bitwise equal on a given device.
+ */
+#ifndef PLP_H_
+#define PLP_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  PLP_OK = 0,
+  PLP_ERR_ARG = 1,        /* null pointer / bad flag / bad size                                   */
+  PLP_ERR_SHAPE = 2,      /* size mismatch or beyond a supported limit (e.g. nnz >= 2^31)          */
+  PLP_ERR_DOMAIN = 3,     /* p not in (1,2], eps <= 0 with p < 2, k < 1, k > 32    */
+  PLP_ERR_GRAPH = 4,      /* asymmetric, diagonal entry, w <= 0, unsorted/duplicate or
+                             out-of-range column */
+  PLP_ERR_DEGENERATE = 5, /* B_l = 0 (zero column)    */
+  PLP_ERR_RANK = 6,       /* Cholesky of Y^T Y failed: the retraction step must be rejected        */
+  PLP_ERR_NONFINITE = 7,  /* non-finite input or result detected                                    */
+  PLP_ERR_CUDA = 8,       /* CUDA runtime error (message in plp_last_error)                        */
+  PLP_ERR_OOM = 9,        /* device allocation failed                                               */
+  PLP_ERR_EMPTY = 10      /* empty cluster where the metric needs |C| > 0    */
+} plp_status;
+
+enum { PLP_HESS_SPARSE = 0, PLP_HESS_FULL = 1 };          /* reading #5 */
+enum { PLP_VALIDATE = 1u, PLP_VALIDATE_SYMMETRIC = 2u };  /* plp_create_graph flags */
+
+typedef struct plp_ctx plp_ctx;
+typedef struct plp_graph plp_graph;
+
+const char* plp_last_error(void);
+const char* plp_version(void);
+
+/* ---------------------------------------------------------------------------------------------- */
+/* Context                                                                                          */
+/* ---------------------------------------------------------------------------------------------- */
+/* device: CUDA ordinal.  stream: a cudaStream_t (NULL = legacy default stream).  Allocates the
+ * ctx workspaces (CTA partials, k x k scratch) on the device. */
+plp_status plp_ctx_create(int device, void* stream, plp_ctx** out);
+plp_status plp_ctx_set_stream(plp_ctx* ctx, void* stream);
+plp_status plp_ctx_destroy(plp_ctx* ctx);
+/* Number of CTAs the edge kernel launches (the fixed reduction grid); informational. */
+plp_status plp_ctx_info(const plp_ctx* ctx, int* num_sms, int* max_ctas);
+
+/* ---------------------------------------------------------------------------------------------- */
+/* Host-side graph utilities (no GPU needed; used for setup)                    */
+/* ---------------------------------------------------------------------------------------------- */
+/* Checks the CSR of rows [0, n_rows) with columns in [0, n_cols): row_ptr monotone with
+ * row_ptr[0] = 0, columns strictly increasing per row, no diagonal entry (col == row for
+ * row < n_rows), w > 0 and finite.  With symmetric != 0 (requires n_rows == n_cols) also checks
+ * w_ij == w_ji bitwise (the paper's undirected graph G(V,E,W)).
+ * Returns PLP_ERR_GRAPH with the first offending (i, j) in plp_last_error. */
+plp_status plp_validate_csr(int64_t n_rows, int64_t n_cols, const int64_t* row_ptr,
+                            const int32_t* col, const double* w, int symmetric);
+/* Reverse Cuthill-McKee ordering of a symmetric CSR (n x n): perm[new] = old.  Per connected
+ * component (components in order of their lowest-degree / lowest-id start node), BFS from a
+ * pseudo-peripheral node with neighbours visited in (degree, id) order; the whole order is then
+ * reversed.  Deterministic.  Used so that U_j gathers hit L2. */
+plp_status plp_rcm_order(int64_t n, const int64_t* row_ptr, const int32_t* col, int64_t* perm);
+/* Relabels a symmetric CSR: new node a is old node perm[a].  Output arrays are caller-allocated
+ * (n+1, nnz, nnz); columns of each output row are sorted. */
+plp_status plp_permute_csr(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* w,
+                           const int64_t* perm, int64_t* row_ptr_out, int32_t* col_out,
+                           double* w_out);
+/* Contiguous row-block partition of n rows into `parts` blocks balancing the per-row cost
+ * cost_row + cost_nnz * deg(i) (e.g. 32k and 12 bytes): bounds[0] = 0, bounds[parts] = n. */
+plp_status plp_partition_rows(int64_t n, const int64_t* row_ptr, int parts, double cost_row,
+                              double cost_nnz, int64_t* bounds);
+/* Halo plan for the owned rows [r0, r1) of a global CSR: halo = sorted unique global ids of the
+ * columns outside [r0, r1).  Call once with halo == NULL to get *n_halo, then again with a
+ * caller array of that size.  Local column ids: owned j -> j - r0, halo h -> (r1 - r0) + index of
+ * h in halo.  col_local (size row_ptr[r1] - row_ptr[r0]) is written when non-NULL.
+ * Because ownership ranges are contiguous and halo is sorted, the halo rows owned by one peer
+ * form one contiguous slice of it: a received peer message lands in place (no unpack). */
+plp_status plp_halo_plan(const int64_t* row_ptr, const int32_t* col, int64_t r0, int64_t r1,
+                         int64_t* n_halo, int64_t* halo, int32_t* col_local);
+
+/* ---------------------------------------------------------------------------------------------- */
+/* Graph                                                                                            */
+/* ---------------------------------------------------------------------------------------------- */
+/* Uploads a host CSR of n_rows rows whose columns index the n_cols rows of U/eta (n_cols ==
+ * n_rows on one GPU; owned + halo rows on P ranks).  flags: PLP_VALIDATE runs plp_validate_csr
+ * first (PLP_VALIDATE_SYMMETRIC adds the symmetry check).  Device storage: int32 row_ptr (nnz must
+ * be < 2^31, else PLP_ERR_SHAPE), int32 col, fp64 w.  Holds its own workspace. */
+plp_status plp_create_graph(plp_ctx* ctx, int64_t n_rows, int64_t n_cols, const int64_t* row_ptr,
+                            const int32_t* col, const double* w, uint32_t flags, plp_graph** out);
+plp_status plp_graph_info(const plp_graph* g, int64_t* n_rows, int64_t* n_cols, int64_t* nnz);
+plp_status plp_destroy_graph(plp_graph* g);
+
+/* ---------------------------------------------------------------------------------------------- */
+/* F_p, EucGrad, EucHessianEta                                              */
+/* ---------------------------------------------------------------------------------------------- */
+/* Notation: A_l = 1/2 sum_i sum_{j in N(i)} w_ij |U_il - U_jl|^p (reading #1), B_l = sum_i
+ * |U_il|^p, F = sum_l A_l / B_l.  AB arrays hold [A_0..A_{k-1}, B_0..B_{k-1}].
+ *
+ * plp_fgrad: F (device double[1]), AB_out (device double[2k]) and, if G != NULL, the Euclidean
+ * gradient G_il = (p/B_l)((Delta_p u^l)_i - (A_l/B_l) phi_p(U_il))  (reading #4).  With G it runs
+ * two edge passes (objective, then gradient with the fresh AB).  Rank-local: F and AB are sums over
+ * this rank's rows (single GPU: the global values).  Hot calls do not synchronise, so B_l = 0
+ * (PLP_ERR_DEGENERATE) shows up as a non-finite F on the device; the Python binding checks it. */
+plp_status plp_fgrad(plp_ctx* ctx, const plp_graph* g, int k, const double* U, double p,
+                     double* F, double* AB_out, double* G);
+
+/* plp_hessvec: Hv = H eta at U, one edge pass.  AB_in (device, 2k): the GLOBAL A, B at the same U
+ * and p (from plp_fgrad).  mode PLP_HESS_SPARSE: Alg. 1 with D[l] = diag(H^l), H[l] = diag(H^l) -
+ * H^l for H^l = p(p-1)[Lap(w~)/B - (A/B^2) diag(cap(|u|)^{p-2})], w~_ij = w_ij cap(|u_i-u_j|)^{p-2},
+ * cap(x) = max(x, eps) (readings #5, #6, #8).  mode PLP_HESS_FULL adds the rank-two terms of the
+ * exact Hessian of A/B and then needs G_in = the Euclidean gradient at U (from plp_fgrad); single
+ * rank only (P ranks: use plp_edge_pass + plp_full_epilogue).  eps: curvature cap (1e-9 default). */
+plp_status plp_hessvec(plp_ctx* ctx, const plp_graph* g, int k, const double* U, const double* eta,
+                       double p, const double* AB_in, int mode, double eps, const double* G_in,
+                       double* Hv);
+
+/* plp_fgrad_hessvec: the benchmark unit -- F, G and Hv in ONE edge pass (one power per
+ * edge-column, shared by F, G and Hv).  AB_in (device) as for plp_hessvec; if AB_in == NULL the
+ * objective pass runs first (two edge passes).  AB_out (device, nullable) receives the A, B
+ * recomputed by the fused pass (equals AB_in up to rounding: a built-in consistency check).
+ * G, Hv (device, n_rows x k, nullable).  mode as for plp_hessvec (FULL: single rank). */
+plp_status plp_fgrad_hessvec(plp_ctx* ctx, const plp_graph* g, int k, const double* U,
+                             const double* eta, double p, const double* AB_in, int mode, double eps,
+                             double* F, double* AB_out, double* G, double* Hv);
+
+/* Low-level pieces for P ranks.  plp_edge_pass runs one edge pass:
+ *   AB_in == NULL: objective only (G, Hv, dots_out must be NULL); otherwise G / Hv when non-NULL.
+ * AB_out (device 2k, nullable): this rank's A, B partial sums.  dots_out (device 2k, nullable,
+ * needs eta and AB_in): this rank's [alpha_l = sum_i p phi_p(U_il) eta_il,
+ * gamma_l = sum_i G_il eta_il] with G the gradient at U computed inside the pass (stored only if
+ * G != NULL).  eta may be NULL when Hv and dots_out are NULL. */
+plp_status plp_edge_pass(plp_ctx* ctx, const plp_graph* g, int k, const double* U,
+                         const double* eta, double p, double eps, const double* AB_in,
+                         double* AB_out, double* dots_out, double* G, double* Hv);
+/* Full-mode rank-two epilogue, elementwise over n_rows x k with GLOBAL AB and dots:
+ *   gB = p phi_p(u), gA = B G + (A/B) gB, beta = B gamma + (A/B) alpha,
+ *   Hv += -(gA alpha + gB beta)/B^2 + 2 A gB alpha / B^3        (reading #5). */
+plp_status plp_full_epilogue(plp_ctx* ctx, int64_t n_rows, int k, const double* U, double p,
+                             const double* AB, const double* dots, const double* G, double* Hv);
+/* F = sum_l A_l / B_l from a (global) AB, on the device. */
+plp_status plp_objective_from_ab(plp_ctx* ctx, int k, const double* AB, double* F);
+
+/* ---------------------------------------------------------------------------------------------- */
+/* Tall-skinny Grassmann kernels                                           */
+/* ---------------------------------------------------------------------------------------------- */
+/* out (device k x k, row-major) = X^T Y over n rows; fixed-order reduction. */
+plp_status plp_gram(plp_ctx* ctx, int64_t n, int k, const double* X, const double* Y, double* out);
+/* Horizontal projection at U (Grassmann):
+ *   out = G - U (U^T G).  out may alias G.  Single rank (P ranks: plp_gram + all-reduce +
+ *   plp_apply_sub). */
+plp_status plp_project(plp_ctx* ctx, int64_t n, int k, const double* U, const double* G,
+                       double* out);
+/* out = X - U M  (M device k x k).  out may alias X. */
+plp_status plp_apply_sub(plp_ctx* ctx, int64_t n, int k, const double* U, const double* M,
+                         const double* X, double* out);
+/* QR retraction: Q = the Q factor of U + xi with R_ii > 0, by Cholesky-QR2
+ * (C = Y^T Y, R = chol(C), Q = Y R^-1, twice).  R_out (device k x k, nullable) = the product of
+ * both R factors.  If the Cholesky of a Gram is not positive definite returns PLP_ERR_RANK (this
+ * call synchronises the stream to read the flag).  Q may alias U or xi.  Single rank. */
+plp_status plp_retract(plp_ctx* ctx, int64_t n, int k, const double* U, const double* xi, double* Q,
+                       double* R_out);
+/* Pieces for P ranks: C (device k x k, all-reduced by the caller) -> R upper, R_ii > 0 (device);
+ * *info (device int) = 0 or the 1-based failing pivot.  Then Q = (X [+ Y]) R^-1. */
+plp_status plp_cholesky(plp_ctx* ctx, int k, const double* C, double* R, int* info);
+plp_status plp_apply_rinv(plp_ctx* ctx, int64_t n, int k, const double* X, const double* Y,
+                          const double* R, double* Q);
+/* <x, y> = sum_{i,l} x_il y_il (device double[1]); y = a x + b y. */
+plp_status plp_dot(plp_ctx* ctx, int64_t n, int k, const double* x, const double* y, double* out);
+plp_status plp_axpby(plp_ctx* ctx, int64_t n, int k, double a, const double* x, double b,
+                     double* y);
+/* Row gather (halo packing, reordering): out[r] = X[idx[r]] for r < m (idx device int64). */
+plp_status plp_gather_rows(plp_ctx* ctx, int64_t m, int k, const int64_t* idx, const double* X,
+                           double* out);
+
+/* ---------------------------------------------------------------------------------------------- */
+/* k-means discretisation and RCut                                        */
+/* ---------------------------------------------------------------------------------------------- */
+/* k-means on the n rows of X (n x dim, device), `clusters` clusters (1 <= clusters, dim <= 32,
+ * n >= clusters).  uniforms: HOST restarts x clusters values in [0,1) for k-means++ seeding (the
+ * same array the oracle gets).  Algorithm (reading #13): per restart, seed (first centre
+ * floor(u0 n); centre m = smallest i with cumsum(D^2)_i > u_m sum D^2; if sum D^2 = 0 then
+ * floor(u_m n)), assign (nearest, ties -> lowest index), then repeat {update means (empty cluster
+ * -> the point farthest from its own centroid, lowest index); assign} until sse == 0,
+ * |sse_prev - sse| < rel_tol sse_prev, or max_iters updates.  Best restart = lowest sse.
+ * Outputs: labels (device int32 n), centroids (device clusters x dim), *sse and *iters (HOST).
+ * Synchronises (the loop is host-driven).  Single rank. */
+plp_status plp_kmeans(plp_ctx* ctx, int64_t n, int dim, int clusters, const double* X,
+                      const double* uniforms, int restarts, int max_iters, double rel_tol,
+                      int32_t* labels, double* centroids, double* sse, int* iters);
+/* RCut = sum_c cut(C_c, ~C_c) / |C_c| over the graph's rows; labels (device
+ * int32, n_cols entries so halo labels resolve).  Outputs (device, nullable): cut[clusters],
+ * sizes[clusters] (int64), rcut[1].  Empty cluster -> rcut = NaN (device; the binding raises). */
+plp_status plp_rcut(plp_ctx* ctx, const plp_graph* g, int clusters, const int32_t* labels,
+                    double* cut, int64_t* sizes, double* rcut);
+
+/* ---------------------------------------------------------------------------------------------- */
+/* Diagnostics                                                                                      */
+/* ---------------------------------------------------------------------------------------------- */
+/* Evaluates the edge kernel's power policy for this (p, eps) on n device values a[i] >= 0:
+ * s[i] = cap(a_i)^{p-2}, t[i] = a_i^{p-1} (exactly what the fused pass uses per edge-column).
+ * For accuracy tests of the custom fp64 powers. */
+plp_status plp_debug_pow(plp_ctx* ctx, int64_t n, const double* a, double p, double eps, double* s,
+                         double* t);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PLP_H_ */

@@ -1,0 +1,179 @@
+// Context, graph handle, error reporting and argument checks of libplp (plp.h).
+#include <cmath>
+#include <cstdarg>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "plp_internal.h"
+#include "pow64.cuh"
+
+namespace plp {
+
+static thread_local char g_err[512] = "";
+
+plp_status set_error(plp_status st, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return st;
+}
+
+plp_status cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaErrorMemoryAllocation)
+    return set_error(PLP_ERR_OOM, "%s: %s", what, cudaGetErrorString(e));
+  return set_error(PLP_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+plp_status check_p(double p, double eps) {
+  if (!(p > 1.0 && p <= 2.0)) return set_error(PLP_ERR_DOMAIN, "p = %g not in (1, 2]", p);
+  if (p < 2.0 && !(eps > 0.0 && std::isfinite(eps)))
+    return set_error(PLP_ERR_DOMAIN, "eps = %g must be > 0 when p < 2", eps);
+  return PLP_OK;
+}
+
+plp_status check_k(int k) {
+  if (k < 1 || k > PLP_MAX_K) return set_error(PLP_ERR_DOMAIN, "k = %d not in [1, 32]", k);
+  return PLP_OK;
+}
+
+// Tables of the generic power (pow64.cuh), computed on the host in long double.
+static void fill_pow_tables(PowTables* t) {
+  for (int j = 0; j < 128; ++j) {
+    const long double c = 1.0L + (j + 0.5L) / 128.0L;
+    const double invc = (double)(1.0L / c);
+    t->logt[j].x = invc;
+    t->logt[j].y = (double)(-log2l((long double)invc));
+  }
+  for (int j = 0; j < 64; ++j) t->expt[j] = (double)exp2l((long double)j / 64.0L);
+}
+
+}  // namespace plp
+
+using namespace plp;
+
+extern "C" const char* plp_last_error(void) { return g_err; }
+extern "C" const char* plp_version(void) { return "libplp 0.1 (sm_100a)"; }
+
+extern "C" plp_status plp_ctx_create(int device, void* stream, plp_ctx** out) {
+  if (!out) return set_error(PLP_ERR_ARG, "out is null");
+  *out = nullptr;
+  PLP_CUDA(cudaSetDevice(device));
+  plp_ctx* c = new (std::nothrow) plp_ctx();
+  if (!c) return set_error(PLP_ERR_OOM, "host allocation failed");
+  c->device = device;
+  c->stream = (cudaStream_t)stream;
+  cudaDeviceProp pr;
+  cudaError_t e = cudaGetDeviceProperties(&pr, device);
+  if (e != cudaSuccess) { delete c; return cuda_check(e, "cudaGetDeviceProperties"); }
+  c->num_sms = pr.multiProcessorCount;
+  c->max_ctas = c->num_sms * 8;
+  const size_t part = (size_t)c->max_ctas * 4 * PLP_MAX_K * sizeof(double);
+  const size_t scr = (size_t)16 * PLP_MAX_K * PLP_MAX_K * sizeof(double);
+  if ((e = cudaMalloc(&c->partials, part)) != cudaSuccess ||
+      (e = cudaMalloc(&c->scratch, scr)) != cudaSuccess ||
+      (e = cudaMalloc(&c->flag, 64)) != cudaSuccess ||
+      (e = cudaMalloc(&c->iscratch, 64 * sizeof(int64_t))) != cudaSuccess ||
+      (e = cudaMalloc(&c->pow_tables, sizeof(PowTables))) != cudaSuccess) {
+    plp_ctx_destroy(c);
+    return cuda_check(e, "cudaMalloc(ctx workspace)");
+  }
+  PowTables t;
+  fill_pow_tables(&t);
+  if ((e = cudaMemcpy(c->pow_tables, &t, sizeof(t), cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemset(c->scratch, 0, scr)) != cudaSuccess ||
+      (e = cudaMemset(c->flag, 0, 64)) != cudaSuccess) {
+    plp_ctx_destroy(c);
+    return cuda_check(e, "ctx init");
+  }
+  *out = c;
+  return PLP_OK;
+}
+
+extern "C" plp_status plp_ctx_set_stream(plp_ctx* ctx, void* stream) {
+  if (!ctx) return set_error(PLP_ERR_ARG, "ctx is null");
+  ctx->stream = (cudaStream_t)stream;
+  return PLP_OK;
+}
+
+extern "C" plp_status plp_ctx_destroy(plp_ctx* ctx) {
+  if (!ctx) return PLP_OK;
+  cudaFree(ctx->partials);
+  cudaFree(ctx->scratch);
+  cudaFree(ctx->flag);
+  cudaFree(ctx->iscratch);
+  cudaFree(ctx->pow_tables);
+  cudaFree(ctx->km_best);
+  delete ctx;
+  return PLP_OK;
+}
+
+extern "C" plp_status plp_ctx_info(const plp_ctx* ctx, int* num_sms, int* max_ctas) {
+  if (!ctx) return set_error(PLP_ERR_ARG, "ctx is null");
+  if (num_sms) *num_sms = ctx->num_sms;
+  if (max_ctas) *max_ctas = ctx->max_ctas;
+  return PLP_OK;
+}
+
+extern "C" plp_status plp_create_graph(plp_ctx* ctx, int64_t n_rows, int64_t n_cols,
+                                       const int64_t* row_ptr, const int32_t* col, const double* w,
+                                       uint32_t flags, plp_graph** out) {
+  if (!ctx || !out || !row_ptr || (!col && row_ptr[n_rows] > 0) || (!w && row_ptr[n_rows] > 0))
+    return set_error(PLP_ERR_ARG, "null argument");
+  *out = nullptr;
+  if (n_rows < 0 || n_cols < n_rows) return set_error(PLP_ERR_SHAPE, "need 0 <= n_rows <= n_cols");
+  if (n_cols >= ((int64_t)1 << 31)) return set_error(PLP_ERR_SHAPE, "n_cols must be < 2^31");
+  const int64_t nnz = row_ptr[n_rows];
+  if (nnz < 0 || nnz >= ((int64_t)1 << 31)) return set_error(PLP_ERR_SHAPE, "nnz must be < 2^31");
+  if (flags & (PLP_VALIDATE | PLP_VALIDATE_SYMMETRIC)) {
+    plp_status st = plp_validate_csr(n_rows, n_cols, row_ptr, col, w,
+                                     (flags & PLP_VALIDATE_SYMMETRIC) ? 1 : 0);
+    if (st) return st;
+  }
+  PLP_CUDA(cudaSetDevice(ctx->device));
+  plp_graph* g = new (std::nothrow) plp_graph();
+  if (!g) return set_error(PLP_ERR_OOM, "host allocation failed");
+  g->ctx = ctx;
+  g->n_rows = n_rows;
+  g->n_cols = n_cols;
+  g->nnz = nnz;
+  std::vector<int32_t> rp32((size_t)n_rows + 1);
+  for (int64_t i = 0; i <= n_rows; ++i) rp32[i] = (int32_t)row_ptr[i];
+  cudaError_t e;
+  if ((e = cudaMalloc(&g->rp, sizeof(int32_t) * (n_rows + 1))) != cudaSuccess ||
+      (e = cudaMalloc(&g->col, sizeof(int32_t) * (nnz > 0 ? nnz : 1))) != cudaSuccess ||
+      (e = cudaMalloc(&g->w, sizeof(double) * (nnz > 0 ? nnz : 1))) != cudaSuccess) {
+    plp_destroy_graph(g);
+    return cuda_check(e, "cudaMalloc(graph)");
+  }
+  if ((e = cudaMemcpy(g->rp, rp32.data(), sizeof(int32_t) * (n_rows + 1), cudaMemcpyHostToDevice)) !=
+          cudaSuccess ||
+      (nnz > 0 && (e = cudaMemcpy(g->col, col, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice)) !=
+                      cudaSuccess) ||
+      (nnz > 0 && (e = cudaMemcpy(g->w, w, sizeof(double) * nnz, cudaMemcpyHostToDevice)) !=
+                      cudaSuccess)) {
+    plp_destroy_graph(g);
+    return cuda_check(e, "cudaMemcpy(graph)");
+  }
+  *out = g;
+  return PLP_OK;
+}
+
+extern "C" plp_status plp_graph_info(const plp_graph* g, int64_t* n_rows, int64_t* n_cols,
+                                     int64_t* nnz) {
+  if (!g) return set_error(PLP_ERR_ARG, "graph is null");
+  if (n_rows) *n_rows = g->n_rows;
+  if (n_cols) *n_cols = g->n_cols;
+  if (nnz) *nnz = g->nnz;
+  return PLP_OK;
+}
+
+extern "C" plp_status plp_destroy_graph(plp_graph* g) {
+  if (!g) return PLP_OK;
+  cudaFree(g->rp);
+  cudaFree(g->col);
+  cudaFree(g->w);
+  delete g;
+  return PLP_OK;
+}

@@ -1,0 +1,370 @@
+// C-ABI entry points of the edge path: F_p, EucGrad, EucHessianEta, the
+// full-mode epilogue (a6) and RCut (a12).  Kernels: edge_kernel.cuh; power policies: pow64.cuh.
+#include <cmath>
+
+#include "edge_inst.cuh"
+#include "plp_internal.h"
+
+namespace plp {
+
+// ---- power-policy dispatch (DESIGN.md §5 "power") ----------------------------------------------
+// p - 2 == -m/D (within 4 ulp: the configs' decimal p = 1.8, 1.2, 1.1 are not exact binary
+// fractions; the exponent difference is < 1e-16, reading #20) selects the root-Newton policy.
+static bool match_root(double p, int D, int* m_out) {
+  const double q = p - 2.0;
+  const long m = lround(-q * D);
+  if (m < 1 || m >= D) return false;
+  const double r = -(double)m / D;
+  const double ulp = std::nextafter(std::fabs(q), INFINITY) - std::fabs(q);
+  if (std::fabs(q - r) > 4.0 * ulp) return false;
+  *m_out = (int)m;
+  return true;
+}
+
+template <class F>
+static plp_status with_pow(plp_ctx* ctx, double p, double eps, F&& f) {
+  int m = 0;
+  if (p == 2.0) {
+    PowP2 pw;
+    pw.eps = eps;
+    pw.pm1 = 1.0;
+    return f(pw);
+  }
+  if (match_root(p, 2, &m)) {
+    PowRoot<2> pw;
+    pw.eps = eps; pw.pm1 = p - 1.0; pw.m = m;
+    return f(pw);
+  }
+  if (match_root(p, 5, &m)) {
+    PowRoot<5> pw;
+    pw.eps = eps; pw.pm1 = p - 1.0; pw.m = m;
+    return f(pw);
+  }
+  if (match_root(p, 10, &m)) {
+    PowRoot<10> pw;
+    pw.eps = eps; pw.pm1 = p - 1.0; pw.m = m;
+    return f(pw);
+  }
+  PowGeneric pw;
+  pw.eps = eps;
+  pw.pm1 = p - 1.0;
+  pw.q = p - 2.0;
+  pw.q64 = 64.0 * (p - 2.0);
+  pw.gtab = reinterpret_cast<const PowTables*>(ctx->pow_tables);
+  pw.tab = nullptr;
+  return f(pw);
+}
+
+plp_status launch_edge(plp_ctx* ctx, const EdgeArgs& a, int* grid) {
+  return with_pow(ctx, a.p, a.eps, [&](const auto& pw) -> plp_status {
+    using P = std::decay_t<decltype(pw)>;
+    if constexpr (std::is_same_v<P, PowP2>) return launch_edge_p2(ctx, a, pw, grid);
+    else if constexpr (std::is_same_v<P, PowRoot<2>>) return launch_edge_root2(ctx, a, pw, grid);
+    else if constexpr (std::is_same_v<P, PowRoot<5>>) return launch_edge_root5(ctx, a, pw, grid);
+    else if constexpr (std::is_same_v<P, PowRoot<10>>) return launch_edge_root10(ctx, a, pw, grid);
+    else return launch_edge_generic(ctx, a, pw, grid);
+  });
+}
+
+static plp_status launch_epilogue(plp_ctx* ctx, const EpiArgs& a, double eps) {
+  return with_pow(ctx, a.p, eps, [&](const auto& pw) -> plp_status {
+    using P = std::decay_t<decltype(pw)>;
+    if constexpr (std::is_same_v<P, PowP2>) return launch_epi_p2(ctx, a, pw);
+    else if constexpr (std::is_same_v<P, PowRoot<2>>) return launch_epi_root2(ctx, a, pw);
+    else if constexpr (std::is_same_v<P, PowRoot<5>>) return launch_epi_root5(ctx, a, pw);
+    else if constexpr (std::is_same_v<P, PowRoot<10>>) return launch_epi_root10(ctx, a, pw);
+    else return launch_epi_generic(ctx, a, pw);
+  });
+}
+
+// ---- fixed-order reduction of CTA partials ------------------------------------------------------
+// One warp per output sum: lane l adds CTAs l, l+32, ... in order, then a fixed xor-tree.
+__global__ void __launch_bounds__(1024) edge_finalize_kernel(int grid, int k, const double* part,
+                                                             double* AB_out, double* dots_out,
+                                                             double* F) {
+  __shared__ double sAB[2 * PLP_MAX_K];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int t = warp; t < 4 * k; t += (blockDim.x >> 5)) {
+    const int q = t / k, cl = t % k;
+    double s = 0.0;
+    for (int b = lane; b < grid; b += 32) s += part[((int64_t)b * 4 + q) * k + cl];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      if (q == 0) s *= 0.5;  // each undirected edge was counted from both endpoints
+      if (q < 2) {
+        sAB[q * k + cl] = s;
+        if (AB_out) AB_out[q * k + cl] = s;
+      } else if (dots_out) {
+        dots_out[(q - 2) * k + cl] = s;
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && F) {
+    double f = 0.0;
+    for (int l = 0; l < k; ++l) f += sAB[l] / sAB[k + l];
+    *F = f;
+  }
+}
+
+plp_status launch_edge_finalize(plp_ctx* ctx, int grid, int k, const double* partials,
+                                double* AB_out, double* dots_out, double* F) {
+  edge_finalize_kernel<<<1, 1024, 0, ctx->stream>>>(grid, k, partials, AB_out, dots_out, F);
+  PLP_LAUNCH_CHECK("edge_finalize_kernel");
+  return PLP_OK;
+}
+
+__global__ void objective_from_ab_kernel(int k, const double* AB, double* F) {
+  if (threadIdx.x == 0) {
+    double f = 0.0;
+    for (int l = 0; l < k; ++l) f += AB[l] / AB[k + l];
+    *F = f;
+  }
+}
+
+// ---- RCut (a12): per-CTA cut/size partials by label, fixed-order --------------------------------
+__global__ void __launch_bounds__(256) rcut_kernel(int64_t n, const int32_t* __restrict__ rp,
+                                                   const int32_t* __restrict__ col,
+                                                   const double* __restrict__ w, int K,
+                                                   const int32_t* __restrict__ lab,
+                                                   double* part_cut, int64_t* part_size,
+                                                   int* bad) {
+  __shared__ int s_lab[256];
+  __shared__ double s_cut[256];
+  double acc_cut = 0.0;
+  int64_t acc_size = 0;
+  const int c = threadIdx.x;  // thread c < K owns cluster c's partials
+  const int64_t tiles = (n + 255) / 256;
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int64_t i = tile * 256 + threadIdx.x;
+    int li = -1;
+    double cut = 0.0;
+    if (i < n) {
+      li = lab[i];
+      if (li < 0 || li >= K) atomicExch(bad, 1);
+      for (int e = rp[i]; e < rp[i + 1]; ++e)
+        if (lab[col[e]] != li) cut += w[e];
+    }
+    s_lab[threadIdx.x] = li;
+    s_cut[threadIdx.x] = cut;
+    __syncthreads();
+    if (c < K) {
+      for (int t = 0; t < 256; ++t)
+        if (s_lab[t] == c) {
+          acc_cut += s_cut[t];
+          acc_size += 1;
+        }
+    }
+    __syncthreads();
+  }
+  if (c < K) {
+    part_cut[(int64_t)blockIdx.x * K + c] = acc_cut;
+    part_size[(int64_t)blockIdx.x * K + c] = acc_size;
+  }
+}
+
+__global__ void rcut_finalize_kernel(int grid, int K, const double* part_cut,
+                                     const int64_t* part_size, double* cut, int64_t* sizes,
+                                     double* rcut) {
+  __shared__ double s_c[PLP_MAX_K];
+  __shared__ int64_t s_n[PLP_MAX_K];
+  const int c = threadIdx.x;
+  if (c < K) {
+    double sc = 0.0;
+    int64_t sn = 0;
+    for (int b = 0; b < grid; ++b) {
+      sc += part_cut[(int64_t)b * K + c];
+      sn += part_size[(int64_t)b * K + c];
+    }
+    s_c[c] = sc;
+    s_n[c] = sn;
+    if (cut) cut[c] = sc;
+    if (sizes) sizes[c] = sn;
+  }
+  __syncthreads();
+  if (c == 0 && rcut) {
+    double r = 0.0;
+    for (int q = 0; q < K; ++q) r += (s_n[q] > 0) ? s_c[q] / (double)s_n[q] : NAN;
+    *rcut = r;
+  }
+}
+
+}  // namespace plp
+
+using namespace plp;
+
+static plp_status check_graph_call(plp_ctx* ctx, const plp_graph* g, int k, const double* U,
+                                   double p, double eps) {
+  if (!ctx || !g || !U) return set_error(PLP_ERR_ARG, "null ctx/graph/U");
+  if (g->ctx != ctx) return set_error(PLP_ERR_ARG, "graph belongs to another ctx");
+  plp_status st = check_k(k);
+  if (st) return st;
+  return check_p(p, eps);
+}
+
+extern "C" plp_status plp_edge_pass(plp_ctx* ctx, const plp_graph* g, int k, const double* U,
+                                    const double* eta, double p, double eps, const double* AB_in,
+                                    double* AB_out, double* dots_out, double* G, double* Hv) {
+  plp_status st = check_graph_call(ctx, g, k, U, p, eps);
+  if (st) return st;
+  if (!AB_in && (G || Hv || dots_out))
+    return set_error(PLP_ERR_ARG, "G/Hv/dots need AB_in (the global A, B at U)");
+  if ((Hv || dots_out) && !eta) return set_error(PLP_ERR_ARG, "Hv/dots need eta");
+  EdgeArgs a{};
+  a.n_rows = g->n_rows;
+  a.rp = g->rp;
+  a.col = g->col;
+  a.w = g->w;
+  a.k = k;
+  a.U = U;
+  a.eta = (Hv || dots_out) ? eta : nullptr;
+  a.AB = AB_in;
+  a.G = G;
+  a.Hv = Hv;
+  a.p = p;
+  a.eps = eps;
+  a.partials = ctx->partials;
+  a.want_dots = dots_out != nullptr;
+  int grid = 0;
+  st = launch_edge(ctx, a, &grid);
+  if (st) return st;
+  if (AB_out || dots_out) return launch_edge_finalize(ctx, grid, k, ctx->partials, AB_out, dots_out, nullptr);
+  return PLP_OK;
+}
+
+extern "C" plp_status plp_objective_from_ab(plp_ctx* ctx, int k, const double* AB, double* F) {
+  if (!ctx || !AB || !F) return set_error(PLP_ERR_ARG, "null argument");
+  plp_status st = check_k(k);
+  if (st) return st;
+  objective_from_ab_kernel<<<1, 32, 0, ctx->stream>>>(k, AB, F);
+  PLP_LAUNCH_CHECK("objective_from_ab_kernel");
+  return PLP_OK;
+}
+
+extern "C" plp_status plp_full_epilogue(plp_ctx* ctx, int64_t n_rows, int k, const double* U,
+                                        double p, const double* AB, const double* dots,
+                                        const double* G, double* Hv) {
+  if (!ctx || !U || !AB || !dots || !G || !Hv) return set_error(PLP_ERR_ARG, "null argument");
+  plp_status st = check_k(k);
+  if (st) return st;
+  st = check_p(p, 1.0);
+  if (st) return st;
+  if (n_rows <= 0) return PLP_OK;
+  EpiArgs e{n_rows, k, U, p, AB, dots, G, Hv};
+  // The epilogue needs phi_p(u) only (no curvature): the cap value is irrelevant, pass 1.
+  return launch_epilogue(ctx, e, 1.0);
+}
+
+// scratch layout (doubles): [0, 2K) AB of an objective pass, [2K, 4K) dots, [4K, 6K) AB recomputed
+// by a fused pass (when the caller passes no AB_out)
+static double* scratch_ab(plp_ctx* ctx) { return ctx->scratch; }
+static double* scratch_dots(plp_ctx* ctx) { return ctx->scratch + 2 * PLP_MAX_K; }
+static double* scratch_ab2(plp_ctx* ctx) { return ctx->scratch + 4 * PLP_MAX_K; }
+
+extern "C" plp_status plp_fgrad(plp_ctx* ctx, const plp_graph* g, int k, const double* U, double p,
+                                double* F, double* AB_out, double* G) {
+  plp_status st = check_graph_call(ctx, g, k, U, p, 1.0);
+  if (st) return st;
+  double* ab = AB_out ? AB_out : scratch_ab(ctx);
+  EdgeArgs a{};
+  a.n_rows = g->n_rows; a.rp = g->rp; a.col = g->col; a.w = g->w; a.k = k; a.U = U;
+  a.p = p; a.eps = 1.0; a.partials = ctx->partials;
+  int grid = 0;
+  st = launch_edge(ctx, a, &grid);  // objective pass
+  if (st) return st;
+  st = launch_edge_finalize(ctx, grid, k, ctx->partials, ab, nullptr, F);
+  if (st) return st;
+  if (G) {
+    EdgeArgs b = a;
+    b.AB = ab;
+    b.G = G;
+    st = launch_edge(ctx, b, &grid);  // gradient pass with the fresh A, B
+    if (st) return st;
+  }
+  return PLP_OK;
+}
+
+extern "C" plp_status plp_hessvec(plp_ctx* ctx, const plp_graph* g, int k, const double* U,
+                                  const double* eta, double p, const double* AB_in, int mode,
+                                  double eps, const double* G_in, double* Hv) {
+  plp_status st = check_graph_call(ctx, g, k, U, p, eps);
+  if (st) return st;
+  if (!eta || !AB_in || !Hv) return set_error(PLP_ERR_ARG, "hessvec needs eta, AB_in and Hv");
+  if (mode != PLP_HESS_SPARSE && mode != PLP_HESS_FULL) return set_error(PLP_ERR_ARG, "bad mode");
+  if (mode == PLP_HESS_FULL && !G_in)
+    return set_error(PLP_ERR_ARG, "full mode needs G_in (the Euclidean gradient at U)");
+  const bool full = mode == PLP_HESS_FULL;
+  st = plp_edge_pass(ctx, g, k, U, eta, p, eps, AB_in, nullptr, full ? scratch_dots(ctx) : nullptr,
+                     nullptr, Hv);
+  if (st || !full) return st;
+  return plp_full_epilogue(ctx, g->n_rows, k, U, p, AB_in, scratch_dots(ctx), G_in, Hv);
+}
+
+extern "C" plp_status plp_fgrad_hessvec(plp_ctx* ctx, const plp_graph* g, int k, const double* U,
+                                        const double* eta, double p, const double* AB_in, int mode,
+                                        double eps, double* F, double* AB_out, double* G,
+                                        double* Hv) {
+  plp_status st = check_graph_call(ctx, g, k, U, p, eps);
+  if (st) return st;
+  if (mode != PLP_HESS_SPARSE && mode != PLP_HESS_FULL) return set_error(PLP_ERR_ARG, "bad mode");
+  if (Hv && !eta) return set_error(PLP_ERR_ARG, "Hv needs eta");
+  const bool full = mode == PLP_HESS_FULL && Hv != nullptr;
+  if (full && !G) return set_error(PLP_ERR_ARG, "full mode needs the G output buffer");
+  if (!AB_in) {  // objective pass first (two edge passes)
+    st = plp_edge_pass(ctx, g, k, U, nullptr, p, eps, nullptr, scratch_ab(ctx), nullptr, nullptr,
+                       nullptr);
+    if (st) return st;
+    AB_in = scratch_ab(ctx);
+  }
+  EdgeArgs a{};
+  a.n_rows = g->n_rows; a.rp = g->rp; a.col = g->col; a.w = g->w; a.k = k; a.U = U;
+  a.eta = Hv ? eta : nullptr;
+  a.AB = AB_in; a.G = G; a.Hv = Hv; a.p = p; a.eps = eps; a.partials = ctx->partials;
+  a.want_dots = full;
+  int grid = 0;
+  st = launch_edge(ctx, a, &grid);
+  if (st) return st;
+  if (AB_out || full || F) {
+    // F and AB_out come from the fused pass's own A', B' (single rank: the global values)
+    st = launch_edge_finalize(ctx, grid, k, ctx->partials, AB_out ? AB_out : scratch_ab2(ctx),
+                              full ? scratch_dots(ctx) : nullptr, F);
+    if (st) return st;
+  }
+  if (full) return plp_full_epilogue(ctx, g->n_rows, k, U, p, AB_in, scratch_dots(ctx), G, Hv);
+  return PLP_OK;
+}
+
+extern "C" plp_status plp_debug_pow(plp_ctx* ctx, int64_t n, const double* a, double p, double eps,
+                                    double* s, double* t) {
+  if (!ctx || !a || !s || !t || n < 0) return set_error(PLP_ERR_ARG, "bad argument");
+  plp_status st = check_p(p, eps);
+  if (st) return st;
+  if (n == 0) return PLP_OK;
+  return with_pow(ctx, p, eps, [&](const auto& pw) -> plp_status {
+    using P = std::decay_t<decltype(pw)>;
+    if constexpr (std::is_same_v<P, PowP2>) return launch_dbg_p2(ctx, n, a, s, t, pw);
+    else if constexpr (std::is_same_v<P, PowRoot<2>>) return launch_dbg_root2(ctx, n, a, s, t, pw);
+    else if constexpr (std::is_same_v<P, PowRoot<5>>) return launch_dbg_root5(ctx, n, a, s, t, pw);
+    else if constexpr (std::is_same_v<P, PowRoot<10>>) return launch_dbg_root10(ctx, n, a, s, t, pw);
+    else return launch_dbg_generic(ctx, n, a, s, t, pw);
+  });
+}
+
+extern "C" plp_status plp_rcut(plp_ctx* ctx, const plp_graph* g, int clusters,
+                               const int32_t* labels, double* cut, int64_t* sizes, double* rcut) {
+  if (!ctx || !g || !labels) return set_error(PLP_ERR_ARG, "null argument");
+  if (clusters < 1 || clusters > PLP_MAX_K) return set_error(PLP_ERR_DOMAIN, "clusters must be in [1, 32]");
+  int grid = (int)((g->n_rows + 255) / 256);
+  if (grid > ctx->max_ctas) grid = ctx->max_ctas;
+  if (grid < 1) grid = 1;
+  double* pc = ctx->partials;
+  int64_t* ps = reinterpret_cast<int64_t*>(ctx->partials + (int64_t)ctx->max_ctas * PLP_MAX_K);
+  PLP_CUDA(cudaMemsetAsync(ctx->flag, 0, sizeof(int), ctx->stream));
+  rcut_kernel<<<grid, 256, 0, ctx->stream>>>(g->n_rows, g->rp, g->col, g->w, clusters, labels, pc,
+                                              ps, ctx->flag);
+  PLP_LAUNCH_CHECK("rcut_kernel");
+  rcut_finalize_kernel<<<1, 32, 0, ctx->stream>>>(grid, clusters, pc, ps, cut, sizes, rcut);
+  PLP_LAUNCH_CHECK("rcut_finalize_kernel");
+  return PLP_OK;
+}

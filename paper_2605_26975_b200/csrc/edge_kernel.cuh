@@ -1,0 +1,256 @@
+// The fused F / EucGrad / EucHessianEta edge kernel.
+//
+// One pass over the CSR computes, per row i and column l:
+//   per stored edge (i, j):  d = U_il - U_jl, a = |d|,  s = cap(a)^{p-2}, t = a^{p-1}  (one power)
+//       A'_l   += w_ij t a                      (Eq. (1) numerator, halved at the end; reading #1)
+//       L_il   += w_ij copysign(t, d)           ((Delta_p u)_i)
+//       HA_il  += w_ij s (eta_il - eta_jl)      (Laplacian of w~ applied to eta; Alg. 1 lines 7-9)
+//   per node:  sn = cap(|U_il|)^{p-2}, tn = |U_il|^{p-1}:   B'_l += tn |U_il|
+//       G_il  = (p/B_l) (L_il - (A_l/B_l) copysign(tn, U_il))                  (reading #4)
+//       Hv_il = p(p-1)/B_l HA_il - p(p-1) A_l/B_l^2 sn eta_il                  (Alg. 1, #5)
+// Thread mapping ("one warp or sub-warp per row with the k columns vectorised", north star):
+//   a group of LPR lanes owns a row; lane li owns columns [li*CPL, li*CPL + CPL); a gathered
+//   neighbour row U_j (8k bytes) is read by the group as LPR contiguous CPL-vectors (coalesced);
+//   col_idx/w are broadcast within the group.  Persistent grid-stride loop over row groups; each
+//   CTA reduces its A', B', alpha, gamma partials in a fixed order (no atomics).
+#pragma once
+#include "plp_internal.h"
+#include "pow64.cuh"
+
+namespace plp {
+
+template <int CPL>
+__device__ __forceinline__ void ld_vec(const double* __restrict__ p, double (&v)[CPL]) {
+  if constexpr (CPL % 2 == 0) {
+#pragma unroll
+    for (int c = 0; c < CPL; c += 2) {
+      const double2 t = __ldg(reinterpret_cast<const double2*>(p + c));
+      v[c] = t.x;
+      v[c + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) v[c] = __ldg(p + c);
+  }
+}
+
+template <int CPL>
+__device__ __forceinline__ void st_vec(double* __restrict__ p, const double (&v)[CPL]) {
+  if constexpr (CPL % 2 == 0) {
+#pragma unroll
+    for (int c = 0; c < CPL; c += 2) *reinterpret_cast<double2*>(p + c) = make_double2(v[c], v[c + 1]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) p[c] = v[c];
+  }
+}
+
+constexpr int kEdgeThreads = 256;
+
+template <int CPL, int LPR, class POW, bool HAS_ETA>
+__global__ void __launch_bounds__(kEdgeThreads, 2) edge_kernel(EdgeArgs a, POW pw) {
+  extern __shared__ double4 smem_raw[];
+  if constexpr (POW::kNeedsTables) {
+    pw.init_smem(smem_raw);
+    __syncthreads();
+  }
+  constexpr int RPW = 32 / LPR;  // rows per warp
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int grp = lane / LPR;
+  const int li = lane % LPR;
+  const int rows_per_iter = (blockDim.x >> 5) * RPW;
+  const int k = a.k;
+  const int c0 = li * CPL;
+  const bool active = c0 < k;  // k even when CPL is even, so a lane owns all or none of its columns
+  const double p = a.p;
+  const double pp1 = p * (p - 1.0);
+
+  double cG[CPL], cAB[CPL], cHA[CPL], cHB[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) cG[c] = cAB[c] = cHA[c] = cHB[c] = 0.0;
+  if (a.AB != nullptr && active) {
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const double A = a.AB[c0 + c], B = a.AB[k + c0 + c];
+      cG[c] = p / B;                 // p / B
+      cAB[c] = A / B;                // A / B
+      cHA[c] = pp1 / B;              // p(p-1) / B
+      cHB[c] = pp1 * A / (B * B);    // p(p-1) A / B^2
+    }
+  }
+  double accA[CPL], accB[CPL], accAl[CPL], accGa[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) accA[c] = accB[c] = accAl[c] = accGa[c] = 0.0;
+
+  const int32_t* __restrict__ rp = a.rp;
+  const int32_t* __restrict__ col = a.col;
+  const double* __restrict__ wt = a.w;
+  const double* __restrict__ U = a.U;
+  const double* __restrict__ eta = a.eta;
+
+  if (active) {
+    for (int64_t row = (int64_t)blockIdx.x * rows_per_iter + warp * RPW + grp; row < a.n_rows;
+         row += (int64_t)gridDim.x * rows_per_iter) {
+      const int e0 = __ldg(rp + row), e1 = __ldg(rp + row + 1);
+      double ui[CPL], ei[CPL];
+      ld_vec<CPL>(U + row * k + c0, ui);
+      if constexpr (HAS_ETA) ld_vec<CPL>(eta + row * k + c0, ei);
+      double L[CPL], HA[CPL], Ar[CPL];
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) L[c] = HA[c] = Ar[c] = 0.0;
+
+      constexpr int UNR = (CPL <= 2) ? 4 : 2;
+      int e = e0;
+      for (; e + UNR <= e1; e += UNR) {
+        int j[UNR];
+        double wv[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          j[u] = __ldg(col + e + u);
+          wv[u] = __ldg(wt + e + u);
+        }
+        double uj[UNR][CPL], ej[UNR][CPL];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          ld_vec<CPL>(U + (int64_t)j[u] * k + c0, uj[u]);
+          if constexpr (HAS_ETA) ld_vec<CPL>(eta + (int64_t)j[u] * k + c0, ej[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) {
+            const double d = ui[c] - uj[u][c];
+            const double ad = fabs(d);
+            double s, t;
+            pw.eval(ad, s, t);
+            Ar[c] = fma(wv[u], t * ad, Ar[c]);
+            L[c] = fma(wv[u], copysign(t, d), L[c]);
+            if constexpr (HAS_ETA) HA[c] = fma(wv[u] * s, ei[c] - ej[u][c], HA[c]);
+          }
+        }
+      }
+      for (; e < e1; ++e) {
+        const int j = __ldg(col + e);
+        const double wv = __ldg(wt + e);
+        double uj[CPL], ej[CPL];
+        ld_vec<CPL>(U + (int64_t)j * k + c0, uj);
+        if constexpr (HAS_ETA) ld_vec<CPL>(eta + (int64_t)j * k + c0, ej);
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const double d = ui[c] - uj[c];
+          const double ad = fabs(d);
+          double s, t;
+          pw.eval(ad, s, t);
+          Ar[c] = fma(wv, t * ad, Ar[c]);
+          L[c] = fma(wv, copysign(t, d), L[c]);
+          if constexpr (HAS_ETA) HA[c] = fma(wv * s, ei[c] - ej[c], HA[c]);
+        }
+      }
+
+      // ---- row epilogue: node terms, outputs, partial sums ----
+      double g[CPL], h[CPL];
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const double au = fabs(ui[c]);
+        double sn, tn;
+        pw.eval(au, sn, tn);
+        accA[c] += Ar[c];
+        accB[c] += tn * au;
+        const double phi = copysign(tn, ui[c]);
+        g[c] = cG[c] * (L[c] - cAB[c] * phi);
+        if constexpr (HAS_ETA) {
+          h[c] = cHA[c] * HA[c] - cHB[c] * sn * ei[c];
+          if (a.want_dots) accAl[c] = fma(p * phi, ei[c], accAl[c]);
+        } else {
+          h[c] = 0.0;
+        }
+      }
+      if (a.G != nullptr) st_vec<CPL>(a.G + row * k + c0, g);
+      if constexpr (HAS_ETA) {
+        if (a.Hv != nullptr) st_vec<CPL>(a.Hv + row * k + c0, h);
+        if (a.want_dots) {
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) accGa[c] = fma(g[c], ei[c], accGa[c]);
+        }
+      }
+    }
+  }
+
+  // ---- fixed-order CTA reduction of the partial sums ----
+  __syncthreads();
+  double* red = reinterpret_cast<double*>(smem_raw);  // [4][CPL][blockDim]
+  const int nt = blockDim.x;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    red[(0 * CPL + c) * nt + threadIdx.x] = accA[c];
+    red[(1 * CPL + c) * nt + threadIdx.x] = accB[c];
+    red[(2 * CPL + c) * nt + threadIdx.x] = accAl[c];
+    red[(3 * CPL + c) * nt + threadIdx.x] = accGa[c];
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < 4 * k; t += nt) {
+    const int q = t / k, cl = t % k;
+    const int l = cl / CPL, c = cl % CPL;
+    const double* base = red + (q * CPL + c) * nt;
+    double s = 0.0;
+    for (int w = 0; w < (nt >> 5); ++w)
+      for (int gg = 0; gg < RPW; ++gg) s += base[w * 32 + gg * LPR + l];
+    a.partials[((int64_t)blockIdx.x * 4 + q) * k + cl] = s;
+  }
+}
+
+template <int CPL, int LPR, class POW, bool HAS_ETA>
+plp_status launch_edge_shape(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int* grid_out) {
+  auto kern = edge_kernel<CPL, LPR, POW, HAS_ETA>;
+  const size_t red_bytes = (size_t)4 * CPL * kEdgeThreads * sizeof(double);
+  const size_t tab_bytes = POW::kNeedsTables ? sizeof(PowTables) : 0;
+  const size_t smem = red_bytes > tab_bytes ? red_bytes : tab_bytes;
+  static int occ = -1;  // per instantiation (device-independent enough for one process)
+  if (occ < 0) {
+    if (smem > 48 * 1024)
+      PLP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int o = 0;
+    PLP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kEdgeThreads, smem));
+    occ = o < 1 ? 1 : o;
+  }
+  const int rows_per_iter = (kEdgeThreads / 32) * (32 / LPR);
+  int64_t need = (a.n_rows + rows_per_iter - 1) / rows_per_iter;
+  int grid = occ * ctx->num_sms;
+  if (grid > ctx->max_ctas) grid = ctx->max_ctas;
+  if (need < grid) grid = (int)(need > 0 ? need : 1);
+  kern<<<grid, kEdgeThreads, smem, ctx->stream>>>(a, pw);
+  PLP_LAUNCH_CHECK("edge_kernel");
+  *grid_out = grid;
+  return PLP_OK;
+}
+
+// Dispatch on k (and alignment) to a (CPL, LPR) shape.
+template <class POW>
+plp_status launch_edge_pow(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int* grid) {
+  const int k = a.k;
+  auto al16 = [](const void* ptr) { return ((uintptr_t)ptr & 15u) == 0; };
+  const bool vec_ok = (k % 2 == 0) && al16(a.U) && (a.eta == nullptr || al16(a.eta)) &&
+                      (a.G == nullptr || al16(a.G)) && (a.Hv == nullptr || al16(a.Hv));
+  const bool he = a.eta != nullptr;
+#define PLP_SHAPE(C, L)                                                                 \
+  return he ? launch_edge_shape<C, L, POW, true>(ctx, a, pw, grid)                      \
+            : launch_edge_shape<C, L, POW, false>(ctx, a, pw, grid)
+  if (vec_ok) {
+    const int half = k / 2;
+    if (half <= 1) PLP_SHAPE(2, 1);
+    if (half <= 2) PLP_SHAPE(2, 2);
+    if (half <= 4) PLP_SHAPE(2, 4);
+    if (half <= 8) PLP_SHAPE(2, 8);
+    PLP_SHAPE(2, 16);
+  }
+  if (k <= 1) PLP_SHAPE(1, 1);
+  if (k <= 2) PLP_SHAPE(1, 2);
+  if (k <= 4) PLP_SHAPE(1, 4);
+  if (k <= 8) PLP_SHAPE(1, 8);
+  if (k <= 16) PLP_SHAPE(1, 16);
+  PLP_SHAPE(1, 32);
+#undef PLP_SHAPE
+}
+
+}  // namespace plp

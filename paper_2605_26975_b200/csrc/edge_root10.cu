@@ -1,0 +1,18 @@
+// Instantiation unit of the fused edge kernel for the power policy PowRoot<10> (see edge_kernel.cuh).
+#include "edge_inst.cuh"
+#include "edge_kernel.cuh"
+
+namespace plp {
+plp_status launch_edge_root10(plp_ctx* ctx, const EdgeArgs& a, const PowRoot<10>& pw, int* grid) {
+  return launch_edge_pow(ctx, a, pw, grid);
+}
+plp_status launch_epi_root10(plp_ctx* ctx, const EpiArgs& a, const PowRoot<10>& pw) {
+  return launch_epi(ctx, a, pw);
+}
+}  // namespace plp
+namespace plp {
+plp_status launch_dbg_root10(plp_ctx* ctx, int64_t n, const double* a, double* s, double* t,
+                            const PowRoot<10>& pw) {
+  return launch_dbg(ctx, n, a, s, t, pw);
+}
+}  // namespace plp

@@ -1,0 +1,335 @@
+// k-means discretisation of the embedding (reading #13).
+// Device kernels for k-means++ seeding (D^2 update, chunked cumulative sums, pick), the fused
+// Lloyd assign + per-CTA centroid/count/SSE partials (fixed order, no atomics), empty-cluster
+// repair (farthest point, lowest index), driven by a host loop with one small D2H per iteration.
+#include <cstring>
+#include <vector>
+
+#include "plp_internal.h"
+
+namespace plp {
+
+constexpr int kKmThreads = 128;  // points per tile
+constexpr int kChunk = 256;      // seeding cumsum chunk
+
+// squared distance, ascending coordinates, no FMA contraction (same rounding as a plain loop)
+__device__ __forceinline__ double km_dist2(const double* x, int xs, const double* c, int dim) {
+  double s = 0.0;
+  for (int d = 0; d < dim; ++d) {
+    const double t = __dsub_rn(x[d * xs], c[d]);
+    s = __dadd_rn(s, __dmul_rn(t, t));
+  }
+  return s;
+}
+
+// D2[i] = dist2(x_i, c) (first) or min(D2[i], dist2(x_i, c))
+__global__ void km_d2_kernel(int64_t n, int dim, const double* __restrict__ X,
+                             const double* __restrict__ c, double* __restrict__ D2, int first) {
+  __shared__ double cs[PLP_MAX_K];
+  if (threadIdx.x < dim) cs[threadIdx.x] = c[threadIdx.x];
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double d = km_dist2(X + i * dim, 1, cs, dim);
+    D2[i] = first ? d : (d < D2[i] ? d : D2[i]);
+  }
+}
+
+// chunk sums (sequential within each chunk of kChunk points)
+__global__ void km_chunk_kernel(int64_t n, const double* __restrict__ D2, double* __restrict__ cs) {
+  const int64_t nch = (n + kChunk - 1) / kChunk;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nch;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    const int64_t e = (c + 1) * kChunk < n ? (c + 1) * kChunk : n;
+    for (int64_t i = c * kChunk; i < e; ++i) s += D2[i];
+    cs[c] = s;
+  }
+}
+
+// One block: S = sum D2 (thread ranges of chunks, then a sequential pass over thread sums),
+// target = u S, smallest i with cumsum_i > target (n-1 if none; floor(u n) if S == 0).
+// Copies X[pick] to cent_row.
+__global__ void __launch_bounds__(1024) km_pick_kernel(int64_t n, int dim, const double* __restrict__ X,
+                                                       const double* __restrict__ D2,
+                                                       const double* __restrict__ cs, double u,
+                                                       double* __restrict__ cent_row,
+                                                       int64_t* pick_out) {
+  __shared__ double ts[1024];
+  __shared__ int64_t s_pick;
+  const int64_t nch = (n + kChunk - 1) / kChunk;
+  const int T = blockDim.x;
+  const int64_t per = (nch + T - 1) / T;
+  const int t = threadIdx.x;
+  double s = 0.0;
+  for (int64_t c = t * per; c < (t + 1) * per && c < nch; ++c) s += cs[c];
+  ts[t] = s;
+  __syncthreads();
+  if (t == 0) {
+    double S = 0.0;
+    for (int q = 0; q < T; ++q) S += ts[q];
+    int64_t pick = n - 1;
+    if (S > 0.0) {
+      const double target = u * S;
+      double run = 0.0;
+      int q = 0;
+      for (; q < T; ++q) {
+        if (run + ts[q] > target) break;
+        run += ts[q];
+      }
+      if (q < T) {
+        int64_t c = q * per;
+        const int64_t cend = ((int64_t)q + 1) * per < nch ? ((int64_t)q + 1) * per : nch;
+        for (; c < cend; ++c) {
+          if (run + cs[c] > target) break;
+          run += cs[c];
+        }
+        if (c < cend) {
+          const int64_t e = (c + 1) * kChunk < n ? (c + 1) * kChunk : n;
+          for (int64_t i = c * kChunk; i < e; ++i) {
+            run += D2[i];
+            if (run > target) {
+              pick = i;
+              break;
+            }
+          }
+        }
+      }
+    } else {
+      pick = (int64_t)floor(u * (double)n);
+      if (pick >= n) pick = n - 1;
+    }
+    s_pick = pick;
+    if (pick_out) *pick_out = pick;
+  }
+  __syncthreads();
+  if (t < dim) cent_row[t] = X[s_pick * dim + t];
+}
+
+// Fused assign (nearest centroid, ties -> lowest index) + per-CTA partials:
+// part[b][0 .. K*dim) sums, [K*dim, K*dim+K) counts, [K*dim+K] sse.
+__global__ void __launch_bounds__(kKmThreads) km_assign_kernel(int64_t n, int dim, int K,
+                                                               const double* __restrict__ X,
+                                                               const double* __restrict__ cent,
+                                                               int32_t* __restrict__ lab,
+                                                               double* __restrict__ best_d,
+                                                               double* __restrict__ part) {
+  __shared__ double cs[PLP_MAX_K * PLP_MAX_K];
+  __shared__ double xs[kKmThreads * (PLP_MAX_K + 1)];
+  __shared__ int ls[kKmThreads];
+  __shared__ double bs[kKmThreads];
+  const int pitch = dim | 1;
+  for (int i = threadIdx.x; i < K * dim; i += blockDim.x) cs[i] = cent[i];
+  const int E = K * dim + K + 1;
+  double acc[9];
+  for (int q = 0; q < 9; ++q) acc[q] = 0.0;
+  const int64_t tiles = (n + kKmThreads - 1) / kKmThreads;
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int64_t p0 = tile * kKmThreads;
+    const int np = (int)((n - p0) < kKmThreads ? (n - p0) : kKmThreads);
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < np * dim; idx += blockDim.x)
+      xs[(idx / dim) * pitch + idx % dim] = X[p0 * dim + idx];
+    __syncthreads();
+    const int t = threadIdx.x;
+    if (t < np) {
+      int bc = 0;
+      double bd = km_dist2(xs + t * pitch, 1, cs, dim);
+      for (int c = 1; c < K; ++c) {
+        const double d = km_dist2(xs + t * pitch, 1, cs + c * dim, dim);
+        if (d < bd) { bd = d; bc = c; }
+      }
+      lab[p0 + t] = bc;
+      best_d[p0 + t] = bd;
+      ls[t] = bc;
+      bs[t] = bd;
+    }
+    __syncthreads();
+    for (int q = 0; q * kKmThreads + threadIdx.x < E; ++q) {
+      const int e = q * kKmThreads + threadIdx.x;
+      double s = 0.0;
+      if (e < K * dim) {
+        const int c = e / dim, d = e % dim;
+        for (int p = 0; p < np; ++p)
+          if (ls[p] == c) s += xs[p * pitch + d];
+      } else if (e < K * dim + K) {
+        const int c = e - K * dim;
+        for (int p = 0; p < np; ++p)
+          if (ls[p] == c) s += 1.0;
+      } else {
+        for (int p = 0; p < np; ++p) s += bs[p];
+      }
+      acc[q] += s;
+    }
+  }
+  for (int q = 0; q * kKmThreads + threadIdx.x < E; ++q)
+    part[(int64_t)blockIdx.x * E + q * kKmThreads + threadIdx.x] = acc[q];
+}
+
+// red = [sums K*dim | counts K | sse]; cent[c] = sums/count where count > 0 (empty: unchanged)
+__global__ void km_update_kernel(int K, int dim, const double* __restrict__ red, double* cent) {
+  for (int e = threadIdx.x; e < K * dim; e += blockDim.x) {
+    const int c = e / dim;
+    const double cnt = red[K * dim + c];
+    if (cnt > 0.0) cent[e] = red[e] / cnt;
+  }
+}
+
+// argmax of best_d (lowest index on ties): per-block partials then a final pass
+__global__ void km_argmax_kernel(int64_t n, const double* __restrict__ v, double* pv, int64_t* pi) {
+  __shared__ double sv[256];
+  __shared__ int64_t si[256];
+  double bv = -INFINITY;
+  int64_t bi = n;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (v[i] > bv) { bv = v[i]; bi = i; }
+  sv[threadIdx.x] = bv;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      const double ov = sv[threadIdx.x + o];
+      const int64_t oi = si[threadIdx.x + o];
+      if (ov > sv[threadIdx.x] || (ov == sv[threadIdx.x] && oi < si[threadIdx.x])) {
+        sv[threadIdx.x] = ov;
+        si[threadIdx.x] = oi;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    pv[blockIdx.x] = sv[0];
+    pi[blockIdx.x] = si[0];
+  }
+}
+
+__global__ void km_reseed_kernel(int grid, int dim, int c, const double* pv, const int64_t* pi,
+                                 const double* __restrict__ X, double* cent, double* best_d) {
+  __shared__ int64_t far;
+  if (threadIdx.x == 0) {
+    double bv = -INFINITY;
+    int64_t bi = 0;
+    for (int b = 0; b < grid; ++b)
+      if (pv[b] > bv || (pv[b] == bv && pi[b] < bi)) { bv = pv[b]; bi = pi[b]; }
+    far = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x < dim) cent[c * dim + threadIdx.x] = X[far * dim + threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x == 0) best_d[far] = -1.0;
+}
+
+__global__ void km_sum_kernel(int grid, int E, const double* part, double* out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int e = warp; e < E; e += (blockDim.x >> 5)) {
+    double s = 0.0;
+    for (int b = lane; b < grid; b += 32) s += part[(int64_t)b * E + e];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[e] = s;
+  }
+}
+
+}  // namespace plp
+
+using namespace plp;
+
+extern "C" plp_status plp_kmeans(plp_ctx* ctx, int64_t n, int dim, int K, const double* X,
+                                 const double* uniforms, int restarts, int max_iters,
+                                 double rel_tol, int32_t* labels, double* centroids, double* sse,
+                                 int* iters) {
+  if (!ctx || !X || !uniforms || !labels || !centroids || !sse)
+    return set_error(PLP_ERR_ARG, "null argument");
+  if (dim < 1 || dim > PLP_MAX_K || K < 1 || K > PLP_MAX_K)
+    return set_error(PLP_ERR_DOMAIN, "dim and clusters must be in [1, 32]");
+  if (n < K) return set_error(PLP_ERR_SHAPE, "need n >= clusters");
+  if (restarts < 1 || max_iters < 0) return set_error(PLP_ERR_ARG, "restarts >= 1, max_iters >= 0");
+  cudaStream_t st = ctx->stream;
+  // workspace: best_d (n), D2 (n), chunk sums, labels + centroids of the running restart
+  const int64_t nch = (n + kChunk - 1) / kChunk;
+  const size_t need = (size_t)(2 * n + nch + K * dim + (n + 1) / 2 + 64);
+  if (ctx->km_cap < need) {
+    cudaFree(ctx->km_best);
+    ctx->km_best = nullptr;
+    ctx->km_cap = 0;
+    PLP_CUDA(cudaMalloc(&ctx->km_best, need * sizeof(double)));
+    ctx->km_cap = need;
+  }
+  double* best_d = ctx->km_best;
+  double* D2 = best_d + n;
+  double* csum = D2 + n;
+  double* cent = csum + nch;
+  int32_t* lab = reinterpret_cast<int32_t*>(cent + K * dim);
+  const int E = K * dim + K + 1;
+  int grid = (int)((n + kKmThreads - 1) / kKmThreads);
+  if (grid > ctx->max_ctas) grid = ctx->max_ctas;
+  const int64_t part_cap = (int64_t)ctx->max_ctas * 4 * PLP_MAX_K;
+  if ((int64_t)grid * E > part_cap) grid = (int)(part_cap / E);
+  double* red = ctx->scratch + 256;  // E <= 32*32+33 doubles
+  int gridn = (int)((n + 255) / 256);
+  if (gridn > ctx->max_ctas) gridn = ctx->max_ctas;
+  double* pv = ctx->partials;
+  int64_t* pi = reinterpret_cast<int64_t*>(ctx->partials + ctx->max_ctas);
+  std::vector<double> host(E);
+  double best = INFINITY;
+  int best_iters = 0;
+  for (int r = 0; r < restarts; ++r) {
+    const double* u = uniforms + (int64_t)r * K;
+    // ---- k-means++ seeding ----
+    int64_t c0 = (int64_t)floor(u[0] * (double)n);
+    if (c0 >= n) c0 = n - 1;
+    PLP_CUDA(cudaMemcpyAsync(cent, X + c0 * dim, sizeof(double) * dim, cudaMemcpyDeviceToDevice, st));
+    for (int m = 1; m < K; ++m) {
+      km_d2_kernel<<<gridn, 256, 0, st>>>(n, dim, X, cent + (int64_t)(m - 1) * dim, D2, m == 1);
+      PLP_LAUNCH_CHECK("km_d2_kernel");
+      const int gc = (int)((nch + 255) / 256);
+      km_chunk_kernel<<<gc, 256, 0, st>>>(n, D2, csum);
+      PLP_LAUNCH_CHECK("km_chunk_kernel");
+      km_pick_kernel<<<1, 1024, 0, st>>>(n, dim, X, D2, csum, u[m], cent + (int64_t)m * dim, nullptr);
+      PLP_LAUNCH_CHECK("km_pick_kernel");
+    }
+    // ---- Lloyd ----
+    auto assign = [&](double* sse_out, std::vector<double>& h) -> plp_status {
+      km_assign_kernel<<<grid, kKmThreads, 0, st>>>(n, dim, K, X, cent, lab, best_d, ctx->partials);
+      PLP_LAUNCH_CHECK("km_assign_kernel");
+      km_sum_kernel<<<1, 1024, 0, st>>>(grid, E, ctx->partials, red);
+      PLP_LAUNCH_CHECK("km_sum_kernel");
+      PLP_CUDA(cudaMemcpyAsync(h.data(), red, sizeof(double) * E, cudaMemcpyDeviceToHost, st));
+      PLP_CUDA(cudaStreamSynchronize(st));
+      *sse_out = h[E - 1];
+      return PLP_OK;
+    };
+    double cur = 0.0;
+    plp_status s = assign(&cur, host);
+    if (s) return s;
+    int it = 0;
+    while (it < max_iters) {
+      km_update_kernel<<<1, 256, 0, st>>>(K, dim, red, cent);
+      PLP_LAUNCH_CHECK("km_update_kernel");
+      for (int c = 0; c < K; ++c) {
+        if (host[K * dim + c] > 0.0) continue;  // empty cluster -> farthest point
+        km_argmax_kernel<<<gridn, 256, 0, st>>>(n, best_d, pv, pi);
+        PLP_LAUNCH_CHECK("km_argmax_kernel");
+        km_reseed_kernel<<<1, 32, 0, st>>>(gridn, dim, c, pv, pi, X, cent, best_d);
+        PLP_LAUNCH_CHECK("km_reseed_kernel");
+      }
+      double nxt = 0.0;
+      if ((s = assign(&nxt, host))) return s;
+      ++it;
+      const bool conv = (cur == 0.0) || (fabs(cur - nxt) < rel_tol * cur);
+      cur = nxt;
+      if (conv) break;
+    }
+    if (cur < best) {
+      best = cur;
+      best_iters = it;
+      PLP_CUDA(cudaMemcpyAsync(labels, lab, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st));
+      PLP_CUDA(cudaMemcpyAsync(centroids, cent, sizeof(double) * K * dim, cudaMemcpyDeviceToDevice, st));
+    }
+  }
+  PLP_CUDA(cudaStreamSynchronize(st));
+  *sse = best;
+  if (iters) *iters = best_iters;
+  return PLP_OK;
+}

@@ -1,0 +1,76 @@
+// Internal declarations of libplp (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "plp.h"
+
+#define PLP_MAX_K 32
+
+struct plp_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 0;
+  int max_ctas = 0;          // edge/dense kernels' fixed reduction grid upper bound
+  double* partials = nullptr;  // max_ctas * 4 * PLP_MAX_K doubles
+  double* scratch = nullptr;   // 8 * PLP_MAX_K * PLP_MAX_K doubles (Grams, R, AB, dots)
+  int* flag = nullptr;         // device status flags (Cholesky info, ...)
+  int64_t* iscratch = nullptr; // device int64 scratch (argmax index, sizes)
+  void* pow_tables = nullptr;  // device PowTables for the generic power (pow64.cuh)
+  // k-means workspace (grown at plp_kmeans entry if needed; not a hot edge call)
+  double* km_best = nullptr;
+  size_t km_cap = 0;
+};
+
+struct plp_graph {
+  plp_ctx* ctx = nullptr;
+  int64_t n_rows = 0, n_cols = 0, nnz = 0;
+  int32_t* rp = nullptr;   // device int32 row_ptr[n_rows+1]
+  int32_t* col = nullptr;  // device int32 col[nnz]
+  double* w = nullptr;     // device fp64 w[nnz]
+};
+
+namespace plp {
+
+plp_status set_error(plp_status st, const char* fmt, ...);
+plp_status cuda_check(cudaError_t e, const char* what);
+
+#define PLP_CUDA(x)                                              \
+  do {                                                           \
+    cudaError_t e_ = (x);                                        \
+    if (e_ != cudaSuccess) return ::plp::cuda_check(e_, #x);     \
+  } while (0)
+
+#define PLP_LAUNCH_CHECK(what)                                   \
+  do {                                                           \
+    cudaError_t e_ = cudaGetLastError();                         \
+    if (e_ != cudaSuccess) return ::plp::cuda_check(e_, what);   \
+  } while (0)
+
+plp_status check_p(double p, double eps);
+plp_status check_k(int k);
+
+// Edge kernel launcher (edge.cu).
+struct EdgeArgs {
+  int64_t n_rows;
+  const int32_t* rp;
+  const int32_t* col;
+  const double* w;
+  int k;
+  const double* U;
+  const double* eta;
+  const double* AB;     // global A,B for the coefficients (nullptr: objective only)
+  double* G;
+  double* Hv;
+  double p, eps;
+  double* partials;     // [grid][4][k]: A, B, alpha, gamma partial sums
+  int want_dots;
+};
+plp_status launch_edge(plp_ctx* ctx, const EdgeArgs& a, int* grid_out);
+// Fixed-order reduction of edge partials: AB_out (2k), dots_out (2k), F (1); any may be null.
+plp_status launch_edge_finalize(plp_ctx* ctx, int grid, int k, const double* partials,
+                                double* AB_out, double* dots_out, double* F);
+
+}  // namespace plp
