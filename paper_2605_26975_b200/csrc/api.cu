@@ -28,8 +28,9 @@ plp_status cuda_check(cudaError_t e, const char* what) {
 
 plp_status check_p(double p, double eps) {
   if (!(p > 1.0 && p <= 2.0)) return set_error(PLP_ERR_DOMAIN, "p = %g not in (1, 2]", p);
-  if (p < 2.0 && !(eps > 0.0 && std::isfinite(eps)))
-    return set_error(PLP_ERR_DOMAIN, "eps = %g must be > 0 when p < 2", eps);
+  if (p < 2.0 && !(eps >= 1e-300 && eps < 1e300))
+    return set_error(PLP_ERR_DOMAIN, "eps = %g must be a normal double in [1e-300, 1e300) when p < 2",
+                     eps);
   return PLP_OK;
 }
 

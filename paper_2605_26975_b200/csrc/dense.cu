@@ -231,7 +231,9 @@ static double* dslot(plp_ctx* ctx, int s) { return ctx->scratch + 256 + (size_t)
 
 static plp_status gram(plp_ctx* ctx, int64_t n, int k, const double* X, const double* Xa,
                        const double* Y, const double* Ya, double* out) {
-  const int grid = grid_for(ctx, (n + kGramRows - 1) / kGramRows, 1);
+  int grid = grid_for(ctx, (n + kGramRows - 1) / kGramRows, 1);
+  const int cap = (int)(((int64_t)ctx->max_ctas * 4 * PLP_MAX_K) / (k * k));  // partials capacity
+  if (grid > cap) grid = cap;
   gram_kernel<<<grid, kGramThreads, 0, ctx->stream>>>(n, k, X, Xa, Y, Ya, ctx->partials);
   PLP_LAUNCH_CHECK("gram_kernel");
   sum_partials_kernel<<<1, 1024, 0, ctx->stream>>>(grid, k * k, ctx->partials, out);

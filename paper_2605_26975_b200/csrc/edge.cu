@@ -21,33 +21,38 @@ static bool match_root(double p, int D, int* m_out) {
   return true;
 }
 
+template <class P>
+static P base_pol(double p, double eps) {
+  P pw{};
+  pw.eps = eps;
+  pw.eps_bits = __builtin_bit_cast(long long, eps);
+  pw.pm1 = p - 1.0;
+  return pw;
+}
+
 template <class F>
 static plp_status with_pow(plp_ctx* ctx, double p, double eps, F&& f) {
   int m = 0;
-  if (p == 2.0) {
-    PowP2 pw;
-    pw.eps = eps;
-    pw.pm1 = 1.0;
-    return f(pw);
-  }
-  if (match_root(p, 2, &m)) {
-    PowRoot<2> pw;
-    pw.eps = eps; pw.pm1 = p - 1.0; pw.m = m;
-    return f(pw);
-  }
+  if (p == 2.0) return f(base_pol<PowP2>(p, eps));
+  if (match_root(p, 2, &m)) return f(base_pol<PowR2M1>(p, eps));
   if (match_root(p, 5, &m)) {
-    PowRoot<5> pw;
-    pw.eps = eps; pw.pm1 = p - 1.0; pw.m = m;
-    return f(pw);
+    switch (m) {
+      case 1: return f(base_pol<PowR5M1>(p, eps));
+      case 2: return f(base_pol<PowR5M2>(p, eps));
+      case 3: return f(base_pol<PowR5M3>(p, eps));
+      default: return f(base_pol<PowR5M4>(p, eps));
+    }
   }
   if (match_root(p, 10, &m)) {
-    PowRoot<10> pw;
-    pw.eps = eps; pw.pm1 = p - 1.0; pw.m = m;
-    return f(pw);
+    switch (m) {
+      case 1: return f(base_pol<PowR10M1>(p, eps));
+      case 3: return f(base_pol<PowR10M3>(p, eps));
+      case 7: return f(base_pol<PowR10M7>(p, eps));
+      case 9: return f(base_pol<PowR10M9>(p, eps));
+      default: break;  // even m matched D = 5, m = 5 matched D = 2
+    }
   }
-  PowGeneric pw;
-  pw.eps = eps;
-  pw.pm1 = p - 1.0;
+  PowGeneric pw = base_pol<PowGeneric>(p, eps);
   pw.q = p - 2.0;
   pw.q64 = 64.0 * (p - 2.0);
   pw.gtab = reinterpret_cast<const PowTables*>(ctx->pow_tables);
@@ -56,25 +61,13 @@ static plp_status with_pow(plp_ctx* ctx, double p, double eps, F&& f) {
 }
 
 plp_status launch_edge(plp_ctx* ctx, const EdgeArgs& a, int* grid) {
-  return with_pow(ctx, a.p, a.eps, [&](const auto& pw) -> plp_status {
-    using P = std::decay_t<decltype(pw)>;
-    if constexpr (std::is_same_v<P, PowP2>) return launch_edge_p2(ctx, a, pw, grid);
-    else if constexpr (std::is_same_v<P, PowRoot<2>>) return launch_edge_root2(ctx, a, pw, grid);
-    else if constexpr (std::is_same_v<P, PowRoot<5>>) return launch_edge_root5(ctx, a, pw, grid);
-    else if constexpr (std::is_same_v<P, PowRoot<10>>) return launch_edge_root10(ctx, a, pw, grid);
-    else return launch_edge_generic(ctx, a, pw, grid);
-  });
+  return with_pow(ctx, a.p, a.eps,
+                  [&](const auto& pw) -> plp_status { return launch_edge_pol(ctx, a, pw, grid); });
 }
 
 static plp_status launch_epilogue(plp_ctx* ctx, const EpiArgs& a, double eps) {
-  return with_pow(ctx, a.p, eps, [&](const auto& pw) -> plp_status {
-    using P = std::decay_t<decltype(pw)>;
-    if constexpr (std::is_same_v<P, PowP2>) return launch_epi_p2(ctx, a, pw);
-    else if constexpr (std::is_same_v<P, PowRoot<2>>) return launch_epi_root2(ctx, a, pw);
-    else if constexpr (std::is_same_v<P, PowRoot<5>>) return launch_epi_root5(ctx, a, pw);
-    else if constexpr (std::is_same_v<P, PowRoot<10>>) return launch_epi_root10(ctx, a, pw);
-    else return launch_epi_generic(ctx, a, pw);
-  });
+  return with_pow(ctx, a.p, eps,
+                  [&](const auto& pw) -> plp_status { return launch_epi_pol(ctx, a, pw); });
 }
 
 // ---- fixed-order reduction of CTA partials ------------------------------------------------------
@@ -223,7 +216,7 @@ extern "C" plp_status plp_edge_pass(plp_ctx* ctx, const plp_graph* g, int k, con
   a.G = G;
   a.Hv = Hv;
   a.p = p;
-  a.eps = eps;
+  a.eps = Hv ? eps : kNoCap;  // the cap only enters the Hessian weights (reading #6)
   a.partials = ctx->partials;
   a.want_dots = dots_out != nullptr;
   int grid = 0;
@@ -253,7 +246,7 @@ extern "C" plp_status plp_full_epilogue(plp_ctx* ctx, int64_t n_rows, int k, con
   if (n_rows <= 0) return PLP_OK;
   EpiArgs e{n_rows, k, U, p, AB, dots, G, Hv};
   // The epilogue needs phi_p(u) only (no curvature): the cap value is irrelevant, pass 1.
-  return launch_epilogue(ctx, e, 1.0);
+  return launch_epilogue(ctx, e, kNoCap);  // needs phi_p(u) only: no curvature cap
 }
 
 // scratch layout (doubles): [0, 2K) AB of an objective pass, [2K, 4K) dots, [4K, 6K) AB recomputed
@@ -269,7 +262,7 @@ extern "C" plp_status plp_fgrad(plp_ctx* ctx, const plp_graph* g, int k, const d
   double* ab = AB_out ? AB_out : scratch_ab(ctx);
   EdgeArgs a{};
   a.n_rows = g->n_rows; a.rp = g->rp; a.col = g->col; a.w = g->w; a.k = k; a.U = U;
-  a.p = p; a.eps = 1.0; a.partials = ctx->partials;
+  a.p = p; a.eps = kNoCap; a.partials = ctx->partials;  // F and G never use the cap
   int grid = 0;
   st = launch_edge(ctx, a, &grid);  // objective pass
   if (st) return st;
@@ -342,12 +335,7 @@ extern "C" plp_status plp_debug_pow(plp_ctx* ctx, int64_t n, const double* a, do
   if (st) return st;
   if (n == 0) return PLP_OK;
   return with_pow(ctx, p, eps, [&](const auto& pw) -> plp_status {
-    using P = std::decay_t<decltype(pw)>;
-    if constexpr (std::is_same_v<P, PowP2>) return launch_dbg_p2(ctx, n, a, s, t, pw);
-    else if constexpr (std::is_same_v<P, PowRoot<2>>) return launch_dbg_root2(ctx, n, a, s, t, pw);
-    else if constexpr (std::is_same_v<P, PowRoot<5>>) return launch_dbg_root5(ctx, n, a, s, t, pw);
-    else if constexpr (std::is_same_v<P, PowRoot<10>>) return launch_dbg_root10(ctx, n, a, s, t, pw);
-    else return launch_dbg_generic(ctx, n, a, s, t, pw);
+    return launch_dbg_pol(ctx, n, a, s, t, pw);
   });
 }
 

@@ -1,16 +1,11 @@
-// Per-power-policy launchers (each instantiated in its own translation unit, edge_<pow>.cu, so
-// the ~20 kernel shapes per policy compile in parallel).
+// Per-power-policy launchers.  Each policy is instantiated in its own translation unit
+// (edge_<NAME>.cu, generated from PLP_POW_LIST) so the kernel shapes compile in parallel; the
+// overloads below let the dispatcher in edge.cu pick the launcher from the policy's type.
 #pragma once
 #include "plp_internal.h"
 #include "pow64.cuh"
 
 namespace plp {
-
-plp_status launch_edge_p2(plp_ctx*, const EdgeArgs&, const PowP2&, int*);
-plp_status launch_edge_root2(plp_ctx*, const EdgeArgs&, const PowRoot<2>&, int*);
-plp_status launch_edge_root5(plp_ctx*, const EdgeArgs&, const PowRoot<5>&, int*);
-plp_status launch_edge_root10(plp_ctx*, const EdgeArgs&, const PowRoot<10>&, int*);
-plp_status launch_edge_generic(plp_ctx*, const EdgeArgs&, const PowGeneric&, int*);
 
 struct EpiArgs {
   int64_t n;
@@ -22,17 +17,13 @@ struct EpiArgs {
   const double* G;
   double* Hv;
 };
-plp_status launch_epi_p2(plp_ctx*, const EpiArgs&, const PowP2&);
-plp_status launch_epi_root2(plp_ctx*, const EpiArgs&, const PowRoot<2>&);
-plp_status launch_epi_root5(plp_ctx*, const EpiArgs&, const PowRoot<5>&);
-plp_status launch_epi_root10(plp_ctx*, const EpiArgs&, const PowRoot<10>&);
-plp_status launch_epi_generic(plp_ctx*, const EpiArgs&, const PowGeneric&);
 
-plp_status launch_dbg_p2(plp_ctx*, int64_t, const double*, double*, double*, const PowP2&);
-plp_status launch_dbg_root2(plp_ctx*, int64_t, const double*, double*, double*, const PowRoot<2>&);
-plp_status launch_dbg_root5(plp_ctx*, int64_t, const double*, double*, double*, const PowRoot<5>&);
-plp_status launch_dbg_root10(plp_ctx*, int64_t, const double*, double*, double*, const PowRoot<10>&);
-plp_status launch_dbg_generic(plp_ctx*, int64_t, const double*, double*, double*, const PowGeneric&);
+#define PLP_DECL_POLICY(NAME, TYPE)                                                          \
+  plp_status launch_edge_pol(plp_ctx*, const EdgeArgs&, const TYPE&, int*);                 \
+  plp_status launch_epi_pol(plp_ctx*, const EpiArgs&, const TYPE&);                          \
+  plp_status launch_dbg_pol(plp_ctx*, int64_t, const double*, double*, double*, const TYPE&);
+PLP_POW_LIST(PLP_DECL_POLICY)
+#undef PLP_DECL_POLICY
 
 template <class POW>
 __global__ void __launch_bounds__(256) debug_pow_kernel(int64_t n, const double* a, double* s,

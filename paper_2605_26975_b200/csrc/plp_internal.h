@@ -8,6 +8,9 @@
 #include "plp.h"
 
 #define PLP_MAX_K 32
+// Cap used by passes that need no curvature (objective, gradient, full-mode epilogue): s is then
+// unused and t = a^{p-1} must stay on the fast path for every a > 0 (pow64.cuh).
+constexpr double kNoCap = 1e-300;
 
 struct plp_ctx {
   int device = 0;
