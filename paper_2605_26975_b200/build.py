@@ -27,9 +27,9 @@ def _headers():
         [os.path.join(ROOT, "include", "plp.h")]
 
 
-def _compile(src: str, ptxas_v: bool) -> str:
-    obj = os.path.join(OBJ, os.path.basename(src) + ".o")
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+def _compile(src: str, ptxas_v: bool, obj_dir: str = OBJ, extra=()) -> str:
+    obj = os.path.join(obj_dir, os.path.basename(src) + ".o")
+    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", src, "-o", obj]
     if ptxas_v and src.endswith(".cu"):
         cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -38,7 +38,11 @@ def _compile(src: str, ptxas_v: bool) -> str:
     return r.stderr if ptxas_v else obj
 
 
-def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False, obj_dir: str = OBJ,
+          lib: str = LIB, extra=()) -> str:
+    """Compile (incrementally) and link libplp.so.  `extra` nvcc flags and a separate obj_dir/lib
+    build tuning variants (tools/tune_edge.py)."""
+    OBJ, LIB = obj_dir, lib  # noqa: N806
     os.makedirs(OBJ, exist_ok=True)
     srcs = _sources()
     hdr_t = max(os.path.getmtime(h) for h in _headers())
@@ -49,7 +53,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
             todo.append(s)
     if todo:
         with cf.ThreadPoolExecutor(max_workers=min(len(todo), os.cpu_count() or 4)) as ex:
-            outs = list(ex.map(lambda s: _compile(s, ptxas_v), todo))
+            outs = list(ex.map(lambda s: _compile(s, ptxas_v, OBJ, extra), todo))
         if ptxas_v:
             for s, o in zip(todo, outs):
                 print(f"== {os.path.basename(s)}\n{o}", file=sys.stderr)

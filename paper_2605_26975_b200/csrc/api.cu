@@ -1,4 +1,5 @@
 // Context, graph handle, error reporting and argument checks of libplp (plp.h).
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstring>
@@ -141,7 +142,24 @@ extern "C" plp_status plp_create_graph(plp_ctx* ctx, int64_t n_rows, int64_t n_c
   g->nnz = nnz;
   std::vector<int32_t> rp32((size_t)n_rows + 1);
   for (int64_t i = 0; i <= n_rows; ++i) rp32[i] = (int32_t)row_ptr[i];
+  // Row schedule: within windows of kSchedWindow consecutive rows, rows by decreasing degree
+  // (stable), so that the row groups of one warp see near-equal degrees (no divergence) while
+  // the window keeps the U_j gathers L2-local.  Row results do not depend on it.
+  std::vector<int32_t> sched((size_t)(n_rows > 0 ? n_rows : 1));
+  for (int64_t w0 = 0; w0 < n_rows; w0 += kSchedWindow) {
+    const int64_t w1 = std::min<int64_t>(n_rows, w0 + kSchedWindow);
+    for (int64_t i = w0; i < w1; ++i) sched[i] = (int32_t)i;
+    std::stable_sort(sched.begin() + w0, sched.begin() + w1, [&](int32_t x, int32_t y) {
+      return (rp32[x + 1] - rp32[x]) > (rp32[y + 1] - rp32[y]);
+    });
+  }
   cudaError_t e;
+  if ((e = cudaMalloc(&g->sched, sizeof(int32_t) * sched.size())) != cudaSuccess ||
+      (e = cudaMemcpy(g->sched, sched.data(), sizeof(int32_t) * sched.size(), cudaMemcpyHostToDevice)) !=
+          cudaSuccess) {
+    plp_destroy_graph(g);
+    return cuda_check(e, "graph schedule");
+  }
   if ((e = cudaMalloc(&g->rp, sizeof(int32_t) * (n_rows + 1))) != cudaSuccess ||
       (e = cudaMalloc(&g->col, sizeof(int32_t) * (nnz > 0 ? nnz : 1))) != cudaSuccess ||
       (e = cudaMalloc(&g->w, sizeof(double) * (nnz > 0 ? nnz : 1))) != cudaSuccess) {
@@ -175,6 +193,7 @@ extern "C" plp_status plp_destroy_graph(plp_graph* g) {
   cudaFree(g->rp);
   cudaFree(g->col);
   cudaFree(g->w);
+  cudaFree(g->sched);
   delete g;
   return PLP_OK;
 }

@@ -26,7 +26,17 @@ static P base_pol(double p, double eps) {
   P pw{};
   pw.eps = eps;
   pw.eps_bits = __builtin_bit_cast(long long, eps);
+  pw.q = p - 2.0;
   pw.pm1 = p - 1.0;
+  pw.s_eps = std::pow(eps, p - 2.0);  // cap(a)^{p-2} for a < eps, as the oracle computes it
+  return pw;
+}
+
+template <int D, int M>
+static PowRoot<D, M> root_pol(double p, double eps) {
+  PowRoot<D, M> pw = base_pol<PowRoot<D, M>>(p, eps);
+  pw.c1 = (double)M / D;                   // (1 - e)^{-M/D} = 1 + c1 e + c2 e^2 + O(e^3)
+  pw.c2 = pw.c1 * (pw.c1 + 1.0) / 2.0;
   return pw;
 }
 
@@ -34,26 +44,25 @@ template <class F>
 static plp_status with_pow(plp_ctx* ctx, double p, double eps, F&& f) {
   int m = 0;
   if (p == 2.0) return f(base_pol<PowP2>(p, eps));
-  if (match_root(p, 2, &m)) return f(base_pol<PowR2M1>(p, eps));
+  if (match_root(p, 2, &m)) return f(root_pol<2, 1>(p, eps));
   if (match_root(p, 5, &m)) {
     switch (m) {
-      case 1: return f(base_pol<PowR5M1>(p, eps));
-      case 2: return f(base_pol<PowR5M2>(p, eps));
-      case 3: return f(base_pol<PowR5M3>(p, eps));
-      default: return f(base_pol<PowR5M4>(p, eps));
+      case 1: return f(root_pol<5, 1>(p, eps));
+      case 2: return f(root_pol<5, 2>(p, eps));
+      case 3: return f(root_pol<5, 3>(p, eps));
+      default: return f(root_pol<5, 4>(p, eps));
     }
   }
   if (match_root(p, 10, &m)) {
     switch (m) {
-      case 1: return f(base_pol<PowR10M1>(p, eps));
-      case 3: return f(base_pol<PowR10M3>(p, eps));
-      case 7: return f(base_pol<PowR10M7>(p, eps));
-      case 9: return f(base_pol<PowR10M9>(p, eps));
+      case 1: return f(root_pol<10, 1>(p, eps));
+      case 3: return f(root_pol<10, 3>(p, eps));
+      case 7: return f(root_pol<10, 7>(p, eps));
+      case 9: return f(root_pol<10, 9>(p, eps));
       default: break;  // even m matched D = 5, m = 5 matched D = 2
     }
   }
   PowGeneric pw = base_pol<PowGeneric>(p, eps);
-  pw.q = p - 2.0;
   pw.q64 = 64.0 * (p - 2.0);
   pw.gtab = reinterpret_cast<const PowTables*>(ctx->pow_tables);
   pw.tab = nullptr;
@@ -84,7 +93,6 @@ __global__ void __launch_bounds__(1024) edge_finalize_kernel(int grid, int k, co
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) {
-      if (q == 0) s *= 0.5;  // each undirected edge was counted from both endpoints
       if (q < 2) {
         sAB[q * k + cl] = s;
         if (AB_out) AB_out[q * k + cl] = s;
@@ -207,6 +215,7 @@ extern "C" plp_status plp_edge_pass(plp_ctx* ctx, const plp_graph* g, int k, con
   EdgeArgs a{};
   a.n_rows = g->n_rows;
   a.rp = g->rp;
+  a.sched = g->sched;
   a.col = g->col;
   a.w = g->w;
   a.k = k;
@@ -261,7 +270,8 @@ extern "C" plp_status plp_fgrad(plp_ctx* ctx, const plp_graph* g, int k, const d
   if (st) return st;
   double* ab = AB_out ? AB_out : scratch_ab(ctx);
   EdgeArgs a{};
-  a.n_rows = g->n_rows; a.rp = g->rp; a.col = g->col; a.w = g->w; a.k = k; a.U = U;
+  a.n_rows = g->n_rows; a.rp = g->rp; a.sched = g->sched; a.col = g->col; a.w = g->w; a.k = k;
+  a.U = U;
   a.p = p; a.eps = kNoCap; a.partials = ctx->partials;  // F and G never use the cap
   int grid = 0;
   st = launch_edge(ctx, a, &grid);  // objective pass
@@ -311,7 +321,8 @@ extern "C" plp_status plp_fgrad_hessvec(plp_ctx* ctx, const plp_graph* g, int k,
     AB_in = scratch_ab(ctx);
   }
   EdgeArgs a{};
-  a.n_rows = g->n_rows; a.rp = g->rp; a.col = g->col; a.w = g->w; a.k = k; a.U = U;
+  a.n_rows = g->n_rows; a.rp = g->rp; a.sched = g->sched; a.col = g->col; a.w = g->w; a.k = k;
+  a.U = U;
   a.eta = Hv ? eta : nullptr;
   a.AB = AB_in; a.G = G; a.Hv = Hv; a.p = p; a.eps = eps; a.partials = ctx->partials;
   a.want_dots = full;

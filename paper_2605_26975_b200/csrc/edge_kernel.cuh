@@ -1,18 +1,22 @@
 // The fused F / EucGrad / EucHessianEta edge kernel.
 //
 // One pass over the CSR computes, per row i and column l:
-//   per stored edge (i, j):  d = U_il - U_jl, a = |d|,  s = cap(a)^{p-2}, t = a^{p-1}  (one power)
-//       A'_l   += w_ij t a                      (Eq. (1) numerator, halved at the end; reading #1)
-//       L_il   += w_ij copysign(t, d)           ((Delta_p u)_i)
-//       HA_il  += w_ij s (eta_il - eta_jl)      (Laplacian of w~ applied to eta; Alg. 1 lines 7-9)
-//   per node:  sn = cap(|U_il|)^{p-2}, tn = |U_il|^{p-1}:   B'_l += tn |U_il|
+//   per stored edge (i, j):  d = U_il - U_jl, a = |d|,  s = cap(a)^{p-2} (the one power), and
+//                            dL with s dL = phi_p(d)  (dL = d unless a < eps)
+//       L_il   += (w_ij s) dL                   ((Delta_p u)_i)
+//       HA_il  += (w_ij s) (eta_il - eta_jl)    (Laplacian of w~ applied to eta; Alg. 1 lines 7-9)
+//   per node:  sn = cap(|U_il|)^{p-2}, tn = |U_il|^{p-1}:
+//       A'_l  += U_il L_il                      (= A_l summed over all rows: <u, Delta_p u> = A)
+//       B'_l  += tn |U_il|                      (Eq. (1) denominator)
 //       G_il  = (p/B_l) (L_il - (A_l/B_l) copysign(tn, U_il))                  (reading #4)
 //       Hv_il = p(p-1)/B_l HA_il - p(p-1) A_l/B_l^2 sn eta_il                  (Alg. 1, #5)
 // Thread mapping ("one warp or sub-warp per row with the k columns vectorised", north star):
 //   a group of LPR lanes owns a row; lane li owns columns [li*CPL, li*CPL + CPL); a gathered
 //   neighbour row U_j (8k bytes) is read by the group as LPR contiguous CPL-vectors (coalesced);
-//   col_idx/w are broadcast within the group.  Persistent grid-stride loop over row groups; each
-//   CTA reduces its A', B', alpha, gamma partials in a fixed order (no atomics).
+//   col_idx/w are broadcast within the group.  Rows are taken in the graph's schedule order
+//   (degree-sorted within windows, plp_create_graph) so the groups of a warp have near-equal
+//   degrees.  Persistent grid-stride loop; each CTA reduces its A', B', alpha, gamma partials in a
+//   fixed order (no atomics).
 #pragma once
 #include "plp_internal.h"
 #include "pow64.cuh"
@@ -46,9 +50,68 @@ __device__ __forceinline__ void st_vec(double* __restrict__ p, const double (&v)
 }
 
 constexpr int kEdgeThreads = 256;
+// Tuning knobs (tools/tune_edge.py builds variants): edges unrolled per step, min CTAs per SM
+// (register cap), and 4-column lanes for k % 4 == 0.
+#ifndef PLP_EDGE_UNR
+#define PLP_EDGE_UNR 4
+#endif
+#ifndef PLP_EDGE_MINB
+#define PLP_EDGE_MINB 2
+#endif
+#ifndef PLP_EDGE_CPL4
+#define PLP_EDGE_CPL4 0
+#endif
+
+// One stored edge (weight wv, wse = wv eps^{p-2}) for the lane's CPL columns; branch-free.
+template <int CPL, class POW, bool HAS_ETA>
+__device__ __forceinline__ void edge_update(const POW& pw, double wv, double wse,
+                                            const double (&ui)[CPL], const double (&uj)[CPL],
+                                            const double (&ei)[CPL], const double (&ej)[CPL],
+                                            double (&L)[CPL], double (&HA)[CPL], unsigned& bad) {
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const double d = ui[c] - uj[c];
+    if constexpr (POW::kIsP2) {
+      L[c] = fma(wv, d, L[c]);
+      if constexpr (HAS_ETA) HA[c] = fma(wv, ei[c] - ej[c], HA[c]);
+    } else {
+      const double wsr = wv * pw.pow_raw(d, bad);  // w |d|^{p-2}
+      L[c] = fma(wsr, d, L[c]);                    // w phi_p(d)
+      if constexpr (HAS_ETA) {
+        const double wc = pw.abs_below_cap(d) ? wse : wsr;  // w cap(|d|)^{p-2}
+        HA[c] = fma(wc, ei[c] - ej[c], HA[c]);
+      }
+    }
+  }
+}
+
+// Exact (libdevice) recomputation of a row's sums when some |d| left the fast domain (rare).
+template <int CPL, class POW, bool HAS_ETA>
+__device__ __forceinline__ void edge_row_exact(const POW& pw, int e0, int e1, const int32_t* col,
+                                            const double* wt, const double* U, const double* eta,
+                                            int k, int c0, const double (&ui)[CPL],
+                                            const double (&ei)[CPL], double (&L)[CPL],
+                                            double (&HA)[CPL]) {
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) L[c] = HA[c] = 0.0;
+  for (int e = e0; e < e1; ++e) {
+    const int64_t j = col[e];
+    const double wv = wt[e];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const double d = ui[c] - U[j * k + c0 + c];
+      const double a = fabs(d);
+      L[c] += wv * ((a != 0.0) ? copysign(pow(a, pw.pm1), d) : 0.0);
+      if constexpr (HAS_ETA) {
+        const double s = (a < pw.eps) ? pw.s_eps : pow(a, pw.q);
+        HA[c] += wv * s * (ei[c] - eta[j * k + c0 + c]);
+      }
+    }
+  }
+}
 
 template <int CPL, int LPR, class POW, bool HAS_ETA>
-__global__ void __launch_bounds__(kEdgeThreads, 2) edge_kernel(EdgeArgs a, POW pw) {
+__global__ void __launch_bounds__(kEdgeThreads, PLP_EDGE_MINB) edge_kernel(EdgeArgs a, POW pw) {
   extern __shared__ double4 smem_raw[];
   if constexpr (POW::kNeedsTables) {
     pw.init_smem(smem_raw);
@@ -73,10 +136,10 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) edge_kernel(EdgeArgs a, POW p
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
       const double A = a.AB[c0 + c], B = a.AB[k + c0 + c];
-      cG[c] = p / B;                 // p / B
-      cAB[c] = A / B;                // A / B
-      cHA[c] = pp1 / B;              // p(p-1) / B
-      cHB[c] = pp1 * A / (B * B);    // p(p-1) A / B^2
+      cG[c] = p / B;               // p / B
+      cAB[c] = A / B;              // A / B
+      cHA[c] = pp1 / B;            // p(p-1) / B
+      cHB[c] = pp1 * A / (B * B);  // p(p-1) A / B^2
     }
   }
   double accA[CPL], accB[CPL], accAl[CPL], accGa[CPL];
@@ -85,22 +148,25 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) edge_kernel(EdgeArgs a, POW p
 
   const int32_t* __restrict__ rp = a.rp;
   const int32_t* __restrict__ col = a.col;
+  const int32_t* __restrict__ sched = a.sched;
   const double* __restrict__ wt = a.w;
   const double* __restrict__ U = a.U;
   const double* __restrict__ eta = a.eta;
 
   if (active) {
-    for (int64_t row = (int64_t)blockIdx.x * rows_per_iter + warp * RPW + grp; row < a.n_rows;
-         row += (int64_t)gridDim.x * rows_per_iter) {
+    for (int64_t idx = (int64_t)blockIdx.x * rows_per_iter + warp * RPW + grp; idx < a.n_rows;
+         idx += (int64_t)gridDim.x * rows_per_iter) {
+      const int row = __ldg(sched + idx);
       const int e0 = __ldg(rp + row), e1 = __ldg(rp + row + 1);
       double ui[CPL], ei[CPL];
-      ld_vec<CPL>(U + row * k + c0, ui);
-      if constexpr (HAS_ETA) ld_vec<CPL>(eta + row * k + c0, ei);
-      double L[CPL], HA[CPL], Ar[CPL];
+      ld_vec<CPL>(U + (int64_t)row * k + c0, ui);
+      if constexpr (HAS_ETA) ld_vec<CPL>(eta + (int64_t)row * k + c0, ei);
+      double L[CPL], HA[CPL];
 #pragma unroll
-      for (int c = 0; c < CPL; ++c) L[c] = HA[c] = Ar[c] = 0.0;
+      for (int c = 0; c < CPL; ++c) L[c] = HA[c] = 0.0;
 
-      constexpr int UNR = (CPL <= 2) ? 4 : 2;
+      constexpr int UNR = (CPL <= 2) ? PLP_EDGE_UNR : (PLP_EDGE_UNR + 1) / 2;
+      unsigned bad = 0;
       int e = e0;
       for (; e + UNR <= e1; e += UNR) {
         int j[UNR];
@@ -118,16 +184,8 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) edge_kernel(EdgeArgs a, POW p
         }
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
-#pragma unroll
-          for (int c = 0; c < CPL; ++c) {
-            const double d = ui[c] - uj[u][c];
-            const double ad = fabs(d);
-            double s, t;
-            pw.eval(ad, s, t);
-            Ar[c] = fma(wv[u], t * ad, Ar[c]);
-            L[c] = fma(wv[u], copysign(t, d), L[c]);
-            if constexpr (HAS_ETA) HA[c] = fma(wv[u] * s, ei[c] - ej[u][c], HA[c]);
-          }
+          const double wse = HAS_ETA && !POW::kIsP2 ? wv[u] * pw.s_eps : 0.0;
+          edge_update<CPL, POW, HAS_ETA>(pw, wv[u], wse, ui, uj[u], ei, ej[u], L, HA, bad);
         }
       }
       for (; e < e1; ++e) {
@@ -136,17 +194,10 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) edge_kernel(EdgeArgs a, POW p
         double uj[CPL], ej[CPL];
         ld_vec<CPL>(U + (int64_t)j * k + c0, uj);
         if constexpr (HAS_ETA) ld_vec<CPL>(eta + (int64_t)j * k + c0, ej);
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) {
-          const double d = ui[c] - uj[c];
-          const double ad = fabs(d);
-          double s, t;
-          pw.eval(ad, s, t);
-          Ar[c] = fma(wv, t * ad, Ar[c]);
-          L[c] = fma(wv, copysign(t, d), L[c]);
-          if constexpr (HAS_ETA) HA[c] = fma(wv * s, ei[c] - ej[c], HA[c]);
-        }
+        const double wse = HAS_ETA && !POW::kIsP2 ? wv * pw.s_eps : 0.0;
+        edge_update<CPL, POW, HAS_ETA>(pw, wv, wse, ui, uj, ei, ej, L, HA, bad);
       }
+      if (bad) edge_row_exact<CPL, POW, HAS_ETA>(pw, e0, e1, col, wt, U, eta, k, c0, ui, ei, L, HA);
 
       // ---- row epilogue: node terms, outputs, partial sums ----
       double g[CPL], h[CPL];
@@ -155,8 +206,8 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) edge_kernel(EdgeArgs a, POW p
         const double au = fabs(ui[c]);
         double sn, tn;
         pw.eval(au, sn, tn);
-        accA[c] += Ar[c];
-        accB[c] += tn * au;
+        accA[c] = fma(ui[c], L[c], accA[c]);
+        accB[c] = fma(tn, au, accB[c]);
         const double phi = copysign(tn, ui[c]);
         g[c] = cG[c] * (L[c] - cAB[c] * phi);
         if constexpr (HAS_ETA) {
@@ -166,9 +217,9 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) edge_kernel(EdgeArgs a, POW p
           h[c] = 0.0;
         }
       }
-      if (a.G != nullptr) st_vec<CPL>(a.G + row * k + c0, g);
+      if (a.G != nullptr) st_vec<CPL>(a.G + (int64_t)row * k + c0, g);
       if constexpr (HAS_ETA) {
-        if (a.Hv != nullptr) st_vec<CPL>(a.Hv + row * k + c0, h);
+        if (a.Hv != nullptr) st_vec<CPL>(a.Hv + (int64_t)row * k + c0, h);
         if (a.want_dots) {
 #pragma unroll
           for (int c = 0; c < CPL; ++c) accGa[c] = fma(g[c], ei[c], accGa[c]);
@@ -206,7 +257,7 @@ plp_status launch_edge_shape(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int
   const size_t red_bytes = (size_t)4 * CPL * kEdgeThreads * sizeof(double);
   const size_t tab_bytes = POW::kNeedsTables ? sizeof(PowTables) : 0;
   const size_t smem = red_bytes > tab_bytes ? red_bytes : tab_bytes;
-  static int occ = -1;  // per instantiation (device-independent enough for one process)
+  static int occ = -1;  // per instantiation
   if (occ < 0) {
     if (smem > 48 * 1024)
       PLP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -236,6 +287,15 @@ plp_status launch_edge_pow(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int* 
 #define PLP_SHAPE(C, L)                                                                 \
   return he ? launch_edge_shape<C, L, POW, true>(ctx, a, pw, grid)                      \
             : launch_edge_shape<C, L, POW, false>(ctx, a, pw, grid)
+  if constexpr (PLP_EDGE_CPL4 != 0) {
+    if (vec_ok && k % 4 == 0) {
+      const int quarter = k / 4;
+      if (quarter <= 1) PLP_SHAPE(4, 1);
+      if (quarter <= 2) PLP_SHAPE(4, 2);
+      if (quarter <= 4) PLP_SHAPE(4, 4);
+      PLP_SHAPE(4, 8);
+    }
+  }
   if (vec_ok) {
     const int half = k / 2;
     if (half <= 1) PLP_SHAPE(2, 1);

@@ -30,10 +30,12 @@ struct plp_ctx {
 struct plp_graph {
   plp_ctx* ctx = nullptr;
   int64_t n_rows = 0, n_cols = 0, nnz = 0;
-  int32_t* rp = nullptr;   // device int32 row_ptr[n_rows+1]
-  int32_t* col = nullptr;  // device int32 col[nnz]
-  double* w = nullptr;     // device fp64 w[nnz]
+  int32_t* rp = nullptr;     // device int32 row_ptr[n_rows+1]
+  int32_t* col = nullptr;    // device int32 col[nnz]
+  double* w = nullptr;       // device fp64 w[nnz]
+  int32_t* sched = nullptr;  // device row schedule: rows sorted by degree within windows
 };
+constexpr int kSchedWindow = 2048;  // rows per degree-sorting window (stays L2-local)
 
 namespace plp {
 
@@ -59,6 +61,7 @@ plp_status check_k(int k);
 struct EdgeArgs {
   int64_t n_rows;
   const int32_t* rp;
+  const int32_t* sched;
   const int32_t* col;
   const double* w;
   int k;

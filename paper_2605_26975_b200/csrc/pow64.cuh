@@ -1,22 +1,24 @@
-// fp64 power kernels for the edge pass: s = cap(a)^{p-2} and t = a^{p-1} for a = |u_i - u_j|
-// (readings #6 and #8 of DESIGN.md §3).  One power per edge-column is shared by F (a^p = t a),
-// the gradient (phi_p = copysign(t, d)) and the Hessian weight (s) -- SURVEY.md §8(a) a7.
+// fp64 power kernels for the edge pass (readings #6 and #8 of DESIGN.md §3).
 //
-// libdevice pow costs ~120 fp64-pipe slots per call on B200 (measured 134 G pow/s), which would
-// make the edge pass fp64-ALU bound many times over the HBM roofline.  Cheaper policies, each
-// accurate to a few ulp (tests/test_gpu_parity.py::test_power_policies_accuracy):
-//   PowP2          p == 2:            s = 1, t = a                         (no power at all)
-//   PowRoot<D, M>  p - 2 == -M/D:     x = 2^(D q) x', x' in [1, 2^D) by integer exponent
-//                                     arithmetic; y = x'^{-1/D} from an fp32 MUFU seed and one
-//                                     cubic-corrected Newton step (error O(e^3) ~ 1e-18);
-//                                     s = y^M 2^{-qM}  (7 + log2-chain fp64 ops)
-//   PowGeneric     any p in (1, 2]:   table-driven log2 (128 entries) + exp2 (64 entries),
-//                                     degree-5 polynomials, ~19 fp64 ops
-// Every policy computes s = pow_q(max(a, eps)) and t = s * a; for the rare a < eps the exact
-// t = a^{p-1} is recomputed with libdevice (t = 0 at a = 0), so F and the gradient never see the
-// cap.  The max and the a < eps test run on the integer pipe: for non-negative doubles the bit
-// patterns order like the values.  Domain: eps and every a are normal doubles below 2^1000
-// (|U| entries < 1e150); eps >= 1e-300 is enforced by check_p.
+// Per stored edge-column the fused pass needs ONE power, s_raw = |d|^{p-2} with d = u_i - u_j:
+//   (Delta_p u)_i += w s_raw d            (= w phi_p(d) = w |d|^{p-1} sign(d); 0 at d = 0)
+//   (H eta)_i     += w s_cap (eta_i - eta_j),   s_cap = cap(|d|)^{p-2} = (|d| < eps ? eps^{p-2} : s_raw)
+// so F (through <u, Delta_p u> = A), the gradient and the Hessian share it.
+//
+// libdevice pow costs ~120 fp64-pipe slots per call on B200 (measured 134 G pow/s): many times
+// the HBM roofline.  Cheaper policies, each accurate to a few ulp
+// (tests/test_gpu_parity.py::test_power_policies_accuracy):
+//   PowP2          p == 2:          s = 1                                (no power at all)
+//   PowRoot<D, M>  p - 2 == -M/D:   y0 = x^{-1/D} from an fp32 MUFU seed, e = 1 - x y0^D, then
+//                                   x^{-M/D} = y0^M (1 + c1 e + c2 e^2) + O(e^3): a second-order
+//                                   expansion of the exact correction (|e| ~ 1e-6 so the error is
+//                                   ~1e-18); 7 fp64 ops at p = 1.2 (D = 5, M = 4)
+//   PowGeneric     any p in (1, 2]: table-driven log2 (128 entries) + exp2 (64 entries),
+//                                   degree-5 polynomials, ~19 fp64 ops
+// The edge form is branch-free on the fast domain {0} U [2^-120, 2^120): exact zeros (ties) give
+// a finite s_raw that multiplies d = 0.  Anything else sets a flag and the row is recomputed with
+// libdevice (edge_kernel.cuh), so every input follows the definitions.  The cap test runs on the
+// integer pipe: for non-negative doubles the bit patterns order like the values.
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
@@ -28,11 +30,26 @@ struct PowTables {
   double expt[64];    // 2^(j/64)
 };
 
+constexpr unsigned kHiMin = (1023u - 120u) << 20;  // hi word of 2^-120
+constexpr unsigned kHiMax = (1023u + 120u) << 20;  // hi word of 2^120
+
 // ---- bit helpers (integer pipe only) ------------------------------------------------------------
-// positive normal double in [2^-126, 2^127] -> float, mantissa truncated to 20 bits
-__device__ __forceinline__ float d2f_trunc(double x) {
-  const unsigned hi = (unsigned)__double2hiint(x);
-  return __uint_as_float((hi - (896u << 20)) << 3);
+__device__ __forceinline__ unsigned abs_hi(double d) {
+  return (unsigned)__double2hiint(d) & 0x7FFFFFFFu;
+}
+// 1 if |d| is outside the fast domain {0} U [2^-120, 2^120) (|d| < 2^-1022 with a zero high word
+// counts as 0)
+__device__ __forceinline__ unsigned out_of_domain(unsigned ahi) {
+  return (unsigned)(ahi - 1u < kHiMin - 1u) | (unsigned)(ahi >= kHiMax);
+}
+__device__ __forceinline__ void flag_out_of_domain(unsigned ahi, unsigned& bad) {
+  bad |= out_of_domain(ahi);
+}
+// float with the exponent and top 20 mantissa bits of the double whose |hi word| is `ahi`
+// (ahi clamped to >= 2^-120 so the float is normal)
+__device__ __forceinline__ float seed_float(unsigned ahi) {
+  const unsigned h = ahi > kHiMin ? ahi : kHiMin;
+  return __uint_as_float((h - (896u << 20)) << 3);
 }
 // positive normal float -> double (exact)
 __device__ __forceinline__ double f2d_exact(float f) {
@@ -58,70 +75,108 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
   return y;
 }
 
-template <int E>
-__device__ __forceinline__ double ipow(double y) {
-  if constexpr (E == 0) return 1.0;
-  else if constexpr (E == 1) return y;
-  else if constexpr (E % 2 == 0) { const double h = ipow<E / 2>(y); return h * h; }
-  else return ipow<E - 1>(y) * y;
-}
-
 // ---- policies -------------------------------------------------------------------------------
 struct PowBase {
-  double eps;         // curvature cap (> 0 when p < 2)
-  long long eps_bits; // bit pattern of eps (integer compare == value compare for >= 0)
-  double pm1;         // p - 1 (rare branch)
+  double eps;          // curvature cap (> 0 when p < 2)
+  long long eps_bits;  // bit pattern of eps (integer compare == value compare for >= 0)
+  double q;            // p - 2
+  double pm1;          // p - 1
+  double s_eps;        // eps^{p-2} (host glibc pow: the value the oracle's cap gives)
+  double c1, c2;       // expansion coefficients of PowRoot (kernel parameters, not immediates)
   __device__ __forceinline__ void init_smem(void*) {}
+  __device__ __forceinline__ bool below_cap(double a) const {  // a >= 0
+    return __double_as_longlong(a) < eps_bits;
+  }
+  __device__ __forceinline__ bool abs_below_cap(double d) const {  // |d| < eps, integer pipe
+    // compare (|hi|, lo) with eps's words; written on the words so the compiler cannot turn the
+    // sign mask into an fp64 |d| (a DADD on the fp64 pipe)
+    const unsigned long long a =
+        ((unsigned long long)abs_hi(d) << 32) | (unsigned)__double2loint(d);
+    return a < (unsigned long long)eps_bits;
+  }
 };
 
 struct PowP2 : PowBase {
   static constexpr bool kNeedsTables = false;
+  static constexpr bool kIsP2 = true;
+  __device__ __forceinline__ double pow_raw(double, unsigned&) const { return 1.0; }
+  // node form: s = cap(a)^0 = 1, t = a^1
   __device__ __forceinline__ void eval(double a, double& s, double& t) const {
     s = 1.0;
     t = a;
   }
 };
 
+// node form shared by the capped policies: s = cap(a)^{p-2}, t = a^{p-1} (a >= 0), with the
+// exact libdevice results below the cap and outside the fast domain (rare, divergent).
 template <class Derived>
 struct PowCapped : PowBase {
+  static constexpr bool kIsP2 = false;
   __device__ __forceinline__ void eval(double a, double& s, double& t) const {
-    const long long ab = __double_as_longlong(a);
-    const bool small = ab < eps_bits;  // a < eps  (a >= 0)
-    const double ac = __longlong_as_double(small ? eps_bits : ab);
-    s = static_cast<const Derived*>(this)->pow_q(ac);
+    unsigned bad = 0;
+    s = static_cast<const Derived*>(this)->pow_raw(a, bad);
     t = s * a;
-    if (small) t = (ab != 0) ? pow(a, pm1) : 0.0;  // rare: exact a^{p-1} below the cap
+    if (bad | (unsigned)below_cap(a)) {
+      if (below_cap(a)) {
+        s = s_eps;
+        t = (a != 0.0) ? pow(a, pm1) : 0.0;
+      } else {
+        s = pow(a, q);
+        t = s * a;
+      }
+    }
   }
 };
+
+// y0^D and y0^M with shared products
+template <int D, int M>
+__device__ __forceinline__ void root_powers(double y, double& yD, double& yM) {
+  const double y2 = y * y;
+  if constexpr (D == 2) {
+    yD = y2;
+    yM = y;  // M = 1
+  } else {
+    const double y4 = y2 * y2;
+    const double y5 = y4 * y;
+    if constexpr (D == 5) {
+      yD = y5;
+      if constexpr (M == 1) yM = y;
+      else if constexpr (M == 2) yM = y2;
+      else if constexpr (M == 3) yM = y2 * y;
+      else yM = y4;
+    } else {  // D == 10
+      yD = y5 * y5;
+      if constexpr (M == 1) yM = y;
+      else if constexpr (M == 3) yM = y2 * y;
+      else if constexpr (M == 7) yM = y5 * y2;
+      else yM = y5 * y4;
+    }
+  }
+}
 
 template <int D, int M>
 struct PowRoot : PowCapped<PowRoot<D, M>> {
   static constexpr bool kNeedsTables = false;
-  // x^{-M/D} for a positive normal x
-  __device__ __forceinline__ double pow_q(double x) const {
-    const int hi = __double2hiint(x);
-    const int ex = ((hi >> 20) & 0x7FF) - 1023;
-    constexpr int OFF = 1100;  // divisible by D in {2, 5, 10}: floor division of ex by D
-    const int qd = (int)((unsigned)(ex + OFF) / (unsigned)D) - OFF / D;
-    const int r = ex - qd * D;  // 0 <= r < D
-    const double xs = __hiloint2double((hi & 0x000FFFFF) | ((1023 + r) << 20), __double2loint(x));
-    const float xf = d2f_trunc(xs);  // xs in [1, 2^D)
+  // |d|^{-M/D}; branch-free; sets `bad` outside the fast domain
+  __device__ __forceinline__ double pow_raw(double d, unsigned& bad) const {
+    const unsigned ahi = abs_hi(d);
+    bad |= out_of_domain(ahi);
+    const float xf = seed_float(ahi);
     float yf;
     if constexpr (D == 2) yf = rsqrt_approx(xf);
     else yf = ex2_approx(lg2_approx(xf) * (-1.0f / (float)D));
     const double y0 = f2d_exact(yf);
-    const double e = fma(-xs, ipow<D>(y0), 1.0);  // 1 - xs y0^D  (|e| ~ 1e-6)
-    constexpr double C1 = 1.0 / D, C2 = (D + 1.0) / (2.0 * D * D);
-    const double c = fma(e, C2, C1);
-    const double y = fma(y0 * e, c, y0);  // xs^{-1/D} to O(e^3)
-    return scale_pow2(ipow<M>(y), -qd * M);
+    double yD, yM;
+    root_powers<D, M>(y0, yD, yM);
+    const double e = fma(-fabs(d), yD, 1.0);  // 1 - x y0^D
+    const double c = fma(this->c2, e, this->c1);
+    return fma(yM * e, c, yM);
   }
 };
 
 struct PowGeneric : PowCapped<PowGeneric> {
   static constexpr bool kNeedsTables = true;
-  double q;    // p - 2
-  double q64;  // 64 (p - 2)
+  double q64;             // 64 (p - 2)
   const PowTables* gtab;  // global copy
   const PowTables* tab;   // shared-memory copy (set by init_smem)
   __device__ __forceinline__ void init_smem(void* smem) {
@@ -131,9 +186,12 @@ struct PowGeneric : PowCapped<PowGeneric> {
     for (int i = threadIdx.x; i < (int)(sizeof(PowTables) / 8); i += blockDim.x) dst[i] = src[i];
     tab = st;
   }
-  __device__ __forceinline__ double pow_q(double x) const {
-    const int hi = __double2hiint(x);
-    const int lo = __double2loint(x);
+  // |d|^{p-2}; branch-free; sets `bad` outside the fast domain
+  __device__ __forceinline__ double pow_raw(double d, unsigned& bad) const {
+    const unsigned ahi = abs_hi(d);
+    bad |= out_of_domain(ahi);
+    const int hi = (int)(ahi > kHiMin ? ahi : kHiMin);
+    const int lo = __double2loint(d);
     const int ex = (hi >> 20) - 1023;
     const int j = (hi >> 13) & 127;
     const double m = __hiloint2double((hi & 0x000FFFFF) | 0x3FF00000, lo);  // [1, 2)
@@ -150,7 +208,7 @@ struct PowGeneric : PowCapped<PowGeneric> {
     P = fma(P, r, L0);
     // (double)ex via the 2^52 + 2^31 magic (one DADD, no I2F)
     const double exd = __hiloint2double(0x43300000, ex ^ 0x80000000) - 4503601774854144.0;
-    const double lg = fma(r, P, exd + tj.y);  // log2(x)
+    const double lg = fma(r, P, exd + tj.y);  // log2|d|
     // exp2(q * lg) with a 64-entry table
     const double y64 = lg * q64;
     const double kd = y64 + 6755399441055744.0;  // 0x1.8p52: round to integer

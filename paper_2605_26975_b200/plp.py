@@ -13,7 +13,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libplp.so")
+LIB_PATH = os.environ.get("PLP_LIB") or os.path.join(_HERE, "libplp.so")  # PLP_LIB: tuning variants
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libplp.so not built at {LIB_PATH}: run `python -c 'import __graft_entry__ as g; "

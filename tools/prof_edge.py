@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--order", default="rcm")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--p", type=float, default=None)
+    ap.add_argument("--events", action="store_true", help="also time the edge kernel with CUDA events")
     args = ap.parse_args()
     k, p = CONFIG_KP[args.config]
     if args.p is not None:
@@ -42,6 +43,24 @@ def main():
     torch.cuda.synchronize()
     print(f"{args.config} n={g.n} nnz={g.nnz} k={k} p={p}: {1e3 * (time.time() - t0) / args.reps:.3f} ms/call "
           f"F={outs[0].item():.12g}")
+    if args.events:
+        import json
+        Gr, Hv = outs[2], outs[3]
+        for _ in range(3):
+            plp.edge_pass(ctx, G, U, eta, p, 1e-9, AB_in=AB, G=Gr, Hv=Hv)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.reps + 1)]
+        torch.cuda.synchronize()
+        ev[0].record()
+        for i in range(args.reps):
+            plp.edge_pass(ctx, G, U, eta, p, 1e-9, AB_in=AB, G=Gr, Hv=Hv)
+            ev[i + 1].record()
+        torch.cuda.synchronize()
+        ts = sorted(ev[i].elapsed_time(ev[i + 1]) for i in range(args.reps))
+        byts = 12 * g.nnz + 4 * (g.n + 1) + 32 * g.n * k
+        print(json.dumps({"config": args.config, "k": k, "p": p, "kernel_ms_median": ts[len(ts) // 2],
+                          "kernel_ms_min": ts[0], "GBps": byts / (ts[len(ts) // 2] * 1e-3) / 1e9,
+                          "GNNZk": g.nnz * k / (ts[len(ts) // 2] * 1e-3) / 1e9,
+                          "F": outs[0].item()}))
 
 
 if __name__ == "__main__":

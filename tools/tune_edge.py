@@ -1,0 +1,60 @@
+"""Build / time variants of the edge kernel (unroll, register cap, lanes per row).
+
+  python tools/tune_edge.py build            # here (CPU): cross-compile every variant
+  python tools/tune_edge.py run [--config C5] # on the GPU box: time each variant (CUDA events)
+Variants land in paper_2605_26975_b200/variants/<name>/libplp.so (git-ignored, travel with gpurun).
+"""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+VDIR = os.path.join(ROOT, "paper_2605_26975_b200", "variants")
+
+VARIANTS = {
+    "u4_b2": ["-DPLP_EDGE_UNR=4", "-DPLP_EDGE_MINB=2"],
+    "u2_b2": ["-DPLP_EDGE_UNR=2", "-DPLP_EDGE_MINB=2"],
+    "u2_b3": ["-DPLP_EDGE_UNR=2", "-DPLP_EDGE_MINB=3"],
+    "u4_b3": ["-DPLP_EDGE_UNR=4", "-DPLP_EDGE_MINB=3"],
+    "c4_u4_b2": ["-DPLP_EDGE_UNR=4", "-DPLP_EDGE_MINB=2", "-DPLP_EDGE_CPL4=1"],
+    "c4_u2_b2": ["-DPLP_EDGE_UNR=2", "-DPLP_EDGE_MINB=2", "-DPLP_EDGE_CPL4=1"],
+    "c4_u2_b3": ["-DPLP_EDGE_UNR=2", "-DPLP_EDGE_MINB=3", "-DPLP_EDGE_CPL4=1"],
+}
+
+
+def build(names):
+    from paper_2605_26975_b200.build import build as b
+    for name in names:
+        d = os.path.join(VDIR, name)
+        os.makedirs(d, exist_ok=True)
+        b(obj_dir=os.path.join(d, "obj"), lib=os.path.join(d, "libplp.so"), extra=VARIANTS[name])
+        print("built", name, flush=True)
+
+
+def run(names, config, reps):
+    res = {}
+    for name in names:
+        env = dict(os.environ, PLP_LIB=os.path.join(VDIR, name, "libplp.so"))
+        out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "prof_edge.py"), "--config", config,
+                              "--reps", str(reps), "--events"], env=env, capture_output=True, text=True)
+        line = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+        res[name] = json.loads(line[-1]) if line else {"error": out.stderr[-2000:]}
+        print(name, res[name], flush=True)
+    return res
+
+
+if __name__ == "__main__":
+    cmd = sys.argv[1]
+    names = [a for a in sys.argv[2:] if not a.startswith("--")] or list(VARIANTS)
+    config = "C5"
+    if "--config" in sys.argv:
+        config = sys.argv[sys.argv.index("--config") + 1]
+        names = [n for n in names if n != config]
+    if cmd == "build":
+        build(names)
+    else:
+        r = run(names, config, 20)
+        os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+        json.dump(r, open(os.path.join(ROOT, "gpurun_out", f"tune_{config}.json"), "w"), indent=1)
