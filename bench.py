@@ -2,7 +2,7 @@
 
 A step = one plp_fgrad_hessvec call (SURVEY.md §8(a) a7 = a2..a5 fused, sparse-mode Hessian) on
 the workload config (default C5: 8,388,608 uniform points in [0,1]^2, symmetrised 6-NN graph,
-Gaussian weights, k = 8, p = 1.2, RCM order), with A, B at U supplied from a preceding plp_fgrad
+Gaussian weights, k = 8, p = 1.2, tile order = RCM + BFS-grown 128-row tiles), with A, B at U supplied from a preceding plp_fgrad
 (the trust-region rho-test always has them).  Inputs (CSR 0.71 GB + U, eta 1.07 GB)
 exceed the 126 MB L2, so no flush is needed between steps.
 
@@ -66,12 +66,12 @@ def get_graph(name: str, order: str):
     t0 = time.time()
     g = make_config(name)
     log(f"[bench] generated {name}: n={g.n} nnz={g.nnz} in {time.time() - t0:.1f}s")
-    if order == "rcm":
+    if order in ("rcm", "tile"):
         t0 = time.time()
-        perm = plp.rcm_order(g.row_ptr, g.col)
+        perm = plp.rcm_order(g.row_ptr, g.col) if order == "rcm" else plp.tile_order(g.row_ptr, g.col)
         rp, col, w = plp.permute_csr(g.row_ptr, g.col, g.w, perm)
         g = Graph(name, g.n, rp, col, w)
-        log(f"[bench] RCM reorder in {time.time() - t0:.1f}s")
+        log(f"[bench] {order} reorder in {time.time() - t0:.1f}s")
     try:
         os.makedirs(os.path.dirname(cache), exist_ok=True)
         np.savez(cache + ".tmp.npz", n=g.n, rp=g.row_ptr, col=g.col, w=g.w)
@@ -170,7 +170,7 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     k, p = CONFIG_KP[args.config]
-    g = get_graph(args.config, "rcm")
+    g = get_graph(args.config, args.order)
     vals, dts = [], []
     desc, cores = "", 0
     for s in range(args.warmup + args.steps):
@@ -184,7 +184,7 @@ def run_reference(args, rank, world):
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic", "impl": "reference",
            "config": {"workload": args.config, "desc": CONFIG_DESC.get(args.config, args.config),
-                      "n": g.n, "nnz": g.nnz, "k": k, "p": p, "order": "rcm"},
+                      "n": g.n, "nnz": g.nnz, "k": k, "p": p, "order": args.order},
            "cpu_baseline": {"value": val, "unit": "GNNZ*k/s", "cores": cores, "kind": "oracle",
                             "sample": desc},
            "e2e": {"value": val, "unit": "GNNZ*k/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -344,7 +344,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="plp", choices=["plp", "reference"])
     ap.add_argument("--config", default="C5", choices=sorted(CONFIG_KP))
-    ap.add_argument("--order", default="rcm", choices=["rcm", "none"])
+    ap.add_argument("--order", default="tile", choices=["tile", "rcm", "none"])
     ap.add_argument("--mode", default="sparse", choices=["sparse", "full"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -52,6 +52,7 @@ typedef enum {
 
 enum { PLP_HESS_SPARSE = 0, PLP_HESS_FULL = 1 };          /* reading #5 */
 enum { PLP_VALIDATE = 1u, PLP_VALIDATE_SYMMETRIC = 2u };  /* plp_create_graph flags */
+enum { PLP_TILE_ROWS = 128 };  /* rows per tile of the tiled edge kernel (plp_tile_order) */
 
 typedef struct plp_ctx plp_ctx;
 typedef struct plp_graph plp_graph;
@@ -85,6 +86,11 @@ plp_status plp_validate_csr(int64_t n_rows, int64_t n_cols, const int64_t* row_p
  * pseudo-peripheral node with neighbours visited in (degree, id) order; the whole order is then
  * reversed.  Deterministic.  Used so that U_j gathers hit L2. */
 plp_status plp_rcm_order(int64_t n, const int64_t* row_ptr, const int32_t* col, int64_t* perm);
+/* Tile ordering for the tiled edge kernel: RCM sweep, then tiles of `tile` nodes
+ * (pass PLP_TILE_ROWS) grown by BFS along the sweep, nodes within a tile by decreasing degree.
+ * perm[new] = old.  Relabel with plp_permute_csr; U and eta must then use the new order. */
+plp_status plp_tile_order(int64_t n, const int64_t* row_ptr, const int32_t* col, int tile,
+                          int64_t* perm);
 /* Relabels a symmetric CSR: new node a is old node perm[a].  Output arrays are caller-allocated
  * (n+1, nnz, nnz); columns of each output row are sorted. */
 plp_status plp_permute_csr(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* w,

@@ -118,6 +118,70 @@ extern "C" plp_status plp_ctx_info(const plp_ctx* ctx, int* num_sms, int* max_ct
   return PLP_OK;
 }
 
+// Tiled representation for edge_tiled.cuh (see plp_graph): per tile of PLP_TILE_ROWS rows, every
+// internal undirected edge gets one slot (assigned at its upper row, shared by both directions)
+// and every external edge its own slot.  Tiling is skipped (the row kernel is used) if a tile
+// would overflow the 16-bit slot / offset fields.
+static plp_status build_tiles(plp_graph* g, const int64_t* rp, const int32_t* col) {
+  const int64_t n = g->n_rows;
+  const int T = PLP_TILE_ROWS;
+  const int64_t nt = (n + T - 1) / T;
+  std::vector<int32_t> enc((size_t)g->nnz + 16, 0);
+  std::vector<int32_t> slot_of((size_t)g->nnz, -1);
+  std::vector<int32_t> ext;
+  std::vector<int4> meta((size_t)nt + 1);
+  int max_slots = 0, max_nnz = 0;
+  for (int64_t t = 0; t < nt; ++t) {
+    const int64_t r0 = t * T, r1 = std::min<int64_t>(n, r0 + T);
+    const int64_t e0 = rp[r0], e1 = rp[r1];
+    int n_int = 0, n_ext = 0;
+    const int ext_off = (int)ext.size();
+    for (int64_t i = r0; i < r1; ++i) {
+      for (int64_t e = rp[i]; e < rp[i + 1]; ++e) {
+        const int64_t j = col[e];
+        if (j >= r0 && j < r1) {
+          int s;
+          if (j > i) {
+            s = slot_of[e] = n_int++;
+          } else {  // partner (j, i) sits in the earlier row j
+            int64_t f = rp[j];
+            while (f < rp[j + 1] && col[f] != i) ++f;
+            if (f == rp[j + 1] || slot_of[f] < 0) return PLP_OK;  // not symmetric: no tiling
+            s = slot_of[f];
+          }
+          enc[e] = (int32_t)(0x80000000u | ((uint32_t)(j - r0) << 16) | (uint32_t)s);
+        } else {
+          enc[e] = n_ext++;
+          ext.push_back((int32_t)j);
+        }
+      }
+    }
+    if (n_int >= 65536 || n_ext >= 65536 || e1 - e0 >= 65536) return PLP_OK;
+    meta[t] = make_int4((int)e0, ext_off, n_int, n_ext);
+    max_slots = std::max(max_slots, n_int + n_ext);
+    max_nnz = std::max(max_nnz, (int)(e1 - e0));
+  }
+  meta[nt] = make_int4((int)g->nnz, (int)ext.size(), 0, 0);
+  ext.resize(ext.size() + 16, 0);
+  cudaError_t e;
+  if ((e = cudaMalloc(&g->enc, sizeof(int32_t) * enc.size())) != cudaSuccess ||
+      (e = cudaMalloc(&g->ext_col, sizeof(int32_t) * ext.size())) != cudaSuccess ||
+      (e = cudaMalloc(&g->tile_meta, sizeof(int4) * meta.size())) != cudaSuccess)
+    return cuda_check(e, "cudaMalloc(tiles)");
+  if ((e = cudaMemcpy(g->enc, enc.data(), sizeof(int32_t) * enc.size(), cudaMemcpyHostToDevice)) !=
+          cudaSuccess ||
+      (e = cudaMemcpy(g->ext_col, ext.data(), sizeof(int32_t) * ext.size(), cudaMemcpyHostToDevice)) !=
+          cudaSuccess ||
+      (e = cudaMemcpy(g->tile_meta, meta.data(), sizeof(int4) * meta.size(), cudaMemcpyHostToDevice)) !=
+          cudaSuccess)
+    return cuda_check(e, "cudaMemcpy(tiles)");
+  g->tiled = true;
+  g->n_tiles = nt;
+  g->max_slots = max_slots;
+  g->max_nnz = max_nnz;
+  return PLP_OK;
+}
+
 extern "C" plp_status plp_create_graph(plp_ctx* ctx, int64_t n_rows, int64_t n_cols,
                                        const int64_t* row_ptr, const int32_t* col, const double* w,
                                        uint32_t flags, plp_graph** out) {
@@ -160,9 +224,10 @@ extern "C" plp_status plp_create_graph(plp_ctx* ctx, int64_t n_rows, int64_t n_c
     plp_destroy_graph(g);
     return cuda_check(e, "graph schedule");
   }
-  if ((e = cudaMalloc(&g->rp, sizeof(int32_t) * (n_rows + 1))) != cudaSuccess ||
-      (e = cudaMalloc(&g->col, sizeof(int32_t) * (nnz > 0 ? nnz : 1))) != cudaSuccess ||
-      (e = cudaMalloc(&g->w, sizeof(double) * (nnz > 0 ? nnz : 1))) != cudaSuccess) {
+  // (+16 elements of padding: the tiled kernel's bulk copies round ranges up to 16 bytes)
+  if ((e = cudaMalloc(&g->rp, sizeof(int32_t) * (n_rows + 1 + 16))) != cudaSuccess ||
+      (e = cudaMalloc(&g->col, sizeof(int32_t) * (nnz + 16))) != cudaSuccess ||
+      (e = cudaMalloc(&g->w, sizeof(double) * (nnz + 16))) != cudaSuccess) {
     plp_destroy_graph(g);
     return cuda_check(e, "cudaMalloc(graph)");
   }
@@ -174,6 +239,11 @@ extern "C" plp_status plp_create_graph(plp_ctx* ctx, int64_t n_rows, int64_t n_c
                       cudaSuccess)) {
     plp_destroy_graph(g);
     return cuda_check(e, "cudaMemcpy(graph)");
+  }
+  plp_status st = build_tiles(g, row_ptr, col);
+  if (st) {
+    plp_destroy_graph(g);
+    return st;
   }
   *out = g;
   return PLP_OK;
@@ -194,6 +264,9 @@ extern "C" plp_status plp_destroy_graph(plp_graph* g) {
   cudaFree(g->col);
   cudaFree(g->w);
   cudaFree(g->sched);
+  cudaFree(g->enc);
+  cudaFree(g->ext_col);
+  cudaFree(g->tile_meta);
   delete g;
   return PLP_OK;
 }

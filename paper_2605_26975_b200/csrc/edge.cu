@@ -195,6 +195,24 @@ __global__ void rcut_finalize_kernel(int grid, int K, const double* part_cut,
 
 using namespace plp;
 
+static EdgeArgs graph_args(const plp_graph* g) {
+  EdgeArgs a{};
+  a.n_rows = g->n_rows;
+  a.rp = g->rp;
+  a.sched = g->sched;
+  a.col = g->col;
+  a.w = g->w;
+  if (g->tiled) {
+    a.enc = g->enc;
+    a.ext_col = g->ext_col;
+    a.tile_meta = g->tile_meta;
+    a.n_tiles = g->n_tiles;
+    a.max_slots = g->max_slots;
+    a.max_nnz = g->max_nnz;
+  }
+  return a;
+}
+
 static plp_status check_graph_call(plp_ctx* ctx, const plp_graph* g, int k, const double* U,
                                    double p, double eps) {
   if (!ctx || !g || !U) return set_error(PLP_ERR_ARG, "null ctx/graph/U");
@@ -212,12 +230,7 @@ extern "C" plp_status plp_edge_pass(plp_ctx* ctx, const plp_graph* g, int k, con
   if (!AB_in && (G || Hv || dots_out))
     return set_error(PLP_ERR_ARG, "G/Hv/dots need AB_in (the global A, B at U)");
   if ((Hv || dots_out) && !eta) return set_error(PLP_ERR_ARG, "Hv/dots need eta");
-  EdgeArgs a{};
-  a.n_rows = g->n_rows;
-  a.rp = g->rp;
-  a.sched = g->sched;
-  a.col = g->col;
-  a.w = g->w;
+  EdgeArgs a = graph_args(g);
   a.k = k;
   a.U = U;
   a.eta = (Hv || dots_out) ? eta : nullptr;
@@ -269,8 +282,8 @@ extern "C" plp_status plp_fgrad(plp_ctx* ctx, const plp_graph* g, int k, const d
   plp_status st = check_graph_call(ctx, g, k, U, p, 1.0);
   if (st) return st;
   double* ab = AB_out ? AB_out : scratch_ab(ctx);
-  EdgeArgs a{};
-  a.n_rows = g->n_rows; a.rp = g->rp; a.sched = g->sched; a.col = g->col; a.w = g->w; a.k = k;
+  EdgeArgs a = graph_args(g);
+  a.k = k;
   a.U = U;
   a.p = p; a.eps = kNoCap; a.partials = ctx->partials;  // F and G never use the cap
   int grid = 0;
@@ -320,8 +333,8 @@ extern "C" plp_status plp_fgrad_hessvec(plp_ctx* ctx, const plp_graph* g, int k,
     if (st) return st;
     AB_in = scratch_ab(ctx);
   }
-  EdgeArgs a{};
-  a.n_rows = g->n_rows; a.rp = g->rp; a.sched = g->sched; a.col = g->col; a.w = g->w; a.k = k;
+  EdgeArgs a = graph_args(g);
+  a.k = k;
   a.U = U;
   a.eta = Hv ? eta : nullptr;
   a.AB = AB_in; a.G = G; a.Hv = Hv; a.p = p; a.eps = eps; a.partials = ctx->partials;

@@ -1,11 +1,11 @@
 // Instantiation unit of the fused edge kernel, full-mode epilogue and power diagnostic for the
 // power policy PowR2M1 (see pow64.cuh, edge_kernel.cuh, edge_inst.cuh).
 #include "edge_inst.cuh"
-#include "edge_kernel.cuh"
+#include "edge_tiled.cuh"
 
 namespace plp {
 plp_status launch_edge_pol(plp_ctx* ctx, const EdgeArgs& a, const PowR2M1& pw, int* grid) {
-  return launch_edge_pow(ctx, a, pw, grid);
+  return launch_edge_any(ctx, a, pw, grid);
 }
 plp_status launch_epi_pol(plp_ctx* ctx, const EpiArgs& a, const PowR2M1& pw) {
   return launch_epi(ctx, a, pw);

@@ -1,0 +1,382 @@
+// Tiled fused F / EucGrad / EucHessianEta edge kernel.
+//
+// The graph is cut into tiles of PLP_TILE_ROWS consecutive rows (compact graph regions after
+// plp_tile_order).  A persistent CTA loops over tiles:
+//   stage   one thread issues TMA bulk copies (cp.async.bulk, mbarrier completion) of the tile's
+//           contiguous U rows, eta rows, row_ptr, encoded columns and weights into shared memory;
+//   phase 0 every edge the tile must evaluate gets a work-list entry: each INTERNAL undirected
+//           edge (both ends in the tile) once, at its upper row, and each EXTERNAL edge;
+//   phase 1 a flat, balanced sweep over the work list computes the one power per edge-column:
+//             internal slot: cL = w s_raw (u_i - u_j), wc = w cap(|d|)^{p-2}        (U_j from smem)
+//             external slot: cL = w s_raw d,           cH = wc (eta_i - eta_j)     (U_j, eta_j from
+//                                                                                   global / L2)
+//   phase 2 each row walks its CSR row in order (the oracle's order) and sums
+//             L_i  += +-cL   (internal: + at the upper row, - at the lower row: d is antisymmetric)
+//             HA_i += wc (eta_i - eta_j)  (internal)  or  cH  (external),
+//           then the row epilogue of the row kernel (node terms, G, Hv, partial sums).
+// Each internal undirected edge costs one power instead of two and its U_j / eta_j come from shared
+// memory, which takes most of the gather traffic off L2 (ncu showed L2 as the next bound of the
+// row kernel).  Every reduction is in a fixed order: results are deterministic.
+#pragma once
+#include <cstdlib>
+
+#include "edge_kernel.cuh"
+
+namespace plp {
+
+constexpr int kTileRows = PLP_TILE_ROWS;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+struct TiledLayout {
+  unsigned ut, et, w, enc, rp, list, val, tab, total;
+};
+__host__ __device__ inline unsigned align16u(unsigned x) { return (x + 15u) & ~15u; }
+// Shared-memory layout (byte offsets), identical on host and device.
+__host__ __device__ inline TiledLayout tiled_layout(int k, int max_nnz, int max_slots, int cpl,
+                                                     bool tables) {
+  TiledLayout L;
+  unsigned o = 16;  // mbarrier
+  L.ut = o; o += align16u(kTileRows * k * 8);
+  L.et = o; o += align16u(kTileRows * k * 8);
+  L.w = o; o += align16u((max_nnz + 4) * 8);
+  L.enc = o; o += align16u((max_nnz + 8) * 4);
+  L.rp = o; o += align16u((kTileRows + 1 + 8) * 4);
+  L.list = o; o += align16u(max_slots * 4 + 4);
+  L.val = o;
+  unsigned vb = (unsigned)max_slots * k * 16;
+  const unsigned red = 4u * cpl * kEdgeThreads * 8;  // final CTA reduction reuses the value area
+  o += align16u(vb > red ? vb : red);
+  L.tab = o;
+  if (tables) o += align16u(sizeof(PowTables));
+  L.total = o;
+  return L;
+}
+
+template <int CPL>
+__device__ __forceinline__ void lds_vec(const double* p, double (&v)[CPL]) {
+  if constexpr (CPL % 2 == 0) {
+#pragma unroll
+    for (int c = 0; c < CPL; c += 2) {
+      const double2 t = *reinterpret_cast<const double2*>(p + c);
+      v[c] = t.x;
+      v[c + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) v[c] = p[c];
+  }
+}
+
+template <int CPL, int LPR, class POW, bool HAS_ETA>
+__global__ void __launch_bounds__(kEdgeThreads, 2) edge_tiled_kernel(EdgeArgs a, POW pw) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int k = a.k;
+  const TiledLayout Ly = tiled_layout(k, a.max_nnz, a.max_slots, CPL, POW::kNeedsTables);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm);
+  double* Ut = reinterpret_cast<double*>(sm + Ly.ut);
+  double* Et = reinterpret_cast<double*>(sm + Ly.et);
+  double* Wt = reinterpret_cast<double*>(sm + Ly.w);
+  int32_t* Ct = reinterpret_cast<int32_t*>(sm + Ly.enc);
+  int32_t* Rt = reinterpret_cast<int32_t*>(sm + Ly.rp);
+  int32_t* list = reinterpret_cast<int32_t*>(sm + Ly.list);
+  double2* val = reinterpret_cast<double2*>(sm + Ly.val);
+  if constexpr (POW::kNeedsTables) pw.init_smem(sm + Ly.tab);
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31;
+  const int li = lane % LPR;
+  const int grp = threadIdx.x / LPR;  // group id within the CTA
+  const int G = blockDim.x / LPR;     // groups per CTA
+  const int c0 = li * CPL;
+  const bool active = c0 < k;
+  const double p = a.p;
+  const double pp1 = p * (p - 1.0);
+
+  double cG[CPL], cAB[CPL], cHA[CPL], cHB[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) cG[c] = cAB[c] = cHA[c] = cHB[c] = 0.0;
+  if (a.AB != nullptr && active) {
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const double A = a.AB[c0 + c], B = a.AB[k + c0 + c];
+      cG[c] = p / B;
+      cAB[c] = A / B;
+      cHA[c] = pp1 / B;
+      cHB[c] = pp1 * A / (B * B);
+    }
+  }
+  double accA[CPL], accB[CPL], accAl[CPL], accGa[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) accA[c] = accB[c] = accAl[c] = accGa[c] = 0.0;
+
+  unsigned parity = 0;
+  for (int64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x, parity ^= 1u) {
+    const int4 tm = __ldg(a.tile_meta + t);  // (e0, ext_off, n_int, n_ext)
+    const int e0 = tm.x, e1 = __ldg(&a.tile_meta[t + 1].x);
+    const int n_int = tm.z, n_slots = tm.z + tm.w;
+    const int64_t r0 = t * kTileRows;
+    const int nrows = (int)((a.n_rows - r0) < kTileRows ? (a.n_rows - r0) : kTileRows);
+    // staging offsets: bulk copies need 16-byte aligned global sources
+    const int w_off = e0 & 1, c_off = e0 & 3, r_off = (int)(r0 & 3);
+    // ---- stage the tile (one elected thread issues the TMA bulk copies) ----
+    if (threadIdx.x == 0) {
+      fence_proxy_async();  // order earlier generic smem accesses before the async writes
+      const unsigned bu = (unsigned)(nrows * k * 8);
+      const unsigned bw = align16u((unsigned)(e1 - e0 + w_off) * 8);
+      const unsigned bc = align16u((unsigned)(e1 - e0 + c_off) * 4);
+      const unsigned br = align16u((unsigned)(nrows + 1 + r_off) * 4);
+      mbar_expect_tx(bar, bu * (HAS_ETA ? 2u : 1u) + bw + bc + br);
+      tma_bulk_g2s(Ut, a.U + r0 * k, bu, bar);
+      if constexpr (HAS_ETA) tma_bulk_g2s(Et, a.eta + r0 * k, bu, bar);
+      tma_bulk_g2s(Wt, a.w + (e0 - w_off), bw, bar);
+      tma_bulk_g2s(Ct, a.enc + (e0 - c_off), bc, bar);
+      tma_bulk_g2s(Rt, a.rp + (r0 - r_off), br, bar);
+    }
+    mbar_wait(bar, parity);
+    const double* W = Wt + w_off;
+    const int32_t* C = Ct + c_off;
+    const int32_t* R = Rt + r_off;
+
+    // ---- phase 0: work list (internal edges at their upper row, external edges) ----
+    for (int rl = grp; rl < nrows; rl += G) {
+      const int b = R[rl] - e0, e = R[rl + 1] - e0;
+      for (int q = b + li; q < e; q += LPR) {
+        const int c = C[q];
+        if (c < 0) {
+          const int jl = (c >> 16) & 0x7FFF;
+          if (jl > rl) list[c & 0xFFFF] = (rl << 16) | q;
+        } else {
+          list[n_int + c] = (rl << 16) | q;
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---- phase 1: one power per listed edge-column ----
+    if (active) {
+      for (int s = grp; s < n_slots; s += G) {
+        const int ent = list[s];
+        const int rl = ent >> 16, q = ent & 0xFFFF;
+        const double wv = W[q];
+        double ui[CPL], uj[CPL], ei[CPL], ej[CPL];
+        lds_vec<CPL>(Ut + rl * k + c0, ui);
+        const bool internal = s < n_int;
+        if (internal) {
+          const int jl = (C[q] >> 16) & 0x7FFF;
+          lds_vec<CPL>(Ut + jl * k + c0, uj);
+        } else {
+          const int64_t j = __ldg(a.ext_col + tm.y + (s - n_int));
+          ld_vec<CPL>(a.U + j * k + c0, uj);
+          if constexpr (HAS_ETA) {
+            ld_vec<CPL>(a.eta + j * k + c0, ej);
+            lds_vec<CPL>(Et + rl * k + c0, ei);
+          }
+        }
+        const double wse = POW::kIsP2 ? wv : wv * pw.s_eps;
+        unsigned bad = 0;
+        double2 out[CPL];
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const double d = ui[c] - uj[c];
+          double ws, wc;
+          if constexpr (POW::kIsP2) {
+            ws = wv;
+            wc = wv;
+          } else {
+            ws = wv * pw.pow_raw(d, bad);
+            wc = pw.abs_below_cap(d) ? wse : ws;
+          }
+          out[c].x = ws * d;  // w phi_p(u_i - u_j)
+          out[c].y = wc;
+          if constexpr (HAS_ETA) {
+            if (!internal) out[c].y = wc * (ei[c] - ej[c]);
+          }
+        }
+        if (bad) {  // rare: some |d| outside the fast power domain -> exact libdevice values
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) {
+            const double d = ui[c] - uj[c], ad = fabs(d);
+            const double s_raw = (ad != 0.0) ? pow(ad, pw.q) : 0.0;
+            const double wc = (ad < pw.eps) ? wse : wv * s_raw;
+            out[c].x = (ad != 0.0) ? wv * copysign(pow(ad, pw.pm1), d) : 0.0;
+            out[c].y = wc;
+            if constexpr (HAS_ETA) {
+              if (!internal) out[c].y = wc * (ei[c] - ej[c]);
+            }
+          }
+        }
+        double2* vs = val + (int64_t)s * k + c0;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) vs[c] = out[c];
+      }
+    }
+    __syncthreads();
+
+    // ---- phase 2: per-row sums in CSR order + row epilogue ----
+    if (active) {
+      for (int rl = grp; rl < nrows; rl += G) {
+        const int b = R[rl] - e0, e = R[rl + 1] - e0;
+        double ui[CPL], ei[CPL], L[CPL], HA[CPL];
+        lds_vec<CPL>(Ut + rl * k + c0, ui);
+        if constexpr (HAS_ETA) lds_vec<CPL>(Et + rl * k + c0, ei);
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) L[c] = HA[c] = 0.0;
+        for (int q = b; q < e; ++q) {
+          const int c = C[q];
+          const bool internal = c < 0;
+          const int jl = (c >> 16) & 0x7FFF;
+          const int slot = internal ? (c & 0xFFFF) : (n_int + c);
+          const double2* vs = val + (int64_t)slot * k + c0;
+          const bool neg = internal && jl < rl;
+          double ej[CPL];
+          if constexpr (HAS_ETA) lds_vec<CPL>(Et + (internal ? jl : 0) * k + c0, ej);
+#pragma unroll
+          for (int c2 = 0; c2 < CPL; ++c2) {
+            const double2 v = vs[c2];
+            L[c2] += neg ? -v.x : v.x;
+            if constexpr (HAS_ETA) HA[c2] = fma(v.y, internal ? (ei[c2] - ej[c2]) : 1.0, HA[c2]);
+          }
+        }
+        const int64_t row = r0 + rl;
+        double g[CPL], h[CPL];
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const double au = fabs(ui[c]);
+          double sn, tn;
+          pw.eval(au, sn, tn);
+          accA[c] = fma(ui[c], L[c], accA[c]);
+          accB[c] = fma(tn, au, accB[c]);
+          const double phi = copysign(tn, ui[c]);
+          g[c] = cG[c] * (L[c] - cAB[c] * phi);
+          if constexpr (HAS_ETA) {
+            h[c] = cHA[c] * HA[c] - cHB[c] * sn * ei[c];
+            if (a.want_dots) accAl[c] = fma(p * phi, ei[c], accAl[c]);
+          } else {
+            h[c] = 0.0;
+          }
+        }
+        if (a.G != nullptr) st_vec<CPL>(a.G + row * k + c0, g);
+        if constexpr (HAS_ETA) {
+          if (a.Hv != nullptr) st_vec<CPL>(a.Hv + row * k + c0, h);
+          if (a.want_dots) {
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) accGa[c] = fma(g[c], ei[c], accGa[c]);
+          }
+        }
+      }
+    }
+    __syncthreads();  // the next tile's bulk copies overwrite the staging buffers
+  }
+
+  // ---- fixed-order CTA reduction of the partial sums (reuses the value area) ----
+  double* red = reinterpret_cast<double*>(sm + Ly.val);  // [4][CPL][blockDim]
+  const int nt = blockDim.x;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    red[(0 * CPL + c) * nt + threadIdx.x] = accA[c];
+    red[(1 * CPL + c) * nt + threadIdx.x] = accB[c];
+    red[(2 * CPL + c) * nt + threadIdx.x] = accAl[c];
+    red[(3 * CPL + c) * nt + threadIdx.x] = accGa[c];
+  }
+  __syncthreads();
+  for (int tt = threadIdx.x; tt < 4 * k; tt += nt) {
+    const int q = tt / k, cl = tt % k;
+    const int l = cl / CPL, c = cl % CPL;
+    const double* base = red + (q * CPL + c) * nt;
+    double s = 0.0;
+    for (int th = l; th < nt; th += LPR) s += base[th];
+    a.partials[((int64_t)blockIdx.x * 4 + q) * k + cl] = s;
+  }
+}
+
+// Launches the tiled kernel when the graph is tiled, k is even (16-byte column pairs), the dense
+// arrays are 16-byte aligned and the tile fits in shared memory; returns *used = false otherwise.
+template <int LPR, class POW, bool HAS_ETA>
+plp_status launch_tiled_shape(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int* grid_out) {
+  auto kern = edge_tiled_kernel<2, LPR, POW, HAS_ETA>;
+  const TiledLayout Ly = tiled_layout(a.k, a.max_nnz, a.max_slots, 2, POW::kNeedsTables);
+  static int attr_set = 0;
+  static int occ = 1;
+  if (attr_set < (int)Ly.total) {
+    PLP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ly.total));
+    attr_set = (int)Ly.total;
+    int o = 0;
+    PLP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kEdgeThreads, Ly.total));
+    occ = o < 1 ? 1 : o;
+  }
+  int64_t grid = (int64_t)occ * ctx->num_sms;
+  if (grid > ctx->max_ctas) grid = ctx->max_ctas;
+  if (grid > a.n_tiles) grid = a.n_tiles > 0 ? a.n_tiles : 1;
+  kern<<<(int)grid, kEdgeThreads, Ly.total, ctx->stream>>>(a, pw);
+  PLP_LAUNCH_CHECK("edge_tiled_kernel");
+  *grid_out = (int)grid;
+  return PLP_OK;
+}
+
+template <class POW>
+plp_status try_launch_tiled(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int* grid, bool* used) {
+  *used = false;
+  const int k = a.k;
+  auto al16 = [](const void* ptr) { return ((uintptr_t)ptr & 15u) == 0; };
+  static const bool force_rows = getenv("PLP_EDGE_ROWS") != nullptr;  // A/B switch for tests
+  if (force_rows || a.enc == nullptr || k % 2 != 0 || !al16(a.U) || (a.eta && !al16(a.eta)) ||
+      (a.G && !al16(a.G)) || (a.Hv && !al16(a.Hv)))
+    return PLP_OK;
+  const TiledLayout Ly = tiled_layout(k, a.max_nnz, a.max_slots, 2, POW::kNeedsTables);
+  if (Ly.total > 220u * 1024u) return PLP_OK;
+  *used = true;
+  const bool he = a.eta != nullptr;
+  const int half = k / 2;
+#define PLP_TSHAPE(L)                                                              \
+  return he ? launch_tiled_shape<L, POW, true>(ctx, a, pw, grid)                   \
+            : launch_tiled_shape<L, POW, false>(ctx, a, pw, grid)
+  if (half <= 1) PLP_TSHAPE(1);
+  if (half <= 2) PLP_TSHAPE(2);
+  if (half <= 4) PLP_TSHAPE(4);
+  if (half <= 8) PLP_TSHAPE(8);
+  PLP_TSHAPE(16);
+#undef PLP_TSHAPE
+}
+
+// Edge-pass entry for one power policy: the tiled kernel when it applies, else the row kernel.
+template <class POW>
+plp_status launch_edge_any(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int* grid) {
+  bool used = false;
+  plp_status st = try_launch_tiled(ctx, a, pw, grid, &used);
+  if (st || used) return st;
+  return launch_edge_pow(ctx, a, pw, grid);
+}
+
+}  // namespace plp

@@ -118,6 +118,49 @@ extern "C" plp_status plp_rcm_order(int64_t n, const int64_t* rp, const int32_t*
   return PLP_OK;
 }
 
+// Tile ordering: RCM sweep, then tiles of T nodes grown by BFS from the first unassigned node of
+// the sweep (restarting from the next unassigned sweep node when a BFS runs dry), nodes of a tile
+// sorted by decreasing degree.  Consecutive T-row ranges of the relabelled graph are then compact
+// graph regions: most edges have both ends in one tile (C5: ~91% at T = 256), so the tiled edge
+// kernel reads them from shared memory and evaluates each such undirected edge once.
+extern "C" plp_status plp_tile_order(int64_t n, const int64_t* rp, const int32_t* col, int tile,
+                                     int64_t* perm) {
+  if (!rp || !perm || n < 0 || tile < 1) return set_error(PLP_ERR_ARG, "bad argument");
+  std::vector<int64_t> rcm(n);
+  plp_status st = plp_rcm_order(n, rp, col, rcm.data());
+  if (st) return st;
+  std::vector<char> used(n, 0);
+  std::vector<int64_t> queue;
+  queue.reserve(tile);
+  int64_t out = 0, oi = 0;
+  while (out < n) {
+    const int64_t t0 = out;
+    while (out < n && out - t0 < tile) {
+      while (oi < n && used[rcm[oi]]) ++oi;
+      if (oi >= n) break;
+      queue.clear();
+      queue.push_back(rcm[oi]);
+      used[rcm[oi]] = 1;
+      perm[out++] = rcm[oi];
+      for (size_t h = 0; h < queue.size() && out - t0 < tile; ++h) {
+        const int64_t v = queue[h];
+        for (int64_t e = rp[v]; e < rp[v + 1] && out - t0 < tile; ++e) {
+          const int64_t j = col[e];
+          if (!used[j]) {
+            used[j] = 1;
+            queue.push_back(j);
+            perm[out++] = j;
+          }
+        }
+      }
+    }
+    std::stable_sort(perm + t0, perm + out, [&](int64_t a, int64_t b) {
+      return (rp[a + 1] - rp[a]) > (rp[b + 1] - rp[b]);
+    });
+  }
+  return PLP_OK;
+}
+
 extern "C" plp_status plp_permute_csr(int64_t n, const int64_t* rp, const int32_t* col,
                                       const double* w, const int64_t* perm, int64_t* rp_out,
                                       int32_t* col_out, double* w_out) {

@@ -34,6 +34,18 @@ struct plp_graph {
   int32_t* col = nullptr;    // device int32 col[nnz]
   double* w = nullptr;       // device fp64 w[nnz]
   int32_t* sched = nullptr;  // device row schedule: rows sorted by degree within windows
+  // Tiled representation (edge_tiled.cuh): tiles of PLP_TILE_ROWS consecutive rows.
+  //   enc[e]: internal edge (both ends in the tile) -> 0x80000000 | (j - r0) << 16 | slot of the
+  //           undirected edge;  external edge -> its external slot in the tile
+  //   ext_col[tile_meta.x + s]: global column of external slot s;  tile_meta = (ext_off, n_int,
+  //   n_ext, nnz of the tile)
+  bool tiled = false;
+  int32_t* enc = nullptr;
+  int32_t* ext_col = nullptr;
+  int4* tile_meta = nullptr;
+  int64_t n_tiles = 0;
+  int max_slots = 0;  // max over tiles of n_int + n_ext
+  int max_nnz = 0;    // max over tiles of the tile's nnz
 };
 constexpr int kSchedWindow = 2048;  // rows per degree-sorting window (stays L2-local)
 
@@ -73,6 +85,12 @@ struct EdgeArgs {
   double p, eps;
   double* partials;     // [grid][4][k]: A, B, alpha, gamma partial sums
   int want_dots;
+  // tiled representation (nullptr enc: use the row kernel)
+  const int32_t* enc;
+  const int32_t* ext_col;
+  const int4* tile_meta;
+  int64_t n_tiles;
+  int max_slots, max_nnz;
 };
 plp_status launch_edge(plp_ctx* ctx, const EdgeArgs& a, int* grid_out);
 // Fixed-order reduction of edge partials: AB_out (2k), dots_out (2k), F (1); any may be null.

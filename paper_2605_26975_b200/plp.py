@@ -42,8 +42,9 @@ SYMBOLS = [
     "plp_hessvec", "plp_fgrad_hessvec", "plp_edge_pass", "plp_full_epilogue",
     "plp_objective_from_ab", "plp_gram", "plp_project", "plp_apply_sub", "plp_retract",
     "plp_cholesky", "plp_apply_rinv", "plp_dot", "plp_axpby", "plp_gather_rows", "plp_kmeans",
-    "plp_rcut", "plp_debug_pow",
+    "plp_rcut", "plp_debug_pow", "plp_tile_order",
 ]
+TILE_ROWS = 128  # PLP_TILE_ROWS in include/plp.h
 
 
 class PlpError(RuntimeError):
@@ -355,6 +356,15 @@ def rcm_order(row_ptr, col):
     c, cp = _host(col, np.int32)
     perm = np.empty(rp.size - 1, dtype=np.int64)
     _ck(_lib.plp_rcm_order(C_I64(rp.size - 1), rpp, cp, VP(perm.ctypes.data)), "plp_rcm_order")
+    return perm
+
+
+def tile_order(row_ptr, col, tile: int = TILE_ROWS):
+    """RCM sweep + BFS-grown tiles of `tile` nodes (perm[new] = old) for the tiled edge kernel."""
+    rp, rpp = _host(row_ptr, np.int64)
+    c, cp = _host(col, np.int32)
+    perm = np.empty(rp.size - 1, dtype=np.int64)
+    _ck(_lib.plp_tile_order(C_I64(rp.size - 1), rpp, cp, int(tile), VP(perm.ctypes.data)), "plp_tile_order")
     return perm
 
 

@@ -43,6 +43,11 @@ def graph(name):
             from paper_2605_26975_b200 import plp as mod
             g0 = make_config("C5", n=100_000)
             g = permute_graph(g0, mod.rcm_order(g0.row_ptr, g0.col))
+        elif name in ("C5t", "C3t", "C2t"):
+            from paper_2605_26975_b200 import plp as mod
+            base = {"C5t": ("C5", 100_000), "C3t": ("C3", 40 ** 3), "C2t": ("C2", None)}[name]
+            g0 = make_config(base[0], n=base[1])
+            g = permute_graph(g0, mod.tile_order(g0.row_ptr, g0.col))
         elif name == "P5":
             g = path_graph(5)
         elif name == "K2":
@@ -92,6 +97,9 @@ CASES = [
     # odd and extreme k
     ("C1", 1, 1.5), ("C1", 5, 1.2), ("C1", 7, 1.1), ("C1", 16, 1.5), ("C1", 32, 1.2),
     ("C1", 31, 2.0), ("C1", 12, 1.8), ("P5", 2, 1.5), ("K2", 1, 1.2), ("iso", 3, 1.5),
+    # tile-ordered graphs (tiled kernel: internal edges from shared memory, one power each)
+    ("C5t", 8, 1.2), ("C5t", 8, 2.0), ("C5t", 8, 1.37), ("C5t", 8, 1.5), ("C5t", 4, 1.1),
+    ("C5t", 16, 1.8), ("C3t", 8, 1.5), ("C2t", 2, 1.1), ("iso", 4, 1.2), ("C1", 20, 1.2),
 ]
 
 
@@ -105,7 +113,8 @@ def test_fused_sparse_parity(plp, ctx, name, k, p):
 
 
 @pytest.mark.parametrize("name,k,p", [("C1", 3, 1.5), ("C2", 2, 1.1), ("C4s", 20, 1.2),
-                                      ("C1", 5, 1.37), ("C1", 8, 2.0)])
+                                      ("C1", 5, 1.37), ("C1", 8, 2.0), ("C5t", 8, 1.2),
+                                      ("C3t", 8, 1.37)])
 def test_fused_full_parity(plp, ctx, name, k, p):
     g = graph(name)
     U = draw_U(g.n, k, seed=3)
@@ -123,17 +132,60 @@ def test_ab_in_null_runs_objective_first(plp, ctx):
 
 @pytest.mark.parametrize("p", [1.5, 1.2, 1.37, 2.0])
 @pytest.mark.parametrize("eps", [1e-9, 0.3])
-def test_ties_zeros_and_cap(plp, ctx, p, eps):
+@pytest.mark.parametrize("name,k", [("C1", 3), ("C5t", 4)])
+def test_ties_zeros_and_cap(plp, ctx, p, eps, name, k):
     """Exact ties u_i = u_j and exact zeros u_i = 0 (reading #6): the cap decision is taken on the
-    same IEEE |u_i - u_j| on both sides; eps = 0.3 exercises the rare branch 0 < a < eps."""
-    g = graph("C1")
+    same IEEE |u_i - u_j| on both sides; eps = 0.3 puts many edges below the cap.  k = 3 runs the
+    row kernel, k = 4 on a tile-ordered graph the tiled kernel."""
+    g = graph(name)
     rng = streams(8)[1]
-    U = np.round(rng.standard_normal((g.n, 3)) * 2.0) / 4.0  # many ties and zeros
+    U = np.round(rng.standard_normal((g.n, k)) * 2.0) / 4.0  # many ties and zeros
     U[:, 0] += 0.01  # keep every column nonzero
-    eta = draw_eta(g.n, 3, 8)
+    eta = draw_eta(g.n, k, 8)
     for mode in (0, 1):
         res = run_gpu(plp, ctx, g, U, eta, p, mode, eps)
         check(res, g, U, eta, p, mode, eps)
+
+
+def test_out_of_fast_domain_differences(plp, ctx):
+    """|u_i - u_j| below 2^-120 (but nonzero) or above 2^120 leaves the fast power domain: the
+    row / slot is recomputed with libdevice and still matches the oracle."""
+    for name, k in (("C1", 3), ("C5t", 4)):
+        g = graph(name)
+        U = draw_U(g.n, k, 21)
+        U[:, 1] = (1.0 + np.arange(g.n) * 1e-2) * 1e-38  # |u_i - u_j| ~ 1e-40 < 2^-120
+        U[:7, 0] *= 1e125  # a few huge entries
+        eta = draw_eta(g.n, k, 21)
+        res = run_gpu(plp, ctx, g, U, eta, 1.5, 0, 1e-300)
+        check(res, g, U, eta, 1.5, 0, 1e-300)
+
+
+def test_tiled_and_row_kernels_agree(plp, ctx, tmp_path):
+    """The same call with the tiled kernel and (in a subprocess, PLP_EDGE_ROWS=1) with the row
+    kernel: both within 1e-12 of each other (different summation association only)."""
+    import os
+    import subprocess
+    import sys
+    g = graph("C5t")
+    U, eta = draw_U(g.n, 8, 31), draw_eta(g.n, 8, 31)
+    res = run_gpu(plp, ctx, g, U, eta, 1.2, 0, 1e-9)
+    script = tmp_path / "rows.py"
+    script.write_text(
+        "import sys, numpy as np, torch\n"
+        f"sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})\n"
+        f"sys.path.insert(0, {os.path.dirname(os.path.abspath(__file__))!r})\n"
+        "from test_gpu_parity import graph, run_gpu\n"
+        "from paper_2605_26975_b200 import plp\n"
+        "from plp_inputs import draw_U, draw_eta\n"
+        "g = graph('C5t'); U, eta = draw_U(g.n, 8, 31), draw_eta(g.n, 8, 31)\n"
+        "r = run_gpu(plp, plp.Context(0), g, U, eta, 1.2, 0, 1e-9)\n"
+        f"np.savez({str(tmp_path / 'rows.npz')!r}, G=r['G'], Hv=r['Hv'], AB=r['AB'])\n")
+    env = dict(os.environ, PLP_EDGE_ROWS="1")
+    subprocess.check_call([sys.executable, str(script)], env=env)
+    z = np.load(tmp_path / "rows.npz")
+    assert colwise_relerr(res["G"], z["G"]) < 1e-12
+    assert colwise_relerr(res["Hv"], z["Hv"]) < 1e-12
+    assert scalar_relerr(res["AB"], z["AB"]) < 1e-12
 
 
 def test_misaligned_views_use_scalar_path(plp, ctx):

@@ -21,7 +21,7 @@ from plp_inputs import draw_U, draw_eta  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C5")
-    ap.add_argument("--order", default="rcm")
+    ap.add_argument("--order", default="tile")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--p", type=float, default=None)
     ap.add_argument("--events", action="store_true", help="also time the edge kernel with CUDA events")
