@@ -141,6 +141,7 @@ static plp_status build_tiles(plp_graph* g, const int64_t* rp, const int32_t* co
         const int64_t j = col[e];
         if (j >= r0 && j < r1) {
           int s;
+          uint32_t lower = 0;
           if (j > i) {
             s = slot_of[e] = n_int++;
           } else {  // partner (j, i) sits in the earlier row j
@@ -148,15 +149,17 @@ static plp_status build_tiles(plp_graph* g, const int64_t* rp, const int32_t* co
             while (f < rp[j + 1] && col[f] != i) ++f;
             if (f == rp[j + 1] || slot_of[f] < 0) return PLP_OK;  // not symmetric: no tiling
             s = slot_of[f];
+            lower = 1;
           }
-          enc[e] = (int32_t)(0x80000000u | ((uint32_t)(j - r0) << 16) | (uint32_t)s);
+          if (s >= 32768) return PLP_OK;
+          enc[e] = (int32_t)(0x80000000u | ((uint32_t)(j - r0) << 16) | (lower << 15) | (uint32_t)s);
         } else {
           enc[e] = n_ext++;
           ext.push_back((int32_t)j);
         }
       }
     }
-    if (n_int >= 65536 || n_ext >= 65536 || e1 - e0 >= 65536) return PLP_OK;
+    if (n_int >= 32768 || n_ext >= 32768 || e1 - e0 >= 65536) return PLP_OK;
     meta[t] = make_int4((int)e0, ext_off, n_int, n_ext);
     max_slots = std::max(max_slots, n_int + n_ext);
     max_nnz = std::max(max_nnz, (int)(e1 - e0));

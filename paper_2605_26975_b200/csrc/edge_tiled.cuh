@@ -95,6 +95,16 @@ __device__ __forceinline__ void lds_vec(const double* p, double (&v)[CPL]) {
   }
 }
 
+// Exact slot value with libdevice powers (rare: |d| below the cap, a tie, or outside the fast
+// domain): (w phi_p(d), w cap(|d|)^{p-2} * de) with de = 1 for internal slots.
+static __device__ __noinline__ double2 slot_exact(double d, double wv, double q, double pm1, double eps,
+                                           double s_eps, double de) {
+  const double ad = fabs(d);
+  const double cl = (ad != 0.0) ? wv * copysign(pow(ad, pm1), d) : 0.0;
+  const double wc = (ad < eps) ? wv * s_eps : wv * pow(ad, q);
+  return make_double2(cl, wc * de);
+}
+
 template <int CPL, int LPR, class POW, bool HAS_ETA>
 __global__ void __launch_bounds__(kEdgeThreads, 2) edge_tiled_kernel(EdgeArgs a, POW pw) {
   extern __shared__ __align__(16) unsigned char sm[];
@@ -174,70 +184,79 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) edge_tiled_kernel(EdgeArgs a,
       const int b = R[rl] - e0, e = R[rl + 1] - e0;
       for (int q = b + li; q < e; q += LPR) {
         const int c = C[q];
-        if (c < 0) {
-          const int jl = (c >> 16) & 0x7FFF;
-          if (jl > rl) list[c & 0xFFFF] = (rl << 16) | q;
-        } else {
-          list[n_int + c] = (rl << 16) | q;
-        }
+        if (c >= 0) list[n_int + c] = (rl << 16) | q;          // external
+        else if (!(c & 0x8000)) list[c & 0x7FFF] = (rl << 16) | q;  // internal, upper row
       }
     }
     __syncthreads();
 
     // ---- phase 1: one power per listed edge-column ----
     if (active) {
-      for (int s = grp; s < n_slots; s += G) {
+      // internal undirected edges: U_i, U_j from shared memory; value (w phi_p(d), w cap^{p-2})
+      for (int s = grp; s < n_int; s += G) {
         const int ent = list[s];
         const int rl = ent >> 16, q = ent & 0xFFFF;
         const double wv = W[q];
-        double ui[CPL], uj[CPL], ei[CPL], ej[CPL];
+        const int jl = (C[q] >> 16) & 0x7FFF;
+        double ui[CPL], uj[CPL];
         lds_vec<CPL>(Ut + rl * k + c0, ui);
-        const bool internal = s < n_int;
-        if (internal) {
-          const int jl = (C[q] >> 16) & 0x7FFF;
-          lds_vec<CPL>(Ut + jl * k + c0, uj);
-        } else {
-          const int64_t j = __ldg(a.ext_col + tm.y + (s - n_int));
-          ld_vec<CPL>(a.U + j * k + c0, uj);
-          if constexpr (HAS_ETA) {
-            ld_vec<CPL>(a.eta + j * k + c0, ej);
-            lds_vec<CPL>(Et + rl * k + c0, ei);
-          }
-        }
-        const double wse = POW::kIsP2 ? wv : wv * pw.s_eps;
-        unsigned bad = 0;
+        lds_vec<CPL>(Ut + jl * k + c0, uj);
         double2 out[CPL];
+        bool rare = false;
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
           const double d = ui[c] - uj[c];
-          double ws, wc;
           if constexpr (POW::kIsP2) {
-            ws = wv;
-            wc = wv;
+            out[c] = make_double2(wv * d, wv);
           } else {
-            ws = wv * pw.pow_raw(d, bad);
-            wc = pw.abs_below_cap(d) ? wse : ws;
-          }
-          out[c].x = ws * d;  // w phi_p(u_i - u_j)
-          out[c].y = wc;
-          if constexpr (HAS_ETA) {
-            if (!internal) out[c].y = wc * (ei[c] - ej[c]);
+            unsigned unused = 0;
+            rare |= !pw.fast(d);
+            const double ws = wv * pw.pow_raw(d, unused);
+            out[c] = make_double2(ws * d, ws);
           }
         }
-        if (bad) {  // rare: some |d| outside the fast power domain -> exact libdevice values
+        if (rare) {  // |d| below the cap (incl. ties) or outside the fast domain: exact values
 #pragma unroll
-          for (int c = 0; c < CPL; ++c) {
-            const double d = ui[c] - uj[c], ad = fabs(d);
-            const double s_raw = (ad != 0.0) ? pow(ad, pw.q) : 0.0;
-            const double wc = (ad < pw.eps) ? wse : wv * s_raw;
-            out[c].x = (ad != 0.0) ? wv * copysign(pow(ad, pw.pm1), d) : 0.0;
-            out[c].y = wc;
-            if constexpr (HAS_ETA) {
-              if (!internal) out[c].y = wc * (ei[c] - ej[c]);
-            }
+          for (int c = 0; c < CPL; ++c)
+            out[c] = slot_exact(ui[c] - uj[c], wv, pw.q, pw.pm1, pw.eps, pw.s_eps, 1.0);
+        }
+        double2* vs = val + s * k + c0;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) vs[c] = out[c];
+      }
+      // external edges: U_j, eta_j gathered from global memory (L2); value (w phi_p(d), cH)
+      for (int s = n_int + grp; s < n_slots; s += G) {
+        const int ent = list[s];
+        const int rl = ent >> 16, q = ent & 0xFFFF;
+        const double wv = W[q];
+        const int64_t j = __ldg(a.ext_col + tm.y + (s - n_int));
+        double ui[CPL], uj[CPL], ei[CPL], ej[CPL];
+        ld_vec<CPL>(a.U + j * k + c0, uj);
+        if constexpr (HAS_ETA) ld_vec<CPL>(a.eta + j * k + c0, ej);
+        lds_vec<CPL>(Ut + rl * k + c0, ui);
+        if constexpr (HAS_ETA) lds_vec<CPL>(Et + rl * k + c0, ei);
+        double2 out[CPL];
+        bool rare = false;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const double d = ui[c] - uj[c];
+          const double de = HAS_ETA ? ei[c] - ej[c] : 0.0;
+          if constexpr (POW::kIsP2) {
+            out[c] = make_double2(wv * d, wv * de);
+          } else {
+            unsigned unused = 0;
+            rare |= !pw.fast(d);
+            const double ws = wv * pw.pow_raw(d, unused);
+            out[c] = make_double2(ws * d, ws * de);
           }
         }
-        double2* vs = val + (int64_t)s * k + c0;
+        if (rare) {
+#pragma unroll
+          for (int c = 0; c < CPL; ++c)
+            out[c] = slot_exact(ui[c] - uj[c], wv, pw.q, pw.pm1, pw.eps, pw.s_eps,
+                                HAS_ETA ? ei[c] - ej[c] : 0.0);
+        }
+        double2* vs = val + s * k + c0;
 #pragma unroll
         for (int c = 0; c < CPL; ++c) vs[c] = out[c];
       }
@@ -257,15 +276,15 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) edge_tiled_kernel(EdgeArgs a,
           const int c = C[q];
           const bool internal = c < 0;
           const int jl = (c >> 16) & 0x7FFF;
-          const int slot = internal ? (c & 0xFFFF) : (n_int + c);
-          const double2* vs = val + (int64_t)slot * k + c0;
-          const bool neg = internal && jl < rl;
+          const int slot = internal ? (c & 0x7FFF) : (n_int + c);
+          const double2* vs = val + slot * k + c0;
+          const int flip = (c & 0x8000) << 16;  // sign bit: the lower row gets -w phi_p(d)
           double ej[CPL];
           if constexpr (HAS_ETA) lds_vec<CPL>(Et + (internal ? jl : 0) * k + c0, ej);
 #pragma unroll
           for (int c2 = 0; c2 < CPL; ++c2) {
             const double2 v = vs[c2];
-            L[c2] += neg ? -v.x : v.x;
+            L[c2] += __hiloint2double(__double2hiint(v.x) ^ flip, __double2loint(v.x));
             if constexpr (HAS_ETA) HA[c2] = fma(v.y, internal ? (ei[c2] - ej[c2]) : 1.0, HA[c2]);
           }
         }

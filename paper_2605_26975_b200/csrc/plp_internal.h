@@ -35,8 +35,9 @@ struct plp_graph {
   double* w = nullptr;       // device fp64 w[nnz]
   int32_t* sched = nullptr;  // device row schedule: rows sorted by degree within windows
   // Tiled representation (edge_tiled.cuh): tiles of PLP_TILE_ROWS consecutive rows.
-  //   enc[e]: internal edge (both ends in the tile) -> 0x80000000 | (j - r0) << 16 | slot of the
-  //           undirected edge;  external edge -> its external slot in the tile
+  //   enc[e]: internal edge (both ends in the tile) -> 0x80000000 | (j - r0) << 16 | lower << 15
+  //           | slot of the undirected edge (lower = 1 when j < i); external edge -> its external
+  //           slot in the tile
   //   ext_col[tile_meta.x + s]: global column of external slot s;  tile_meta = (ext_off, n_int,
   //   n_ext, nnz of the tile)
   bool tiled = false;

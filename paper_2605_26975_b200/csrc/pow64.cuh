@@ -42,9 +42,6 @@ __device__ __forceinline__ unsigned abs_hi(double d) {
 __device__ __forceinline__ unsigned out_of_domain(unsigned ahi) {
   return (unsigned)(ahi - 1u < kHiMin - 1u) | (unsigned)(ahi >= kHiMax);
 }
-__device__ __forceinline__ void flag_out_of_domain(unsigned ahi, unsigned& bad) {
-  bad |= out_of_domain(ahi);
-}
 // float with the exponent and top 20 mantissa bits of the double whose |hi word| is `ahi`
 // (ahi clamped to >= 2^-120 so the float is normal)
 __device__ __forceinline__ float seed_float(unsigned ahi) {
@@ -79,6 +76,7 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
 struct PowBase {
   double eps;          // curvature cap (> 0 when p < 2)
   long long eps_bits;  // bit pattern of eps (integer compare == value compare for >= 0)
+  long long fast_lo;   // bit pattern of max(eps, 2^-120): |d| >= this (and < 2^120) is "fast"
   double q;            // p - 2
   double pm1;          // p - 1
   double s_eps;        // eps^{p-2} (host glibc pow: the value the oracle's cap gives)
@@ -86,6 +84,12 @@ struct PowBase {
   __device__ __forceinline__ void init_smem(void*) {}
   __device__ __forceinline__ bool below_cap(double a) const {  // a >= 0
     return __double_as_longlong(a) < eps_bits;
+  }
+  // |d| in [max(eps, 2^-120), 2^120): no cap and the branch-free power is valid (integer pipe)
+  __device__ __forceinline__ bool fast(double d) const {
+    const unsigned ahi = abs_hi(d);
+    const unsigned long long a = ((unsigned long long)ahi << 32) | (unsigned)__double2loint(d);
+    return (a >= (unsigned long long)fast_lo) & (ahi < kHiMax);
   }
   __device__ __forceinline__ bool abs_below_cap(double d) const {  // |d| < eps, integer pipe
     // compare (|hi|, lo) with eps's words; written on the words so the compiler cannot turn the
