@@ -130,7 +130,7 @@ static plp_status build_tiles(plp_graph* g, const int64_t* rp, const int32_t* co
   std::vector<int32_t> slot_of((size_t)g->nnz, -1);
   std::vector<int32_t> ext;
   std::vector<int4> meta((size_t)nt + 1);
-  int max_slots = 0, max_nnz = 0;
+  int max_slots = 0, max_nnz = 0, max_ext = 0;
   for (int64_t t = 0; t < nt; ++t) {
     const int64_t r0 = t * T, r1 = std::min<int64_t>(n, r0 + T);
     const int64_t e0 = rp[r0], e1 = rp[r1];
@@ -151,17 +151,24 @@ static plp_status build_tiles(plp_graph* g, const int64_t* rp, const int32_t* co
             s = slot_of[f];
             lower = 1;
           }
-          if (s >= 32768) return PLP_OK;
-          enc[e] = (int32_t)(0x80000000u | ((uint32_t)(j - r0) << 16) | (lower << 15) | (uint32_t)s);
+          enc[e] = (int32_t)((lower << 31) | ((uint32_t)(j - r0) << 16) | (uint32_t)s);
         } else {
-          enc[e] = n_ext++;
+          enc[e] = -1 - n_ext++;  // external: finalised below, once n_int is known
           ext.push_back((int32_t)j);
         }
       }
     }
-    if (n_int >= 32768 || n_ext >= 32768 || e1 - e0 >= 65536) return PLP_OK;
+    if (n_int + n_ext >= 65536 || T + n_ext >= 32768 || e1 - e0 >= 65536) return PLP_OK;
+    for (int64_t e = e0; e < e1; ++e) {
+      const int64_t j = col[e];
+      if (!(j >= r0 && j < r1)) {  // external: eta row T + x of the tile table, slot n_int + x
+        const int x = -1 - enc[e];
+        enc[e] = (int32_t)(((uint32_t)(T + x) << 16) | (uint32_t)(n_int + x));
+      }
+    }
     meta[t] = make_int4((int)e0, ext_off, n_int, n_ext);
     max_slots = std::max(max_slots, n_int + n_ext);
+    max_ext = std::max(max_ext, n_ext);
     max_nnz = std::max(max_nnz, (int)(e1 - e0));
   }
   meta[nt] = make_int4((int)g->nnz, (int)ext.size(), 0, 0);
@@ -182,6 +189,7 @@ static plp_status build_tiles(plp_graph* g, const int64_t* rp, const int32_t* co
   g->n_tiles = nt;
   g->max_slots = max_slots;
   g->max_nnz = max_nnz;
+  g->max_ext = max_ext;
   return PLP_OK;
 }
 

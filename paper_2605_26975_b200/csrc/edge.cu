@@ -210,6 +210,7 @@ static EdgeArgs graph_args(const plp_graph* g) {
     a.n_tiles = g->n_tiles;
     a.max_slots = g->max_slots;
     a.max_nnz = g->max_nnz;
+    a.max_ext = g->max_ext;
   }
   return a;
 }

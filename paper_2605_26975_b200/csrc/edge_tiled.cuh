@@ -4,19 +4,19 @@
 // plp_tile_order).  A persistent CTA loops over tiles:
 //   stage   one thread issues TMA bulk copies (cp.async.bulk, mbarrier completion) of the tile's
 //           contiguous U rows, eta rows, row_ptr, encoded columns and weights into shared memory;
-//   phase 0 every edge the tile must evaluate gets a work-list entry: each INTERNAL undirected
-//           edge (both ends in the tile) once, at its upper row, and each EXTERNAL edge;
-//   phase 1 a flat, balanced sweep over the work list computes the one power per edge-column:
-//             internal slot: cL = w s_raw (u_i - u_j), wc = w cap(|d|)^{p-2}        (U_j from smem)
-//             external slot: cL = w s_raw d,           cH = wc (eta_i - eta_j)     (U_j, eta_j from
-//                                                                                   global / L2)
+//   phase 0 every edge that owns a value slot adds itself to the tile's work list: each INTERNAL
+//           undirected edge (both ends in the tile) once, at its upper row, and each EXTERNAL edge;
+//   phase 1 flat, balanced sweeps over the work list compute the one power per edge-column:
+//             slot value (cL, wc) = (w phi_p(u_i - u_j), w cap(|u_i - u_j|)^{p-2})
+//           internal: U_j from shared memory; external: U_j and eta_j gathered from global memory
+//           (L2), eta_j kept in the tile's eta table at row T + x;
 //   phase 2 each row walks its CSR row in order (the oracle's order) and sums
-//             L_i  += +-cL   (internal: + at the upper row, - at the lower row: d is antisymmetric)
-//             HA_i += wc (eta_i - eta_j)  (internal)  or  cH  (external),
-//           then the row epilogue of the row kernel (node terms, G, Hv, partial sums).
-// Each internal undirected edge costs one power instead of two and its U_j / eta_j come from shared
-// memory, which takes most of the gather traffic off L2 (ncu showed L2 as the next bound of the
-// row kernel).  Every reduction is in a fixed order: results are deterministic.
+//             L_i  += cL  (sign flipped at the lower row of an internal edge: d is antisymmetric)
+//             HA_i += wc (eta_i - eta_j)
+//           then the row epilogue (node terms, G, Hv, partial sums of A, B, alpha, gamma).
+// Each internal undirected edge costs one power instead of two, and its U_j / eta_j come from
+// shared memory, which takes most of the gather traffic off L2.  Every reduction is in a fixed
+// order: results are deterministic.
 #pragma once
 #include <cstdlib>
 
@@ -56,22 +56,23 @@ __device__ __forceinline__ void fence_proxy_async() {
 }
 
 struct TiledLayout {
-  unsigned ut, et, w, enc, rp, list, val, tab, total;
+  unsigned coef, ut, et, w, enc, rp, list, val, tab, total;
 };
 __host__ __device__ inline unsigned align16u(unsigned x) { return (x + 15u) & ~15u; }
 // Shared-memory layout (byte offsets), identical on host and device.
-__host__ __device__ inline TiledLayout tiled_layout(int k, int max_nnz, int max_slots, int cpl,
-                                                     bool tables) {
+__host__ __device__ inline TiledLayout tiled_layout(int k, int max_nnz, int max_slots, int max_ext,
+                                                     int cpl, bool tables) {
   TiledLayout L;
   unsigned o = 16;  // mbarrier
+  L.coef = o; o += align16u(4 * k * 8);
   L.ut = o; o += align16u(kTileRows * k * 8);
-  L.et = o; o += align16u(kTileRows * k * 8);
+  L.et = o; o += align16u((kTileRows + max_ext) * k * 8);
   L.w = o; o += align16u((max_nnz + 4) * 8);
   L.enc = o; o += align16u((max_nnz + 8) * 4);
   L.rp = o; o += align16u((kTileRows + 1 + 8) * 4);
   L.list = o; o += align16u(max_slots * 4 + 4);
   L.val = o;
-  unsigned vb = (unsigned)max_slots * k * 16;
+  const unsigned vb = (unsigned)max_slots * k * 16;
   const unsigned red = 4u * cpl * kEdgeThreads * 8;  // final CTA reduction reuses the value area
   o += align16u(vb > red ? vb : red);
   L.tab = o;
@@ -94,23 +95,58 @@ __device__ __forceinline__ void lds_vec(const double* p, double (&v)[CPL]) {
     for (int c = 0; c < CPL; ++c) v[c] = p[c];
   }
 }
+template <int CPL>
+__device__ __forceinline__ void sts_vec(double* p, const double (&v)[CPL]) {
+  if constexpr (CPL % 2 == 0) {
+#pragma unroll
+    for (int c = 0; c < CPL; c += 2) *reinterpret_cast<double2*>(p + c) = make_double2(v[c], v[c + 1]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) p[c] = v[c];
+  }
+}
 
 // Exact slot value with libdevice powers (rare: |d| below the cap, a tie, or outside the fast
-// domain): (w phi_p(d), w cap(|d|)^{p-2} * de) with de = 1 for internal slots.
-static __device__ __noinline__ double2 slot_exact(double d, double wv, double q, double pm1, double eps,
-                                           double s_eps, double de) {
+// power domain): (w phi_p(d), w cap(|d|)^{p-2}).
+static __device__ __noinline__ double2 slot_exact(double d, double wv, double q, double pm1,
+                                                  double eps, double s_eps) {
   const double ad = fabs(d);
   const double cl = (ad != 0.0) ? wv * copysign(pow(ad, pm1), d) : 0.0;
   const double wc = (ad < eps) ? wv * s_eps : wv * pow(ad, q);
-  return make_double2(cl, wc * de);
+  return make_double2(cl, wc);
 }
 
-template <int CPL, int LPR, class POW, bool HAS_ETA>
+// Slot values of the lane's CPL columns for one edge (weight wv, d = ui - uj).
+template <int CPL, class POW>
+__device__ __forceinline__ void slot_values(const POW& pw, double wv, const double (&ui)[CPL],
+                                            const double (&uj)[CPL], double2 (&out)[CPL]) {
+  bool rare = false;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const double d = ui[c] - uj[c];
+    if constexpr (POW::kIsP2) {
+      out[c] = make_double2(wv * d, wv);
+    } else {
+      unsigned unused = 0;
+      rare |= !pw.fast(d);
+      const double ws = wv * pw.pow_raw(d, unused);
+      out[c] = make_double2(ws * d, ws);
+    }
+  }
+  if (rare) {
+#pragma unroll
+    for (int c = 0; c < CPL; ++c)
+      out[c] = slot_exact(ui[c] - uj[c], wv, pw.q, pw.pm1, pw.eps, pw.s_eps);
+  }
+}
+
+template <int CPL, int LPR, int KT, class POW, bool HAS_ETA>
 __global__ void __launch_bounds__(kEdgeThreads, 2) edge_tiled_kernel(EdgeArgs a, POW pw) {
   extern __shared__ __align__(16) unsigned char sm[];
-  const int k = a.k;
-  const TiledLayout Ly = tiled_layout(k, a.max_nnz, a.max_slots, CPL, POW::kNeedsTables);
+  const int k = KT ? KT : a.k;
+  const TiledLayout Ly = tiled_layout(k, a.max_nnz, a.max_slots, a.max_ext, CPL, POW::kNeedsTables);
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm);
+  double* coef = reinterpret_cast<double*>(sm + Ly.coef);  // [4][k]: p/B, A/B, p(p-1)/B, p(p-1)A/B^2
   double* Ut = reinterpret_cast<double*>(sm + Ly.ut);
   double* Et = reinterpret_cast<double*>(sm + Ly.et);
   double* Wt = reinterpret_cast<double*>(sm + Ly.w);
@@ -119,9 +155,20 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) edge_tiled_kernel(EdgeArgs a,
   int32_t* list = reinterpret_cast<int32_t*>(sm + Ly.list);
   double2* val = reinterpret_cast<double2*>(sm + Ly.val);
   if constexpr (POW::kNeedsTables) pw.init_smem(sm + Ly.tab);
+  const double p = a.p;
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (a.AB != nullptr) {
+    const double pp1 = p * (p - 1.0);
+    for (int l = threadIdx.x; l < k; l += blockDim.x) {
+      const double A = a.AB[l], B = a.AB[k + l];
+      coef[l] = p / B;
+      coef[k + l] = A / B;
+      coef[2 * k + l] = pp1 / B;
+      coef[3 * k + l] = pp1 * A / (B * B);
+    }
   }
   __syncthreads();
 
@@ -131,22 +178,7 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) edge_tiled_kernel(EdgeArgs a,
   const int G = blockDim.x / LPR;     // groups per CTA
   const int c0 = li * CPL;
   const bool active = c0 < k;
-  const double p = a.p;
-  const double pp1 = p * (p - 1.0);
 
-  double cG[CPL], cAB[CPL], cHA[CPL], cHB[CPL];
-#pragma unroll
-  for (int c = 0; c < CPL; ++c) cG[c] = cAB[c] = cHA[c] = cHB[c] = 0.0;
-  if (a.AB != nullptr && active) {
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) {
-      const double A = a.AB[c0 + c], B = a.AB[k + c0 + c];
-      cG[c] = p / B;
-      cAB[c] = A / B;
-      cHA[c] = pp1 / B;
-      cHB[c] = pp1 * A / (B * B);
-    }
-  }
   double accA[CPL], accB[CPL], accAl[CPL], accGa[CPL];
 #pragma unroll
   for (int c = 0; c < CPL; ++c) accA[c] = accB[c] = accAl[c] = accGa[c] = 0.0;
@@ -179,83 +211,57 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) edge_tiled_kernel(EdgeArgs a,
     const int32_t* C = Ct + c_off;
     const int32_t* R = Rt + r_off;
 
-    // ---- phase 0: work list (internal edges at their upper row, external edges) ----
+    // ---- phase 0: work list (slot -> row << 16 | edge) ----
     for (int rl = grp; rl < nrows; rl += G) {
       const int b = R[rl] - e0, e = R[rl + 1] - e0;
       for (int q = b + li; q < e; q += LPR) {
         const int c = C[q];
-        if (c >= 0) list[n_int + c] = (rl << 16) | q;          // external
-        else if (!(c & 0x8000)) list[c & 0x7FFF] = (rl << 16) | q;  // internal, upper row
+        if (c >= 0) list[c & 0xFFFF] = (rl << 16) | q;  // slot owner: internal upper or external
       }
     }
     __syncthreads();
 
     // ---- phase 1: one power per listed edge-column ----
     if (active) {
-      // internal undirected edges: U_i, U_j from shared memory; value (w phi_p(d), w cap^{p-2})
-      for (int s = grp; s < n_int; s += G) {
-        const int ent = list[s];
-        const int rl = ent >> 16, q = ent & 0xFFFF;
-        const double wv = W[q];
-        const int jl = (C[q] >> 16) & 0x7FFF;
-        double ui[CPL], uj[CPL];
-        lds_vec<CPL>(Ut + rl * k + c0, ui);
-        lds_vec<CPL>(Ut + jl * k + c0, uj);
-        double2 out[CPL];
-        bool rare = false;
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) {
-          const double d = ui[c] - uj[c];
-          if constexpr (POW::kIsP2) {
-            out[c] = make_double2(wv * d, wv);
-          } else {
-            unsigned unused = 0;
-            rare |= !pw.fast(d);
-            const double ws = wv * pw.pow_raw(d, unused);
-            out[c] = make_double2(ws * d, ws);
-          }
-        }
-        if (rare) {  // |d| below the cap (incl. ties) or outside the fast domain: exact values
-#pragma unroll
-          for (int c = 0; c < CPL; ++c)
-            out[c] = slot_exact(ui[c] - uj[c], wv, pw.q, pw.pm1, pw.eps, pw.s_eps, 1.0);
-        }
+      // internal undirected edges, two slots per step for ILP
+      for (int s = grp; s < n_int; s += 2 * G) {
+        const int s2 = s + G;
+        const bool two = s2 < n_int;
+        const int ent = list[s], ent2 = list[two ? s2 : s];
+        const int q = ent & 0xFFFF, q2 = ent2 & 0xFFFF;
+        double ui[CPL], uj[CPL], ui2[CPL], uj2[CPL];
+        lds_vec<CPL>(Ut + (ent >> 16) * k + c0, ui);
+        lds_vec<CPL>(Ut + ((C[q] >> 16) & 0x7FFF) * k + c0, uj);
+        lds_vec<CPL>(Ut + (ent2 >> 16) * k + c0, ui2);
+        lds_vec<CPL>(Ut + ((C[q2] >> 16) & 0x7FFF) * k + c0, uj2);
+        double2 out[CPL], out2[CPL];
+        slot_values<CPL>(pw, W[q], ui, uj, out);
+        slot_values<CPL>(pw, W[q2], ui2, uj2, out2);
         double2* vs = val + s * k + c0;
 #pragma unroll
         for (int c = 0; c < CPL; ++c) vs[c] = out[c];
+        if (two) {
+          double2* vs2 = val + s2 * k + c0;
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) vs2[c] = out2[c];
+        }
       }
-      // external edges: U_j, eta_j gathered from global memory (L2); value (w phi_p(d), cH)
+      // external edges: U_j, eta_j gathered from global memory (L2)
       for (int s = n_int + grp; s < n_slots; s += G) {
         const int ent = list[s];
-        const int rl = ent >> 16, q = ent & 0xFFFF;
-        const double wv = W[q];
-        const int64_t j = __ldg(a.ext_col + tm.y + (s - n_int));
-        double ui[CPL], uj[CPL], ei[CPL], ej[CPL];
+        const int q = ent & 0xFFFF;
+        const int x = s - n_int;
+        const int64_t j = __ldg(a.ext_col + tm.y + x);
+        double ui[CPL], uj[CPL];
         ld_vec<CPL>(a.U + j * k + c0, uj);
-        if constexpr (HAS_ETA) ld_vec<CPL>(a.eta + j * k + c0, ej);
-        lds_vec<CPL>(Ut + rl * k + c0, ui);
-        if constexpr (HAS_ETA) lds_vec<CPL>(Et + rl * k + c0, ei);
+        if constexpr (HAS_ETA) {
+          double ej[CPL];
+          ld_vec<CPL>(a.eta + j * k + c0, ej);
+          sts_vec<CPL>(Et + (kTileRows + x) * k + c0, ej);
+        }
+        lds_vec<CPL>(Ut + (ent >> 16) * k + c0, ui);
         double2 out[CPL];
-        bool rare = false;
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) {
-          const double d = ui[c] - uj[c];
-          const double de = HAS_ETA ? ei[c] - ej[c] : 0.0;
-          if constexpr (POW::kIsP2) {
-            out[c] = make_double2(wv * d, wv * de);
-          } else {
-            unsigned unused = 0;
-            rare |= !pw.fast(d);
-            const double ws = wv * pw.pow_raw(d, unused);
-            out[c] = make_double2(ws * d, ws * de);
-          }
-        }
-        if (rare) {
-#pragma unroll
-          for (int c = 0; c < CPL; ++c)
-            out[c] = slot_exact(ui[c] - uj[c], wv, pw.q, pw.pm1, pw.eps, pw.s_eps,
-                                HAS_ETA ? ei[c] - ej[c] : 0.0);
-        }
+        slot_values<CPL>(pw, W[q], ui, uj, out);
         double2* vs = val + s * k + c0;
 #pragma unroll
         for (int c = 0; c < CPL; ++c) vs[c] = out[c];
@@ -274,18 +280,15 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) edge_tiled_kernel(EdgeArgs a,
         for (int c = 0; c < CPL; ++c) L[c] = HA[c] = 0.0;
         for (int q = b; q < e; ++q) {
           const int c = C[q];
-          const bool internal = c < 0;
-          const int jl = (c >> 16) & 0x7FFF;
-          const int slot = internal ? (c & 0x7FFF) : (n_int + c);
-          const double2* vs = val + slot * k + c0;
-          const int flip = (c & 0x8000) << 16;  // sign bit: the lower row gets -w phi_p(d)
+          const double2* vs = val + (c & 0xFFFF) * k + c0;
+          const int flip = c & 0x80000000;  // the lower row of an internal edge gets -cL
           double ej[CPL];
-          if constexpr (HAS_ETA) lds_vec<CPL>(Et + (internal ? jl : 0) * k + c0, ej);
+          if constexpr (HAS_ETA) lds_vec<CPL>(Et + ((c >> 16) & 0x7FFF) * k + c0, ej);
 #pragma unroll
           for (int c2 = 0; c2 < CPL; ++c2) {
             const double2 v = vs[c2];
             L[c2] += __hiloint2double(__double2hiint(v.x) ^ flip, __double2loint(v.x));
-            if constexpr (HAS_ETA) HA[c2] = fma(v.y, internal ? (ei[c2] - ej[c2]) : 1.0, HA[c2]);
+            if constexpr (HAS_ETA) HA[c2] = fma(v.y, ei[c2] - ej[c2], HA[c2]);
           }
         }
         const int64_t row = r0 + rl;
@@ -298,9 +301,9 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) edge_tiled_kernel(EdgeArgs a,
           accA[c] = fma(ui[c], L[c], accA[c]);
           accB[c] = fma(tn, au, accB[c]);
           const double phi = copysign(tn, ui[c]);
-          g[c] = cG[c] * (L[c] - cAB[c] * phi);
+          g[c] = coef[c0 + c] * (L[c] - coef[k + c0 + c] * phi);
           if constexpr (HAS_ETA) {
-            h[c] = cHA[c] * HA[c] - cHB[c] * sn * ei[c];
+            h[c] = coef[2 * k + c0 + c] * HA[c] - coef[3 * k + c0 + c] * sn * ei[c];
             if (a.want_dots) accAl[c] = fma(p * phi, ei[c], accAl[c]);
           } else {
             h[c] = 0.0;
@@ -340,12 +343,10 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) edge_tiled_kernel(EdgeArgs a,
   }
 }
 
-// Launches the tiled kernel when the graph is tiled, k is even (16-byte column pairs), the dense
-// arrays are 16-byte aligned and the tile fits in shared memory; returns *used = false otherwise.
-template <int LPR, class POW, bool HAS_ETA>
+template <int LPR, int KT, class POW, bool HAS_ETA>
 plp_status launch_tiled_shape(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int* grid_out) {
-  auto kern = edge_tiled_kernel<2, LPR, POW, HAS_ETA>;
-  const TiledLayout Ly = tiled_layout(a.k, a.max_nnz, a.max_slots, 2, POW::kNeedsTables);
+  auto kern = edge_tiled_kernel<2, LPR, KT, POW, HAS_ETA>;
+  const TiledLayout Ly = tiled_layout(a.k, a.max_nnz, a.max_slots, a.max_ext, 2, POW::kNeedsTables);
   static int attr_set = 0;
   static int occ = 1;
   if (attr_set < (int)Ly.total) {
@@ -364,6 +365,8 @@ plp_status launch_tiled_shape(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, in
   return PLP_OK;
 }
 
+// Launches the tiled kernel when the graph is tiled, k is even (16-byte column pairs), the dense
+// arrays are 16-byte aligned and the tile fits in shared memory; *used = false otherwise.
 template <class POW>
 plp_status try_launch_tiled(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int* grid, bool* used) {
   *used = false;
@@ -373,19 +376,21 @@ plp_status try_launch_tiled(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int*
   if (force_rows || a.enc == nullptr || k % 2 != 0 || !al16(a.U) || (a.eta && !al16(a.eta)) ||
       (a.G && !al16(a.G)) || (a.Hv && !al16(a.Hv)))
     return PLP_OK;
-  const TiledLayout Ly = tiled_layout(k, a.max_nnz, a.max_slots, 2, POW::kNeedsTables);
+  const TiledLayout Ly = tiled_layout(k, a.max_nnz, a.max_slots, a.max_ext, 2, POW::kNeedsTables);
   if (Ly.total > 220u * 1024u) return PLP_OK;
   *used = true;
   const bool he = a.eta != nullptr;
   const int half = k / 2;
-#define PLP_TSHAPE(L)                                                              \
-  return he ? launch_tiled_shape<L, POW, true>(ctx, a, pw, grid)                   \
-            : launch_tiled_shape<L, POW, false>(ctx, a, pw, grid)
-  if (half <= 1) PLP_TSHAPE(1);
-  if (half <= 2) PLP_TSHAPE(2);
-  if (half <= 4) PLP_TSHAPE(4);
-  if (half <= 8) PLP_TSHAPE(8);
-  PLP_TSHAPE(16);
+#define PLP_TSHAPE(L, KT)                                                          \
+  return he ? launch_tiled_shape<L, KT, POW, true>(ctx, a, pw, grid)               \
+            : launch_tiled_shape<L, KT, POW, false>(ctx, a, pw, grid)
+  if (k == 2) PLP_TSHAPE(1, 2);
+  if (k == 4) PLP_TSHAPE(2, 4);
+  if (k == 8) PLP_TSHAPE(4, 8);
+  if (k == 16) PLP_TSHAPE(8, 16);
+  if (half <= 4) PLP_TSHAPE(4, 0);
+  if (half <= 8) PLP_TSHAPE(8, 0);
+  PLP_TSHAPE(16, 0);
 #undef PLP_TSHAPE
 }
 

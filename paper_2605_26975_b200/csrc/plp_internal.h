@@ -35,11 +35,13 @@ struct plp_graph {
   double* w = nullptr;       // device fp64 w[nnz]
   int32_t* sched = nullptr;  // device row schedule: rows sorted by degree within windows
   // Tiled representation (edge_tiled.cuh): tiles of PLP_TILE_ROWS consecutive rows.
-  //   enc[e]: internal edge (both ends in the tile) -> 0x80000000 | (j - r0) << 16 | lower << 15
-  //           | slot of the undirected edge (lower = 1 when j < i); external edge -> its external
-  //           slot in the tile
-  //   ext_col[tile_meta.x + s]: global column of external slot s;  tile_meta = (ext_off, n_int,
-  //   n_ext, nnz of the tile)
+  //   enc[e] = flip << 31 | erow << 16 | slot, with
+  //     internal edge (both ends in the tile): erow = j - r0, slot = the undirected edge's slot,
+  //                                           flip = 1 at the lower row (j < i)
+  //     external edge:                         erow = T + x, slot = n_int + x (x-th external
+  //                                           edge of the tile), flip = 0
+  //   ext_col[ext_off + x]: global column of the tile's x-th external edge;
+  //   tile_meta = (e0, ext_off, n_int, n_ext), one sentinel entry at n_tiles
   bool tiled = false;
   int32_t* enc = nullptr;
   int32_t* ext_col = nullptr;
@@ -47,6 +49,7 @@ struct plp_graph {
   int64_t n_tiles = 0;
   int max_slots = 0;  // max over tiles of n_int + n_ext
   int max_nnz = 0;    // max over tiles of the tile's nnz
+  int max_ext = 0;    // max over tiles of n_ext
 };
 constexpr int kSchedWindow = 2048;  // rows per degree-sorting window (stays L2-local)
 
@@ -91,7 +94,7 @@ struct EdgeArgs {
   const int32_t* ext_col;
   const int4* tile_meta;
   int64_t n_tiles;
-  int max_slots, max_nnz;
+  int max_slots, max_nnz, max_ext;
 };
 plp_status launch_edge(plp_ctx* ctx, const EdgeArgs& a, int* grid_out);
 // Fixed-order reduction of edge partials: AB_out (2k), dots_out (2k), F (1); any may be null.
