@@ -2,7 +2,8 @@
 
 A step = one plp_fgrad_hessvec call (SURVEY.md §8(a) a7 = a2..a5 fused, sparse-mode Hessian) on
 the workload config (default C5: 8,388,608 uniform points in [0,1]^2, symmetrised 6-NN graph,
-Gaussian weights, k = 8, p = 1.2, tile order = RCM + BFS-grown 128-row tiles), with A, B at U supplied from a preceding plp_fgrad
+Gaussian weights, k = 8, p = 1.2, tile order = RCM + BFS-grown 120-row tiles), with A, B at U
+supplied from a preceding plp_fgrad
 (the trust-region rho-test always has them).  Inputs (CSR 0.71 GB + U, eta 1.07 GB)
 exceed the 126 MB L2, so no flush is needed between steps.
 
@@ -55,7 +56,8 @@ def get_graph(name: str, order: str):
     to save generation time between runs (regenerated when absent)."""
     from plp_inputs import make_config, Graph
     from paper_2605_26975_b200 import plp
-    key = hashlib.sha1(f"{name}-{order}-v1".encode()).hexdigest()[:12]
+    from paper_2605_26975_b200.plp import TILE_ROWS
+    key = hashlib.sha1(f"{name}-{order}-{TILE_ROWS}-v2".encode()).hexdigest()[:12]
     cache = f"/tmp/plp_cache/{name}_{order}_{key}.npz"
     if os.path.exists(cache):
         try:

@@ -125,14 +125,34 @@ extern "C" plp_status plp_ctx_info(const plp_ctx* ctx, int* num_sms, int* max_ct
 static plp_status build_tiles(plp_graph* g, const int64_t* rp, const int32_t* col) {
   const int64_t n = g->n_rows;
   const int T = PLP_TILE_ROWS;
-  const int64_t nt = (n + T - 1) / T;
+  // Tile boundaries: T rows, halved while the tile would exceed the slot / external / nnz caps
+  // that keep two CTAs per SM for k = 8 (kTileMax* in plp_internal.h).
+  std::vector<int32_t> trow{0};
+  for (int64_t r0 = 0; r0 < n;) {
+    int64_t r1 = std::min<int64_t>(n, r0 + T);
+    for (;;) {
+      int64_t ni = 0, ne = 0;
+      for (int64_t i = r0; i < r1; ++i)
+        for (int64_t e = rp[i]; e < rp[i + 1]; ++e) {
+          const int64_t j = col[e];
+          if (j >= r0 && j < r1) ni += (j > i);
+          else ++ne;
+        }
+      const int64_t nz = rp[r1] - rp[r0];
+      if ((ni + ne <= kTileMaxSlots && ne <= kTileMaxExt && nz <= kTileMaxNnz) || r1 - r0 == 1) break;
+      r1 = r0 + (r1 - r0) / 2;
+    }
+    trow.push_back((int32_t)r1);
+    r0 = r1;
+  }
+  const int64_t nt = (int64_t)trow.size() - 1;
   std::vector<int32_t> enc((size_t)g->nnz + 16, 0);
   std::vector<int32_t> slot_of((size_t)g->nnz, -1);
   std::vector<int32_t> ext;
   std::vector<int4> meta((size_t)nt + 1);
   int max_slots = 0, max_nnz = 0, max_ext = 0;
   for (int64_t t = 0; t < nt; ++t) {
-    const int64_t r0 = t * T, r1 = std::min<int64_t>(n, r0 + T);
+    const int64_t r0 = trow[t], r1 = trow[t + 1];
     const int64_t e0 = rp[r0], e1 = rp[r1];
     int n_int = 0, n_ext = 0;
     const int ext_off = (int)ext.size();
@@ -176,7 +196,10 @@ static plp_status build_tiles(plp_graph* g, const int64_t* rp, const int32_t* co
   cudaError_t e;
   if ((e = cudaMalloc(&g->enc, sizeof(int32_t) * enc.size())) != cudaSuccess ||
       (e = cudaMalloc(&g->ext_col, sizeof(int32_t) * ext.size())) != cudaSuccess ||
-      (e = cudaMalloc(&g->tile_meta, sizeof(int4) * meta.size())) != cudaSuccess)
+      (e = cudaMalloc(&g->tile_meta, sizeof(int4) * meta.size())) != cudaSuccess ||
+      (e = cudaMalloc(&g->tile_row, sizeof(int32_t) * trow.size())) != cudaSuccess ||
+      (e = cudaMemcpy(g->tile_row, trow.data(), sizeof(int32_t) * trow.size(), cudaMemcpyHostToDevice)) !=
+          cudaSuccess)
     return cuda_check(e, "cudaMalloc(tiles)");
   if ((e = cudaMemcpy(g->enc, enc.data(), sizeof(int32_t) * enc.size(), cudaMemcpyHostToDevice)) !=
           cudaSuccess ||
@@ -278,6 +301,7 @@ extern "C" plp_status plp_destroy_graph(plp_graph* g) {
   cudaFree(g->enc);
   cudaFree(g->ext_col);
   cudaFree(g->tile_meta);
+  cudaFree(g->tile_row);
   delete g;
   return PLP_OK;
 }

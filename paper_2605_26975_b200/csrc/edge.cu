@@ -207,6 +207,7 @@ static EdgeArgs graph_args(const plp_graph* g) {
     a.enc = g->enc;
     a.ext_col = g->ext_col;
     a.tile_meta = g->tile_meta;
+    a.tile_row = g->tile_row;
     a.n_tiles = g->n_tiles;
     a.max_slots = g->max_slots;
     a.max_nnz = g->max_nnz;

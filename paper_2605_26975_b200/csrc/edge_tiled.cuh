@@ -188,8 +188,8 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) edge_tiled_kernel(EdgeArgs a,
     const int4 tm = __ldg(a.tile_meta + t);  // (e0, ext_off, n_int, n_ext)
     const int e0 = tm.x, e1 = __ldg(&a.tile_meta[t + 1].x);
     const int n_int = tm.z, n_slots = tm.z + tm.w;
-    const int64_t r0 = t * kTileRows;
-    const int nrows = (int)((a.n_rows - r0) < kTileRows ? (a.n_rows - r0) : kTileRows);
+    const int64_t r0 = __ldg(a.tile_row + t);
+    const int nrows = __ldg(a.tile_row + t + 1) - (int)r0;
     // staging offsets: bulk copies need 16-byte aligned global sources
     const int w_off = e0 & 1, c_off = e0 & 3, r_off = (int)(r0 & 3);
     // ---- stage the tile (one elected thread issues the TMA bulk copies) ----

@@ -46,12 +46,16 @@ struct plp_graph {
   int32_t* enc = nullptr;
   int32_t* ext_col = nullptr;
   int4* tile_meta = nullptr;
+  int32_t* tile_row = nullptr;  // first row of each tile (n_tiles + 1 entries)
   int64_t n_tiles = 0;
   int max_slots = 0;  // max over tiles of n_int + n_ext
   int max_nnz = 0;    // max over tiles of the tile's nnz
   int max_ext = 0;    // max over tiles of n_ext
 };
 constexpr int kSchedWindow = 2048;  // rows per degree-sorting window (stays L2-local)
+// Per-tile caps of the tiled kernel (a tile of PLP_TILE_ROWS rows is halved until it fits): with
+// k = 8 they keep the tile's shared memory under ~110 KB, i.e. two CTAs per SM.
+constexpr int kTileMaxSlots = 536, kTileMaxExt = 192, kTileMaxNnz = 992;
 
 namespace plp {
 
@@ -93,6 +97,7 @@ struct EdgeArgs {
   const int32_t* enc;
   const int32_t* ext_col;
   const int4* tile_meta;
+  const int32_t* tile_row;
   int64_t n_tiles;
   int max_slots, max_nnz, max_ext;
 };

@@ -44,7 +44,7 @@ SYMBOLS = [
     "plp_cholesky", "plp_apply_rinv", "plp_dot", "plp_axpby", "plp_gather_rows", "plp_kmeans",
     "plp_rcut", "plp_debug_pow", "plp_tile_order",
 ]
-TILE_ROWS = 128  # PLP_TILE_ROWS in include/plp.h
+TILE_ROWS = 120  # PLP_TILE_ROWS in include/plp.h
 
 
 class PlpError(RuntimeError):
