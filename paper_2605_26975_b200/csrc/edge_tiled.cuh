@@ -54,9 +54,21 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigne
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+__device__ __forceinline__ void l2_prefetch(const void* src, unsigned bytes) {  // bytes % 16 == 0
+  if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
 
 struct TiledLayout {
-  unsigned coef, ut, et, w, enc, rp, list, val, tab, total;
+  unsigned coef, ut, et, w, enc, rp, xc, list, val, tab, total;
 };
 __host__ __device__ inline unsigned align16u(unsigned x) { return (x + 15u) & ~15u; }
 // Shared-memory layout (byte offsets), identical on host and device.
@@ -70,6 +82,7 @@ __host__ __device__ inline TiledLayout tiled_layout(int k, int max_nnz, int max_
   L.w = o; o += align16u((max_nnz + 4) * 8);
   L.enc = o; o += align16u((max_nnz + 8) * 4);
   L.rp = o; o += align16u((kTileRows + 1 + 8) * 4);
+  L.xc = o; o += align16u((max_ext + 8) * 4);
   L.list = o; o += align16u(max_slots * 4 + 4);
   L.val = o;
   const unsigned vb = (unsigned)max_slots * k * 16;
@@ -152,6 +165,7 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) edge_tiled_kernel(EdgeArgs a,
   double* Wt = reinterpret_cast<double*>(sm + Ly.w);
   int32_t* Ct = reinterpret_cast<int32_t*>(sm + Ly.enc);
   int32_t* Rt = reinterpret_cast<int32_t*>(sm + Ly.rp);
+  int32_t* Xt = reinterpret_cast<int32_t*>(sm + Ly.xc);
   int32_t* list = reinterpret_cast<int32_t*>(sm + Ly.list);
   double2* val = reinterpret_cast<double2*>(sm + Ly.val);
   if constexpr (POW::kNeedsTables) pw.init_smem(sm + Ly.tab);
@@ -178,6 +192,9 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) edge_tiled_kernel(EdgeArgs a,
   const int G = blockDim.x / LPR;     // groups per CTA
   const int c0 = li * CPL;
   const bool active = c0 < k;
+  // active lanes of this lane's group (lanes li with li * CPL < k)
+  const int nact = (k + CPL - 1) / CPL < LPR ? (k + CPL - 1) / CPL : LPR;
+  const unsigned gmask = (nact >= 32 ? 0xFFFFFFFFu : ((1u << nact) - 1u)) << (lane - li);
 
   double accA[CPL], accB[CPL], accAl[CPL], accGa[CPL];
 #pragma unroll
@@ -190,8 +207,9 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) edge_tiled_kernel(EdgeArgs a,
     const int n_int = tm.z, n_slots = tm.z + tm.w;
     const int64_t r0 = __ldg(a.tile_row + t);
     const int nrows = __ldg(a.tile_row + t + 1) - (int)r0;
+    const int n_ext = tm.w;
     // staging offsets: bulk copies need 16-byte aligned global sources
-    const int w_off = e0 & 1, c_off = e0 & 3, r_off = (int)(r0 & 3);
+    const int w_off = e0 & 1, c_off = e0 & 3, r_off = (int)(r0 & 3), x_off = tm.y & 3;
     // ---- stage the tile (one elected thread issues the TMA bulk copies) ----
     if (threadIdx.x == 0) {
       fence_proxy_async();  // order earlier generic smem accesses before the async writes
@@ -199,17 +217,48 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) edge_tiled_kernel(EdgeArgs a,
       const unsigned bw = align16u((unsigned)(e1 - e0 + w_off) * 8);
       const unsigned bc = align16u((unsigned)(e1 - e0 + c_off) * 4);
       const unsigned br = align16u((unsigned)(nrows + 1 + r_off) * 4);
-      mbar_expect_tx(bar, bu * (HAS_ETA ? 2u : 1u) + bw + bc + br);
+      const unsigned bx = align16u((unsigned)(n_ext + x_off) * 4);
+      mbar_expect_tx(bar, bu * (HAS_ETA ? 2u : 1u) + bw + bc + br + bx);
       tma_bulk_g2s(Ut, a.U + r0 * k, bu, bar);
       if constexpr (HAS_ETA) tma_bulk_g2s(Et, a.eta + r0 * k, bu, bar);
       tma_bulk_g2s(Wt, a.w + (e0 - w_off), bw, bar);
       tma_bulk_g2s(Ct, a.enc + (e0 - c_off), bc, bar);
       tma_bulk_g2s(Rt, a.rp + (r0 - r_off), br, bar);
+      tma_bulk_g2s(Xt, a.ext_col + (tm.y - x_off), bx, bar);
     }
     mbar_wait(bar, parity);
     const double* W = Wt + w_off;
     const int32_t* C = Ct + c_off;
     const int32_t* R = Rt + r_off;
+    const int32_t* X = Xt + x_off;
+    // external rows U_j (into the first half of their slot's value area) and eta_j (into the tile's
+    // eta table, row T + x): asynchronous 16-byte copies, overlapped with phases 0 and 1a
+    {
+      const int half = k >> 1;  // 16-byte chunks per row
+      const int chunks = n_ext * (HAS_ETA ? k : half);
+      for (int ch = threadIdx.x; ch < chunks; ch += blockDim.x) {
+        const int x = ch / (HAS_ETA ? k : half);
+        const int part = ch - x * (HAS_ETA ? k : half);
+        const int64_t j = X[x];
+        if (part < half)
+          cp_async16(reinterpret_cast<double*>(val + (n_int + x) * k) + 2 * part, a.U + j * k + 2 * part);
+        else
+          cp_async16(Et + (kTileRows + x) * k + 2 * (part - half), a.eta + j * k + 2 * (part - half));
+      }
+      cp_async_commit();
+    }
+    // warm L2 with the CTA's next tile (its bulk copies then hit L2)
+    if (threadIdx.x == 32 && t + gridDim.x < a.n_tiles) {
+      const int64_t tn = t + gridDim.x;
+      const int4 nm = __ldg(a.tile_meta + tn);
+      const int ne1 = __ldg(&a.tile_meta[tn + 1].x);
+      const int64_t nr0 = __ldg(a.tile_row + tn);
+      const int nrn = __ldg(a.tile_row + tn + 1) - (int)nr0;
+      l2_prefetch(a.U + nr0 * k, (unsigned)(nrn * k * 8));
+      if constexpr (HAS_ETA) l2_prefetch(a.eta + nr0 * k, (unsigned)(nrn * k * 8));
+      l2_prefetch(a.w + (nm.x & ~1), align16u((unsigned)(ne1 - (nm.x & ~1)) * 8));
+      l2_prefetch(a.enc + (nm.x & ~3), align16u((unsigned)(ne1 - (nm.x & ~3)) * 4));
+    }
 
     // ---- phase 0: work list (slot -> row << 16 | edge) ----
     for (int rl = grp; rl < nrows; rl += G) {
@@ -246,20 +295,18 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) edge_tiled_kernel(EdgeArgs a,
           for (int c = 0; c < CPL; ++c) vs2[c] = out2[c];
         }
       }
-      // external edges: U_j, eta_j gathered from global memory (L2)
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    if (active) {
+      // external edges: U_j (first half of the slot's value area) and eta_j arrived asynchronously
       for (int s = n_int + grp; s < n_slots; s += G) {
         const int ent = list[s];
         const int q = ent & 0xFFFF;
-        const int x = s - n_int;
-        const int64_t j = __ldg(a.ext_col + tm.y + x);
         double ui[CPL], uj[CPL];
-        ld_vec<CPL>(a.U + j * k + c0, uj);
-        if constexpr (HAS_ETA) {
-          double ej[CPL];
-          ld_vec<CPL>(a.eta + j * k + c0, ej);
-          sts_vec<CPL>(Et + (kTileRows + x) * k + c0, ej);
-        }
+        lds_vec<CPL>(reinterpret_cast<const double*>(val + s * k) + c0, uj);
         lds_vec<CPL>(Ut + (ent >> 16) * k + c0, ui);
+        __syncwarp(gmask);  // every lane of the group has read U_j before the value overwrites it
         double2 out[CPL];
         slot_values<CPL>(pw, W[q], ui, uj, out);
         double2* vs = val + s * k + c0;
