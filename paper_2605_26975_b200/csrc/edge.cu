@@ -27,6 +27,9 @@ static P base_pol(double p, double eps) {
   pw.eps = eps;
   pw.eps_bits = __builtin_bit_cast(long long, eps);
   pw.fast_lo = __builtin_bit_cast(long long, std::fmax(eps, 0x1p-120));
+  const unsigned lo1 = (unsigned)(pw.fast_lo >> 32) + 1u;
+  pw.fast_lo2 = lo1 << 1;
+  pw.fast_span2 = (kHiMax - lo1) << 1;
   pw.q = p - 2.0;
   pw.pm1 = p - 1.0;
   pw.s_eps = std::pow(eps, p - 2.0);  // cap(a)^{p-2} for a < eps, as the oracle computes it

@@ -1,20 +1,24 @@
 // Tiled fused F / EucGrad / EucHessianEta edge kernel.
 //
-// The graph is cut into tiles of PLP_TILE_ROWS consecutive rows (compact graph regions after
-// plp_tile_order).  A persistent CTA loops over tiles:
-//   stage   one thread issues TMA bulk copies (cp.async.bulk, mbarrier completion) of the tile's
-//           contiguous U rows, eta rows, row_ptr, encoded columns and weights into shared memory;
-//   phase 0 every edge that owns a value slot adds itself to the tile's work list: each INTERNAL
-//           undirected edge (both ends in the tile) once, at its upper row, and each EXTERNAL edge;
-//   phase 1 flat, balanced sweeps over the work list compute the one power per edge-column:
-//             slot value (cL, wc) = (w phi_p(u_i - u_j), w cap(|u_i - u_j|)^{p-2})
-//           internal: U_j from shared memory; external: U_j and eta_j gathered from global memory
-//           (L2), eta_j kept in the tile's eta table at row T + x;
-//   phase 2 each row walks its CSR row in order (the oracle's order) and sums
-//             L_i  += cL  (sign flipped at the lower row of an internal edge: d is antisymmetric)
-//             HA_i += wc (eta_i - eta_j)
-//           then the row epilogue (node terms, G, Hv, partial sums of A, B, alpha, gamma).
-// Each internal undirected edge costs one power instead of two, and its U_j / eta_j come from
+// The graph is cut into tiles of <= PLP_TILE_ROWS consecutive rows (compact graph regions after
+// plp_tile_order; host-side caps keep a tile within the shared-memory budget).  A persistent CTA
+// loops over tiles:
+//   stage    one thread issues TMA bulk copies (cp.async.bulk, mbarrier completion) of the tile's
+//            contiguous U rows, eta rows, row_ptr, encoded columns, weights and external-column
+//            list into shared memory, and warms L2 with the CTA's next tile;
+//   gather   all threads start cp.async copies of the external rows U_j, eta_j into the value
+//            slots of the external edges (they land while phases 0 and 1a run);
+//   phase 0  every edge that owns a value slot adds itself to the tile's work list: each INTERNAL
+//            undirected edge (both ends in the tile) once, at its upper row, and each EXTERNAL edge;
+//   phase 1  flat, balanced sweeps over the work list compute the one power per edge-column and
+//            the slot value, from the upper row i's side (d = u_i - u_j):
+//              (cL, cH) = (w |d|^{p-2} d,  w cap(|d|)^{p-2} (eta_i - eta_j))
+//                       = (w phi_p(d),     the w~_ij (eta_i - eta_j) term of Alg. 1);
+//   phase 2  each row walks its CSR row in order (the oracle's order) and sums
+//              L_i += s cL,  HA_i += s cH,  s = -1 at the lower row of an internal edge (both
+//              terms are antisymmetric in (i, j)), +1 otherwise;
+//            then the row epilogue (node terms, G, Hv, partial sums of A, B, alpha, gamma).
+// Each internal undirected edge costs one power instead of two and its U_j / eta_j come from
 // shared memory, which takes most of the gather traffic off L2.  Every reduction is in a fixed
 // order: results are deterministic.
 #pragma once
@@ -73,12 +77,12 @@ struct TiledLayout {
 __host__ __device__ inline unsigned align16u(unsigned x) { return (x + 15u) & ~15u; }
 // Shared-memory layout (byte offsets), identical on host and device.
 __host__ __device__ inline TiledLayout tiled_layout(int k, int max_nnz, int max_slots, int max_ext,
-                                                     int cpl, bool tables) {
+                                                     int cpl, bool eta, bool tables) {
   TiledLayout L;
   unsigned o = 16;  // mbarrier
   L.coef = o; o += align16u(4 * k * 8);
   L.ut = o; o += align16u(kTileRows * k * 8);
-  L.et = o; o += align16u((kTileRows + max_ext) * k * 8);
+  L.et = o; o += eta ? align16u(kTileRows * k * 8) : 0u;
   L.w = o; o += align16u((max_nnz + 4) * 8);
   L.enc = o; o += align16u((max_nnz + 8) * 4);
   L.rp = o; o += align16u((kTileRows + 1 + 8) * 4);
@@ -108,48 +112,41 @@ __device__ __forceinline__ void lds_vec(const double* p, double (&v)[CPL]) {
     for (int c = 0; c < CPL; ++c) v[c] = p[c];
   }
 }
-template <int CPL>
-__device__ __forceinline__ void sts_vec(double* p, const double (&v)[CPL]) {
-  if constexpr (CPL % 2 == 0) {
-#pragma unroll
-    for (int c = 0; c < CPL; c += 2) *reinterpret_cast<double2*>(p + c) = make_double2(v[c], v[c + 1]);
-  } else {
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) p[c] = v[c];
-  }
-}
 
 // Exact slot value with libdevice powers (rare: |d| below the cap, a tie, or outside the fast
-// power domain): (w phi_p(d), w cap(|d|)^{p-2}).
+// power domain): (w phi_p(d), w cap(|d|)^{p-2} de).
 static __device__ __noinline__ double2 slot_exact(double d, double wv, double q, double pm1,
-                                                  double eps, double s_eps) {
+                                                  double eps, double s_eps, double de) {
   const double ad = fabs(d);
   const double cl = (ad != 0.0) ? wv * copysign(pow(ad, pm1), d) : 0.0;
   const double wc = (ad < eps) ? wv * s_eps : wv * pow(ad, q);
-  return make_double2(cl, wc);
+  return make_double2(cl, wc * de);
 }
 
-// Slot values of the lane's CPL columns for one edge (weight wv, d = ui - uj).
-template <int CPL, class POW>
+// Slot values (cL, cH) of the lane's CPL columns for one edge (weight wv, d = ui - uj,
+// de = ei - ej); branch-free except for the rare exact path.
+template <int CPL, class POW, bool HAS_ETA>
 __device__ __forceinline__ void slot_values(const POW& pw, double wv, const double (&ui)[CPL],
-                                            const double (&uj)[CPL], double2 (&out)[CPL]) {
+                                            const double (&uj)[CPL], const double (&ei)[CPL],
+                                            const double (&ej)[CPL], double2 (&out)[CPL]) {
   bool rare = false;
 #pragma unroll
   for (int c = 0; c < CPL; ++c) {
     const double d = ui[c] - uj[c];
+    const double de = HAS_ETA ? ei[c] - ej[c] : 0.0;
     if constexpr (POW::kIsP2) {
-      out[c] = make_double2(wv * d, wv);
+      out[c] = make_double2(wv * d, wv * de);
     } else {
-      unsigned unused = 0;
-      rare |= !pw.fast(d);
-      const double ws = wv * pw.pow_raw(d, unused);
-      out[c] = make_double2(ws * d, ws);
+      rare |= !pw.fast_hi(d);
+      const double ws = wv * pw.pow_fast(d);
+      out[c] = make_double2(ws * d, ws * de);
     }
   }
   if (rare) {
 #pragma unroll
     for (int c = 0; c < CPL; ++c)
-      out[c] = slot_exact(ui[c] - uj[c], wv, pw.q, pw.pm1, pw.eps, pw.s_eps);
+      out[c] = slot_exact(ui[c] - uj[c], wv, pw.q, pw.pm1, pw.eps, pw.s_eps,
+                          HAS_ETA ? ei[c] - ej[c] : 0.0);
   }
 }
 
@@ -157,7 +154,8 @@ template <int CPL, int LPR, int KT, class POW, bool HAS_ETA>
 __global__ void __launch_bounds__(kEdgeThreads, 2) edge_tiled_kernel(EdgeArgs a, POW pw) {
   extern __shared__ __align__(16) unsigned char sm[];
   const int k = KT ? KT : a.k;
-  const TiledLayout Ly = tiled_layout(k, a.max_nnz, a.max_slots, a.max_ext, CPL, POW::kNeedsTables);
+  const TiledLayout Ly =
+      tiled_layout(k, a.max_nnz, a.max_slots, a.max_ext, CPL, HAS_ETA, POW::kNeedsTables);
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm);
   double* coef = reinterpret_cast<double*>(sm + Ly.coef);  // [4][k]: p/B, A/B, p(p-1)/B, p(p-1)A/B^2
   double* Ut = reinterpret_cast<double*>(sm + Ly.ut);
@@ -204,10 +202,9 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) edge_tiled_kernel(EdgeArgs a,
   for (int64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x, parity ^= 1u) {
     const int4 tm = __ldg(a.tile_meta + t);  // (e0, ext_off, n_int, n_ext)
     const int e0 = tm.x, e1 = __ldg(&a.tile_meta[t + 1].x);
-    const int n_int = tm.z, n_slots = tm.z + tm.w;
+    const int n_int = tm.z, n_ext = tm.w, n_slots = tm.z + tm.w;
     const int64_t r0 = __ldg(a.tile_row + t);
     const int nrows = __ldg(a.tile_row + t + 1) - (int)r0;
-    const int n_ext = tm.w;
     // staging offsets: bulk copies need 16-byte aligned global sources
     const int w_off = e0 & 1, c_off = e0 & 3, r_off = (int)(r0 & 3), x_off = tm.y & 3;
     // ---- stage the tile (one elected thread issues the TMA bulk copies) ----
@@ -226,38 +223,34 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) edge_tiled_kernel(EdgeArgs a,
       tma_bulk_g2s(Rt, a.rp + (r0 - r_off), br, bar);
       tma_bulk_g2s(Xt, a.ext_col + (tm.y - x_off), bx, bar);
     }
+    // warm L2 with the CTA's next tile (its bulk copies then hit L2)
+    if (threadIdx.x == 32 && t + gridDim.x < a.n_tiles) {
+      const int64_t tn = t + gridDim.x;
+      const int ne0 = __ldg(&a.tile_meta[tn].x), ne1 = __ldg(&a.tile_meta[tn + 1].x);
+      const int64_t nr0 = __ldg(a.tile_row + tn);
+      const unsigned nb = (unsigned)((__ldg(a.tile_row + tn + 1) - (int)nr0) * k * 8);
+      l2_prefetch(a.U + nr0 * k, nb);
+      if constexpr (HAS_ETA) l2_prefetch(a.eta + nr0 * k, nb);
+      l2_prefetch(a.w + (ne0 & ~1), align16u((unsigned)(ne1 - (ne0 & ~1)) * 8));
+      l2_prefetch(a.enc + (ne0 & ~3), align16u((unsigned)(ne1 - (ne0 & ~3)) * 4));
+    }
     mbar_wait(bar, parity);
     const double* W = Wt + w_off;
     const int32_t* C = Ct + c_off;
     const int32_t* R = Rt + r_off;
     const int32_t* X = Xt + x_off;
-    // external rows U_j (into the first half of their slot's value area) and eta_j (into the tile's
-    // eta table, row T + x): asynchronous 16-byte copies, overlapped with phases 0 and 1a
+    // ---- gather: external rows U_j, eta_j into the two halves of slot n_int + x's value area ----
     {
       const int half = k >> 1;  // 16-byte chunks per row
-      const int chunks = n_ext * (HAS_ETA ? k : half);
-      for (int ch = threadIdx.x; ch < chunks; ch += blockDim.x) {
-        const int x = ch / (HAS_ETA ? k : half);
-        const int part = ch - x * (HAS_ETA ? k : half);
+      const int per = HAS_ETA ? k : half;
+      for (int ch = threadIdx.x; ch < n_ext * per; ch += blockDim.x) {
+        const int x = ch / per, part = ch - x * per;
         const int64_t j = X[x];
-        if (part < half)
-          cp_async16(reinterpret_cast<double*>(val + (n_int + x) * k) + 2 * part, a.U + j * k + 2 * part);
-        else
-          cp_async16(Et + (kTileRows + x) * k + 2 * (part - half), a.eta + j * k + 2 * (part - half));
+        double* dst = reinterpret_cast<double*>(val + (n_int + x) * k);
+        if (part < half) cp_async16(dst + 2 * part, a.U + j * k + 2 * part);
+        else cp_async16(dst + k + 2 * (part - half), a.eta + j * k + 2 * (part - half));
       }
       cp_async_commit();
-    }
-    // warm L2 with the CTA's next tile (its bulk copies then hit L2)
-    if (threadIdx.x == 32 && t + gridDim.x < a.n_tiles) {
-      const int64_t tn = t + gridDim.x;
-      const int4 nm = __ldg(a.tile_meta + tn);
-      const int ne1 = __ldg(&a.tile_meta[tn + 1].x);
-      const int64_t nr0 = __ldg(a.tile_row + tn);
-      const int nrn = __ldg(a.tile_row + tn + 1) - (int)nr0;
-      l2_prefetch(a.U + nr0 * k, (unsigned)(nrn * k * 8));
-      if constexpr (HAS_ETA) l2_prefetch(a.eta + nr0 * k, (unsigned)(nrn * k * 8));
-      l2_prefetch(a.w + (nm.x & ~1), align16u((unsigned)(ne1 - (nm.x & ~1)) * 8));
-      l2_prefetch(a.enc + (nm.x & ~3), align16u((unsigned)(ne1 - (nm.x & ~3)) * 4));
     }
 
     // ---- phase 0: work list (slot -> row << 16 | edge) ----
@@ -270,45 +263,44 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) edge_tiled_kernel(EdgeArgs a,
     }
     __syncthreads();
 
-    // ---- phase 1: one power per listed edge-column ----
+    // ---- phase 1a: internal undirected edges (U, eta of both ends in shared memory) ----
     if (active) {
-      // internal undirected edges, two slots per step for ILP
-      for (int s = grp; s < n_int; s += 2 * G) {
-        const int s2 = s + G;
-        const bool two = s2 < n_int;
-        const int ent = list[s], ent2 = list[two ? s2 : s];
-        const int q = ent & 0xFFFF, q2 = ent2 & 0xFFFF;
-        double ui[CPL], uj[CPL], ui2[CPL], uj2[CPL];
-        lds_vec<CPL>(Ut + (ent >> 16) * k + c0, ui);
-        lds_vec<CPL>(Ut + ((C[q] >> 16) & 0x7FFF) * k + c0, uj);
-        lds_vec<CPL>(Ut + (ent2 >> 16) * k + c0, ui2);
-        lds_vec<CPL>(Ut + ((C[q2] >> 16) & 0x7FFF) * k + c0, uj2);
-        double2 out[CPL], out2[CPL];
-        slot_values<CPL>(pw, W[q], ui, uj, out);
-        slot_values<CPL>(pw, W[q2], ui2, uj2, out2);
+      for (int s = grp; s < n_int; s += G) {
+        const int ent = list[s];
+        const int rl = ent >> 16, q = ent & 0xFFFF;
+        const int jl = (C[q] >> 16) & 0x7FFF;
+        double ui[CPL], uj[CPL], ei[CPL] = {}, ej[CPL] = {};
+        lds_vec<CPL>(Ut + rl * k + c0, ui);
+        lds_vec<CPL>(Ut + jl * k + c0, uj);
+        if constexpr (HAS_ETA) {
+          lds_vec<CPL>(Et + rl * k + c0, ei);
+          lds_vec<CPL>(Et + jl * k + c0, ej);
+        }
+        double2 out[CPL];
+        slot_values<CPL, POW, HAS_ETA>(pw, W[q], ui, uj, ei, ej, out);
         double2* vs = val + s * k + c0;
 #pragma unroll
         for (int c = 0; c < CPL; ++c) vs[c] = out[c];
-        if (two) {
-          double2* vs2 = val + s2 * k + c0;
-#pragma unroll
-          for (int c = 0; c < CPL; ++c) vs2[c] = out2[c];
-        }
       }
     }
     cp_async_wait_all();
     __syncthreads();
+    // ---- phase 1b: external edges (U_j, eta_j arrived asynchronously) ----
     if (active) {
-      // external edges: U_j (first half of the slot's value area) and eta_j arrived asynchronously
       for (int s = n_int + grp; s < n_slots; s += G) {
         const int ent = list[s];
-        const int q = ent & 0xFFFF;
-        double ui[CPL], uj[CPL];
-        lds_vec<CPL>(reinterpret_cast<const double*>(val + s * k) + c0, uj);
-        lds_vec<CPL>(Ut + (ent >> 16) * k + c0, ui);
-        __syncwarp(gmask);  // every lane of the group has read U_j before the value overwrites it
+        const int rl = ent >> 16, q = ent & 0xFFFF;
+        const double* xr = reinterpret_cast<const double*>(val + s * k);  // [U_j | eta_j]
+        double ui[CPL], uj[CPL], ei[CPL] = {}, ej[CPL] = {};
+        lds_vec<CPL>(Ut + rl * k + c0, ui);
+        lds_vec<CPL>(xr + c0, uj);
+        if constexpr (HAS_ETA) {
+          lds_vec<CPL>(Et + rl * k + c0, ei);
+          lds_vec<CPL>(xr + k + c0, ej);
+        }
+        __syncwarp(gmask);  // the whole group has read U_j, eta_j before the value overwrites them
         double2 out[CPL];
-        slot_values<CPL>(pw, W[q], ui, uj, out);
+        slot_values<CPL, POW, HAS_ETA>(pw, W[q], ui, uj, ei, ej, out);
         double2* vs = val + s * k + c0;
 #pragma unroll
         for (int c = 0; c < CPL; ++c) vs[c] = out[c];
@@ -328,14 +320,12 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) edge_tiled_kernel(EdgeArgs a,
         for (int q = b; q < e; ++q) {
           const int c = C[q];
           const double2* vs = val + (c & 0xFFFF) * k + c0;
-          const int flip = c & 0x80000000;  // the lower row of an internal edge gets -cL
-          double ej[CPL];
-          if constexpr (HAS_ETA) lds_vec<CPL>(Et + ((c >> 16) & 0x7FFF) * k + c0, ej);
+          const double sg = c < 0 ? -1.0 : 1.0;  // lower row of an internal edge
 #pragma unroll
           for (int c2 = 0; c2 < CPL; ++c2) {
             const double2 v = vs[c2];
-            L[c2] += __hiloint2double(__double2hiint(v.x) ^ flip, __double2loint(v.x));
-            if constexpr (HAS_ETA) HA[c2] = fma(v.y, ei[c2] - ej[c2], HA[c2]);
+            L[c2] = fma(sg, v.x, L[c2]);
+            if constexpr (HAS_ETA) HA[c2] = fma(sg, v.y, HA[c2]);
           }
         }
         const int64_t row = r0 + rl;
@@ -390,10 +380,11 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) edge_tiled_kernel(EdgeArgs a,
   }
 }
 
-template <int LPR, int KT, class POW, bool HAS_ETA>
+template <int CPL, int LPR, int KT, class POW, bool HAS_ETA>
 plp_status launch_tiled_shape(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int* grid_out) {
-  auto kern = edge_tiled_kernel<2, LPR, KT, POW, HAS_ETA>;
-  const TiledLayout Ly = tiled_layout(a.k, a.max_nnz, a.max_slots, a.max_ext, 2, POW::kNeedsTables);
+  auto kern = edge_tiled_kernel<CPL, LPR, KT, POW, HAS_ETA>;
+  const TiledLayout Ly =
+      tiled_layout(a.k, a.max_nnz, a.max_slots, a.max_ext, CPL, HAS_ETA, POW::kNeedsTables);
   static int attr_set = 0;
   static int occ = 1;
   if (attr_set < (int)Ly.total) {
@@ -412,6 +403,10 @@ plp_status launch_tiled_shape(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, in
   return PLP_OK;
 }
 
+#ifndef PLP_TILED_CPL
+#define PLP_TILED_CPL 4  // columns per lane at k % 4 == 0 (tools/tune_edge.py)
+#endif
+
 // Launches the tiled kernel when the graph is tiled, k is even (16-byte column pairs), the dense
 // arrays are 16-byte aligned and the tile fits in shared memory; *used = false otherwise.
 template <class POW>
@@ -423,21 +418,26 @@ plp_status try_launch_tiled(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int*
   if (force_rows || a.enc == nullptr || k % 2 != 0 || !al16(a.U) || (a.eta && !al16(a.eta)) ||
       (a.G && !al16(a.G)) || (a.Hv && !al16(a.Hv)))
     return PLP_OK;
-  const TiledLayout Ly = tiled_layout(k, a.max_nnz, a.max_slots, a.max_ext, 2, POW::kNeedsTables);
+  const TiledLayout Ly =
+      tiled_layout(k, a.max_nnz, a.max_slots, a.max_ext, 4, a.eta != nullptr, POW::kNeedsTables);
+  (void)Ly;
   if (Ly.total > 220u * 1024u) return PLP_OK;
   *used = true;
   const bool he = a.eta != nullptr;
   const int half = k / 2;
-#define PLP_TSHAPE(L, KT)                                                          \
-  return he ? launch_tiled_shape<L, KT, POW, true>(ctx, a, pw, grid)               \
-            : launch_tiled_shape<L, KT, POW, false>(ctx, a, pw, grid)
-  if (k == 2) PLP_TSHAPE(1, 2);
-  if (k == 4) PLP_TSHAPE(2, 4);
-  if (k == 8) PLP_TSHAPE(4, 8);
-  if (k == 16) PLP_TSHAPE(8, 16);
-  if (half <= 4) PLP_TSHAPE(4, 0);
-  if (half <= 8) PLP_TSHAPE(8, 0);
-  PLP_TSHAPE(16, 0);
+#define PLP_TSHAPE(C, L, KT)                                                          \
+  return he ? launch_tiled_shape<C, L, KT, POW, true>(ctx, a, pw, grid)               \
+            : launch_tiled_shape<C, L, KT, POW, false>(ctx, a, pw, grid)
+  if (k == 8) {
+    if constexpr (PLP_TILED_CPL == 4) PLP_TSHAPE(4, 2, 8);
+    else PLP_TSHAPE(2, 4, 8);
+  }
+  if (k == 2) PLP_TSHAPE(2, 1, 2);
+  if (k == 4) PLP_TSHAPE(2, 2, 4);
+  if (k == 16) PLP_TSHAPE(4, 4, 16);
+  if (half <= 4) PLP_TSHAPE(2, 4, 0);
+  if (half <= 8) PLP_TSHAPE(2, 8, 0);
+  PLP_TSHAPE(2, 16, 0);
 #undef PLP_TSHAPE
 }
 

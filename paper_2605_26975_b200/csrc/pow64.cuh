@@ -77,6 +77,8 @@ struct PowBase {
   double eps;          // curvature cap (> 0 when p < 2)
   long long eps_bits;  // bit pattern of eps (integer compare == value compare for >= 0)
   long long fast_lo;   // bit pattern of max(eps, 2^-120): |d| >= this (and < 2^120) is "fast"
+  unsigned fast_lo2;   // (hi(fast_lo) + 1) << 1: the conservative hi-word form used by fast_hi
+  unsigned fast_span2; // (kHiMax - (hi(fast_lo) + 1)) << 1
   double q;            // p - 2
   double pm1;          // p - 1
   double s_eps;        // eps^{p-2} (host glibc pow: the value the oracle's cap gives)
@@ -90,6 +92,12 @@ struct PowBase {
     const unsigned ahi = abs_hi(d);
     const unsigned long long a = ((unsigned long long)ahi << 32) | (unsigned)__double2loint(d);
     return (a >= (unsigned long long)fast_lo) & (ahi < kHiMax);
+  }
+  // Conservative two-instruction form of fast(): true only if |d| is in the fast domain (a |d|
+  // sharing its high word with the lower bound counts as not fast and takes the exact path).
+  __device__ __forceinline__ bool fast_hi(double d) const {
+    const unsigned h2 = (unsigned)__double2hiint(d) << 1;  // drops the sign bit
+    return h2 - fast_lo2 < fast_span2;
   }
   __device__ __forceinline__ bool abs_below_cap(double d) const {  // |d| < eps, integer pipe
     // compare (|hi|, lo) with eps's words; written on the words so the compiler cannot turn the
@@ -161,6 +169,20 @@ __device__ __forceinline__ void root_powers(double y, double& yD, double& yM) {
 template <int D, int M>
 struct PowRoot : PowCapped<PowRoot<D, M>> {
   static constexpr bool kNeedsTables = false;
+  // |d|^{-M/D}, valid on the fast domain only (no clamping: callers test fast_hi()); one IMAD
+  // turns the high word into the float seed argument (the shift drops the sign bit)
+  __device__ __forceinline__ double pow_fast(double d) const {
+    const float xf = __uint_as_float(((unsigned)__double2hiint(d) << 3) + 0x40000000u);
+    float yf;
+    if constexpr (D == 2) yf = rsqrt_approx(xf);
+    else yf = ex2_approx(lg2_approx(xf) * (-1.0f / (float)D));
+    const double y0 = f2d_exact(yf);
+    double yD, yM;
+    root_powers<D, M>(y0, yD, yM);
+    const double e = fma(-fabs(d), yD, 1.0);  // 1 - x y0^D
+    const double c = fma(this->c2, e, this->c1);
+    return fma(yM * e, c, yM);
+  }
   // |d|^{-M/D}; branch-free; sets `bad` outside the fast domain
   __device__ __forceinline__ double pow_raw(double d, unsigned& bad) const {
     const unsigned ahi = abs_hi(d);
@@ -189,6 +211,10 @@ struct PowGeneric : PowCapped<PowGeneric> {
     double* dst = reinterpret_cast<double*>(st);
     for (int i = threadIdx.x; i < (int)(sizeof(PowTables) / 8); i += blockDim.x) dst[i] = src[i];
     tab = st;
+  }
+  __device__ __forceinline__ double pow_fast(double d) const {
+    unsigned unused = 0;
+    return pow_raw(d, unused);
   }
   // |d|^{p-2}; branch-free; sets `bad` outside the fast domain
   __device__ __forceinline__ double pow_raw(double d, unsigned& bad) const {

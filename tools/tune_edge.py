@@ -14,13 +14,8 @@ sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "paper_2605_26975_b200", "variants")
 
 VARIANTS = {
-    "u4_b2": ["-DPLP_EDGE_UNR=4", "-DPLP_EDGE_MINB=2"],
-    "u2_b2": ["-DPLP_EDGE_UNR=2", "-DPLP_EDGE_MINB=2"],
-    "u2_b3": ["-DPLP_EDGE_UNR=2", "-DPLP_EDGE_MINB=3"],
-    "u4_b3": ["-DPLP_EDGE_UNR=4", "-DPLP_EDGE_MINB=3"],
-    "c4_u4_b2": ["-DPLP_EDGE_UNR=4", "-DPLP_EDGE_MINB=2", "-DPLP_EDGE_CPL4=1"],
-    "c4_u2_b2": ["-DPLP_EDGE_UNR=2", "-DPLP_EDGE_MINB=2", "-DPLP_EDGE_CPL4=1"],
-    "c4_u2_b3": ["-DPLP_EDGE_UNR=2", "-DPLP_EDGE_MINB=3", "-DPLP_EDGE_CPL4=1"],
+    "t_c4": [],
+    "t_c2": ["-DPLP_TILED_CPL=2"],
 }
 
 
