@@ -67,6 +67,9 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
+__device__ __forceinline__ void cp_async_wait_staged() {  // all but the most recent group
+  asm volatile("cp.async.wait_group 1;" ::: "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
@@ -81,15 +84,17 @@ __host__ __device__ inline TiledLayout tiled_layout(int k, int max_nnz, int max_
   TiledLayout L;
   unsigned o = 16;  // mbarrier
   L.coef = o; o += align16u(4 * k * 8);
-  L.ut = o; o += align16u(kTileRows * k * 8);
-  L.et = o; o += eta ? align16u(kTileRows * k * 8) : 0u;
+  // rows of U and eta are padded to k + 2 doubles and value slots to k + 1 double2: consecutive
+  // rows / slots then start on different banks (no shared-memory bank conflicts between groups)
+  L.ut = o; o += align16u(kTileRows * (k + 2) * 8);
+  L.et = o; o += eta ? align16u(kTileRows * (k + 2) * 8) : 0u;
   L.w = o; o += align16u((max_nnz + 4) * 8);
   L.enc = o; o += align16u((max_nnz + 8) * 4);
   L.rp = o; o += align16u((kTileRows + 1 + 8) * 4);
   L.xc = o; o += align16u((max_ext + 8) * 4);
   L.list = o; o += align16u(max_slots * 4 + 4);
   L.val = o;
-  const unsigned vb = (unsigned)max_slots * k * 16;
+  const unsigned vb = (unsigned)max_slots * (k + 1) * 16;
   const unsigned red = 4u * cpl * kEdgeThreads * 8;  // final CTA reduction reuses the value area
   o += align16u(vb > red ? vb : red);
   L.tab = o;
@@ -154,6 +159,8 @@ template <int CPL, int LPR, int KT, class POW, bool HAS_ETA>
 __global__ void __launch_bounds__(kEdgeThreads, 2) edge_tiled_kernel(EdgeArgs a, POW pw) {
   extern __shared__ __align__(16) unsigned char sm[];
   const int k = KT ? KT : a.k;
+  const int us = k + 2;   // padded smem row stride of U and eta (doubles)
+  const int vs1 = k + 1;  // padded value-slot stride (double2)
   const TiledLayout Ly =
       tiled_layout(k, a.max_nnz, a.max_slots, a.max_ext, CPL, HAS_ETA, POW::kNeedsTables);
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm);
@@ -207,17 +214,14 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) edge_tiled_kernel(EdgeArgs a,
     const int nrows = __ldg(a.tile_row + t + 1) - (int)r0;
     // staging offsets: bulk copies need 16-byte aligned global sources
     const int w_off = e0 & 1, c_off = e0 & 3, r_off = (int)(r0 & 3), x_off = tm.y & 3;
-    // ---- stage the tile (one elected thread issues the TMA bulk copies) ----
+    // ---- stage the tile: TMA bulk copies of the CSR pieces (one elected thread) ----
     if (threadIdx.x == 0) {
       fence_proxy_async();  // order earlier generic smem accesses before the async writes
-      const unsigned bu = (unsigned)(nrows * k * 8);
       const unsigned bw = align16u((unsigned)(e1 - e0 + w_off) * 8);
       const unsigned bc = align16u((unsigned)(e1 - e0 + c_off) * 4);
       const unsigned br = align16u((unsigned)(nrows + 1 + r_off) * 4);
       const unsigned bx = align16u((unsigned)(n_ext + x_off) * 4);
-      mbar_expect_tx(bar, bu * (HAS_ETA ? 2u : 1u) + bw + bc + br + bx);
-      tma_bulk_g2s(Ut, a.U + r0 * k, bu, bar);
-      if constexpr (HAS_ETA) tma_bulk_g2s(Et, a.eta + r0 * k, bu, bar);
+      mbar_expect_tx(bar, bw + bc + br + bx);
       tma_bulk_g2s(Wt, a.w + (e0 - w_off), bw, bar);
       tma_bulk_g2s(Ct, a.enc + (e0 - c_off), bc, bar);
       tma_bulk_g2s(Rt, a.rp + (r0 - r_off), br, bar);
@@ -234,6 +238,17 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) edge_tiled_kernel(EdgeArgs a,
       l2_prefetch(a.w + (ne0 & ~1), align16u((unsigned)(ne1 - (ne0 & ~1)) * 8));
       l2_prefetch(a.enc + (ne0 & ~3), align16u((unsigned)(ne1 - (ne0 & ~3)) * 4));
     }
+    // ---- stage U and eta rows into padded rows (cp.async, 16-byte chunks, all threads) ----
+    const int half = k >> 1;  // 16-byte chunks per row
+    {
+      const int per = HAS_ETA ? k : half;
+      for (int ch = threadIdx.x; ch < nrows * per; ch += blockDim.x) {
+        const int r = ch / per, part = ch - r * per;
+        if (part < half) cp_async16(Ut + r * us + 2 * part, a.U + (r0 + r) * k + 2 * part);
+        else cp_async16(Et + r * us + 2 * (part - half), a.eta + (r0 + r) * k + 2 * (part - half));
+      }
+      cp_async_commit();
+    }
     mbar_wait(bar, parity);
     const double* W = Wt + w_off;
     const int32_t* C = Ct + c_off;
@@ -241,12 +256,11 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) edge_tiled_kernel(EdgeArgs a,
     const int32_t* X = Xt + x_off;
     // ---- gather: external rows U_j, eta_j into the two halves of slot n_int + x's value area ----
     {
-      const int half = k >> 1;  // 16-byte chunks per row
       const int per = HAS_ETA ? k : half;
       for (int ch = threadIdx.x; ch < n_ext * per; ch += blockDim.x) {
         const int x = ch / per, part = ch - x * per;
         const int64_t j = X[x];
-        double* dst = reinterpret_cast<double*>(val + (n_int + x) * k);
+        double* dst = reinterpret_cast<double*>(val + (n_int + x) * vs1);
         if (part < half) cp_async16(dst + 2 * part, a.U + j * k + 2 * part);
         else cp_async16(dst + k + 2 * (part - half), a.eta + j * k + 2 * (part - half));
       }
@@ -261,6 +275,7 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) edge_tiled_kernel(EdgeArgs a,
         if (c >= 0) list[c & 0xFFFF] = (rl << 16) | q;  // slot owner: internal upper or external
       }
     }
+    cp_async_wait_staged();  // U, eta rows of the tile (the external gathers may still fly)
     __syncthreads();
 
     // ---- phase 1a: internal undirected edges (U, eta of both ends in shared memory) ----
@@ -270,15 +285,15 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) edge_tiled_kernel(EdgeArgs a,
         const int rl = ent >> 16, q = ent & 0xFFFF;
         const int jl = (C[q] >> 16) & 0x7FFF;
         double ui[CPL], uj[CPL], ei[CPL] = {}, ej[CPL] = {};
-        lds_vec<CPL>(Ut + rl * k + c0, ui);
-        lds_vec<CPL>(Ut + jl * k + c0, uj);
+        lds_vec<CPL>(Ut + rl * us + c0, ui);
+        lds_vec<CPL>(Ut + jl * us + c0, uj);
         if constexpr (HAS_ETA) {
-          lds_vec<CPL>(Et + rl * k + c0, ei);
-          lds_vec<CPL>(Et + jl * k + c0, ej);
+          lds_vec<CPL>(Et + rl * us + c0, ei);
+          lds_vec<CPL>(Et + jl * us + c0, ej);
         }
         double2 out[CPL];
         slot_values<CPL, POW, HAS_ETA>(pw, W[q], ui, uj, ei, ej, out);
-        double2* vs = val + s * k + c0;
+        double2* vs = val + s * vs1 + c0;
 #pragma unroll
         for (int c = 0; c < CPL; ++c) vs[c] = out[c];
       }
@@ -290,18 +305,18 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) edge_tiled_kernel(EdgeArgs a,
       for (int s = n_int + grp; s < n_slots; s += G) {
         const int ent = list[s];
         const int rl = ent >> 16, q = ent & 0xFFFF;
-        const double* xr = reinterpret_cast<const double*>(val + s * k);  // [U_j | eta_j]
+        const double* xr = reinterpret_cast<const double*>(val + s * vs1);  // [U_j | eta_j]
         double ui[CPL], uj[CPL], ei[CPL] = {}, ej[CPL] = {};
-        lds_vec<CPL>(Ut + rl * k + c0, ui);
+        lds_vec<CPL>(Ut + rl * us + c0, ui);
         lds_vec<CPL>(xr + c0, uj);
         if constexpr (HAS_ETA) {
-          lds_vec<CPL>(Et + rl * k + c0, ei);
+          lds_vec<CPL>(Et + rl * us + c0, ei);
           lds_vec<CPL>(xr + k + c0, ej);
         }
         __syncwarp(gmask);  // the whole group has read U_j, eta_j before the value overwrites them
         double2 out[CPL];
         slot_values<CPL, POW, HAS_ETA>(pw, W[q], ui, uj, ei, ej, out);
-        double2* vs = val + s * k + c0;
+        double2* vs = val + s * vs1 + c0;
 #pragma unroll
         for (int c = 0; c < CPL; ++c) vs[c] = out[c];
       }
@@ -313,13 +328,13 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) edge_tiled_kernel(EdgeArgs a,
       for (int rl = grp; rl < nrows; rl += G) {
         const int b = R[rl] - e0, e = R[rl + 1] - e0;
         double ui[CPL], ei[CPL], L[CPL], HA[CPL];
-        lds_vec<CPL>(Ut + rl * k + c0, ui);
-        if constexpr (HAS_ETA) lds_vec<CPL>(Et + rl * k + c0, ei);
+        lds_vec<CPL>(Ut + rl * us + c0, ui);
+        if constexpr (HAS_ETA) lds_vec<CPL>(Et + rl * us + c0, ei);
 #pragma unroll
         for (int c = 0; c < CPL; ++c) L[c] = HA[c] = 0.0;
         for (int q = b; q < e; ++q) {
           const int c = C[q];
-          const double2* vs = val + (c & 0xFFFF) * k + c0;
+          const double2* vs = val + (c & 0xFFFF) * vs1 + c0;
           const double sg = c < 0 ? -1.0 : 1.0;  // lower row of an internal edge
 #pragma unroll
           for (int c2 = 0; c2 < CPL; ++c2) {
