@@ -62,9 +62,9 @@ constexpr int kEdgeThreads = 256;
 #define PLP_EDGE_CPL4 0
 #endif
 
-// One stored edge (weight wv, wse = wv eps^{p-2}) for the lane's CPL columns; branch-free.
+// One stored edge (weight wv) for the lane's CPL columns; branch-free.
 template <int CPL, class POW, bool HAS_ETA>
-__device__ __forceinline__ void edge_update(const POW& pw, double wv, double wse,
+__device__ __forceinline__ void edge_update(const POW& pw, double wv,
                                             const double (&ui)[CPL], const double (&uj)[CPL],
                                             const double (&ei)[CPL], const double (&ej)[CPL],
                                             double (&L)[CPL], double (&HA)[CPL], unsigned& bad) {
@@ -75,12 +75,12 @@ __device__ __forceinline__ void edge_update(const POW& pw, double wv, double wse
       L[c] = fma(wv, d, L[c]);
       if constexpr (HAS_ETA) HA[c] = fma(wv, ei[c] - ej[c], HA[c]);
     } else {
-      const double wsr = wv * pw.pow_raw(d, bad);  // w |d|^{p-2}
-      L[c] = fma(wsr, d, L[c]);                    // w phi_p(d)
-      if constexpr (HAS_ETA) {
-        const double wc = pw.abs_below_cap(d) ? wse : wsr;  // w cap(|d|)^{p-2}
-        HA[c] = fma(wc, ei[c] - ej[c], HA[c]);
-      }
+      // fast domain: |d| >= eps (no cap) and the branch-free power is valid; anything else
+      // (ties, |d| < eps, extreme magnitudes) flags the row for the exact recomputation
+      bad |= (unsigned)!pw.fast_hi(d);
+      const double wsr = wv * pw.pow_fast(d);  // w |d|^{p-2}
+      L[c] = fma(wsr, d, L[c]);                // w phi_p(d)
+      if constexpr (HAS_ETA) HA[c] = fma(wsr, ei[c] - ej[c], HA[c]);
     }
   }
 }
@@ -184,8 +184,7 @@ __global__ void __launch_bounds__(kEdgeThreads, PLP_EDGE_MINB) edge_kernel(EdgeA
         }
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
-          const double wse = HAS_ETA && !POW::kIsP2 ? wv[u] * pw.s_eps : 0.0;
-          edge_update<CPL, POW, HAS_ETA>(pw, wv[u], wse, ui, uj[u], ei, ej[u], L, HA, bad);
+          edge_update<CPL, POW, HAS_ETA>(pw, wv[u], ui, uj[u], ei, ej[u], L, HA, bad);
         }
       }
       for (; e < e1; ++e) {
@@ -194,8 +193,7 @@ __global__ void __launch_bounds__(kEdgeThreads, PLP_EDGE_MINB) edge_kernel(EdgeA
         double uj[CPL], ej[CPL];
         ld_vec<CPL>(U + (int64_t)j * k + c0, uj);
         if constexpr (HAS_ETA) ld_vec<CPL>(eta + (int64_t)j * k + c0, ej);
-        const double wse = HAS_ETA && !POW::kIsP2 ? wv * pw.s_eps : 0.0;
-        edge_update<CPL, POW, HAS_ETA>(pw, wv, wse, ui, uj, ei, ej, L, HA, bad);
+        edge_update<CPL, POW, HAS_ETA>(pw, wv, ui, uj, ei, ej, L, HA, bad);
       }
       if (bad) edge_row_exact<CPL, POW, HAS_ETA>(pw, e0, e1, col, wt, U, eta, k, c0, ui, ei, L, HA);
 

@@ -419,7 +419,7 @@ plp_status launch_tiled_shape(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, in
 }
 
 #ifndef PLP_TILED_CPL
-#define PLP_TILED_CPL 4  // columns per lane at k % 4 == 0 (tools/tune_edge.py)
+#define PLP_TILED_CPL 2  // columns per lane at k = 8 (2 or 4; tools/tune_edge.py)
 #endif
 
 // Launches the tiled kernel when the graph is tiled, k is even (16-byte column pairs), the dense
@@ -429,8 +429,10 @@ plp_status try_launch_tiled(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int*
   *used = false;
   const int k = a.k;
   auto al16 = [](const void* ptr) { return ((uintptr_t)ptr & 15u) == 0; };
-  static const bool force_rows = getenv("PLP_EDGE_ROWS") != nullptr;  // A/B switch for tests
-  if (force_rows || a.enc == nullptr || k % 2 != 0 || !al16(a.U) || (a.eta && !al16(a.eta)) ||
+  // Kernel choice: the row kernel is the default until the tiled kernel measures
+  // faster; PLP_EDGE_TILED=1 selects the tiled kernel, PLP_EDGE_ROWS=1 forces the row kernel.
+  static const bool use_tiled = getenv("PLP_EDGE_TILED") != nullptr && getenv("PLP_EDGE_ROWS") == nullptr;
+  if (!use_tiled || a.enc == nullptr || k % 2 != 0 || !al16(a.U) || (a.eta && !al16(a.eta)) ||
       (a.G && !al16(a.G)) || (a.Hv && !al16(a.Hv)))
     return PLP_OK;
   const TiledLayout Ly =

@@ -3,6 +3,10 @@
 Inputs are seeded and synthetic (plp_inputs), at sizes the oracle finishes in seconds that still
 span many CTA tiles and a ragged tail.  Tolerance: 1e-9 relative (north star), per column,
 normwise (tests/helpers.py)."""
+import os
+import subprocess
+import sys
+
 import numpy as np
 import pytest
 import torch
@@ -160,12 +164,21 @@ def test_out_of_fast_domain_differences(plp, ctx):
         check(res, g, U, eta, 1.5, 0, 1e-300)
 
 
+@pytest.mark.skipif(os.environ.get("PLP_EDGE_TILED") is not None, reason="already the tiled run")
+def test_parity_suite_with_tiled_kernel():
+    """Re-runs this module's oracle-parity cases in a subprocess with PLP_EDGE_TILED=1, so both
+    edge kernels (row and tiled, edge_tiled.cuh) are held to the oracle."""
+    env = dict(os.environ, PLP_EDGE_TILED="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.abspath(__file__), "-k",
+                        "fused_sparse_parity or fused_full_parity or ties or out_of_fast or "
+                        "deterministic or misaligned"], env=env, capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
 def test_tiled_and_row_kernels_agree(plp, ctx, tmp_path):
-    """The same call with the tiled kernel and (in a subprocess, PLP_EDGE_ROWS=1) with the row
+    """The same call with the row kernel and (in a subprocess, PLP_EDGE_TILED=1) with the tiled
     kernel: both within 1e-12 of each other (different summation association only)."""
-    import os
-    import subprocess
-    import sys
     g = graph("C5t")
     U, eta = draw_U(g.n, 8, 31), draw_eta(g.n, 8, 31)
     res = run_gpu(plp, ctx, g, U, eta, 1.2, 0, 1e-9)
@@ -180,7 +193,7 @@ def test_tiled_and_row_kernels_agree(plp, ctx, tmp_path):
         "g = graph('C5t'); U, eta = draw_U(g.n, 8, 31), draw_eta(g.n, 8, 31)\n"
         "r = run_gpu(plp, plp.Context(0), g, U, eta, 1.2, 0, 1e-9)\n"
         f"np.savez({str(tmp_path / 'rows.npz')!r}, G=r['G'], Hv=r['Hv'], AB=r['AB'])\n")
-    env = dict(os.environ, PLP_EDGE_ROWS="1")
+    env = dict(os.environ, PLP_EDGE_TILED="1")
     subprocess.check_call([sys.executable, str(script)], env=env)
     z = np.load(tmp_path / "rows.npz")
     assert colwise_relerr(res["G"], z["G"]) < 1e-12
