@@ -52,7 +52,9 @@ struct plp_graph {
   int max_nnz = 0;    // max over tiles of the tile's nnz
   int max_ext = 0;    // max over tiles of n_ext
 };
-constexpr int kSchedWindow = 2048;  // rows per degree-sorting window (stays L2-local)
+// rows per degree-sorting window: small enough that a CTA's rows per iteration stay contiguous
+// (neighbour rows of a tile-ordered graph then hit L1)
+constexpr int kSchedWindow = 32;
 // Per-tile caps of the tiled kernel (a tile of PLP_TILE_ROWS rows is halved until it fits): with
 // k = 8 they keep the tile's shared memory under ~110 KB, i.e. two CTAs per SM.
 constexpr int kTileMaxSlots = 536, kTileMaxExt = 192, kTileMaxNnz = 992;

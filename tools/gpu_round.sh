@@ -1,0 +1,27 @@
+#!/bin/bash
+# One GPU box session: tests, smoke, bench (plain), then the ncu launch list of the same bench
+# command and one full ncu capture of the edge kernel.  Outputs land in gpurun_out/.
+#   /usr/local/graft/bin/gpurun --timeout 2400 -- 'bash tools/gpu_round.sh [TAG]'
+set -u
+TAG=${1:-r01}
+OUT=gpurun_out
+mkdir -p $OUT
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/smi_$TAG.txt 2>&1
+python -m pytest tests -m gpu -q --timeout 1500 -p no:cacheprovider > $OUT/gpu_tests_$TAG.log 2>&1
+echo "TESTS_RC=$?" >> $OUT/gpu_tests_$TAG.log
+python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke_$TAG.log 2>&1
+echo "SMOKE_RC=$?" >> $OUT/smoke_$TAG.log
+python bench.py --steps 20 --warmup 5 > $OUT/bench_$TAG.json 2> $OUT/bench_$TAG.err
+echo "BENCH_RC=$?" >> $OUT/bench_$TAG.err
+python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_ref_$TAG.json 2> $OUT/bench_ref_$TAG.err
+# launch list of the bench command (cold, serialised: compare shares, not absolutes)
+python bench.py --steps 3 --warmup 3 --no-cpu > $OUT/bench_small_$TAG.json 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+    --log-file $OUT/launches_$TAG.csv python bench.py --steps 3 --warmup 3 --no-cpu \
+    > $OUT/ncu_launches_$TAG.log 2>&1
+echo "NCU_LAUNCHES_RC=$?" >> $OUT/ncu_launches_$TAG.log
+# full capture of the dominant kernel (edge pass) on the bench workload
+python tools/prof_edge.py --reps 3 > $OUT/prof_plain_$TAG.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:edge_ -s 1 -c 1 \
+    -o $OUT/prof_edge_$TAG python tools/prof_edge.py --reps 3 > $OUT/ncu_full_$TAG.log 2>&1
+echo "NCU_FULL_RC=$?" >> $OUT/ncu_full_$TAG.log
