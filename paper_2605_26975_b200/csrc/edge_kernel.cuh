@@ -154,10 +154,15 @@ __global__ void __launch_bounds__(kEdgeThreads, PLP_EDGE_MINB) edge_kernel(EdgeA
   const double* __restrict__ eta = a.eta;
 
   if (active) {
-    for (int64_t idx = (int64_t)blockIdx.x * rows_per_iter + warp * RPW + grp; idx < a.n_rows;
-         idx += (int64_t)gridDim.x * rows_per_iter) {
-      const int row = __ldg(sched + idx);
-      const int e0 = __ldg(rp + row), e1 = __ldg(rp + row + 1);
+    const int64_t stride = (int64_t)gridDim.x * rows_per_iter;
+    int64_t idx = (int64_t)blockIdx.x * rows_per_iter + warp * RPW + grp;
+    // software pipeline: the next row's schedule entry and row bounds are loaded one iteration
+    // ahead, so each row starts with its edge metadata already in flight
+    int row = idx < a.n_rows ? __ldg(sched + idx) : 0;
+    int e0 = idx < a.n_rows ? __ldg(rp + row) : 0, e1 = idx < a.n_rows ? __ldg(rp + row + 1) : 0;
+    for (; idx < a.n_rows; idx += stride) {
+      const int64_t idxn = idx + stride;
+      const int rown = idxn < a.n_rows ? __ldg(sched + idxn) : row;
       double ui[CPL], ei[CPL];
       ld_vec<CPL>(U + (int64_t)row * k + c0, ui);
       if constexpr (HAS_ETA) ld_vec<CPL>(eta + (int64_t)row * k + c0, ei);
@@ -165,16 +170,18 @@ __global__ void __launch_bounds__(kEdgeThreads, PLP_EDGE_MINB) edge_kernel(EdgeA
 #pragma unroll
       for (int c = 0; c < CPL; ++c) L[c] = HA[c] = 0.0;
 
+      // edges in batches of UNR; the last batch is padded with weight-0 copies of the first edge
       constexpr int UNR = (CPL <= 2) ? PLP_EDGE_UNR : (PLP_EDGE_UNR + 1) / 2;
       unsigned bad = 0;
-      int e = e0;
-      for (; e + UNR <= e1; e += UNR) {
+      const int jpad = e0 < e1 ? __ldg(col + e0) : row;
+      for (int e = e0; e < e1; e += UNR) {
         int j[UNR];
         double wv[UNR];
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
-          j[u] = __ldg(col + e + u);
-          wv[u] = __ldg(wt + e + u);
+          const bool v = e + u < e1;
+          j[u] = v ? __ldg(col + e + u) : jpad;
+          wv[u] = v ? __ldg(wt + e + u) : 0.0;
         }
         double uj[UNR][CPL], ej[UNR][CPL];
 #pragma unroll
@@ -187,14 +194,7 @@ __global__ void __launch_bounds__(kEdgeThreads, PLP_EDGE_MINB) edge_kernel(EdgeA
           edge_update<CPL, POW, HAS_ETA>(pw, wv[u], ui, uj[u], ei, ej[u], L, HA, bad);
         }
       }
-      for (; e < e1; ++e) {
-        const int j = __ldg(col + e);
-        const double wv = __ldg(wt + e);
-        double uj[CPL], ej[CPL];
-        ld_vec<CPL>(U + (int64_t)j * k + c0, uj);
-        if constexpr (HAS_ETA) ld_vec<CPL>(eta + (int64_t)j * k + c0, ej);
-        edge_update<CPL, POW, HAS_ETA>(pw, wv, ui, uj, ei, ej, L, HA, bad);
-      }
+      const int e0n = __ldg(rp + rown), e1n = __ldg(rp + rown + 1);
       if (bad) edge_row_exact<CPL, POW, HAS_ETA>(pw, e0, e1, col, wt, U, eta, k, c0, ui, ei, L, HA);
 
       // ---- row epilogue: node terms, outputs, partial sums ----
@@ -223,6 +223,9 @@ __global__ void __launch_bounds__(kEdgeThreads, PLP_EDGE_MINB) edge_kernel(EdgeA
           for (int c = 0; c < CPL; ++c) accGa[c] = fma(g[c], ei[c], accGa[c]);
         }
       }
+      row = rown;
+      e0 = e0n;
+      e1 = e1n;
     }
   }
 

@@ -22,6 +22,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
 echo "NCU_LAUNCHES_RC=$?" >> $OUT/ncu_launches_$TAG.log
 # full capture of the dominant kernel (edge pass) on the bench workload
 python tools/prof_edge.py --reps 3 > $OUT/prof_plain_$TAG.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:edge_ -s 1 -c 1 \
+ncu --set full --clock-control none --import-source on -k "regex:edge_(kernel|tiled_kernel)" -s 1 -c 1 \
     -o $OUT/prof_edge_$TAG python tools/prof_edge.py --reps 3 > $OUT/ncu_full_$TAG.log 2>&1
 echo "NCU_FULL_RC=$?" >> $OUT/ncu_full_$TAG.log

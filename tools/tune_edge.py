@@ -14,8 +14,10 @@ sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "paper_2605_26975_b200", "variants")
 
 VARIANTS = {
-    "t_c4": [],
-    "t_c2": ["-DPLP_TILED_CPL=2"],
+    "r_u4": ["-DPLP_EDGE_UNR=4"],
+    "r_u6": ["-DPLP_EDGE_UNR=6"],
+    "r_u8": ["-DPLP_EDGE_UNR=8"],
+    "r_u8_b1": ["-DPLP_EDGE_UNR=8", "-DPLP_EDGE_MINB=1"],
 }
 
 
