@@ -278,7 +278,7 @@ def run_plp(args, rank, world):
             except Exception:
                 traffic = None
         roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                "traffic": traffic, "kernel": "edge_kernel<2,4,PowRoot<5>,eta>",
+                "traffic": traffic, "kernel": plp.last_edge_kernel(),
                 "kernel_ms": kms, "algorithmic_bytes": byts, "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"}
 
     # ---- end to end through the public API: pinned host inputs in, results out, every step ----

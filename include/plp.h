@@ -233,6 +233,12 @@ plp_status plp_rcut(plp_ctx* ctx, const plp_graph* g, int clusters, const int32_
 plp_status plp_debug_pow(plp_ctx* ctx, int64_t n, const double* a, double p, double eps, double* s,
                          double* t);
 
+/* Name and template shape of the last edge kernel this process launched (any context), e.g.
+ * "edge_staged_kernel<K=8,CPL=4,LPR=2,UNR=1,pow=R5M4,eta=1>"; "" before the first launch.  The
+ * pointer refers to a static buffer, valid until the next edge launch.  Diagnostics only (the
+ * bench reports which kernel its roofline figure belongs to; tests check the dispatch). */
+const char* plp_last_edge_kernel(void);
+
 #ifdef __cplusplus
 }
 #endif

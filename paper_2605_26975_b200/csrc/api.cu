@@ -56,7 +56,15 @@ static void fill_pow_tables(PowTables* t) {
 using namespace plp;
 
 extern "C" const char* plp_last_error(void) { return g_err; }
-extern "C" const char* plp_version(void) { return "libplp 0.1 (sm_100a)"; }
+extern "C" const char* plp_version(void) { return "libplp 0.2 (sm_100a)"; }
+
+static char g_last_edge_kernel[160] = "";
+void plp::note_edge_kernel(const char* family, int kc, int cpl, int lpr, int unr, const char* pow,
+                           int eta) {
+  snprintf(g_last_edge_kernel, sizeof(g_last_edge_kernel), "%s<K=%d,CPL=%d,LPR=%d,UNR=%d,pow=%s,eta=%d>",
+           family, kc, cpl, lpr, unr, pow, eta);
+}
+extern "C" const char* plp_last_edge_kernel(void) { return g_last_edge_kernel; }
 
 extern "C" plp_status plp_ctx_create(int device, void* stream, plp_ctx** out) {
   if (!out) return set_error(PLP_ERR_ARG, "out is null");
@@ -243,7 +251,12 @@ extern "C" plp_status plp_create_graph(plp_ctx* ctx, int64_t n_rows, int64_t n_c
   // Row schedule: within windows of kSchedWindow consecutive rows, rows by decreasing degree
   // (stable), so that the row groups of one warp see near-equal degrees (no divergence) while
   // the window keeps the U_j gathers L2-local.  Row results do not depend on it.
-  std::vector<int32_t> sched((size_t)(n_rows > 0 ? n_rows : 1));
+  // (+16 entries: the staged kernel's bulk copies round the schedule slice up to 16 bytes)
+  std::vector<int32_t> sched((size_t)n_rows + 16, 0);
+  for (int64_t c0 = 0; c0 < n_rows; c0 += kSchedWindow) {
+    const int64_t c1 = std::min<int64_t>(n_rows, c0 + kSchedWindow);
+    g->max_chunk_nnz = std::max<int>(g->max_chunk_nnz, rp32[c1] - rp32[c0]);
+  }
   for (int64_t w0 = 0; w0 < n_rows; w0 += kSchedWindow) {
     const int64_t w1 = std::min<int64_t>(n_rows, w0 + kSchedWindow);
     for (int64_t i = w0; i < w1; ++i) sched[i] = (int32_t)i;

@@ -1,6 +1,7 @@
 // C-ABI entry points of the edge path: F_p, EucGrad, EucHessianEta, the
 // full-mode epilogue (a6) and RCut (a12).  Kernels: edge_kernel.cuh; power policies: pow64.cuh.
 #include <cmath>
+#include <cstdlib>
 
 #include "edge_inst.cuh"
 #include "plp_internal.h"
@@ -206,6 +207,8 @@ static EdgeArgs graph_args(const plp_graph* g) {
   a.sched = g->sched;
   a.col = g->col;
   a.w = g->w;
+  a.max_chunk_nnz = g->max_chunk_nnz;
+  if (const char* v = getenv("PLP_DEBUG_LDX")) a.ldx = atoi(v);  // layout experiments only
   if (g->tiled) {
     a.enc = g->enc;
     a.ext_col = g->ext_col;

@@ -21,11 +21,23 @@
 #include "plp_internal.h"
 #include "pow64.cuh"
 
+#ifndef PLP_LD256
+#define PLP_LD256 1  // 256-bit gathers for 4-column lanes
+#endif
+
 namespace plp {
 
 template <int CPL>
 __device__ __forceinline__ void ld_vec(const double* __restrict__ p, double (&v)[CPL]) {
-  if constexpr (CPL % 2 == 0) {
+  if constexpr (CPL % 4 == 0 && PLP_LD256) {
+    // 256-bit loads (LDG.E.ENL2.256 on sm_100a): a 4-column lane segment in one request (the
+    // launchers select CPL = 4 only for 32-byte aligned arrays)
+#pragma unroll
+    for (int c = 0; c < CPL; c += 4)
+      asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                   : "=d"(v[c]), "=d"(v[c + 1]), "=d"(v[c + 2]), "=d"(v[c + 3])
+                   : "l"(p + c));
+  } else if constexpr (CPL % 2 == 0) {
 #pragma unroll
     for (int c = 0; c < CPL; c += 2) {
       const double2 t = __ldg(reinterpret_cast<const double2*>(p + c));
@@ -40,7 +52,13 @@ __device__ __forceinline__ void ld_vec(const double* __restrict__ p, double (&v)
 
 template <int CPL>
 __device__ __forceinline__ void st_vec(double* __restrict__ p, const double (&v)[CPL]) {
-  if constexpr (CPL % 2 == 0) {
+  if constexpr (CPL % 4 == 0) {
+#pragma unroll
+    for (int c = 0; c < CPL; c += 4)
+      asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p + c), "d"(v[c]), "d"(v[c + 1]),
+                   "d"(v[c + 2]), "d"(v[c + 3])
+                   : "memory");
+  } else if constexpr (CPL % 2 == 0) {
 #pragma unroll
     for (int c = 0; c < CPL; c += 2) *reinterpret_cast<double2*>(p + c) = make_double2(v[c], v[c + 1]);
   } else {
@@ -273,6 +291,8 @@ plp_status launch_edge_shape(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int
   if (need < grid) grid = (int)(need > 0 ? need : 1);
   kern<<<grid, kEdgeThreads, smem, ctx->stream>>>(a, pw);
   PLP_LAUNCH_CHECK("edge_kernel");
+  note_edge_kernel("edge_kernel", 0, CPL, LPR, (CPL <= 2) ? PLP_EDGE_UNR : (PLP_EDGE_UNR + 1) / 2,
+                   POW::kName, HAS_ETA);
   *grid_out = grid;
   return PLP_OK;
 }

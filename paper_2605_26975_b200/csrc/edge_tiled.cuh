@@ -24,55 +24,13 @@
 #pragma once
 #include <cstdlib>
 
+#include "async_copy.cuh"
 #include "edge_kernel.cuh"
+#include "edge_staged.cuh"
 
 namespace plp {
 
 constexpr int kTileRows = PLP_TILE_ROWS;
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void l2_prefetch(const void* src, unsigned bytes) {  // bytes % 16 == 0
-  if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void cp_async_wait_staged() {  // all but the most recent group
-  asm volatile("cp.async.wait_group 1;" ::: "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-}
 
 struct TiledLayout {
   unsigned coef, ut, et, w, enc, rp, xc, list, val, tab, total;
@@ -414,6 +372,7 @@ plp_status launch_tiled_shape(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, in
   if (grid > a.n_tiles) grid = a.n_tiles > 0 ? a.n_tiles : 1;
   kern<<<(int)grid, kEdgeThreads, Ly.total, ctx->stream>>>(a, pw);
   PLP_LAUNCH_CHECK("edge_tiled_kernel");
+  note_edge_kernel("edge_tiled_kernel", KT, CPL, LPR, 1, POW::kName, HAS_ETA);
   *grid_out = (int)grid;
   return PLP_OK;
 }
@@ -458,13 +417,22 @@ plp_status try_launch_tiled(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int*
 #undef PLP_TSHAPE
 }
 
-// Edge-pass entry for one power policy: the tiled kernel when it applies, else the row kernel.
+// Edge-pass entry for one power policy: the staged row kernel by default;
+// PLP_EDGE_TILED=1 selects the tiled kernel (where it applies), PLP_EDGE_ROWS=1 the unstaged row
+// kernel (both kept for comparison measurements).
 template <class POW>
 plp_status launch_edge_any(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int* grid) {
+#ifdef PLP_TUNE_ONLY  // tuning builds (tools/tune_edge.py): the staged kernel's k = 8 shape only
+  if (a.k != 8) return set_error(PLP_ERR_ARG, "tuning build: k = 8 only");
+  return launch_staged_pow(ctx, a, pw, grid);
+#else
   bool used = false;
   plp_status st = try_launch_tiled(ctx, a, pw, grid, &used);
   if (st || used) return st;
-  return launch_edge_pow(ctx, a, pw, grid);
+  static const bool rows = getenv("PLP_EDGE_ROWS") != nullptr;
+  if (rows) return launch_edge_pow(ctx, a, pw, grid);
+  return launch_staged_pow(ctx, a, pw, grid);
+#endif
 }
 
 }  // namespace plp

@@ -51,6 +51,7 @@ struct plp_graph {
   int max_slots = 0;  // max over tiles of n_int + n_ext
   int max_nnz = 0;    // max over tiles of the tile's nnz
   int max_ext = 0;    // max over tiles of n_ext
+  int max_chunk_nnz = 0;  // max nnz over chunks of kSchedWindow rows (staged kernel ring slots)
 };
 // rows per degree-sorting window: small enough that a CTA's rows per iteration stay contiguous
 // (neighbour rows of a tile-ordered graph then hit L1)
@@ -77,6 +78,8 @@ plp_status cuda_check(cudaError_t e, const char* what);
   } while (0)
 
 plp_status check_p(double p, double eps);
+// records the last launched edge kernel's name (plp_last_edge_kernel)
+void note_edge_kernel(const char* family, int kc, int cpl, int lpr, int unr, const char* pow, int eta);
 plp_status check_k(int k);
 
 // Edge kernel launcher (edge.cu).
@@ -102,6 +105,9 @@ struct EdgeArgs {
   const int32_t* tile_row;
   int64_t n_tiles;
   int max_slots, max_nnz, max_ext;
+  // staged kernel (edge_staged.cuh): largest chunk nnz of the graph, ring slot capacity
+  int max_chunk_nnz, chunk_cap;
+  int ldx;  // row stride (elements) of U and eta in the staged kernel; 0 = k (contiguous)
 };
 plp_status launch_edge(plp_ctx* ctx, const EdgeArgs& a, int* grid_out);
 // Fixed-order reduction of edge partials: AB_out (2k), dots_out (2k), F (1); any may be null.

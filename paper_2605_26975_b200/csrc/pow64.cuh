@@ -109,6 +109,7 @@ struct PowBase {
 };
 
 struct PowP2 : PowBase {
+  static constexpr const char* kName = "P2";
   static constexpr bool kNeedsTables = false;
   static constexpr bool kIsP2 = true;
   __device__ __forceinline__ double pow_raw(double, unsigned&) const { return 1.0; }
@@ -168,6 +169,8 @@ __device__ __forceinline__ void root_powers(double y, double& yD, double& yM) {
 
 template <int D, int M>
 struct PowRoot : PowCapped<PowRoot<D, M>> {
+  static constexpr const char* kName = D == 2 ? "R2M1" : D == 5 ? (M == 1 ? "R5M1" : M == 2 ? "R5M2" : M == 3 ? "R5M3" : "R5M4")
+                                     : (M == 1 ? "R10M1" : M == 3 ? "R10M3" : M == 7 ? "R10M7" : "R10M9");
   static constexpr bool kNeedsTables = false;
   // |d|^{-M/D}, valid on the fast domain only (no clamping: callers test fast_hi()); one IMAD
   // turns the high word into the float seed argument (the shift drops the sign bit)
@@ -201,6 +204,7 @@ struct PowRoot : PowCapped<PowRoot<D, M>> {
 };
 
 struct PowGeneric : PowCapped<PowGeneric> {
+  static constexpr const char* kName = "GEN";
   static constexpr bool kNeedsTables = true;
   double q64;             // 64 (p - 2)
   const PowTables* gtab;  // global copy

@@ -29,6 +29,7 @@ VALIDATE, VALIDATE_SYMMETRIC = 1, 2
 
 _lib.plp_last_error.restype = ctypes.c_char_p
 _lib.plp_version.restype = ctypes.c_char_p
+_lib.plp_last_edge_kernel.restype = ctypes.c_char_p
 
 C_I64 = ctypes.c_int64
 C_D = ctypes.c_double
@@ -42,9 +43,14 @@ SYMBOLS = [
     "plp_hessvec", "plp_fgrad_hessvec", "plp_edge_pass", "plp_full_epilogue",
     "plp_objective_from_ab", "plp_gram", "plp_project", "plp_apply_sub", "plp_retract",
     "plp_cholesky", "plp_apply_rinv", "plp_dot", "plp_axpby", "plp_gather_rows", "plp_kmeans",
-    "plp_rcut", "plp_debug_pow", "plp_tile_order",
+    "plp_rcut", "plp_debug_pow", "plp_tile_order", "plp_last_edge_kernel",
 ]
 TILE_ROWS = 120  # PLP_TILE_ROWS in include/plp.h
+
+
+def last_edge_kernel() -> str:
+    """plp_last_edge_kernel(): the last edge kernel launched (diagnostics)."""
+    return _lib.plp_last_edge_kernel().decode()
 
 
 class PlpError(RuntimeError):

@@ -164,25 +164,36 @@ def test_out_of_fast_domain_differences(plp, ctx):
         check(res, g, U, eta, 1.5, 0, 1e-300)
 
 
-@pytest.mark.skipif(os.environ.get("PLP_EDGE_TILED") is not None, reason="already the tiled run")
-def test_parity_suite_with_tiled_kernel():
-    """Re-runs this module's oracle-parity cases in a subprocess with PLP_EDGE_TILED=1, so both
-    edge kernels (row and tiled, edge_tiled.cuh) are held to the oracle."""
-    env = dict(os.environ, PLP_EDGE_TILED="1")
+ALT_KERNELS = {"tiled": "PLP_EDGE_TILED", "rows": "PLP_EDGE_ROWS"}
+
+
+@pytest.mark.parametrize("kernel", sorted(ALT_KERNELS))
+def test_parity_suite_with_alternative_kernel(kernel):
+    """Re-runs this module's oracle-parity cases in a subprocess with the tiled kernel
+    (PLP_EDGE_TILED=1, edge_tiled.cuh) or the unstaged row kernel (PLP_EDGE_ROWS=1,
+    edge_kernel.cuh), so every edge kernel, not only the default staged one, is held to the
+    oracle."""
+    if any(os.environ.get(v) for v in ALT_KERNELS.values()):
+        pytest.skip("already an alternative-kernel run")
+    env = dict(os.environ, **{ALT_KERNELS[kernel]: "1"})
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
                         os.path.abspath(__file__), "-k",
                         "fused_sparse_parity or fused_full_parity or ties or out_of_fast or "
-                        "deterministic or misaligned"], env=env, capture_output=True, text=True)
+                        "deterministic or misaligned or chunk_fallback"], env=env, capture_output=True,
+                       text=True)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
-def test_tiled_and_row_kernels_agree(plp, ctx, tmp_path):
-    """The same call with the row kernel and (in a subprocess, PLP_EDGE_TILED=1) with the tiled
-    kernel: both within 1e-12 of each other (different summation association only)."""
+@pytest.mark.parametrize("kernel", sorted(ALT_KERNELS))
+def test_default_and_alternative_kernels_agree(plp, ctx, tmp_path, kernel):
+    """The same call with the default (staged) kernel and, in a subprocess, with the tiled or
+    the unstaged row kernel: within 1e-12 of each other (summation association only)."""
+    if any(os.environ.get(v) for v in ALT_KERNELS.values()):
+        pytest.skip("already an alternative-kernel run")
     g = graph("C5t")
     U, eta = draw_U(g.n, 8, 31), draw_eta(g.n, 8, 31)
     res = run_gpu(plp, ctx, g, U, eta, 1.2, 0, 1e-9)
-    script = tmp_path / "rows.py"
+    script = tmp_path / "alt.py"
     script.write_text(
         "import sys, numpy as np, torch\n"
         f"sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})\n"
@@ -192,13 +203,34 @@ def test_tiled_and_row_kernels_agree(plp, ctx, tmp_path):
         "from plp_inputs import draw_U, draw_eta\n"
         "g = graph('C5t'); U, eta = draw_U(g.n, 8, 31), draw_eta(g.n, 8, 31)\n"
         "r = run_gpu(plp, plp.Context(0), g, U, eta, 1.2, 0, 1e-9)\n"
-        f"np.savez({str(tmp_path / 'rows.npz')!r}, G=r['G'], Hv=r['Hv'], AB=r['AB'])\n")
-    env = dict(os.environ, PLP_EDGE_TILED="1")
+        f"np.savez({str(tmp_path / 'alt.npz')!r}, G=r['G'], Hv=r['Hv'], AB=r['AB'])\n")
+    env = dict(os.environ, **{ALT_KERNELS[kernel]: "1"})
     subprocess.check_call([sys.executable, str(script)], env=env)
-    z = np.load(tmp_path / "rows.npz")
+    z = np.load(tmp_path / "alt.npz")
     assert colwise_relerr(res["G"], z["G"]) < 1e-12
     assert colwise_relerr(res["Hv"], z["Hv"]) < 1e-12
     assert scalar_relerr(res["AB"], z["AB"]) < 1e-12
+
+
+@pytest.mark.parametrize("k", [8, 4, 6])
+def test_chunk_fallback_high_degree(plp, ctx, k):
+    """Rows of degree ~150 (a chunk of 32 rows then exceeds the staged kernel's shared-memory slot,
+    so those chunks read col / w from global memory) mixed with low-degree rows (staged chunks):
+    both paths against the oracle."""
+    rng = streams(77)[0]
+    n = 4000
+    pairs = set()
+    for i in range(n):
+        deg = 150 if (i // 32) % 3 == 0 else 4
+        for j in rng.integers(0, n, size=deg // 2):
+            if j != i:
+                pairs.add((min(i, int(j)), max(i, int(j))))
+    ij = np.array(sorted(pairs))
+    w = rng.uniform(0.1, 1.0, size=len(ij))
+    g = csr_from_undirected(n, ij[:, 0], ij[:, 1], w, name="hub")
+    U, eta = draw_U(g.n, k, 9), draw_eta(g.n, k, 9)
+    res = run_gpu(plp, ctx, g, U, eta, 1.2, 0, 1e-9)
+    check(res, g, U, eta, 1.2, 0, 1e-9)
 
 
 def test_misaligned_views_use_scalar_path(plp, ctx):

@@ -5,6 +5,7 @@
 Variants land in paper_2605_26975_b200/variants/<name>/libplp.so (git-ignored, travel with gpurun).
 """
 import json
+import shutil
 import os
 import subprocess
 import sys
@@ -14,10 +15,13 @@ sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "paper_2605_26975_b200", "variants")
 
 VARIANTS = {
-    "r_u4": ["-DPLP_EDGE_UNR=4"],
-    "r_u6": ["-DPLP_EDGE_UNR=6"],
-    "r_u8": ["-DPLP_EDGE_UNR=8"],
-    "r_u8_b1": ["-DPLP_EDGE_UNR=8", "-DPLP_EDGE_MINB=1"],
+    "c4_ct_256": ["-DPLP_STAGED_CPL8=4", "-DPLP_STAGED_UNR=2", "-DPLP_STAGED_CONTIG=1", "-DPLP_LD256=1"],
+    "c4_ct_128": ["-DPLP_STAGED_CPL8=4", "-DPLP_STAGED_UNR=2", "-DPLP_STAGED_CONTIG=1", "-DPLP_LD256=0"],
+    "c4_il_256": ["-DPLP_STAGED_CPL8=4", "-DPLP_STAGED_UNR=2", "-DPLP_STAGED_CONTIG=0", "-DPLP_LD256=1"],
+    "c4_il_128": ["-DPLP_STAGED_CPL8=4", "-DPLP_STAGED_UNR=2", "-DPLP_STAGED_CONTIG=0", "-DPLP_LD256=0"],
+    "c2_ct": ["-DPLP_STAGED_CPL8=2", "-DPLP_STAGED_UNR=2", "-DPLP_STAGED_CONTIG=1"],
+    "c2_ct_u4": ["-DPLP_STAGED_CPL8=2", "-DPLP_STAGED_UNR=4", "-DPLP_STAGED_CONTIG=1"],
+    "c2_il": ["-DPLP_STAGED_CPL8=2", "-DPLP_STAGED_UNR=2", "-DPLP_STAGED_CONTIG=0"],
 }
 
 
@@ -26,7 +30,8 @@ def build(names):
     for name in names:
         d = os.path.join(VDIR, name)
         os.makedirs(d, exist_ok=True)
-        b(obj_dir=os.path.join(d, "obj"), lib=os.path.join(d, "libplp.so"), extra=VARIANTS[name])
+        b(obj_dir=os.path.join(d, "obj"), lib=os.path.join(d, "libplp.so"), extra=VARIANTS[name] + ["-DPLP_TUNE_ONLY"])
+        shutil.rmtree(os.path.join(d, "obj"), ignore_errors=True)
         print("built", name, flush=True)
 
 
