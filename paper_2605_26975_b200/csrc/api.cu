@@ -224,6 +224,65 @@ static plp_status build_tiles(plp_graph* g, const int64_t* rp, const int32_t* co
   return PLP_OK;
 }
 
+// Halo tiles for edge_halo.cuh (see plp_graph): per tile of PLP_HALO_TILE consecutive rows its
+// sorted distinct outside columns, and per stored edge the tile-local neighbour index.  Skipped
+// (nullptr halo_enc) when a tile's buffers could not fit in shared memory even at k = 8.
+static plp_status build_halo_tiles(plp_graph* g, const int64_t* rp, const int32_t* col) {
+  const int64_t n = g->n_rows;
+  const int T = PLP_HALO_TILE;
+  const int64_t nt = (n + T - 1) / T;
+  if (nt == 0) return PLP_OK;
+  std::vector<int64_t> xoff((size_t)nt + 1, 0);
+  std::vector<int32_t> xs;
+  int max_ext = 0, max_nnz = 0;
+  std::vector<int32_t> tmp;
+  for (int64_t t = 0; t < nt; ++t) {
+    const int64_t r0 = t * T, r1 = std::min<int64_t>(n, r0 + T);
+    tmp.clear();
+    for (int64_t e = rp[r0]; e < rp[r1]; ++e)
+      if (col[e] < r0 || col[e] >= r1) tmp.push_back(col[e]);
+    std::sort(tmp.begin(), tmp.end());
+    tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+    xs.insert(xs.end(), tmp.begin(), tmp.end());
+    xoff[t + 1] = (int64_t)xs.size();
+    max_ext = std::max<int>(max_ext, (int)tmp.size());
+    max_nnz = std::max<int64_t>(max_nnz, rp[r1] - rp[r0]);
+  }
+  const int ext_cap = (max_ext + 3) & ~3, nnz_cap = (max_nnz + 3) & ~3;
+  const double bytes_k8 = 2.0 * ((T + ext_cap) * 128.0 + nnz_cap * 12.0 + 4096.0);
+  if (bytes_k8 > 224.0 * 1024.0) return PLP_OK;
+  std::vector<int32_t> enc((size_t)g->nnz + 16, 0);
+  // per tile a slot of ext_cap + 4 ints: n_ext, rp[r0], rp[r1], 0, then the halo columns
+  const int64_t LS = ext_cap + 4;
+  std::vector<int32_t> ext((size_t)(nt * LS + 16), -1);
+  for (int64_t t = 0; t < nt; ++t) {
+    const int64_t r0 = t * T, r1 = std::min<int64_t>(n, r0 + T);
+    const int32_t* xb = xs.data() + xoff[t];
+    const int32_t* xe = xs.data() + xoff[t + 1];
+    ext[t * LS + 0] = (int32_t)(xe - xb);
+    ext[t * LS + 1] = (int32_t)rp[r0];
+    ext[t * LS + 2] = (int32_t)rp[r1];
+    ext[t * LS + 3] = 0;
+    std::copy(xb, xe, ext.begin() + t * LS + 4);
+    for (int64_t e = rp[r0]; e < rp[r1]; ++e) {
+      const int32_t j = col[e];
+      enc[e] = (j >= r0 && j < r1) ? (int32_t)(j - r0)
+                                   : (int32_t)(T + (std::lower_bound(xb, xe, j) - xb));
+    }
+  }
+  cudaError_t e;
+  if ((e = cudaMalloc(&g->halo_enc, sizeof(int32_t) * enc.size())) != cudaSuccess ||
+      (e = cudaMalloc(&g->halo_ext, sizeof(int32_t) * ext.size())) != cudaSuccess ||
+      (e = cudaMemcpy(g->halo_enc, enc.data(), sizeof(int32_t) * enc.size(), cudaMemcpyHostToDevice)) !=
+          cudaSuccess ||
+      (e = cudaMemcpy(g->halo_ext, ext.data(), sizeof(int32_t) * ext.size(), cudaMemcpyHostToDevice)) !=
+          cudaSuccess)
+    return cuda_check(e, "cudaMalloc/cudaMemcpy(halo tiles)");
+  g->halo_ext_cap = ext_cap;
+  g->halo_nnz_cap = nnz_cap;
+  return PLP_OK;
+}
+
 extern "C" plp_status plp_create_graph(plp_ctx* ctx, int64_t n_rows, int64_t n_cols,
                                        const int64_t* row_ptr, const int32_t* col, const double* w,
                                        uint32_t flags, plp_graph** out) {
@@ -288,6 +347,7 @@ extern "C" plp_status plp_create_graph(plp_ctx* ctx, int64_t n_rows, int64_t n_c
     return cuda_check(e, "cudaMemcpy(graph)");
   }
   plp_status st = build_tiles(g, row_ptr, col);
+  if (!st) st = build_halo_tiles(g, row_ptr, col);
   if (st) {
     plp_destroy_graph(g);
     return st;
@@ -311,6 +371,8 @@ extern "C" plp_status plp_destroy_graph(plp_graph* g) {
   cudaFree(g->col);
   cudaFree(g->w);
   cudaFree(g->sched);
+  cudaFree(g->halo_enc);
+  cudaFree(g->halo_ext);
   cudaFree(g->enc);
   cudaFree(g->ext_col);
   cudaFree(g->tile_meta);

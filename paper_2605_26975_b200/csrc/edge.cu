@@ -208,6 +208,10 @@ static EdgeArgs graph_args(const plp_graph* g) {
   a.col = g->col;
   a.w = g->w;
   a.max_chunk_nnz = g->max_chunk_nnz;
+  a.halo_enc = g->halo_enc;
+  a.halo_ext = g->halo_ext;
+  a.halo_ext_cap = g->halo_ext_cap;
+  a.halo_nnz_cap = g->halo_nnz_cap;
   if (const char* v = getenv("PLP_DEBUG_LDX")) a.ldx = atoi(v);  // layout experiments only
   if (g->tiled) {
     a.enc = g->enc;

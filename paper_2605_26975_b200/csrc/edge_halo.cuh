@@ -1,0 +1,337 @@
+// Halo-tile edge kernel: the fused F / EucGrad / EucHessianEta pass (
+// DESIGN.md §5) with every neighbour row served from shared memory.
+//
+// The rows are cut into tiles of kHaloT = 256 consecutive rows.  plp_create_graph lists, per tile,
+// the distinct columns outside it (the tile's halo, at most halo_ext_cap of them) and re-encodes
+// every stored edge as a tile-local index: j - r0 for an internal neighbour, kHaloT + x for the
+// x-th halo row.  One persistent CTA of 512 threads per SM walks the tiles (interleaved across
+// CTAs, so neighbouring tiles are in flight together and the halo rows hit L2), double-buffered:
+//   * thread 0 stages the tile's contiguous pieces with TMA bulk copies (cp.async.bulk + mbarrier):
+//     its own U / eta rows, row_ptr and schedule slices, (enc, w) ranges, and one tile ahead the
+//     halo list of the next-but-one tile (count, CSR bounds, columns);
+//   * all threads gather the halo rows U_j, eta_j with cp.async (16-byte pieces, 8 rows per warp
+//     instruction at k = 8, indices read from the staged list) after the own rows; each thread's
+//     cp.async.mbarrier.arrive joins the same "full" barrier as the TMA bytes;
+//   * while tile i is computed, tile i + 1 is resident and tile i + 2 is in flight.
+// Rows are processed as in the row kernels (one group of LPR lanes per row, CPL = 2 columns per
+// lane, CSR order per row, one power per stored edge-column), reading U_j / eta_j with LDS.128, so
+// the only global traffic is the streaming of the tile data and the G / Hv stores: the L2 no longer
+// serves ~128 bytes per edge.  Degree-sorted 32-row windows are split between warp pairs so the
+// warps of a tile get equal work (rank slices {0, 3} and {1, 2} of each window).
+#pragma once
+#include "async_copy.cuh"
+#include "edge_kernel.cuh"
+#include "edge_staged.cuh"
+
+namespace plp {
+
+constexpr int kHaloT = PLP_HALO_TILE;  // rows per tile (plp.h)
+constexpr int kHaloThreads = 512;
+constexpr int kHaloWarps = kHaloThreads / 32;
+static_assert(kHaloT == 8 * kSchedWindow && kHaloWarps == 2 * (kHaloT / kSchedWindow), "tile map");
+
+// Per-buffer shared-memory layout (bytes), identical on host and device.
+struct HaloLayout {
+  unsigned rp, sched, enc, w, U, E, bytes;
+};
+__host__ __device__ inline HaloLayout halo_layout(int k, int ext_cap, int nnz_cap) {
+  HaloLayout L;
+  unsigned o = 0;
+  L.rp = o; o += (kHaloT + 8) * 4;
+  L.sched = o; o += kHaloT * 4;
+  L.enc = o; o += (unsigned)(nnz_cap + 16) * 4;
+  o = (o + 15u) & ~15u;
+  L.w = o; o += (unsigned)(nnz_cap + 16) * 8;
+  L.U = o; o += (unsigned)(kHaloT + ext_cap) * (unsigned)k * 8u;
+  L.E = o; o += (unsigned)(kHaloT + ext_cap) * (unsigned)k * 8u;
+  L.bytes = (o + 127u) & ~127u;
+  return L;
+}
+constexpr unsigned kHaloHead = 256;  // mbarriers (full[2], list[3]); tables follow
+__host__ __device__ inline unsigned halo_tab_bytes(bool tables) {
+  return tables ? (unsigned)((sizeof(PowTables) + 127) & ~(size_t)127) : 0u;
+}
+__host__ __device__ inline unsigned halo_lists_off(bool tables) { return kHaloHead + halo_tab_bytes(tables); }
+__host__ __device__ inline unsigned halo_bufs_off(int ext_cap, bool tables) {
+  return (halo_lists_off(tables) + 3u * (unsigned)(ext_cap + 4) * 4u + 127u) & ~127u;
+}
+__host__ __device__ inline unsigned halo_smem_bytes(int k, int ext_cap, int nnz_cap, bool tables) {
+  return halo_bufs_off(ext_cap, tables) + 2u * halo_layout(k, ext_cap, nnz_cap).bytes;
+}
+constexpr unsigned kHaloSmemMax = 225u * 1024u;
+
+#ifndef PLP_HALO_CPL8
+#define PLP_HALO_CPL8 2  // columns per lane at k = 8 (2 or 4)
+#endif
+template <int K>
+constexpr int halo_cpl() { return K == 8 ? PLP_HALO_CPL8 : K == 16 ? 4 : 2; }
+
+template <int K, class POW, bool HAS_ETA>
+__global__ void __launch_bounds__(kHaloThreads, 1) edge_halo_kernel(EdgeArgs a, POW pw) {
+  constexpr int CPL = halo_cpl<K>(), LPR = K / CPL, RPW = 32 / LPR;  // rows per pass
+  constexpr int NS = kSchedWindow / RPW;               // rank slices per 32-row window
+  static_assert(NS % 2 == 0 || NS == 2, "slice count");
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [2] tile data landed
+  uint64_t* lbar = full + 2;                           // [3] halo list landed
+  if constexpr (POW::kNeedsTables) pw.init_smem(smem + kHaloHead);
+  const int ext_cap = a.halo_ext_cap;
+  const int LS = ext_cap + 4;  // list slot: n_ext, eb, ee, pad, columns
+  int* lists = reinterpret_cast<int*>(smem + halo_lists_off(POW::kNeedsTables));
+  const HaloLayout Ly = halo_layout(K, ext_cap, a.halo_nnz_cap);
+  unsigned char* buf0 = smem + halo_bufs_off(ext_cap, POW::kNeedsTables);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int grp = lane / LPR, li = lane % LPR, c0 = li * CPL;
+  if (tid == 0) {
+    // full: thread 0's arrive.expect_tx (TMA bytes) + one cp.async arrival per thread
+    mbar_init(&full[0], 1 + kHaloThreads);
+    mbar_init(&full[1], 1 + kHaloThreads);
+    for (int q = 0; q < 3; ++q) mbar_init(&lbar[q], 1);
+    fence_mbar_init();
+  }
+  const int n_rows = (int)a.n_rows;
+  const int64_t n_tiles = (a.n_rows + kHaloT - 1) / kHaloT;
+  const double p = a.p, pp1 = p * (p - 1.0);
+  double cG[CPL], cAB[CPL], cHA[CPL], cHB[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    cG[c] = cAB[c] = cHA[c] = cHB[c] = 0.0;
+    if (a.AB != nullptr) {
+      const double A = a.AB[c0 + c], B = a.AB[K + c0 + c];
+      cG[c] = p / B;
+      cAB[c] = A / B;
+      cHA[c] = pp1 / B;
+      cHB[c] = pp1 * A / (B * B);
+    }
+  }
+  double accA[CPL], accB[CPL], accAl[CPL], accGa[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) accA[c] = accB[c] = accAl[c] = accGa[c] = 0.0;
+  __syncthreads();
+
+  // (thread 0) stage the halo list of tile t into list slot q
+  auto issue_list = [&](int64_t t, int q) {
+    if (t >= n_tiles) return;
+    mbar_expect_tx(&lbar[q], (unsigned)LS * 4u);
+    tma_bulk_g2s(lists + q * LS, a.halo_ext + t * LS, (unsigned)LS * 4u, &lbar[q]);
+  };
+  // (all threads) stage tile t into buffer b; its halo list is in slot q (use parity lph)
+  auto issue_tile = [&](int64_t t, int b, int q, unsigned lph) {
+    if (t >= n_tiles) return;
+    unsigned char* B = buf0 + (size_t)b * Ly.bytes;
+    const int r0 = (int)(t * kHaloT), r1 = min(r0 + kHaloT, n_rows);
+    constexpr unsigned RB = K * 8u;  // bytes per row
+    mbar_wait(&lbar[q], lph);
+    const int* Lq = lists + q * LS;
+    const int nx = Lq[0];
+    if (tid == 0) {
+      const int eb = Lq[1], ee = Lq[2];
+      const unsigned rp_b = (unsigned)(((r1 + 1 + 3) & ~3) - r0) * 4u;
+      const unsigned sc_b = (unsigned)(((r1 + 3) & ~3) - r0) * 4u;
+      const int cb = eb & ~3, ce = (ee + 3) & ~3, wb = eb & ~1, we = (ee + 1) & ~1;
+      const unsigned enc_b = (unsigned)(ce - cb) * 4u, w_b = (unsigned)(we - wb) * 8u;
+      const unsigned own_b = (unsigned)(r1 - r0) * RB;
+      mbar_expect_tx(&full[b], rp_b + sc_b + enc_b + w_b + (HAS_ETA ? 2u : 1u) * own_b);
+      tma_bulk_g2s(B + Ly.rp, a.rp + r0, rp_b, &full[b]);
+      tma_bulk_g2s(B + Ly.sched, a.sched + r0, sc_b, &full[b]);
+      if (enc_b) {
+        tma_bulk_g2s(B + Ly.enc, a.halo_enc + cb, enc_b, &full[b]);
+        tma_bulk_g2s(B + Ly.w, a.w + wb, w_b, &full[b]);
+      }
+      tma_bulk_g2s(B + Ly.U, a.U + (int64_t)r0 * K, own_b, &full[b]);
+      if constexpr (HAS_ETA) tma_bulk_g2s(B + Ly.E, a.eta + (int64_t)r0 * K, own_b, &full[b]);
+    }
+    // halo rows: PPR lanes per row, 32 / PPR rows per warp instruction
+    constexpr int PPR = K / 2, RPI = 32 / PPR;
+    const int rl = lane / PPR, pc = lane % PPR;
+    for (int x = warp * RPI + rl; x < nx; x += kHaloWarps * RPI) {
+      const int j = Lq[4 + x];
+      const unsigned off = ((unsigned)(kHaloT + x) * K + 2 * pc) * 8u;
+      cp_async16(B + Ly.U + off, a.U + (int64_t)j * K + 2 * pc);
+      if constexpr (HAS_ETA) cp_async16(B + Ly.E + off, a.eta + (int64_t)j * K + 2 * pc);
+    }
+    cp_async_mbar_arrive(&full[b]);
+  };
+
+  const int64_t t0 = blockIdx.x, ts = gridDim.x;
+  if (tid == 0) {
+    issue_list(t0, 0);
+    issue_list(t0 + ts, 1);
+    issue_list(t0 + 2 * ts, 2);
+  }
+  issue_tile(t0, 0, 0, 0u);
+  issue_tile(t0 + ts, 1, 1, 0u);
+  const int h = warp & 1, win = warp >> 1;  // warp pair shares a 32-row window
+  for (int it = 0;; ++it) {
+    const int64_t t = t0 + (int64_t)it * ts;
+    if (t >= n_tiles) break;
+    const int b = it & 1;
+    mbar_wait(&full[b], (unsigned)(it >> 1) & 1u);  // tile t resident
+
+    const unsigned char* B = buf0 + (size_t)b * Ly.bytes;
+    const int* rp_s = reinterpret_cast<const int*>(B + Ly.rp);
+    const int* sc_s = reinterpret_cast<const int*>(B + Ly.sched);
+    const int r0 = (int)(t * kHaloT);
+    const int nr = min(kHaloT, n_rows - r0);
+    const int eb = rp_s[0];
+    const int* enc_s = reinterpret_cast<const int*>(B + Ly.enc) - (eb & ~3);
+    const double* w_s = reinterpret_cast<const double*>(B + Ly.w) - (eb & ~1);
+    const double* tU = reinterpret_cast<const double*>(B + Ly.U) + c0;
+    const double* tE = reinterpret_cast<const double*>(B + Ly.E) + c0;
+
+#pragma unroll 1
+    for (int sl = 0; sl < NS; ++sl) {
+      if ((NS == 2 ? sl : ((sl & 1) ^ ((sl >> 1) & 1))) != h) continue;
+      const int lr = win * kSchedWindow + sl * RPW + grp;  // position in the tile's schedule
+      if (lr >= nr) continue;
+      const int row = sc_s[lr];
+      const int lrow = row - r0;
+      const int e0 = rp_s[lrow], e1 = rp_s[lrow + 1];
+      double ui[CPL], ei[CPL];
+      lds_vec<CPL>(tU + lrow * K, ui);
+      if constexpr (HAS_ETA) lds_vec<CPL>(tE + lrow * K, ei);
+      double L[CPL], HA[CPL], sn[CPL], tn[CPL];
+      unsigned mx = 0;
+#pragma unroll
+      for (int cc = 0; cc < CPL; ++cc) {
+        L[cc] = HA[cc] = 0.0;
+        const double au = fabs(ui[cc]);
+        if constexpr (POW::kIsP2) {
+          sn[cc] = 1.0;
+          tn[cc] = au;
+        } else {
+          mx = max(mx, (unsigned)__double2hiint(au) * 2u - pw.fast_lo2);
+          sn[cc] = pw.pow_fast(au);
+          tn[cc] = sn[cc] * au;
+        }
+      }
+      // pairs of edges as straight-line code (the two dependency chains interleave), then the odd
+      // edge; summation order stays the CSR order
+      int e = e0;
+#pragma unroll 1
+      for (; e + 1 < e1; e += 2) {
+        const int x0 = enc_s[e], x1 = enc_s[e + 1];
+        const double w0 = w_s[e], w1 = w_s[e + 1];
+        double uj0[CPL], ej0[CPL], uj1[CPL], ej1[CPL];
+        lds_vec<CPL>(tU + x0 * K, uj0);
+        lds_vec<CPL>(tU + x1 * K, uj1);
+        if constexpr (HAS_ETA) {
+          lds_vec<CPL>(tE + x0 * K, ej0);
+          lds_vec<CPL>(tE + x1 * K, ej1);
+        }
+        edge_update_mx<CPL, POW, HAS_ETA>(pw, w0, ui, uj0, ei, ej0, L, HA, mx);
+        edge_update_mx<CPL, POW, HAS_ETA>(pw, w1, ui, uj1, ei, ej1, L, HA, mx);
+      }
+      if (e < e1) {
+        const int x0 = enc_s[e];
+        const double w0 = w_s[e];
+        double uj0[CPL], ej0[CPL];
+        lds_vec<CPL>(tU + x0 * K, uj0);
+        if constexpr (HAS_ETA) lds_vec<CPL>(tE + x0 * K, ej0);
+        edge_update_mx<CPL, POW, HAS_ETA>(pw, w0, ui, uj0, ei, ej0, L, HA, mx);
+      }
+      if constexpr (!POW::kIsP2) {
+        if (mx >= pw.fast_span2) {  // rare: exact libdevice recomputation of the row
+          edge_row_exact<CPL, POW, HAS_ETA>(pw, e0, e1, a.col, a.w, a.U, a.eta, K, c0, ui, ei, L, HA);
+#pragma unroll
+          for (int cc = 0; cc < CPL; ++cc) pw.eval(fabs(ui[cc]), sn[cc], tn[cc]);
+        }
+      }
+      double g[CPL], hv[CPL];
+#pragma unroll
+      for (int cc = 0; cc < CPL; ++cc) {
+        accA[cc] = fma(ui[cc], L[cc], accA[cc]);
+        accB[cc] = fma(tn[cc], fabs(ui[cc]), accB[cc]);
+        const double phi = copysign(tn[cc], ui[cc]);
+        g[cc] = cG[cc] * (L[cc] - cAB[cc] * phi);
+        if constexpr (HAS_ETA) {
+          hv[cc] = cHA[cc] * HA[cc] - cHB[cc] * sn[cc] * ei[cc];
+          if (a.want_dots) {
+            accAl[cc] = fma(p * phi, ei[cc], accAl[cc]);
+            accGa[cc] = fma(g[cc], ei[cc], accGa[cc]);
+          }
+        } else {
+          hv[cc] = 0.0;
+        }
+      }
+      if (a.G != nullptr) st_vec<CPL>(a.G + (int64_t)row * K + c0, g);
+      if constexpr (HAS_ETA) {
+        if (a.Hv != nullptr) st_vec<CPL>(a.Hv + (int64_t)row * K + c0, hv);
+      }
+    }
+    __syncthreads();  // buffer b is free
+    if (tid == 0) {
+      fence_proxy_async();  // generic reads of buffer b before its async refill
+      issue_list(t + 3 * ts, it % 3);  // slot of tile t's list (consumed when t was issued)
+    }
+    issue_tile(t + 2 * ts, b, (it + 2) % 3, (unsigned)((it + 2) / 3) & 1u);
+  }
+
+  // ---- fixed-order CTA reduction (reuses buffer 0: every issued copy has been consumed) ----
+  __syncthreads();
+  double* red = reinterpret_cast<double*>(buf0);  // [4][CPL][threads]
+#pragma unroll
+  for (int cc = 0; cc < CPL; ++cc) {
+    red[(0 * CPL + cc) * kHaloThreads + tid] = accA[cc];
+    red[(1 * CPL + cc) * kHaloThreads + tid] = accB[cc];
+    red[(2 * CPL + cc) * kHaloThreads + tid] = accAl[cc];
+    red[(3 * CPL + cc) * kHaloThreads + tid] = accGa[cc];
+  }
+  __syncthreads();
+  for (int tt = tid; tt < 4 * K; tt += kHaloThreads) {
+    const int q = tt / K, cl = tt % K;
+    const int l = cl / CPL, cc = cl % CPL;
+    const double* base = red + (q * CPL + cc) * kHaloThreads;
+    double sum = 0.0;
+    for (int th = l; th < kHaloThreads; th += LPR) sum += base[th];
+    a.partials[((int64_t)blockIdx.x * 4 + q) * K + cl] = sum;
+  }
+}
+
+template <int K, class POW, bool HAS_ETA>
+plp_status launch_halo_shape(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int* grid_out) {
+  auto kern = edge_halo_kernel<K, POW, HAS_ETA>;
+  const unsigned smem = halo_smem_bytes(K, a.halo_ext_cap, a.halo_nnz_cap, POW::kNeedsTables);
+  static unsigned attr_set = 0;
+  if (attr_set < smem) {
+    PLP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_set = smem;
+  }
+  const int64_t n_tiles = (a.n_rows + kHaloT - 1) / kHaloT;
+  int64_t grid = ctx->num_sms;
+  if (grid > ctx->max_ctas) grid = ctx->max_ctas;
+  if (grid > n_tiles) grid = n_tiles > 0 ? n_tiles : 1;
+  kern<<<(int)grid, kHaloThreads, smem, ctx->stream>>>(a, pw);
+  PLP_LAUNCH_CHECK("edge_halo_kernel");
+  note_edge_kernel("edge_halo_kernel", K, halo_cpl<K>(), K / halo_cpl<K>(), 2, POW::kName, HAS_ETA);
+  *grid_out = (int)grid;
+  return PLP_OK;
+}
+
+// The halo kernel applies when the graph has halo tiles, k is 4, 8 or 16, the dense arrays are
+// 16-byte aligned, U / eta are contiguous (ldx == k) and the buffers fit in shared memory.
+template <class POW>
+plp_status try_launch_halo(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int* grid, bool* used) {
+  *used = false;
+  const int k = a.k;
+  auto al16 = [](const void* ptr) { return ((uintptr_t)ptr & 15u) == 0; };
+  if (a.halo_enc == nullptr || (k != 4 && k != 8 && k != 16) || (a.ldx != 0 && a.ldx != k) ||
+      !al16(a.U) || (a.eta && !al16(a.eta)) || (a.G && !al16(a.G)) || (a.Hv && !al16(a.Hv)))
+    return PLP_OK;
+  if (halo_smem_bytes(k, a.halo_ext_cap, a.halo_nnz_cap, POW::kNeedsTables) > kHaloSmemMax) return PLP_OK;
+  *used = true;
+  const bool he = a.eta != nullptr;
+#define PLP_HSHAPE(K)                                                                      \
+  return he ? launch_halo_shape<K, POW, true>(ctx, a, pw, grid)                            \
+            : launch_halo_shape<K, POW, false>(ctx, a, pw, grid)
+#ifdef PLP_TUNE_ONLY
+  PLP_HSHAPE(8);
+#else
+  if (k == 4) PLP_HSHAPE(4);
+  if (k == 8) PLP_HSHAPE(8);
+  PLP_HSHAPE(16);
+#endif
+#undef PLP_HSHAPE
+}
+
+}  // namespace plp

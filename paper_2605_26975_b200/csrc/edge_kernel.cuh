@@ -51,6 +51,21 @@ __device__ __forceinline__ void ld_vec(const double* __restrict__ p, double (&v)
 }
 
 template <int CPL>
+__device__ __forceinline__ void lds_vec(const double* p, double (&v)[CPL]) {
+  if constexpr (CPL % 2 == 0) {
+#pragma unroll
+    for (int c = 0; c < CPL; c += 2) {
+      const double2 t = *reinterpret_cast<const double2*>(p + c);
+      v[c] = t.x;
+      v[c + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) v[c] = p[c];
+  }
+}
+
+template <int CPL>
 __device__ __forceinline__ void st_vec(double* __restrict__ p, const double (&v)[CPL]) {
   if constexpr (CPL % 4 == 0) {
 #pragma unroll

@@ -27,6 +27,7 @@
 #include "async_copy.cuh"
 #include "edge_kernel.cuh"
 #include "edge_staged.cuh"
+#include "edge_halo.cuh"
 
 namespace plp {
 
@@ -61,20 +62,6 @@ __host__ __device__ inline TiledLayout tiled_layout(int k, int max_nnz, int max_
   return L;
 }
 
-template <int CPL>
-__device__ __forceinline__ void lds_vec(const double* p, double (&v)[CPL]) {
-  if constexpr (CPL % 2 == 0) {
-#pragma unroll
-    for (int c = 0; c < CPL; c += 2) {
-      const double2 t = *reinterpret_cast<const double2*>(p + c);
-      v[c] = t.x;
-      v[c + 1] = t.y;
-    }
-  } else {
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) v[c] = p[c];
-  }
-}
 
 // Exact slot value with libdevice powers (rare: |d| below the cap, a tie, or outside the fast
 // power domain): (w phi_p(d), w cap(|d|)^{p-2} de).
@@ -417,13 +404,19 @@ plp_status try_launch_tiled(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int*
 #undef PLP_TSHAPE
 }
 
-// Edge-pass entry for one power policy: the staged row kernel by default;
-// PLP_EDGE_TILED=1 selects the tiled kernel (where it applies), PLP_EDGE_ROWS=1 the unstaged row
-// kernel (both kept for comparison measurements).
+// Edge-pass entry for one power policy: the halo-tile kernel where it applies, else
+// the staged row kernel; PLP_EDGE_STAGED=1 forces the staged kernel, PLP_EDGE_TILED=1 selects the
+// tiled kernel (where it applies), PLP_EDGE_ROWS=1 the unstaged row kernel (kept for comparison
+// measurements and parity tests).
 template <class POW>
 plp_status launch_edge_any(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int* grid) {
-#ifdef PLP_TUNE_ONLY  // tuning builds (tools/tune_edge.py): the staged kernel's k = 8 shape only
+#ifdef PLP_TUNE_ONLY  // tuning builds (tools/tune_edge.py): k = 8 halo or staged shapes only
   if (a.k != 8) return set_error(PLP_ERR_ARG, "tuning build: k = 8 only");
+  bool used_h = false;
+  if (getenv("PLP_EDGE_STAGED") == nullptr) {
+    plp_status sh = try_launch_halo(ctx, a, pw, grid, &used_h);
+    if (sh || used_h) return sh;
+  }
   return launch_staged_pow(ctx, a, pw, grid);
 #else
   bool used = false;
@@ -431,6 +424,11 @@ plp_status launch_edge_any(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int* 
   if (st || used) return st;
   static const bool rows = getenv("PLP_EDGE_ROWS") != nullptr;
   if (rows) return launch_edge_pow(ctx, a, pw, grid);
+  static const bool staged = getenv("PLP_EDGE_STAGED") != nullptr;
+  if (!staged) {
+    st = try_launch_halo(ctx, a, pw, grid, &used);
+    if (st || used) return st;
+  }
   return launch_staged_pow(ctx, a, pw, grid);
 #endif
 }

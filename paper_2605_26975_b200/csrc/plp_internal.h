@@ -52,6 +52,14 @@ struct plp_graph {
   int max_nnz = 0;    // max over tiles of the tile's nnz
   int max_ext = 0;    // max over tiles of n_ext
   int max_chunk_nnz = 0;  // max nnz over chunks of kSchedWindow rows (staged kernel ring slots)
+  // Halo tiles (edge_halo.cuh): tiles of PLP_HALO_TILE rows; per stored edge the tile-local index
+  // (j - r0 inside the tile, PLP_HALO_TILE + x for the x-th halo row); per tile a slot of
+  // halo_ext_cap + 4 ints at halo_ext[t * (halo_ext_cap + 4)]: n_ext, rp[r0], rp[r1], 0, then the
+  // halo columns (-1 padded).  nullptr halo_enc: no halo tiles.
+  int32_t* halo_enc = nullptr;
+  int32_t* halo_ext = nullptr;
+  int halo_ext_cap = 0;  // max halo rows per tile (rounded up to 4)
+  int halo_nnz_cap = 0;  // max stored edges per tile (rounded up to 4)
 };
 // rows per degree-sorting window: small enough that a CTA's rows per iteration stay contiguous
 // (neighbour rows of a tile-ordered graph then hit L1)
@@ -108,6 +116,10 @@ struct EdgeArgs {
   // staged kernel (edge_staged.cuh): largest chunk nnz of the graph, ring slot capacity
   int max_chunk_nnz, chunk_cap;
   int ldx;  // row stride (elements) of U and eta in the staged kernel; 0 = k (contiguous)
+  // halo-tile kernel (edge_halo.cuh)
+  const int32_t* halo_enc;
+  const int32_t* halo_ext;
+  int halo_ext_cap, halo_nnz_cap;
 };
 plp_status launch_edge(plp_ctx* ctx, const EdgeArgs& a, int* grid_out);
 // Fixed-order reduction of edge partials: AB_out (2k), dots_out (2k), F (1); any may be null.

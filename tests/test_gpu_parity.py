@@ -164,7 +164,7 @@ def test_out_of_fast_domain_differences(plp, ctx):
         check(res, g, U, eta, 1.5, 0, 1e-300)
 
 
-ALT_KERNELS = {"tiled": "PLP_EDGE_TILED", "rows": "PLP_EDGE_ROWS"}
+ALT_KERNELS = {"tiled": "PLP_EDGE_TILED", "rows": "PLP_EDGE_ROWS", "staged": "PLP_EDGE_STAGED"}
 
 
 @pytest.mark.parametrize("kernel", sorted(ALT_KERNELS))

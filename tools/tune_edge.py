@@ -15,13 +15,8 @@ sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "paper_2605_26975_b200", "variants")
 
 VARIANTS = {
-    "c4_ct_256": ["-DPLP_STAGED_CPL8=4", "-DPLP_STAGED_UNR=2", "-DPLP_STAGED_CONTIG=1", "-DPLP_LD256=1"],
-    "c4_ct_128": ["-DPLP_STAGED_CPL8=4", "-DPLP_STAGED_UNR=2", "-DPLP_STAGED_CONTIG=1", "-DPLP_LD256=0"],
-    "c4_il_256": ["-DPLP_STAGED_CPL8=4", "-DPLP_STAGED_UNR=2", "-DPLP_STAGED_CONTIG=0", "-DPLP_LD256=1"],
-    "c4_il_128": ["-DPLP_STAGED_CPL8=4", "-DPLP_STAGED_UNR=2", "-DPLP_STAGED_CONTIG=0", "-DPLP_LD256=0"],
-    "c2_ct": ["-DPLP_STAGED_CPL8=2", "-DPLP_STAGED_UNR=2", "-DPLP_STAGED_CONTIG=1"],
-    "c2_ct_u4": ["-DPLP_STAGED_CPL8=2", "-DPLP_STAGED_UNR=4", "-DPLP_STAGED_CONTIG=1"],
-    "c2_il": ["-DPLP_STAGED_CPL8=2", "-DPLP_STAGED_UNR=2", "-DPLP_STAGED_CONTIG=0"],
+    "h_c2": ["-DPLP_HALO_CPL8=2"],
+    "h_c4": ["-DPLP_HALO_CPL8=4"],
 }
 
 
