@@ -76,6 +76,7 @@ __device__ __forceinline__ void edge_update_mx(const POW& pw, double wv, const d
                                                const double (&uj)[CPL], const double (&ei)[CPL],
                                                const double (&ej)[CPL], double (&L)[CPL],
                                                double (&HA)[CPL], unsigned& mx) {
+  unsigned h2[CPL];
 #pragma unroll
   for (int c = 0; c < CPL; ++c) {
     const double d = ui[c] - uj[c];
@@ -83,12 +84,17 @@ __device__ __forceinline__ void edge_update_mx(const POW& pw, double wv, const d
       L[c] = fma(wv, d, L[c]);
       if constexpr (HAS_ETA) HA[c] = fma(wv, ei[c] - ej[c], HA[c]);
     } else {
-      const unsigned h2 = (unsigned)__double2hiint(d) * 2u - pw.fast_lo2;
-      mx = max(mx, h2);
+      h2[c] = (unsigned)__double2hiint(d) * 2u - pw.fast_lo2;
       const double wsr = wv * pw.pow_fast(d);  // w |d|^{p-2}
       L[c] = fma(wsr, d, L[c]);                // w phi_p(d)
       if constexpr (HAS_ETA) HA[c] = fma(wsr, ei[c] - ej[c], HA[c]);
     }
+  }
+  if constexpr (!POW::kIsP2) {
+    // three-input max (VIMNMX3) over the columns' domain tests
+#pragma unroll
+    for (int c = 0; c + 1 < CPL; c += 2) mx = max(mx, max(h2[c], h2[c + 1]));
+    if constexpr (CPL % 2 == 1) mx = max(mx, h2[CPL - 1]);
   }
 }
 

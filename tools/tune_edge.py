@@ -15,8 +15,8 @@ sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "paper_2605_26975_b200", "variants")
 
 VARIANTS = {
-    "h_c2": ["-DPLP_HALO_CPL8=2"],
-    "h_c4": ["-DPLP_HALO_CPL8=4"],
+    "f2f0": ["-DPLP_POW_F2F=0"],
+    "f2f1": ["-DPLP_POW_F2F=1"],
 }
 
 
