@@ -1,0 +1,222 @@
+"""Riemannian trust-region Newton with truncated CG on the Grassmann manifold, with p-continuation
+("Newton's method on the Grassmann manifold ... truncated
+conjugate gradient scheme ... for progressively smaller values of p").
+
+A host driver over the C ABI: every vector operation (F, EucGrad, EucHessianEta, projection,
+curvature correction, dots, axpby, QR retraction, k-means, RCut) runs in libplp's kernels; Python
+only holds the scalars of the trust-region and CG recurrences (read back once per step).  There is
+no CPU fallback.
+
+Geometry (readings, DESIGN.md §3 #21-#24): U in St(n, k) represents a point, the horizontal space is
+{xi : U^T xi = 0} with the Euclidean metric, P(G) = G - U (U^T G), retraction = Q factor of
+U + xi with R_ii > 0.  Riemannian gradient grad = P(G); Riemannian Hessian
+H(xi) = P(EucHess[xi]) - xi sym(U^T G) (the Grassmann curvature term of SPEC.md:345, with the k x k
+matrix symmetrised so that tCG sees a symmetric operator).  EucHess is Alg. 1's sparse Hessian by
+default (plp_hessvec, HESS_SPARSE) or the exact one (HESS_FULL).
+"""
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import torch
+
+from . import plp
+
+
+@dataclass
+class SolverConfig:
+    """SPEC.md:302 (defaults of SPEC.md:382-383; the trust radii are unstated: reading #22)."""
+    grad_tol: float | None = None       # default 1e-6 sqrt(n k)
+    max_outer: int = 200
+    tr_delta0: float | None = None      # default tr_delta_max / 8
+    tr_delta_max: float | None = None   # default sqrt(k)
+    tr_rho_accept: float = 0.1
+    tcg_kappa: float = 0.1
+    tcg_theta: float = 1.0
+    tcg_max_iters: int | None = None    # default min(2 n k, 1000)
+    hessian_mode: int = plp.HESS_SPARSE
+    eps: float = 1e-9
+
+    def resolved(self, n: int, k: int) -> "SolverConfig":
+        c = SolverConfig(**self.__dict__)
+        if c.grad_tol is None:
+            c.grad_tol = 1e-6 * math.sqrt(n * k)
+        if c.tr_delta_max is None:
+            c.tr_delta_max = math.sqrt(k)
+        if c.tr_delta0 is None:
+            c.tr_delta0 = c.tr_delta_max / 8.0
+        if c.tcg_max_iters is None:
+            c.tcg_max_iters = min(2 * n * k, 1000)
+        if not (0.0 < c.tr_rho_accept < 0.25 and c.grad_tol > 0 and c.tr_delta0 <= c.tr_delta_max):
+            raise ValueError("invalid SolverConfig (SPEC.md:303)")
+        return c
+
+
+@dataclass
+class IterRecord:
+    p: float
+    it: int
+    F: float
+    gradnorm: float
+    delta: float
+    tcg_iters: int
+    tcg_status: str
+    rho: float
+    accepted: bool
+    millis: float
+
+
+@dataclass
+class SolveTrace:
+    records: list = field(default_factory=list)
+
+    def csv(self) -> str:
+        head = "p,iter,F,gradnorm,delta,tcg_iters,tcg_status,rho,accepted,millis"
+        rows = [f"{r.p},{r.it},{r.F!r},{r.gradnorm!r},{r.delta!r},{r.tcg_iters},{r.tcg_status},"
+                f"{r.rho!r},{int(r.accepted)},{r.millis:.3f}" for r in self.records]
+        return "\n".join([head] + rows)
+
+
+class _State:
+    """Device state at the current iterate: U, F, AB, G, grad = P(G), S = sym(U^T G)."""
+
+    def __init__(self, solver: "GrassmannTR", U, p: float):
+        s = solver
+        self.U = U
+        self.F, self.AB, self.G = plp.fgrad(s.ctx, s.g, U, p)
+        self.grad = plp.project(s.ctx, U, self.G)
+        # S = sym(U^T G) = (U^T G + G^T U) / 2, two Grams and an axpby in libplp
+        self.S = plp.gram(s.ctx, U, self.G)
+        plp.axpby(s.ctx, 0.5, plp.gram(s.ctx, self.G, U), 0.5, self.S)
+        self.Fv = float(self.F.item())
+
+
+class GrassmannTR:
+    """Trust-region Newton for min F_p(U) over the Grassmann manifold (one graph, one context)."""
+
+    def __init__(self, ctx: plp.Context, g: plp.Graph, k: int, cfg: SolverConfig | None = None):
+        self.ctx, self.g, self.k = ctx, g, k
+        self.cfg = (cfg or SolverConfig()).resolved(g.n_rows, k)
+
+    # -- operators --------------------------------------------------------------------------------
+    def _hess(self, st: _State, p: float, xi):
+        """H(xi) = P(EucHess[xi]) - xi S."""
+        c = self.cfg
+        EH = plp.hessvec(self.ctx, self.g, st.U, xi, p, st.AB, mode=c.hessian_mode, eps=c.eps,
+                         G_in=st.G if c.hessian_mode == plp.HESS_FULL else None)
+        PEH = plp.project(self.ctx, st.U, EH, out=EH)
+        return plp.apply_sub(self.ctx, xi, st.S, PEH, out=PEH)
+
+    def _dot(self, x, y) -> float:
+        return float(plp.dot(self.ctx, x, y).item())
+
+    # -- truncated CG (Steihaug-Toint; Absil-Baker-Gallivan 2007, Alg. 2) ------------------------
+    def tcg(self, st: _State, p: float, delta: float):
+        c = self.cfg
+        ctx = self.ctx
+        eta = torch.zeros_like(st.grad)
+        Heta = torch.zeros_like(st.grad)
+        r = st.grad.clone()
+        z_r = self._dot(r, r)
+        r0 = math.sqrt(z_r)
+        if r0 == 0.0:
+            return eta, Heta, 0, "interior"
+        dlt = torch.zeros_like(r)
+        plp.axpby(ctx, -1.0, r, 0.0, dlt)  # dlt = -r
+        e_Pe, e_Pd, d_Pd = 0.0, 0.0, z_r
+        stop_tol = r0 * min(r0 ** c.tcg_theta, c.tcg_kappa)
+        status = "maxiter"
+        j = 0
+        for j in range(1, c.tcg_max_iters + 1):
+            Hd = self._hess(st, p, dlt)
+            d_Hd = self._dot(dlt, Hd)
+            alpha = z_r / d_Hd if d_Hd != 0.0 else math.inf
+            e_Pe_new = e_Pe + 2.0 * alpha * e_Pd + alpha * alpha * d_Pd
+            if d_Hd <= 0.0 or e_Pe_new >= delta * delta:
+                tau = (-e_Pd + math.sqrt(e_Pd * e_Pd + d_Pd * (delta * delta - e_Pe))) / d_Pd
+                plp.axpby(ctx, tau, dlt, 1.0, eta)
+                plp.axpby(ctx, tau, Hd, 1.0, Heta)
+                status = "negative_curvature" if d_Hd <= 0.0 else "boundary"
+                break
+            e_Pe = e_Pe_new
+            plp.axpby(ctx, alpha, dlt, 1.0, eta)
+            plp.axpby(ctx, alpha, Hd, 1.0, Heta)
+            plp.axpby(ctx, alpha, Hd, 1.0, r)
+            r = plp.project(ctx, st.U, r, out=r)  # keep the residual horizontal
+            z_new = self._dot(r, r)
+            if math.sqrt(z_new) <= stop_tol:
+                status = "converged"
+                break
+            beta = z_new / z_r
+            z_r = z_new
+            plp.axpby(ctx, -1.0, r, beta, dlt)  # dlt = -r + beta dlt
+            e_Pd = beta * (e_Pd + alpha * d_Pd)
+            d_Pd = z_r + beta * beta * d_Pd
+        return eta, Heta, j, status
+
+    # -- outer loop ---------------------------------------------------------------------------------
+    def solve(self, U0, p: float, trace: SolveTrace | None = None):
+        c = self.cfg
+        ctx = self.ctx
+        trace = trace if trace is not None else SolveTrace()
+        st = _State(self, U0, p)
+        if not math.isfinite(st.Fv):
+            raise FloatingPointError(f"non-finite objective at p={p}")
+        delta = c.tr_delta0
+        for it in range(c.max_outer):
+            t0 = time.perf_counter()
+            gnorm = math.sqrt(self._dot(st.grad, st.grad))
+            if gnorm <= c.grad_tol or delta < 1e-14:
+                trace.records.append(IterRecord(p, it, st.Fv, gnorm, delta, 0, "stop", math.nan, False,
+                                                1e3 * (time.perf_counter() - t0)))
+                break
+            eta, Heta, nit, status = self.tcg(st, p, delta)
+            model_dec = -self._dot(st.grad, eta) - 0.5 * self._dot(eta, Heta)
+            try:
+                U_new = plp.retract(ctx, st.U, eta)
+                cand = _State(self, U_new, p)
+                F_new = cand.Fv
+            except plp.PlpError:  # rank-deficient U + eta: a rejected step
+                cand, F_new = None, math.inf
+            if model_dec > 0.0:
+                rho = (st.Fv - F_new) / model_dec
+            else:
+                rho = 1.0 if F_new <= st.Fv else -math.inf
+            accepted = cand is not None and math.isfinite(F_new) and rho > c.tr_rho_accept
+            if rho < 0.25:
+                delta *= 0.5
+            elif rho > 0.75 and status in ("boundary", "negative_curvature"):
+                delta = min(2.0 * delta, c.tr_delta_max)
+            trace.records.append(IterRecord(p, it, F_new if accepted else st.Fv, gnorm, delta, nit,
+                                            status, rho, accepted, 1e3 * (time.perf_counter() - t0)))
+            if accepted:
+                st = cand
+        return st.U, trace
+
+
+def init_embedding(ctx: plp.Context, Z) -> torch.Tensor:
+    """U0 = Q factor of a seeded Gaussian sample Z, by the QR retraction at 0."""
+    return plp.retract(ctx, Z, torch.zeros_like(Z))
+
+
+def continuation_solve(ctx: plp.Context, g: plp.Graph, Z, schedule, cfg: SolverConfig | None = None):
+    """Solve at p = schedule[0] (= 2) from QR(Z), then warm-start each smaller p from the previous
+    solution after QR re-orthonormalisation (reading #23)."""
+    k = Z.shape[1]
+    tr = GrassmannTR(ctx, g, k, cfg)
+    trace = SolveTrace()
+    U = init_embedding(ctx, Z)
+    for j, p in enumerate(schedule):
+        if j > 0:
+            U = plp.retract(ctx, U, torch.zeros_like(U))
+        U, trace = tr.solve(U, float(p), trace)
+    return U, trace
+
+
+def cluster(ctx: plp.Context, g: plp.Graph, U, k: int, uniforms, restarts: int = 10):
+    """Discretisation: k-means on the rows of U, then RCut of the labels."""
+    labels, centroids, sse, _ = plp.kmeans(ctx, U, k, uniforms, restarts=restarts)
+    rc, cut, sizes = plp.rcut(ctx, g, k, labels)
+    return labels, float(rc.item()), sse

@@ -1,0 +1,85 @@
+"""GPU solver (paper_2605_26975_b200/solver.py over the C ABI) against the oracle solver and the
+textbook eigenproblem: the north star's end-to-end acceptance (cluster labels equal up to
+permutation, RCut within 1e-6 relative) on C1 and a reduced C2, p = 2 spectral consistency, the
+first trust-region step against the oracle's, and the solver invariants."""
+import numpy as np
+import pytest
+import scipy.sparse.csgraph as csgraph
+import torch
+
+import oracle
+from oracle import solver as osol
+from plp_inputs import make_config, draw_U, draw_uniforms, random_graph, streams
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mods():
+    from paper_2605_26975_b200 import plp, solver
+    return plp, solver, plp.Context(0)
+
+
+def same_partition(a, b, k):
+    C = np.zeros((k, k), dtype=np.int64)
+    np.add.at(C, (np.asarray(a), np.asarray(b)), 1)
+    return bool(np.all((C > 0).sum(axis=1) == 1) and np.all((C > 0).sum(axis=0) == 1))
+
+
+@pytest.mark.parametrize("seed,n,k", [(1, 60, 2), (2, 120, 4), (3, 200, 2)])
+def test_p2_matches_dense_eigensolver(mods, seed, n, k):
+    plp, solver, ctx = mods
+    g = random_graph(streams(seed)[0], n, avg_deg=5.0, connected=True)
+    G = plp.Graph(ctx, g.row_ptr, g.col, g.w)
+    Z = torch.from_numpy(streams(seed)[1].standard_normal((n, k))).cuda()
+    U, tr = solver.continuation_solve(ctx, G, Z, [2.0], solver.SolverConfig(grad_tol=1e-9))
+    F = oracle.objective(g, U.cpu().numpy(), 2.0)[0]
+    ev = np.sum(np.linalg.eigvalsh(csgraph.laplacian(g.to_scipy()).toarray())[:k])
+    assert abs(F - ev) < 1e-6 * max(1.0, abs(ev))
+
+
+def test_first_trust_region_step_matches_oracle(mods):
+    """One tCG solve at a random orthonormal U (p = 1.5, sparse Hessian): the GPU step equals the
+    oracle's within 1e-9 (same algorithm, different summation order)."""
+    plp, solver, ctx = mods
+    g = make_config("C2", n=5000)
+    k = 2
+    Z = draw_U(g.n, k, 3)
+    Uo, _ = oracle.retract(Z, np.zeros_like(Z))
+    G = plp.Graph(ctx, g.row_ptr, g.col, g.w)
+    tr = solver.GrassmannTR(ctx, G, k)
+    st = solver._State(tr, torch.from_numpy(Uo).cuda(), 1.5)
+    eta, Heta, it, status = tr.tcg(st, 1.5, 0.3)
+    cfg = osol.default_cfg(g.n, k)
+    sto = osol._state(g, Uo, 1.5, osol.oracle_fns())
+    eta_o, Heta_o, it_o, status_o = osol.tcg(
+        lambda xi: osol._hess(g, sto, 1.5, xi, cfg["eps"], "sparse", osol.oracle_fns()), sto["grad"], Uo,
+        0.3, cfg)
+    assert (it, status) == (it_o, status_o)
+    e = eta.cpu().numpy()
+    assert np.max(np.abs(e - eta_o)) <= 1e-9 * np.max(np.abs(eta_o))
+    assert np.max(np.abs(Heta.cpu().numpy() - Heta_o)) <= 1e-9 * np.max(np.abs(Heta_o))
+
+
+@pytest.mark.parametrize("cfg,n,k,sched", [("C1", None, 3, [2.0, 1.8, 1.5, 1.2]),
+                                            ("C2", 20000, 2, [2.0, 1.1])])
+def test_end_to_end_labels_and_rcut_match_oracle(mods, cfg, n, k, sched):
+    """North star: labels agree up to permutation, RCut within 1e-6 relative."""
+    plp, solver, ctx = mods
+    g = make_config(cfg, n=n)
+    Z = draw_U(g.n, k, 0)
+    u = draw_uniforms(10, k)
+    G = plp.Graph(ctx, g.row_ptr, g.col, g.w)
+    U, tr = solver.continuation_solve(ctx, G, torch.from_numpy(Z).cuda(), sched)
+    lab, rc, sse = solver.cluster(ctx, G, U, k, u)
+    Uo, tro = osol.continuation_solve(g, Z, sched)
+    lab_o, _, sse_o, _ = oracle.kmeans(Uo, k, u, restarts=10)
+    rc_o = oracle.rcut(g, lab_o, k)[0]
+    assert same_partition(lab.cpu().numpy(), lab_o, k)
+    assert abs(rc - rc_o) <= 1e-6 * max(abs(rc_o), 1e-300) or abs(rc - rc_o) < 1e-300
+    # invariants of the GPU run
+    Uh = U.cpu().numpy()
+    assert np.max(np.abs(Uh.T @ Uh - np.eye(k))) < 1e-10
+    for p in sched:
+        Fs = [r.F for r in tr.records if r.p == p and r.accepted]
+        assert all(b <= a + 1e-15 * abs(a) for a, b in zip(Fs, Fs[1:]))
