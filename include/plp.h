@@ -53,7 +53,10 @@ typedef enum {
 enum { PLP_HESS_SPARSE = 0, PLP_HESS_FULL = 1 };          /* reading #5 */
 enum { PLP_VALIDATE = 1u, PLP_VALIDATE_SYMMETRIC = 2u };  /* plp_create_graph flags */
 enum { PLP_TILE_ROWS = 120 };  /* rows per tile of the tiled edge kernel (plp_tile_order) */
-enum { PLP_HALO_TILE = 256 };  /* rows per tile of the halo-tile edge kernel */
+#ifndef PLP_HALO_TILE_ROWS
+#define PLP_HALO_TILE_ROWS 224
+#endif
+enum { PLP_HALO_TILE = PLP_HALO_TILE_ROWS };  /* rows per tile of the halo-tile edge kernel */
 
 typedef struct plp_ctx plp_ctx;
 typedef struct plp_graph plp_graph;

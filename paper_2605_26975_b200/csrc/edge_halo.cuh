@@ -6,13 +6,15 @@
 // every stored edge as a tile-local index: j - r0 for an internal neighbour, kHaloT + x for the
 // x-th halo row.  One persistent CTA of 512 threads per SM walks the tiles (interleaved across
 // CTAs, so neighbouring tiles are in flight together and the halo rows hit L2), double-buffered:
-//   * thread 0 stages the tile's contiguous pieces with TMA bulk copies (cp.async.bulk + mbarrier):
-//     its own U / eta rows, row_ptr and schedule slices, (enc, w) ranges, and one tile ahead the
-//     halo list of the next-but-one tile (count, CSR bounds, columns);
-//   * all threads gather the halo rows U_j, eta_j with cp.async (16-byte pieces, 8 rows per warp
-//     instruction at k = 8, indices read from the staged list) after the own rows; each thread's
-//     cp.async.mbarrier.arrive joins the same "full" barrier as the TMA bytes;
-//   * while tile i is computed, tile i + 1 is resident and tile i + 2 is in flight.
+//   * a dedicated producer warp (warp specialisation: 16 consumer warps + 1) stages each tile: lane 0
+//     issues TMA bulk copies (cp.async.bulk + mbarrier) of the tile's own U / eta rows, row_ptr and
+//     schedule slices, (enc, w) ranges, and two tiles ahead the tile's halo list (count, CSR
+//     bounds, columns); the 32 lanes gather the halo rows U_j, eta_j with cp.async (16-byte pieces,
+//     8 rows per instruction at k = 8) whose cp.async.mbarrier.arrive joins the TMA bytes on the
+//     buffer's "full" mbarrier;
+//   * consumers release a buffer with one arrival per warp on its "empty" mbarrier; there is no
+//     CTA-wide barrier per tile, so a warp that finishes early goes on with the next (resident)
+//     tile; while tile i is computed, tile i + 1 is resident and tile i + 2 is in flight.
 // Rows are processed as in the row kernels (one group of LPR lanes per row, CPL = 2 columns per
 // lane, CSR order per row, one power per stored edge-column), reading U_j / eta_j with LDS.128, so
 // the only global traffic is the streaming of the tile data and the G / Hv stores: the L2 no longer
@@ -26,9 +28,9 @@
 namespace plp {
 
 constexpr int kHaloT = PLP_HALO_TILE;  // rows per tile (plp.h)
-constexpr int kHaloThreads = 512;
-constexpr int kHaloWarps = kHaloThreads / 32;
-static_assert(kHaloT == 8 * kSchedWindow && kHaloWarps == 2 * (kHaloT / kSchedWindow), "tile map");
+constexpr int kHaloCWarps = 2 * (kHaloT / kSchedWindow);  // consumers: a warp pair per window
+constexpr int kHaloThreads = (kHaloCWarps + 1) * 32;       // + one producer warp
+static_assert(kHaloT % kSchedWindow == 0 && kHaloThreads <= 16 * 32, "tile map (<= 4 warps per SMSP)");
 
 // Per-buffer shared-memory layout (bytes), identical on host and device.
 struct HaloLayout {
@@ -60,6 +62,9 @@ __host__ __device__ inline unsigned halo_smem_bytes(int k, int ext_cap, int nnz_
 }
 constexpr unsigned kHaloSmemMax = 225u * 1024u;
 
+#ifndef PLP_HALO_L2PF
+#define PLP_HALO_L2PF 1  // producer L2-prefetches the next tile's streamed parts
+#endif
 #ifndef PLP_HALO_CPL8
 #define PLP_HALO_CPL8 2  // columns per lane at k = 8 (2 or 4)
 #endif
@@ -74,6 +79,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1) edge_halo_kernel(EdgeArgs a, 
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [2] tile data landed
   uint64_t* lbar = full + 2;                           // [3] halo list landed
+  uint64_t* empty = full + 5;                          // [2] consumers done with the buffer
   if constexpr (POW::kNeedsTables) pw.init_smem(smem + kHaloHead);
   const int ext_cap = a.halo_ext_cap;
   const int LS = ext_cap + 4;  // list slot: n_ext, eb, ee, pad, columns
@@ -83,9 +89,11 @@ __global__ void __launch_bounds__(kHaloThreads, 1) edge_halo_kernel(EdgeArgs a, 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int grp = lane / LPR, li = lane % LPR, c0 = li * CPL;
   if (tid == 0) {
-    // full: thread 0's arrive.expect_tx (TMA bytes) + one cp.async arrival per thread
-    mbar_init(&full[0], 1 + kHaloThreads);
-    mbar_init(&full[1], 1 + kHaloThreads);
+    // full: the producer's arrive.expect_tx (TMA bytes) + one cp.async arrival per producer lane
+    mbar_init(&full[0], 1 + 32);
+    mbar_init(&full[1], 1 + 32);
+    mbar_init(&empty[0], kHaloCWarps);
+    mbar_init(&empty[1], kHaloCWarps);
     for (int q = 0; q < 3; ++q) mbar_init(&lbar[q], 1);
     fence_mbar_init();
   }
@@ -115,7 +123,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1) edge_halo_kernel(EdgeArgs a, 
     mbar_expect_tx(&lbar[q], (unsigned)LS * 4u);
     tma_bulk_g2s(lists + q * LS, a.halo_ext + t * LS, (unsigned)LS * 4u, &lbar[q]);
   };
-  // (all threads) stage tile t into buffer b; its halo list is in slot q (use parity lph)
+  // (producer warp) stage tile t into buffer b; its halo list is in slot q (use parity lph)
   auto issue_tile = [&](int64_t t, int b, int q, unsigned lph) {
     if (t >= n_tiles) return;
     unsigned char* B = buf0 + (size_t)b * Ly.bytes;
@@ -124,7 +132,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1) edge_halo_kernel(EdgeArgs a, 
     mbar_wait(&lbar[q], lph);
     const int* Lq = lists + q * LS;
     const int nx = Lq[0];
-    if (tid == 0) {
+    if (lane == 0) {
       const int eb = Lq[1], ee = Lq[2];
       const unsigned rp_b = (unsigned)(((r1 + 1 + 3) & ~3) - r0) * 4u;
       const unsigned sc_b = (unsigned)(((r1 + 3) & ~3) - r0) * 4u;
@@ -144,7 +152,8 @@ __global__ void __launch_bounds__(kHaloThreads, 1) edge_halo_kernel(EdgeArgs a, 
     // halo rows: PPR lanes per row, 32 / PPR rows per warp instruction
     constexpr int PPR = K / 2, RPI = 32 / PPR;
     const int rl = lane / PPR, pc = lane % PPR;
-    for (int x = warp * RPI + rl; x < nx; x += kHaloWarps * RPI) {
+#pragma unroll 4
+    for (int x = rl; x < nx; x += RPI) {
       const int j = Lq[4 + x];
       const unsigned off = ((unsigned)(kHaloT + x) * K + 2 * pc) * 8u;
       cp_async16(B + Ly.U + off, a.U + (int64_t)j * K + 2 * pc);
@@ -154,13 +163,44 @@ __global__ void __launch_bounds__(kHaloThreads, 1) edge_halo_kernel(EdgeArgs a, 
   };
 
   const int64_t t0 = blockIdx.x, ts = gridDim.x;
-  if (tid == 0) {
-    issue_list(t0, 0);
-    issue_list(t0 + ts, 1);
-    issue_list(t0 + 2 * ts, 2);
-  }
-  issue_tile(t0, 0, 0, 0u);
-  issue_tile(t0 + ts, 1, 1, 0u);
+  if (warp == kHaloCWarps) {
+    // ---- producer warp: stages tile it into buffer it & 1 once the consumers released it, and
+    // the halo list of tile it + 2 into list slot (it + 2) % 3 (freed by tile it - 1) ----
+    if (lane == 0) {
+      issue_list(t0, 0);
+      issue_list(t0 + ts, 1);
+    }
+    __syncwarp();
+    for (int it = 0;; ++it) {
+      const int64_t t = t0 + (int64_t)it * ts;
+      if (t >= n_tiles) break;
+      const int b = it & 1;
+      if (it >= 2) mbar_wait(&empty[b], (unsigned)((it - 2) >> 1) & 1u);
+      if (lane == 0) fence_proxy_async();  // consumers' generic reads before the async refill
+      __syncwarp();
+      issue_tile(t, b, it % 3, (unsigned)(it / 3) & 1u);
+      if (lane == 0) {
+        issue_list(t + 2 * ts, (it + 2) % 3);
+#if PLP_HALO_L2PF
+        // warm L2 with the next tile's streamed parts (own rows, enc, w), so that its TMA copies,
+        // issued only once the consumers release a buffer, are L2 hits
+        const int64_t tn = t + ts;
+        if (tn < n_tiles) {
+          const int qn = (it + 1) % 3;
+          mbar_wait(&lbar[qn], (unsigned)((it + 1) / 3) & 1u);
+          const int* Ln = lists + qn * LS;
+          const int r0 = (int)(tn * kHaloT), r1 = min(r0 + kHaloT, n_rows);
+          const size_t rows_b = (size_t)(r1 - r0) * K * 8u;
+          l2_prefetch_range(a.U + (int64_t)r0 * K, rows_b);
+          if constexpr (HAS_ETA) l2_prefetch_range(a.eta + (int64_t)r0 * K, rows_b);
+          l2_prefetch_range(a.halo_enc + Ln[1], (size_t)(Ln[2] - Ln[1]) * 4u);
+          l2_prefetch_range(a.w + Ln[1], (size_t)(Ln[2] - Ln[1]) * 8u);
+        }
+#endif
+      }
+      __syncwarp();
+    }
+  } else {
   const int h = warp & 1, win = warp >> 1;  // warp pair shares a 32-row window
   for (int it = 0;; ++it) {
     const int64_t t = t0 + (int64_t)it * ts;
@@ -205,6 +245,8 @@ __global__ void __launch_bounds__(kHaloThreads, 1) edge_halo_kernel(EdgeArgs a, 
           tn[cc] = sn[cc] * au;
         }
       }
+      // pairs of edges as straight-line code (the two dependency chains interleave), then the odd
+      // edge; summation order stays the CSR order
       // pairs of edges as straight-line code (the two dependency chains interleave), then the odd
       // edge; summation order stays the CSR order
       int e = e0;
@@ -259,12 +301,9 @@ __global__ void __launch_bounds__(kHaloThreads, 1) edge_halo_kernel(EdgeArgs a, 
         if (a.Hv != nullptr) st_vec<CPL>(a.Hv + (int64_t)row * K + c0, hv);
       }
     }
-    __syncthreads();  // buffer b is free
-    if (tid == 0) {
-      fence_proxy_async();  // generic reads of buffer b before its async refill
-      issue_list(t + 3 * ts, it % 3);  // slot of tile t's list (consumed when t was issued)
-    }
-    issue_tile(t + 2 * ts, b, (it + 2) % 3, (unsigned)((it + 2) / 3) & 1u);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[b]);  // this warp is done with buffer b
+  }
   }
 
   // ---- fixed-order CTA reduction (reuses buffer 0: every issued copy has been consumed) ----

@@ -15,8 +15,11 @@ sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "paper_2605_26975_b200", "variants")
 
 VARIANTS = {
-    "f2f0": ["-DPLP_POW_F2F=0"],
-    "f2f1": ["-DPLP_POW_F2F=1"],
+    "pf0": ["-DPLP_HALO_L2PF=0"],
+    "pf1": ["-DPLP_HALO_L2PF=1"],
+    "pf1_t256": ["-DPLP_HALO_L2PF=1", "-DPLP_HALO_TILE_ROWS=256"],
+    "pf1_t192": ["-DPLP_HALO_L2PF=1", "-DPLP_HALO_TILE_ROWS=192"],
+    "pf1_t160": ["-DPLP_HALO_L2PF=1", "-DPLP_HALO_TILE_ROWS=160"],
 }
 
 
