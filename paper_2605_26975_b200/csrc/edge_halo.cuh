@@ -230,21 +230,10 @@ __global__ void __launch_bounds__(kHaloThreads, 1) edge_halo_kernel(EdgeArgs a, 
       double ui[CPL], ei[CPL];
       lds_vec<CPL>(tU + lrow * K, ui);
       if constexpr (HAS_ETA) lds_vec<CPL>(tE + lrow * K, ei);
-      double L[CPL], HA[CPL], sn[CPL], tn[CPL];
+      double L[CPL], HA[CPL];
       unsigned mx = 0;
 #pragma unroll
-      for (int cc = 0; cc < CPL; ++cc) {
-        L[cc] = HA[cc] = 0.0;
-        const double au = fabs(ui[cc]);
-        if constexpr (POW::kIsP2) {
-          sn[cc] = 1.0;
-          tn[cc] = au;
-        } else {
-          mx = max(mx, (unsigned)__double2hiint(au) * 2u - pw.fast_lo2);
-          sn[cc] = pw.pow_fast(au);
-          tn[cc] = sn[cc] * au;
-        }
-      }
+      for (int cc = 0; cc < CPL; ++cc) L[cc] = HA[cc] = 0.0;
       // pairs of edges as straight-line code (the two dependency chains interleave), then the odd
       // edge; summation order stays the CSR order
       // pairs of edges as straight-line code (the two dependency chains interleave), then the odd
@@ -271,6 +260,21 @@ __global__ void __launch_bounds__(kHaloThreads, 1) edge_halo_kernel(EdgeArgs a, 
         lds_vec<CPL>(tU + x0 * K, uj0);
         if constexpr (HAS_ETA) lds_vec<CPL>(tE + x0 * K, ej0);
         edge_update_mx<CPL, POW, HAS_ETA>(pw, w0, ui, uj0, ei, ej0, L, HA, mx);
+      }
+      // node terms sn = cap(|u|)^{p-2}, tn = |u|^{p-1}, after the edges (fewer live registers in
+      // the edge loop); same fast-domain test, exact recomputation of the row when it fails
+      double sn[CPL], tn[CPL];
+#pragma unroll
+      for (int cc = 0; cc < CPL; ++cc) {
+        const double au = fabs(ui[cc]);
+        if constexpr (POW::kIsP2) {
+          sn[cc] = 1.0;
+          tn[cc] = au;
+        } else {
+          mx = max(mx, (unsigned)__double2hiint(au) * 2u - pw.fast_lo2);
+          sn[cc] = pw.pow_fast(au);
+          tn[cc] = sn[cc] * au;
+        }
       }
       if constexpr (!POW::kIsP2) {
         if (mx >= pw.fast_span2) {  // rare: exact libdevice recomputation of the row
