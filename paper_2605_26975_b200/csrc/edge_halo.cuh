@@ -62,6 +62,12 @@ __host__ __device__ inline unsigned halo_smem_bytes(int k, int ext_cap, int nnz_
 }
 constexpr unsigned kHaloSmemMax = 225u * 1024u;
 
+#ifndef PLP_HALO_SLEEP_NS
+#define PLP_HALO_SLEEP_NS 64  // producer back-off between polls of the "empty" barrier
+#endif
+#ifndef PLP_HALO_EB
+#define PLP_HALO_EB 2  // edges per straight-line batch in the halo kernel (2 or 4)
+#endif
 #ifndef PLP_HALO_L2PF
 #define PLP_HALO_L2PF 1  // producer L2-prefetches the next tile's streamed parts
 #endif
@@ -175,7 +181,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1) edge_halo_kernel(EdgeArgs a, 
       const int64_t t = t0 + (int64_t)it * ts;
       if (t >= n_tiles) break;
       const int b = it & 1;
-      if (it >= 2) mbar_wait(&empty[b], (unsigned)((it - 2) >> 1) & 1u);
+      if (it >= 2) mbar_wait_sleep(&empty[b], (unsigned)((it - 2) >> 1) & 1u, PLP_HALO_SLEEP_NS);
       if (lane == 0) fence_proxy_async();  // consumers' generic reads before the async refill
       __syncwarp();
       issue_tile(t, b, it % 3, (unsigned)(it / 3) & 1u);
@@ -234,13 +240,32 @@ __global__ void __launch_bounds__(kHaloThreads, 1) edge_halo_kernel(EdgeArgs a, 
       unsigned mx = 0;
 #pragma unroll
       for (int cc = 0; cc < CPL; ++cc) L[cc] = HA[cc] = 0.0;
-      // pairs of edges as straight-line code (the two dependency chains interleave), then the odd
-      // edge; summation order stays the CSR order
-      // pairs of edges as straight-line code (the two dependency chains interleave), then the odd
-      // edge; summation order stays the CSR order
+      // batches of EB edges as straight-line code (their dependency chains interleave), then the
+      // remainder two edges / one edge at a time; summation order stays the CSR order
       int e = e0;
+#if PLP_HALO_EB == 4
+#pragma unroll 1
+      for (; e + 3 < e1; e += 4) {
+        int x[4];
+        double wv[4], uj[4][CPL], ej[4][CPL];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          x[u] = enc_s[e + u];
+          wv[u] = w_s[e + u];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          lds_vec<CPL>(tU + x[u] * K, uj[u]);
+          if constexpr (HAS_ETA) lds_vec<CPL>(tE + x[u] * K, ej[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) edge_update_mx<CPL, POW, HAS_ETA>(pw, wv[u], ui, uj[u], ei, ej[u], L, HA, mx);
+      }
+      if (e + 1 < e1) {
+#else
 #pragma unroll 1
       for (; e + 1 < e1; e += 2) {
+#endif
         const int x0 = enc_s[e], x1 = enc_s[e + 1];
         const double w0 = w_s[e], w1 = w_s[e + 1];
         double uj0[CPL], ej0[CPL], uj1[CPL], ej1[CPL];
@@ -252,6 +277,9 @@ __global__ void __launch_bounds__(kHaloThreads, 1) edge_halo_kernel(EdgeArgs a, 
         }
         edge_update_mx<CPL, POW, HAS_ETA>(pw, w0, ui, uj0, ei, ej0, L, HA, mx);
         edge_update_mx<CPL, POW, HAS_ETA>(pw, w1, ui, uj1, ei, ej1, L, HA, mx);
+#if PLP_HALO_EB == 4
+        e += 2;
+#endif
       }
       if (e < e1) {
         const int x0 = enc_s[e];

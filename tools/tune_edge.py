@@ -15,11 +15,9 @@ sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "paper_2605_26975_b200", "variants")
 
 VARIANTS = {
-    "pf0": ["-DPLP_HALO_L2PF=0"],
-    "pf1": ["-DPLP_HALO_L2PF=1"],
-    "pf1_t256": ["-DPLP_HALO_L2PF=1", "-DPLP_HALO_TILE_ROWS=256"],
-    "pf1_t192": ["-DPLP_HALO_L2PF=1", "-DPLP_HALO_TILE_ROWS=192"],
-    "pf1_t160": ["-DPLP_HALO_L2PF=1", "-DPLP_HALO_TILE_ROWS=160"],
+    "sl64": ["-DPLP_HALO_SLEEP_NS=64"],
+    "sl256": ["-DPLP_HALO_SLEEP_NS=256"],
+    "sl1000": ["-DPLP_HALO_SLEEP_NS=1000"],
 }
 
 
