@@ -250,7 +250,10 @@ static plp_status build_halo_tiles(plp_graph* g, const int64_t* rp, const int32_
   }
   const int ext_cap = (max_ext + 3) & ~3, nnz_cap = (max_nnz + 3) & ~3;
   const double bytes_k8 = 2.0 * ((T + ext_cap) * 128.0 + nnz_cap * 12.0 + 4096.0);
-  if (bytes_k8 > 224.0 * 1024.0) return PLP_OK;
+#ifndef PLP_HALO_CTAS
+#define PLP_HALO_CTAS 1
+#endif
+  if (bytes_k8 > 224.0 * 1024.0 / PLP_HALO_CTAS) return PLP_OK;
   std::vector<int32_t> enc((size_t)g->nnz + 16, 0);
   // per tile a slot of ext_cap + 4 ints: n_ext, rp[r0], rp[r1], 0, then the halo columns
   const int64_t LS = ext_cap + 4;

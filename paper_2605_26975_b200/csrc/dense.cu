@@ -1,6 +1,8 @@
+#include <algorithm>
 // Tall-skinny n x k kernels of the Grassmann solver: Gram products
 // X^T Y with a fixed-order reduction, k x k Cholesky on one warp, row-block apply (X M, X - U M,
 // (X+Y) R^-1), dot, axpby and row gathers.  All HBM-bound: k <= 32 doubles per row.
+#include "dense_mma.cuh"
 #include "plp_internal.h"
 
 namespace plp {
@@ -231,6 +233,19 @@ static double* dslot(plp_ctx* ctx, int s) { return ctx->scratch + 256 + (size_t)
 
 static plp_status gram(plp_ctx* ctx, int64_t n, int k, const double* X, const double* Xa,
                        const double* Y, const double* Ya, double* out) {
+  if (k == 8 || k == 16) {  // fp64 tensor cores (dense_mma.cuh)
+    int grid = ctx->num_sms * 4;
+    const int cap = (int)(((int64_t)ctx->max_ctas * 4 * PLP_MAX_K) / (k * k));
+    if (grid > cap) grid = cap;
+    const int64_t blocks = (n + 3) / 4;
+    if (blocks < (int64_t)grid * 8) grid = (int)std::max<int64_t>(1, (blocks + 7) / 8);
+    if (k == 8) gram_mma_kernel<1><<<grid, kMmaThreads, 0, ctx->stream>>>(n, X, Xa, Y, Ya, ctx->partials);
+    else gram_mma_kernel<2><<<grid, kMmaThreads, 0, ctx->stream>>>(n, X, Xa, Y, Ya, ctx->partials);
+    PLP_LAUNCH_CHECK("gram_mma_kernel");
+    sum_partials_kernel<<<1, 1024, 0, ctx->stream>>>(grid, k * k, ctx->partials, out);
+    PLP_LAUNCH_CHECK("sum_partials_kernel");
+    return PLP_OK;
+  }
   int grid = grid_for(ctx, (n + kGramRows - 1) / kGramRows, 1);
   const int cap = (int)(((int64_t)ctx->max_ctas * 4 * PLP_MAX_K) / (k * k));  // partials capacity
   if (grid > cap) grid = cap;
@@ -243,6 +258,16 @@ static plp_status gram(plp_ctx* ctx, int64_t n, int k, const double* X, const do
 
 static plp_status apply(plp_ctx* ctx, int64_t n, int k, const double* S, double sgn,
                         const double* X, const double* Xa, const double* M, double* out) {
+  auto al16 = [](const void* p) { return ((uintptr_t)p & 15u) == 0; };
+  if ((k == 8 || k == 16) && al16(out) && (S == nullptr || al16(S))) {  // fp64 tensor cores
+    const int64_t blocks = (n + 7) / 8;
+    int64_t grid = (int64_t)ctx->num_sms * 8;
+    if (blocks < grid * 8) grid = std::max<int64_t>(1, (blocks + 7) / 8);
+    if (k == 8) apply_mma_kernel<1><<<(int)grid, kMmaThreads, 0, ctx->stream>>>(n, S, sgn, X, Xa, M, out);
+    else apply_mma_kernel<2><<<(int)grid, kMmaThreads, 0, ctx->stream>>>(n, S, sgn, X, Xa, M, out);
+    PLP_LAUNCH_CHECK("apply_mma_kernel");
+    return PLP_OK;
+  }
   int G = 1;
   while (G < k) G <<= 1;
   const int rows_per_block = 8 * (32 / G);

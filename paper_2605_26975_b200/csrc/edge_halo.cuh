@@ -60,7 +60,10 @@ __host__ __device__ inline unsigned halo_bufs_off(int ext_cap, bool tables) {
 __host__ __device__ inline unsigned halo_smem_bytes(int k, int ext_cap, int nnz_cap, bool tables) {
   return halo_bufs_off(ext_cap, tables) + 2u * halo_layout(k, ext_cap, nnz_cap).bytes;
 }
-constexpr unsigned kHaloSmemMax = 225u * 1024u;
+#ifndef PLP_HALO_CTAS
+#define PLP_HALO_CTAS 1  // resident CTAs per SM (each with its own double buffer)
+#endif
+constexpr unsigned kHaloSmemMax = 225u * 1024u / PLP_HALO_CTAS;
 
 #ifndef PLP_HALO_SLEEP_NS
 #define PLP_HALO_SLEEP_NS 64  // producer back-off between polls of the "empty" barrier
@@ -78,7 +81,7 @@ template <int K>
 constexpr int halo_cpl() { return K == 8 ? PLP_HALO_CPL8 : K == 16 ? 4 : 2; }
 
 template <int K, class POW, bool HAS_ETA>
-__global__ void __launch_bounds__(kHaloThreads, 1) edge_halo_kernel(EdgeArgs a, POW pw) {
+__global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(EdgeArgs a, POW pw) {
   constexpr int CPL = halo_cpl<K>(), LPR = K / CPL, RPW = 32 / LPR;  // rows per pass
   constexpr int NS = kSchedWindow / RPW;               // rank slices per 32-row window
   static_assert(NS % 2 == 0 || NS == 2, "slice count");
@@ -369,7 +372,7 @@ plp_status launch_halo_shape(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int
     attr_set = smem;
   }
   const int64_t n_tiles = (a.n_rows + kHaloT - 1) / kHaloT;
-  int64_t grid = ctx->num_sms;
+  int64_t grid = (int64_t)ctx->num_sms * PLP_HALO_CTAS;
   if (grid > ctx->max_ctas) grid = ctx->max_ctas;
   if (grid > n_tiles) grid = n_tiles > 0 ? n_tiles : 1;
   kern<<<(int)grid, kHaloThreads, smem, ctx->stream>>>(a, pw);

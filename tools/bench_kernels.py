@@ -1,0 +1,101 @@
+"""Per-row timing table (SURVEY.md §8(d) "also reported"): every kernel of the hot path on one
+config, with its algorithmic bytes, achieved GB/s and fraction of the measured HBM peak; plus the
+fused pass under the three node orderings (generator, RCM, tile).  CUDA events on the context's
+stream, median of `reps` launches after warm-up.  Prints one JSON object per row.
+
+  python tools/bench_kernels.py [--config C5] [--reps 20]
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from bench import get_graph, CONFIG_KP, load_peaks, algorithmic_bytes  # noqa: E402
+from paper_2605_26975_b200 import plp  # noqa: E402
+from plp_inputs import draw_U, draw_eta, draw_uniforms  # noqa: E402
+
+
+def timed(fn, reps, stream):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
+    ev[0].record(stream)
+    for i in range(reps):
+        fn()
+        ev[i + 1].record(stream)
+    torch.cuda.synchronize()
+    return float(np.median([ev[i].elapsed_time(ev[i + 1]) for i in range(reps)]))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--orders", default="tile,rcm,natural")
+    args = ap.parse_args()
+    k, p = CONFIG_KP[args.config]
+    peak, kind = load_peaks()
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    ctx = plp.Context(0, stream)
+
+    def row(name, ms, byts, extra=None):
+        gbs = byts / (ms * 1e-3) / 1e9
+        d = {"config": args.config, "row": name, "ms": ms, "algorithmic_bytes": int(byts), "GBps": gbs,
+             "frac_hbm": gbs / peak, "peak": peak, "peak_kind": kind}
+        if extra:
+            d.update(extra)
+        print(json.dumps(d), flush=True)
+
+    for order in args.orders.split(","):
+        g = get_graph(args.config, order)
+        n, nnz = g.n, g.nnz
+        G = plp.Graph(ctx, g.row_ptr, g.col, g.w)
+        U = torch.from_numpy(draw_U(n, k, 0)).cuda()
+        E = torch.from_numpy(draw_eta(n, k, 0)).cuda()
+        F, AB, _ = plp.fgrad(ctx, G, U, p, want_grad=False)
+        Gr = torch.empty(n, k, dtype=torch.float64, device="cuda")
+        Hv = torch.empty_like(Gr)
+        csr = 12 * nnz + 4 * (n + 1)
+        ms = timed(lambda: plp.edge_pass(ctx, G, U, E, p, 1e-9, AB_in=AB, G=Gr, Hv=Hv), args.reps, stream)
+        row(f"a7 fused F/G/Hv edge pass ({order} order)", ms, algorithmic_bytes(n, nnz, k),
+            {"kernel": plp.last_edge_kernel(), "GNNZk": nnz * k / (ms * 1e-3) / 1e9})
+        if order != "tile":
+            continue
+        ms = timed(lambda: plp.fgrad(ctx, G, U, p, want_grad=False), args.reps, stream)
+        row("a3 objective pass F, A, B (plp_fgrad, G = NULL)", ms, csr + 8 * n * k,
+            {"kernel": plp.last_edge_kernel()})
+        ms = timed(lambda: plp.edge_pass(ctx, G, U, None, p, 1e-9, AB_in=AB, G=Gr), args.reps, stream)
+        row("a4 gradient pass with A, B supplied", ms, csr + 16 * n * k, {"kernel": plp.last_edge_kernel()})
+        ms = timed(lambda: plp.hessvec(ctx, G, U, E, p, AB, Hv=Hv), args.reps, stream)
+        row("a5 Hessian-vector product (sparse, Alg. 1)", ms, csr + 24 * n * k, {"kernel": plp.last_edge_kernel()})
+        ms = timed(lambda: plp.hessvec(ctx, G, U, E, p, AB, mode=plp.HESS_FULL, G_in=Gr, Hv=Hv), args.reps, stream)
+        row("a5+a6 Hessian-vector product (full mode: edge pass + rank-two epilogue)", ms,
+            csr + 24 * n * k + 32 * n * k)
+        Q = torch.empty_like(U)
+        ms = timed(lambda: plp.project(ctx, U, Gr, out=Q), args.reps, stream)
+        row("a8 Grassmann projection G - U (U^T G)", ms, 40 * n * k)
+        ms = timed(lambda: plp.retract(ctx, U, Gr, Q=Q), args.reps, stream)
+        row("a9 Cholesky-QR2 retraction", ms, 2 * 24 * n * k)
+        out = torch.empty(1, dtype=torch.float64, device="cuda")
+        ms = timed(lambda: plp.dot(ctx, U, E, out=out), args.reps, stream)
+        row("a10 dot <x, y>", ms, 16 * n * k)
+        ms = timed(lambda: plp.axpby(ctx, 0.5, U, 0.5, Q), args.reps, stream)
+        row("a10 axpby y = a x + b y", ms, 24 * n * k)
+        u = draw_uniforms(1, k)
+        labels, cent, sse, iters = plp.kmeans(ctx, U, k, u, restarts=1, max_iters=20)
+        ms = timed(lambda: plp.kmeans(ctx, U, k, u, restarts=1, max_iters=20), max(3, args.reps // 4), stream)
+        row(f"a11 k-means (1 restart, {iters} Lloyd iterations incl. k-means++ seeding)", ms,
+            iters * (8 * n * k + 4 * n), {"lloyd_iters": iters, "ms_per_lloyd_iter": ms / max(iters, 1)})
+        ms = timed(lambda: plp.rcut(ctx, G, k, labels), args.reps, stream)
+        row("a12 RCut", ms, csr + 4 * n)
+
+
+if __name__ == "__main__":
+    main()

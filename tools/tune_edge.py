@@ -15,9 +15,9 @@ sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "paper_2605_26975_b200", "variants")
 
 VARIANTS = {
-    "sl64": ["-DPLP_HALO_SLEEP_NS=64"],
-    "sl256": ["-DPLP_HALO_SLEEP_NS=256"],
-    "sl1000": ["-DPLP_HALO_SLEEP_NS=1000"],
+    "t96x2": ["-DPLP_HALO_TILE_ROWS=96", "-DPLP_HALO_CTAS=2"],
+    "t128x2": ["-DPLP_HALO_TILE_ROWS=128", "-DPLP_HALO_CTAS=2"],
+    "t64x3": ["-DPLP_HALO_TILE_ROWS=64", "-DPLP_HALO_CTAS=3"],
 }
 
 
@@ -25,8 +25,12 @@ def build(names):
     from paper_2605_26975_b200.build import build as b
     for name in names:
         d = os.path.join(VDIR, name)
+        shutil.rmtree(d, ignore_errors=True)
         os.makedirs(d, exist_ok=True)
-        b(obj_dir=os.path.join(d, "obj"), lib=os.path.join(d, "libplp.so"), extra=VARIANTS[name] + ["-DPLP_TUNE_ONLY"])
+        try:
+            b(obj_dir=os.path.join(d, "obj"), lib=os.path.join(d, "libplp.so"), extra=VARIANTS[name] + ["-DPLP_TUNE_ONLY"])
+        except RuntimeError as e:
+            print("FAILED", name, str(e)[-600:], flush=True)
         shutil.rmtree(os.path.join(d, "obj"), ignore_errors=True)
         print("built", name, flush=True)
 
