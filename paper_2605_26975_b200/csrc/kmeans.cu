@@ -1,3 +1,4 @@
+#include <algorithm>
 // k-means discretisation of the embedding (reading #13).
 // Device kernels for k-means++ seeding (D^2 update, chunked cumulative sums, pick), the fused
 // Lloyd assign + per-CTA centroid/count/SSE partials (fixed order, no atomics), empty-cluster
@@ -5,6 +6,7 @@
 #include <cstring>
 #include <vector>
 
+#include "dense_mma.cuh"
 #include "plp_internal.h"
 
 namespace plp {
@@ -166,6 +168,120 @@ __global__ void __launch_bounds__(kKmThreads) km_assign_kernel(int64_t n, int di
     part[(int64_t)blockIdx.x * E + q * kKmThreads + threadIdx.x] = acc[q];
 }
 
+// Lloyd assign + centroid partials for K <= 8 clusters and dim <= 8 (the configs' C1, C2, C5):
+// one thread per point for the distances (same exact rounding as km_dist2, ties -> lowest index),
+// and the per-cluster sums / counts as one-hot^T X products on the fp64 tensor cores (DMMA
+// m8n8k4: A[c][q] = [label of point q == c], B[q][d] = X[q][d] or 1), 4 points per instruction.
+// Each warp owns a contiguous range of 32-point groups; per-CTA partials in a fixed order, layout
+// [sums K*dim | counts K | sse] like km_assign_kernel.
+template <int DIM>  // DIM = 8: vectorised point loads; DIM = 0: runtime dim <= 8
+__global__ void __launch_bounds__(256) km_assign_mma_kernel(int64_t n, int dim_rt, int K,
+                                                            const double* __restrict__ X,
+                                                            const double* __restrict__ cent,
+                                                            int32_t* __restrict__ lab,
+                                                            double* __restrict__ best_d,
+                                                            double* __restrict__ part) {
+  constexpr int NW = 8;
+  const int dim = DIM > 0 ? DIM : dim_rt;
+  __shared__ __align__(16) double cs[8 * 8];
+  __shared__ double red[NW][8 * 8 + 8 + 1];
+  for (int i = threadIdx.x; i < K * dim; i += blockDim.x) cs[i] = cent[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  const int64_t groups = (n + 31) / 32;
+  const int64_t tw = (int64_t)gridDim.x * NW, wid = (int64_t)blockIdx.x * NW + warp;
+  const int64_t g0 = groups * wid / tw, g1 = groups * (wid + 1) / tw;
+  double s0 = 0.0, s1 = 0.0, sse = 0.0;
+  int cnt = 0;  // lane c < K counts cluster c
+  for (int64_t gr = g0; gr < g1; ++gr) {
+    const int64_t p0 = gr * 32, i = p0 + lane;
+    const bool ok = i < n;
+    double x[8];
+    if constexpr (DIM == 8) {
+      if (ok) {
+#pragma unroll
+        for (int d = 0; d < 8; d += 2) {
+          const double2 t = __ldg(reinterpret_cast<const double2*>(X + i * 8 + d));
+          x[d] = t.x;
+          x[d + 1] = t.y;
+        }
+      } else {
+#pragma unroll
+        for (int d = 0; d < 8; ++d) x[d] = 0.0;
+      }
+    } else {
+#pragma unroll
+      for (int d = 0; d < 8; ++d) x[d] = (ok && d < dim) ? __ldg(X + i * dim + d) : 0.0;
+    }
+    int bc = -1;
+    double bd = 0.0;
+    if (ok) {
+      bd = INFINITY;
+#pragma unroll 1
+      for (int c = 0; c < K; ++c) {
+        double sd = 0.0;
+        if constexpr (DIM == 8) {
+          // centroid row as four 16-byte broadcasts (LDS.128) instead of eight LDS.64
+          const double2* cr = reinterpret_cast<const double2*>(cs + c * 8);
+#pragma unroll
+          for (int d = 0; d < 8; d += 2) {
+            const double2 cc = cr[d / 2];
+            const double t0 = __dsub_rn(x[d], cc.x);
+            sd = __dadd_rn(sd, __dmul_rn(t0, t0));
+            const double t1 = __dsub_rn(x[d + 1], cc.y);
+            sd = __dadd_rn(sd, __dmul_rn(t1, t1));
+          }
+        } else {
+#pragma unroll
+          for (int d = 0; d < 8; ++d) {
+            if (d < dim) {
+              const double t = __dsub_rn(x[d], cs[c * dim + d]);
+              sd = __dadd_rn(sd, __dmul_rn(t, t));
+            }
+          }
+        }
+        if (sd < bd || c == 0) {
+          bd = sd;
+          bc = c;
+        }
+      }
+      lab[i] = bc;
+      best_d[i] = bd;
+      sse += bd;
+    }
+    for (int c = 0; c < K; ++c) {
+      const int m = __popc(__ballot_sync(0xffffffffu, bc == c));
+      if (lane == c) cnt += m;
+    }
+#pragma unroll
+    for (int sb = 0; sb < 8; ++sb) {
+      const int lq = __shfl_sync(0xffffffffu, bc, 4 * sb + q);
+      const int64_t pq = p0 + 4 * sb + q;
+      const double a = (lq == g) ? 1.0 : 0.0;
+      const double b = (pq < n && g < dim) ? __ldg(X + pq * dim + g) : 0.0;
+      dmma884(s0, s1, a, b);
+    }
+  }
+  // per-warp results -> shared, then a fixed-order sum over warps
+  const int E = K * dim + K + 1;
+  if (g < K) {
+    if (2 * q < dim) red[warp][g * dim + 2 * q] = s0;
+    if (2 * q + 1 < dim) red[warp][g * dim + 2 * q + 1] = s1;
+  }
+  if (lane < K) red[warp][K * dim + lane] = (double)cnt;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sse += __shfl_xor_sync(0xffffffffu, sse, o);
+  if (lane == 0) red[warp][E - 1] = sse;
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) t += red[w][e];
+    part[(int64_t)blockIdx.x * E + e] = t;
+  }
+}
+
 // red = [sums K*dim | counts K | sse]; cent[c] = sums/count where count > 0 (empty: unchanged)
 __global__ void km_update_kernel(int K, int dim, const double* __restrict__ red, double* cent) {
   for (int e = threadIdx.x; e < K * dim; e += blockDim.x) {
@@ -290,10 +406,23 @@ extern "C" plp_status plp_kmeans(plp_ctx* ctx, int64_t n, int dim, int K, const 
       PLP_LAUNCH_CHECK("km_pick_kernel");
     }
     // ---- Lloyd ----
+    const bool mma = K <= 8 && dim <= 8;
+    int grid_mma = ctx->num_sms * 4;
+    if ((int64_t)grid_mma * E > part_cap) grid_mma = (int)(part_cap / E);
+    const int64_t groups = (n + 31) / 32;
+    if (groups < (int64_t)grid_mma * 8) grid_mma = (int)std::max<int64_t>(1, (groups + 7) / 8);
     auto assign = [&](double* sse_out, std::vector<double>& h) -> plp_status {
-      km_assign_kernel<<<grid, kKmThreads, 0, st>>>(n, dim, K, X, cent, lab, best_d, ctx->partials);
-      PLP_LAUNCH_CHECK("km_assign_kernel");
-      km_sum_kernel<<<1, 1024, 0, st>>>(grid, E, ctx->partials, red);
+      if (mma) {
+        if (dim == 8 && ((uintptr_t)X & 15u) == 0)
+          km_assign_mma_kernel<8><<<grid_mma, 256, 0, st>>>(n, dim, K, X, cent, lab, best_d, ctx->partials);
+        else
+          km_assign_mma_kernel<0><<<grid_mma, 256, 0, st>>>(n, dim, K, X, cent, lab, best_d, ctx->partials);
+        PLP_LAUNCH_CHECK("km_assign_mma_kernel");
+      } else {
+        km_assign_kernel<<<grid, kKmThreads, 0, st>>>(n, dim, K, X, cent, lab, best_d, ctx->partials);
+        PLP_LAUNCH_CHECK("km_assign_kernel");
+      }
+      km_sum_kernel<<<1, 1024, 0, st>>>(mma ? grid_mma : grid, E, ctx->partials, red);
       PLP_LAUNCH_CHECK("km_sum_kernel");
       PLP_CUDA(cudaMemcpyAsync(h.data(), red, sizeof(double) * E, cudaMemcpyDeviceToHost, st));
       PLP_CUDA(cudaStreamSynchronize(st));

@@ -89,10 +89,14 @@ def main():
         ms = timed(lambda: plp.axpby(ctx, 0.5, U, 0.5, Q), args.reps, stream)
         row("a10 axpby y = a x + b y", ms, 24 * n * k)
         u = draw_uniforms(1, k)
-        labels, cent, sse, iters = plp.kmeans(ctx, U, k, u, restarts=1, max_iters=20)
-        ms = timed(lambda: plp.kmeans(ctx, U, k, u, restarts=1, max_iters=20), max(3, args.reps // 4), stream)
-        row(f"a11 k-means (1 restart, {iters} Lloyd iterations incl. k-means++ seeding)", ms,
-            iters * (8 * n * k + 4 * n), {"lloyd_iters": iters, "ms_per_lloyd_iter": ms / max(iters, 1)})
+        labels, cent, sse, iters = plp.kmeans(ctx, U, k, u, restarts=1, max_iters=20, rel_tol=0.0)
+        ms = timed(lambda: plp.kmeans(ctx, U, k, u, restarts=1, max_iters=20, rel_tol=0.0),
+                   max(3, args.reps // 4), stream)
+        ms0 = timed(lambda: plp.kmeans(ctx, U, k, u, restarts=1, max_iters=0), max(3, args.reps // 4), stream)
+        lloyd = (ms - ms0) / max(iters, 1)
+        row("a11 k-means Lloyd iteration (assign + centroid partials + update, host convergence check)",
+            lloyd, 8 * n * k + 4 * n, {"lloyd_iters": iters})
+        row(f"a11 k-means++ seeding + first assignment ({k - 1} D^2 rounds)", ms0, k * (8 * n * k + 8 * n))
         ms = timed(lambda: plp.rcut(ctx, G, k, labels), args.reps, stream)
         row("a12 RCut", ms, csr + 4 * n)
 

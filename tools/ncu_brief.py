@@ -7,7 +7,7 @@ import subprocess
 import sys
 
 KEYS = [
-    ("time_ms", "gpu__time_duration.sum", 1e-6),
+    ("time_us", "gpu__time_duration.sum", None),
     ("inst_M", "smsp__inst_executed.sum", 1e-6),
     ("issue%", "smsp__issue_active.avg.pct_of_peak_sustained_active", 1),
     ("warps%", "sm__warps_active.avg.pct_of_peak_sustained_active", 1),
@@ -22,16 +22,28 @@ KEYS = [
     ("l2_hit%", "lts__t_sector_hit_rate.pct", 1),
     ("l2%", "lts__throughput.avg.pct_of_peak_sustained_elapsed", 1),
     ("dram%", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", 1),
-    ("dram_GB", "dram__bytes_read.sum", 1e-9),
+    ("dram_rd_GB", "dram__bytes_read.sum", 1),
+    ("dram_wr_GB", "dram__bytes_write.sum", 1),
     ("ld_req_M", "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum", 1e-6),
     ("ld_sect_M", "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", 1e-6),
 ]
 
 
+UNIT = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6,
+        "byte": 1e-9, "Kbyte": 1e-6, "Mbyte": 1e-3, "Gbyte": 1.0}
+
+
 def load(rep):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
-    return dict(zip(rows[0], rows[2]))
+    d = dict(zip(rows[0], rows[2]))
+    for k, u in zip(rows[0], rows[1]):
+        if u in UNIT:  # normalise times to us and bytes to GB
+            try:
+                d[k] = str(float(d[k].replace(",", "")) * UNIT[u])
+            except ValueError:
+                pass
+    return d
 
 
 def num(v):
@@ -45,7 +57,7 @@ reps = sys.argv[1:]
 data = [load(r) for r in reps]
 print(f"{'':22s}" + "".join(f"{r.split('/')[-1][:22]:>24s}" for r in reps))
 for name, key, sc in KEYS:
-    print(f"{name:22s}" + "".join(f"{num(d.get(key, 'nan')) * sc:24.3f}" for d in data))
+    print(f"{name:22s}" + "".join(f"{num(d.get(key, 'nan')) * (sc or 1):24.3f}" for d in data))
 stall = sorted({k for d in data for k in d if k.startswith("smsp__average_warp_latency_issue_stalled_") and k.endswith(".ratio")})
 for k in stall:
     vals = [num(d.get(k, "nan")) for d in data]
