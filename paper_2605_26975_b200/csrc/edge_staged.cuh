@@ -434,6 +434,10 @@ plp_status launch_staged_pow(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int
 #ifdef PLP_TUNE_ONLY
   return set_error(PLP_ERR_ARG, "tuning build: k = 8 only");
 #else
+  // all lanes busy for the configs' odd shapes: k = 20 as 4 lanes x 5 columns (C4), k = 3 as one
+  // lane x 3 columns (C1)
+  if (k == 20) PLP_SSHAPE(20, 5, 4);
+  if (k == 3) PLP_SSHAPE(3, 3, 1);
   if (vec_ok) {
     if (k == 2) PLP_SSHAPE(2, 2, 1);
     if (k == 4) PLP_SSHAPE(4, 2, 2);
