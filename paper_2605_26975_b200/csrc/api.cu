@@ -249,7 +249,10 @@ static plp_status build_halo_tiles(plp_graph* g, const int64_t* rp, const int32_
     max_nnz = std::max<int64_t>(max_nnz, rp[r1] - rp[r0]);
   }
   const int ext_cap = (max_ext + 3) & ~3, nnz_cap = (max_nnz + 3) & ~3;
-  const double bytes_k8 = 2.0 * ((T + ext_cap) * 128.0 + nnz_cap * 12.0 + 4096.0);
+#ifndef PLP_HALO_NBUF
+#define PLP_HALO_NBUF 2
+#endif
+  const double bytes_k8 = PLP_HALO_NBUF * ((T + ext_cap) * 128.0 + nnz_cap * 12.0 + 4096.0);
 #ifndef PLP_HALO_CTAS
 #define PLP_HALO_CTAS 1
 #endif

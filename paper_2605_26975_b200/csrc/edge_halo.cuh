@@ -49,7 +49,11 @@ __host__ __device__ inline HaloLayout halo_layout(int k, int ext_cap, int nnz_ca
   L.bytes = (o + 127u) & ~127u;
   return L;
 }
-constexpr unsigned kHaloHead = 256;  // mbarriers (full[2], list[3]); tables follow
+#ifndef PLP_HALO_NBUF
+#define PLP_HALO_NBUF 2  // tile buffers in flight (2 or 3)
+#endif
+constexpr int kHaloNBuf = PLP_HALO_NBUF;
+constexpr unsigned kHaloHead = 256;  // mbarriers (full[NBUF], list[3], empty[NBUF]); tables follow
 __host__ __device__ inline unsigned halo_tab_bytes(bool tables) {
   return tables ? (unsigned)((sizeof(PowTables) + 127) & ~(size_t)127) : 0u;
 }
@@ -58,7 +62,7 @@ __host__ __device__ inline unsigned halo_bufs_off(int ext_cap, bool tables) {
   return (halo_lists_off(tables) + 3u * (unsigned)(ext_cap + 4) * 4u + 127u) & ~127u;
 }
 __host__ __device__ inline unsigned halo_smem_bytes(int k, int ext_cap, int nnz_cap, bool tables) {
-  return halo_bufs_off(ext_cap, tables) + 2u * halo_layout(k, ext_cap, nnz_cap).bytes;
+  return halo_bufs_off(ext_cap, tables) + (unsigned)kHaloNBuf * halo_layout(k, ext_cap, nnz_cap).bytes;
 }
 #ifndef PLP_HALO_CTAS
 #define PLP_HALO_CTAS 1  // resident CTAs per SM (each with its own double buffer)
@@ -87,8 +91,8 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
   static_assert(NS % 2 == 0 || NS == 2, "slice count");
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [2] tile data landed
-  uint64_t* lbar = full + 2;                           // [3] halo list landed
-  uint64_t* empty = full + 5;                          // [2] consumers done with the buffer
+  uint64_t* lbar = full + kHaloNBuf;                   // [3] halo list landed
+  uint64_t* empty = lbar + 3;                          // [NBUF] consumers done with the buffer
   if constexpr (POW::kNeedsTables) pw.init_smem(smem + kHaloHead);
   const int ext_cap = a.halo_ext_cap;
   const int LS = ext_cap + 4;  // list slot: n_ext, eb, ee, pad, columns
@@ -99,10 +103,10 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
   const int grp = lane / LPR, li = lane % LPR, c0 = li * CPL;
   if (tid == 0) {
     // full: the producer's arrive.expect_tx (TMA bytes) + one cp.async arrival per producer lane
-    mbar_init(&full[0], 1 + 32);
-    mbar_init(&full[1], 1 + 32);
-    mbar_init(&empty[0], kHaloCWarps);
-    mbar_init(&empty[1], kHaloCWarps);
+    for (int q = 0; q < kHaloNBuf; ++q) {
+      mbar_init(&full[q], 1 + 32);
+      mbar_init(&empty[q], kHaloCWarps);
+    }
     for (int q = 0; q < 3; ++q) mbar_init(&lbar[q], 1);
     fence_mbar_init();
   }
@@ -183,8 +187,9 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
     for (int it = 0;; ++it) {
       const int64_t t = t0 + (int64_t)it * ts;
       if (t >= n_tiles) break;
-      const int b = it & 1;
-      if (it >= 2) mbar_wait_sleep(&empty[b], (unsigned)((it - 2) >> 1) & 1u, PLP_HALO_SLEEP_NS);
+      const int b = it % kHaloNBuf;
+      if (it >= kHaloNBuf)
+        mbar_wait_sleep(&empty[b], (unsigned)((it - kHaloNBuf) / kHaloNBuf) & 1u, PLP_HALO_SLEEP_NS);
       if (lane == 0) fence_proxy_async();  // consumers' generic reads before the async refill
       __syncwarp();
       issue_tile(t, b, it % 3, (unsigned)(it / 3) & 1u);
@@ -214,8 +219,8 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
   for (int it = 0;; ++it) {
     const int64_t t = t0 + (int64_t)it * ts;
     if (t >= n_tiles) break;
-    const int b = it & 1;
-    mbar_wait(&full[b], (unsigned)(it >> 1) & 1u);  // tile t resident
+    const int b = it % kHaloNBuf;
+    mbar_wait(&full[b], (unsigned)(it / kHaloNBuf) & 1u);  // tile t resident
 
     const unsigned char* B = buf0 + (size_t)b * Ly.bytes;
     const int* rp_s = reinterpret_cast<const int*>(B + Ly.rp);

@@ -15,9 +15,10 @@ sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "paper_2605_26975_b200", "variants")
 
 VARIANTS = {
-    "t96x2": ["-DPLP_HALO_TILE_ROWS=96", "-DPLP_HALO_CTAS=2"],
-    "t128x2": ["-DPLP_HALO_TILE_ROWS=128", "-DPLP_HALO_CTAS=2"],
-    "t64x3": ["-DPLP_HALO_TILE_ROWS=64", "-DPLP_HALO_CTAS=3"],
+    "t224b2": ["-DPLP_HALO_NBUF=2"],
+    "t160b3": ["-DPLP_HALO_NBUF=3", "-DPLP_HALO_TILE_ROWS=160"],
+    "t192b3": ["-DPLP_HALO_NBUF=3", "-DPLP_HALO_TILE_ROWS=192"],
+    "t128b3": ["-DPLP_HALO_NBUF=3", "-DPLP_HALO_TILE_ROWS=128"],
 }
 
 
