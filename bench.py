@@ -212,7 +212,8 @@ def run_plp(args, rank, world):
     U_h = draw_U(n, k, 0)
     eta_h = draw_eta(n, k, 0)
 
-    if world > 1:
+    sharded = world > 1 or args.sharded
+    if sharded:
         from paper_2605_26975_b200 import dist
         prob = dist.ShardedProblem(ctx, g, k, rank, world, device=dev)
         step = prob.make_step(U_h, eta_h, p, eps, mode)
@@ -233,7 +234,7 @@ def run_plp(args, rank, world):
         nnz_local = nnz
 
     def barrier():
-        if world > 1:
+        if sharded:
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
@@ -258,7 +259,7 @@ def run_plp(args, rank, world):
 
     # ---- dominant kernel alone (edge pass without finalize), per-launch CUDA events ----
     roof = None
-    if world == 1:
+    if not sharded:
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
         torch.cuda.synchronize()
         evs[0].record(stream)
@@ -283,7 +284,7 @@ def run_plp(args, rank, world):
 
     # ---- end to end through the public API: pinned host inputs in, results out, every step ----
     e2e = None
-    if world == 1 and not args.no_e2e:
+    if not sharded and not args.no_e2e:
         U_p = torch.from_numpy(U_h).pin_memory()
         E_p = torch.from_numpy(eta_h).pin_memory()
         G_p = torch.empty(n, k, dtype=torch.float64).pin_memory()
@@ -315,14 +316,14 @@ def run_plp(args, rank, world):
                "ms_per_step": ems}
 
     # ---- consistency: AB recomputed by the fused pass vs AB_in ----
-    if world == 1:
+    if not sharded:
         d = (AB_out - AB_in).abs().max().item() / AB_in.abs().max().item()
         log(f"[bench] AB_out vs AB_in max rel diff {d:.2e}")
 
     if rank != 0:
         return
     cpu = None
-    if world == 1 and not args.no_cpu:
+    if not sharded and not args.no_cpu:
         v, dt, desc, cores = cpu_oracle_sample(g, k, p, eps, rows_frac=args.cpu_frac)
         cpu = {"value": v, "unit": "GNNZ*k/s", "cores": cores, "kind": "oracle", "sample": desc,
                "seconds": dt}
@@ -335,7 +336,8 @@ def run_plp(args, rank, world):
                       "l2": "inputs (1.8 GB) larger than the 126 MB L2; no flush",
                       "parallelism": f"row-blocks x{world}", "nnz_local_rank0": nnz_local},
            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
-           "gpu_launches": 2 * args.steps * (1 if world == 1 else 1)}
+           # per step: edge pass + finalize; sharded: + 2 halo packs (when a peer needs rows) + F
+           "gpu_launches": args.steps * (2 if not sharded else 3 + (2 if world > 1 else 0))}
     print(json.dumps(out), flush=True)
 
 
@@ -349,6 +351,9 @@ def main():
     ap.add_argument("--order", default="tile", choices=["tile", "rcm", "none"])
     ap.add_argument("--mode", default="sparse", choices=["sparse", "full"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the multi-GPU path (row blocks, halo exchange, NCCL all-reduce) even at one "
+                         "rank: exercises dist.ShardedProblem on a single GPU")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-frac", type=float, default=0.25)
     ap.add_argument("--ref-frac", type=float, default=0.1)
@@ -359,14 +364,20 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-    if world > 1:
+    dist_on = world > 1 or args.sharded
+    if dist_on:
         import torch
         torch.cuda.set_device(args.local_rank)
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         torch.distributed.init_process_group("nccl", device_id=torch.device(f"cuda:{args.local_rank}"))
     try:
         run_plp(args, rank, world)
     finally:
-        if world > 1:
+        if dist_on:
             import torch
             torch.distributed.destroy_process_group()
 
