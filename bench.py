@@ -35,8 +35,12 @@ CONFIG_DESC = {
     "C3": "128^3 grid 7-point stencil + 1% long-range edges (w=0.1), k=8, p=1.5",
     "C4": "10-D GMM n=1,000,000, 20 clusters, symmetrised 15-NN, k=20, p=1.2",
     "C2": "two moons n=100,000, 10-NN, k=2, p=1.1",
+    "D23": "Delaunay triangulation of 2^23 uniform points (the paper's delaunay_n23 shape), unit weights, k=8, p=1.2",
+    "D20": "Delaunay triangulation of 2^20 uniform points, unit weights, k=8, p=1.2",
+    "D16": "Delaunay triangulation of 2^16 uniform points, unit weights, k=8, p=1.2",
 }
-CONFIG_KP = {"C5": (8, 1.2), "C3": (8, 1.5), "C4": (20, 1.2), "C2": (2, 1.1), "C1": (3, 1.2)}
+CONFIG_KP = {"C5": (8, 1.2), "C3": (8, 1.5), "C4": (20, 1.2), "C2": (2, 1.1), "C1": (3, 1.2),
+             "D16": (8, 1.2), "D20": (8, 1.2), "D23": (8, 1.2)}
 
 
 def log(*a):

@@ -7,7 +7,7 @@ Recipes follow BASELINE.json `configs` and the conventions in SURVEY.md §8(d); 
 is listed in DESIGN.md §3.
 """
 from .graphs import (  # noqa: F401
-    Graph, CONFIGS, make_config, knn_graph, csr_from_undirected, grid3d_longrange,
+    Graph, CONFIGS, make_config, knn_graph, csr_from_undirected, grid3d_longrange, delaunay_graph,
     blobs_2d, two_moons, gmm, uniform_square, path_graph, cycle_graph, single_edge,
     four_cycle, two_triangles, random_graph, draw_U, draw_eta, draw_uniforms, streams,
     validate_graph, permute_graph,

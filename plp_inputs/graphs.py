@@ -201,6 +201,20 @@ def random_graph(rng, n: int, avg_deg: float = 4.0, connected: bool = True, name
     return csr_from_undirected(n, a, b, wu, name)
 
 
+def delaunay_graph(rng, n: int, name: str = "D") -> Graph:
+    """Stand-in for the paper's SuiteSparse delaunay_n<r> graphs (SURVEY.md §8(f)
+    NEXT-3): the Delaunay triangulation (scipy.spatial.Delaunay, Qhull) of n uniform points in the
+    unit square, every triangle side an undirected edge, unit weights (the SuiteSparse matrices are
+    patterns).  nnz ~ 6 n stored nonzeros, planar, connected."""
+    from scipy.spatial import Delaunay
+    pts = uniform_square(rng, n)
+    tri = Delaunay(pts).simplices.astype(np.int64)
+    a = np.concatenate([tri[:, 0], tri[:, 1], tri[:, 2]])
+    b = np.concatenate([tri[:, 1], tri[:, 2], tri[:, 0]])
+    a, b = _unique_undirected(a, b, n)
+    return csr_from_undirected(n, a, b, np.ones(a.size), name)
+
+
 # ----------------------------------------------------------------------------------------------
 # Configs
 # ----------------------------------------------------------------------------------------------
@@ -211,6 +225,10 @@ CONFIGS = {
     "C3": dict(k=8, p=(1.5,)),
     "C4": dict(k=20, p=(2.0, 1.2)),
     "C5": dict(k=8, p=(1.2,)),
+    # the paper's workload shape (NEXT-3): Delaunay graphs of 2^r uniform points, unit weights
+    "D16": dict(k=4, p=(2.0, 1.5, 1.2)),
+    "D20": dict(k=4, p=(2.0, 1.5, 1.2)),
+    "D23": dict(k=8, p=(1.2,)),
 }
 
 
@@ -234,6 +252,9 @@ def make_config(name: str, seed: int = 0, n: int | None = None) -> Graph:
     if name == "C5":
         pts = uniform_square(rng, 8_388_608 if n is None else n)
         return knn_graph(pts, 6, "C5")
+    if name in ("D16", "D20", "D23"):
+        r = int(name[1:])
+        return delaunay_graph(rng, (1 << r) if n is None else n, name)
     raise KeyError(name)
 
 

@@ -47,9 +47,10 @@ def graph(name):
             from paper_2605_26975_b200 import plp as mod
             g0 = make_config("C5", n=100_000)
             g = permute_graph(g0, mod.rcm_order(g0.row_ptr, g0.col))
-        elif name in ("C5t", "C3t", "C2t"):
+        elif name in ("C5t", "C3t", "C2t", "D16t"):
             from paper_2605_26975_b200 import plp as mod
-            base = {"C5t": ("C5", 100_000), "C3t": ("C3", 40 ** 3), "C2t": ("C2", None)}[name]
+            base = {"C5t": ("C5", 100_000), "C3t": ("C3", 40 ** 3), "C2t": ("C2", None),
+                    "D16t": ("D16", None)}[name]
             g0 = make_config(base[0], n=base[1])
             g = permute_graph(g0, mod.tile_order(g0.row_ptr, g0.col))
         elif name == "P5":
@@ -104,6 +105,8 @@ CASES = [
     # tile-ordered graphs (tiled kernel: internal edges from shared memory, one power each)
     ("C5t", 8, 1.2), ("C5t", 8, 2.0), ("C5t", 8, 1.37), ("C5t", 8, 1.5), ("C5t", 4, 1.1),
     ("C5t", 16, 1.8), ("C3t", 8, 1.5), ("C2t", 2, 1.1), ("iso", 4, 1.2), ("C1", 20, 1.2),
+    # the paper's workload shape: Delaunay graph of 2^16 uniform points (NEXT-3), tile order
+    ("D16t", 8, 1.2), ("D16t", 4, 1.5), ("D16t", 8, 2.0),
 ]
 
 

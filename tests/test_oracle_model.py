@@ -344,3 +344,16 @@ def test_sharded_rows_with_halo_match_global():
     assert np.array_equal(Gl, G[r0:r1])
     Al = oracle.numerators(Loc, U[ext], p)
     assert np.all(Al <= A + 1e-12)
+
+
+def test_delaunay_generator_is_a_triangulation():
+    """The NEXT-3 stand-in for delaunay_n<r>: symmetric, connected, planar
+    (undirected edges <= 3n - 6, Euler), ~6n stored nonzeros, unit weights."""
+    from plp_inputs import delaunay_graph
+    g = delaunay_graph(streams(11)[0], 5000)
+    A = g.to_scipy()
+    assert (A != A.T).nnz == 0
+    assert csgraph.connected_components(A)[0] == 1
+    und = g.nnz // 2
+    assert und <= 3 * g.n - 6 and 5.5 * g.n < g.nnz < 6.0 * g.n
+    assert np.all(g.w == 1.0)
