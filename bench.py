@@ -40,7 +40,7 @@ CONFIG_DESC = {
     "D16": "Delaunay triangulation of 2^16 uniform points, unit weights, k=8, p=1.2",
 }
 CONFIG_KP = {"C5": (8, 1.2), "C3": (8, 1.5), "C4": (20, 1.2), "C2": (2, 1.1), "C1": (3, 1.2),
-             "D16": (8, 1.2), "D20": (8, 1.2), "D23": (8, 1.2)}
+             **{f"D{r}": (8, 1.2) for r in range(14, 24)}}
 
 
 def log(*a):

@@ -252,7 +252,7 @@ def make_config(name: str, seed: int = 0, n: int | None = None) -> Graph:
     if name == "C5":
         pts = uniform_square(rng, 8_388_608 if n is None else n)
         return knn_graph(pts, 6, "C5")
-    if name in ("D16", "D20", "D23"):
+    if name.startswith("D") and name[1:].isdigit():  # D<r>: delaunay_n<r> shape, 2^r points
         r = int(name[1:])
         return delaunay_graph(rng, (1 << r) if n is None else n, name)
     raise KeyError(name)
