@@ -141,7 +141,7 @@ def algorithmic_bytes(n: int, nnz: int, k: int) -> int:
 
 
 # ------------------------------------------------------------------------------------------------
-def cpu_oracle_sample(g, k, p, eps, rows_frac=0.25, reps=1):
+def cpu_oracle_sample(g, k, p, eps, rows_frac=0.25, reps=1, threads=None):
     """Time the fp64 oracle (as it stands) on rows [0, S) of the workload (a local CSR whose
     columns index an extended U, like one rank's shard).  Returns (GNNZ*k/s, seconds, desc, cores)."""
     import oracle
@@ -157,7 +157,10 @@ def cpu_oracle_sample(g, k, p, eps, rows_frac=0.25, reps=1):
     U = draw_U(g.n, k, 0)[ext]
     eta = draw_eta(g.n, k, 0)[ext]
     nnz_s = int(rp_loc[-1])
-    oracle.set_threads(os.cpu_count() or 1)
+    if threads is None:
+        oracle.set_threads(os.cpu_count() or 1)
+    else:
+        oracle.set_threads(threads)
     cores = oracle.get_threads()
     t0 = time.time()
     for _ in range(reps):
@@ -166,9 +169,31 @@ def cpu_oracle_sample(g, k, p, eps, rows_frac=0.25, reps=1):
         Hv = oracle.hessvec(Loc, U, eta, p, eps, "sparse", (A, B))
     dt = (time.time() - t0) / reps
     desc = (f"oracle F+grad+Hv (sparse) on rows [0,{S}) of the workload = {nnz_s} stored nonzeros "
-            f"x k={k} (fraction {rows_frac} of nnz), {cores} OpenMP threads")
+            f"x k={k} (fraction {rows_frac} of nnz), {cores} OpenMP threads on {cpu_model()}")
     del Gr, Hv
     return nnz_s * k / dt / 1e9, dt, desc, cores
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown CPU"
+
+
+def cpu_oracle_single_thread(g, k, p, eps, rows: int = 200_000):
+    """the oracle on one thread too (rows [0, rows) of the workload)."""
+    import oracle
+    v, dt, desc, cores = None, None, None, None
+    nthreads = oracle.get_threads()
+    try:
+        v, dt, desc, cores = cpu_oracle_sample(g, k, p, eps, rows_frac=rows / g.n, threads=1)
+    finally:
+        oracle.set_threads(nthreads)
+    return v, dt
 
 
 def run_reference(args, rank, world):
@@ -329,8 +354,10 @@ def run_plp(args, rank, world):
     cpu = None
     if not sharded and not args.no_cpu:
         v, dt, desc, cores = cpu_oracle_sample(g, k, p, eps, rows_frac=args.cpu_frac)
+        v1, dt1 = cpu_oracle_single_thread(g, k, p, eps)
         cpu = {"value": v, "unit": "GNNZ*k/s", "cores": cores, "kind": "oracle", "sample": desc,
-               "seconds": dt}
+               "seconds": dt, "single_thread_value": v1, "single_thread_seconds": dt1,
+               "cpu_model": cpu_model(), "nproc": os.cpu_count()}
     out = {"metric": "fused grad+Hv GNNZ*k/s", "value": value, "unit": "GNNZ*k/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
