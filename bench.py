@@ -80,8 +80,9 @@ def get_graph(name: str, order: str):
         log(f"[bench] {order} reorder in {time.time() - t0:.1f}s")
     try:
         os.makedirs(os.path.dirname(cache), exist_ok=True)
-        np.savez(cache + ".tmp.npz", n=g.n, rp=g.row_ptr, col=g.col, w=g.w)
-        os.replace(cache + ".tmp.npz", cache)
+        tmp = f"{cache}.{os.getpid()}.tmp.npz"  # one writer per process (ranks race on the cache)
+        np.savez(tmp, n=g.n, rp=g.row_ptr, col=g.col, w=g.w)
+        os.replace(tmp, cache)
     except Exception:
         pass
     return g

@@ -7,7 +7,7 @@ TAG=${1:-r01}
 OUT=gpurun_out
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/smi_$TAG.txt 2>&1
-python -m pytest tests -m gpu -q --timeout 1500 -p no:cacheprovider > $OUT/gpu_tests_$TAG.log 2>&1
+timeout 1700 python -m pytest tests -m gpu -q -p no:cacheprovider > $OUT/gpu_tests_$TAG.log 2>&1
 echo "TESTS_RC=$?" >> $OUT/gpu_tests_$TAG.log
 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke_$TAG.log 2>&1
 echo "SMOKE_RC=$?" >> $OUT/smoke_$TAG.log
@@ -22,6 +22,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
 echo "NCU_LAUNCHES_RC=$?" >> $OUT/ncu_launches_$TAG.log
 # full capture of the dominant kernel (edge pass) on the bench workload
 python tools/prof_edge.py --reps 3 > $OUT/prof_plain_$TAG.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k "regex:edge_(kernel|tiled_kernel)" -s 1 -c 1 \
+ncu --set full --clock-control none --import-source on -k "regex:edge_(halo_|staged_|tiled_)?kernel" -s 1 -c 1 \
     -o $OUT/prof_edge_$TAG python tools/prof_edge.py --reps 3 > $OUT/ncu_full_$TAG.log 2>&1
 echo "NCU_FULL_RC=$?" >> $OUT/ncu_full_$TAG.log

@@ -15,10 +15,8 @@ sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "paper_2605_26975_b200", "variants")
 
 VARIANTS = {
-    "t224b2": ["-DPLP_HALO_NBUF=2"],
-    "t160b3": ["-DPLP_HALO_NBUF=3", "-DPLP_HALO_TILE_ROWS=160"],
-    "t192b3": ["-DPLP_HALO_NBUF=3", "-DPLP_HALO_TILE_ROWS=192"],
-    "t128b3": ["-DPLP_HALO_NBUF=3", "-DPLP_HALO_TILE_ROWS=128"],
+    "h_c2": ["-DPLP_HALO_CPL8=2"],
+    "h_c4": ["-DPLP_HALO_CPL8=4"],
 }
 
 
