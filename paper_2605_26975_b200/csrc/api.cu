@@ -227,7 +227,8 @@ static plp_status build_tiles(plp_graph* g, const int64_t* rp, const int32_t* co
 // Halo tiles for edge_halo.cuh (see plp_graph): per tile of PLP_HALO_TILE consecutive rows its
 // sorted distinct outside columns, and per stored edge the tile-local neighbour index.  Skipped
 // (nullptr halo_enc) when a tile's buffers could not fit in shared memory even at k = 8.
-static plp_status build_halo_tiles(plp_graph* g, const int64_t* rp, const int32_t* col) {
+static plp_status build_halo_tiles(plp_graph* g, const int64_t* rp, const int32_t* col,
+                                   const double* w) {
   const int64_t n = g->n_rows;
   const int T = PLP_HALO_TILE;
   const int64_t nt = (n + T - 1) / T;
@@ -286,6 +287,43 @@ static plp_status build_halo_tiles(plp_graph* g, const int64_t* rp, const int32_
     return cuda_check(e, "cudaMalloc/cudaMemcpy(halo tiles)");
   g->halo_ext_cap = ext_cap;
   g->halo_nnz_cap = nnz_cap;
+  // objective mode: square graph, sorted rows, symmetric with bitwise equal weights
+  if (g->n_rows == g->n_cols) {
+    std::vector<int32_t> nlow((size_t)n + 16, 0);
+    bool ok = true;
+    for (int64_t i = 0; i < n && ok; ++i) {
+      int32_t cnt = 0;
+      for (int64_t e = rp[i]; e < rp[i + 1]; ++e) {
+        const int64_t j = col[e];
+        if (e > rp[i] && col[e - 1] >= j) { ok = false; break; }
+        cnt += j < i;
+        const int32_t* b = col + rp[j];
+        const int32_t* f = std::lower_bound(b, col + rp[j + 1], (int32_t)i);
+        if (f == col + rp[j + 1] || *f != i || w[rp[j] + (f - b)] != w[e] || j == i) { ok = false; break; }
+      }
+      nlow[i] = cnt;
+    }
+    if (ok) {
+      // objective-mode schedule: within each 32-row window, rows by decreasing upper-edge count
+      // (the objective loop of a row pass runs over its rows' upper edges only)
+      std::vector<int32_t> sup((size_t)n + 16, 0);
+      for (int64_t w0 = 0; w0 < n; w0 += kSchedWindow) {
+        const int64_t w1 = std::min<int64_t>(n, w0 + kSchedWindow);
+        for (int64_t i = w0; i < w1; ++i) sup[i] = (int32_t)i;
+        std::stable_sort(sup.begin() + w0, sup.begin() + w1, [&](int32_t x, int32_t y) {
+          return (rp[x + 1] - rp[x] - nlow[x]) > (rp[y + 1] - rp[y] - nlow[y]);
+        });
+      }
+      if ((e = cudaMalloc(&g->nlow, sizeof(int32_t) * nlow.size())) != cudaSuccess ||
+          (e = cudaMemcpy(g->nlow, nlow.data(), sizeof(int32_t) * nlow.size(), cudaMemcpyHostToDevice)) !=
+              cudaSuccess ||
+          (e = cudaMalloc(&g->sched_up, sizeof(int32_t) * sup.size())) != cudaSuccess ||
+          (e = cudaMemcpy(g->sched_up, sup.data(), sizeof(int32_t) * sup.size(), cudaMemcpyHostToDevice)) !=
+              cudaSuccess)
+        return cuda_check(e, "cudaMalloc/cudaMemcpy(nlow)");
+      g->upper_ok = true;
+    }
+  }
   return PLP_OK;
 }
 
@@ -353,7 +391,7 @@ extern "C" plp_status plp_create_graph(plp_ctx* ctx, int64_t n_rows, int64_t n_c
     return cuda_check(e, "cudaMemcpy(graph)");
   }
   plp_status st = build_tiles(g, row_ptr, col);
-  if (!st) st = build_halo_tiles(g, row_ptr, col);
+  if (!st) st = build_halo_tiles(g, row_ptr, col, w);
   if (st) {
     plp_destroy_graph(g);
     return st;
@@ -379,6 +417,8 @@ extern "C" plp_status plp_destroy_graph(plp_graph* g) {
   cudaFree(g->sched);
   cudaFree(g->halo_enc);
   cudaFree(g->halo_ext);
+  cudaFree(g->nlow);
+  cudaFree(g->sched_up);
   cudaFree(g->enc);
   cudaFree(g->ext_col);
   cudaFree(g->tile_meta);

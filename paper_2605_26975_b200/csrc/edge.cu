@@ -212,6 +212,9 @@ static EdgeArgs graph_args(const plp_graph* g) {
   a.halo_ext = g->halo_ext;
   a.halo_ext_cap = g->halo_ext_cap;
   a.halo_nnz_cap = g->halo_nnz_cap;
+  a.nlow = g->nlow;
+  a.sched_up = g->sched_up;
+  a.upper_ok = g->upper_ok ? 1 : 0;
   if (const char* v = getenv("PLP_DEBUG_LDX")) a.ldx = atoi(v);  // layout experiments only
   if (g->tiled) {
     a.enc = g->enc;

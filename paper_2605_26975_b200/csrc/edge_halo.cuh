@@ -34,13 +34,14 @@ static_assert(kHaloT % kSchedWindow == 0 && kHaloThreads <= 16 * 32, "tile map (
 
 // Per-buffer shared-memory layout (bytes), identical on host and device.
 struct HaloLayout {
-  unsigned rp, sched, enc, w, U, E, bytes;
+  unsigned rp, sched, nl, enc, w, U, E, bytes;
 };
-__host__ __device__ inline HaloLayout halo_layout(int k, int ext_cap, int nnz_cap) {
+__host__ __device__ inline HaloLayout halo_layout(int k, int ext_cap, int nnz_cap, bool obj = false) {
   HaloLayout L;
   unsigned o = 0;
   L.rp = o; o += (kHaloT + 8) * 4;
   L.sched = o; o += kHaloT * 4;
+  L.nl = o; o += obj ? (kHaloT + 8) * 4 : 0u;  // lower-edge counts (objective mode only)
   L.enc = o; o += (unsigned)(nnz_cap + 16) * 4;
   o = (o + 15u) & ~15u;
   L.w = o; o += (unsigned)(nnz_cap + 16) * 8;
@@ -61,8 +62,9 @@ __host__ __device__ inline unsigned halo_lists_off(bool tables) { return kHaloHe
 __host__ __device__ inline unsigned halo_bufs_off(int ext_cap, bool tables) {
   return (halo_lists_off(tables) + 3u * (unsigned)(ext_cap + 4) * 4u + 127u) & ~127u;
 }
-__host__ __device__ inline unsigned halo_smem_bytes(int k, int ext_cap, int nnz_cap, bool tables) {
-  return halo_bufs_off(ext_cap, tables) + (unsigned)kHaloNBuf * halo_layout(k, ext_cap, nnz_cap).bytes;
+__host__ __device__ inline unsigned halo_smem_bytes(int k, int ext_cap, int nnz_cap, bool tables,
+                                                    bool obj = false) {
+  return halo_bufs_off(ext_cap, tables) + (unsigned)kHaloNBuf * halo_layout(k, ext_cap, nnz_cap, obj).bytes;
 }
 #ifndef PLP_HALO_CTAS
 #define PLP_HALO_CTAS 1  // resident CTAs per SM (each with its own double buffer)
@@ -84,8 +86,12 @@ constexpr unsigned kHaloSmemMax = 225u * 1024u / PLP_HALO_CTAS;
 template <int K>
 constexpr int halo_cpl() { return K == 8 ? PLP_HALO_CPL8 : K == 16 ? 4 : 2; }
 
-template <int K, class POW, bool HAS_ETA>
-__global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(EdgeArgs a, POW pw) {
+// OBJ: objective-only pass (no eta, no G) on a symmetric graph: A_l = sum over the upper-triangle
+// edges (j > i) of w_ij |u_il - u_jl|^p, i.e. Eq. (1)'s numerator with each undirected edge once
+// (half the powers of the row form); B_l from the node terms as usual.
+template <int K, class POW, bool HAS_ETA, bool OBJ>
+__global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(POW pw, EdgeArgs a) {
+  static_assert(!(OBJ && HAS_ETA), "objective mode has no eta");
   constexpr int CPL = halo_cpl<K>(), LPR = K / CPL, RPW = 32 / LPR;  // rows per pass
   constexpr int NS = kSchedWindow / RPW;               // rank slices per 32-row window
   static_assert(NS % 2 == 0 || NS == 2, "slice count");
@@ -97,7 +103,7 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
   const int ext_cap = a.halo_ext_cap;
   const int LS = ext_cap + 4;  // list slot: n_ext, eb, ee, pad, columns
   int* lists = reinterpret_cast<int*>(smem + halo_lists_off(POW::kNeedsTables));
-  const HaloLayout Ly = halo_layout(K, ext_cap, a.halo_nnz_cap);
+  const HaloLayout Ly = halo_layout(K, ext_cap, a.halo_nnz_cap, OBJ);
   unsigned char* buf0 = smem + halo_bufs_off(ext_cap, POW::kNeedsTables);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int grp = lane / LPR, li = lane % LPR, c0 = li * CPL;
@@ -152,9 +158,10 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
       const int cb = eb & ~3, ce = (ee + 3) & ~3, wb = eb & ~1, we = (ee + 1) & ~1;
       const unsigned enc_b = (unsigned)(ce - cb) * 4u, w_b = (unsigned)(we - wb) * 8u;
       const unsigned own_b = (unsigned)(r1 - r0) * RB;
-      mbar_expect_tx(&full[b], rp_b + sc_b + enc_b + w_b + (HAS_ETA ? 2u : 1u) * own_b);
+      mbar_expect_tx(&full[b], rp_b + (OBJ ? 2u : 1u) * sc_b + enc_b + w_b + (HAS_ETA ? 2u : 1u) * own_b);
       tma_bulk_g2s(B + Ly.rp, a.rp + r0, rp_b, &full[b]);
-      tma_bulk_g2s(B + Ly.sched, a.sched + r0, sc_b, &full[b]);
+      tma_bulk_g2s(B + Ly.sched, (OBJ ? a.sched_up : a.sched) + r0, sc_b, &full[b]);
+      if constexpr (OBJ) tma_bulk_g2s(B + Ly.nl, a.nlow + r0, sc_b, &full[b]);
       if (enc_b) {
         tma_bulk_g2s(B + Ly.enc, a.halo_enc + cb, enc_b, &full[b]);
         tma_bulk_g2s(B + Ly.w, a.w + wb, w_b, &full[b]);
@@ -244,6 +251,80 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
       double ui[CPL], ei[CPL];
       lds_vec<CPL>(tU + lrow * K, ui);
       if constexpr (HAS_ETA) lds_vec<CPL>(tE + lrow * K, ei);
+      if constexpr (OBJ) {
+        // ---- objective mode: the row's upper-triangle edges [e0 + nlow, e1) only ----
+        const int* nl_s = reinterpret_cast<const int*>(B + Ly.nl);
+        const int eu = e0 + nl_s[lrow];
+        double Ar[CPL];
+        unsigned mx = 0;
+#pragma unroll
+        for (int cc = 0; cc < CPL; ++cc) Ar[cc] = 0.0;
+        auto obj_edge = [&](double wv, const double (&uj)[CPL]) {
+#pragma unroll
+          for (int cc = 0; cc < CPL; ++cc) {
+            const double d = ui[cc] - uj[cc];
+            if constexpr (POW::kIsP2) {
+              Ar[cc] = fma(wv * d, d, Ar[cc]);
+            } else {
+              mx = max(mx, (unsigned)__double2hiint(d) * 2u - pw.fast_lo2);
+              const double ws = wv * pw.pow_fast(d);  // w |d|^{p-2}
+              Ar[cc] = fma(ws, d * d, Ar[cc]);        // w |d|^p
+            }
+          }
+        };
+        int e = eu;
+#pragma unroll 1
+        for (; e + 1 < e1; e += 2) {
+          const int x0 = enc_s[e], x1 = enc_s[e + 1];
+          const double w0 = w_s[e], w1 = w_s[e + 1];
+          double uj0[CPL], uj1[CPL];
+          lds_vec<CPL>(tU + x0 * K, uj0);
+          lds_vec<CPL>(tU + x1 * K, uj1);
+          obj_edge(w0, uj0);
+          obj_edge(w1, uj1);
+        }
+        if (e < e1) {
+          double uj0[CPL];
+          lds_vec<CPL>(tU + enc_s[e] * K, uj0);
+          obj_edge(w_s[e], uj0);
+        }
+        double tn[CPL];
+#pragma unroll
+        for (int cc = 0; cc < CPL; ++cc) {
+          const double au = fabs(ui[cc]);
+          if constexpr (POW::kIsP2) {
+            tn[cc] = au;
+          } else {
+            mx = max(mx, (unsigned)__double2hiint(au) * 2u - pw.fast_lo2);
+            tn[cc] = pw.pow_fast(au) * au;
+          }
+        }
+        if constexpr (!POW::kIsP2) {
+          if (mx >= pw.fast_span2) {  // rare: exact libdevice recomputation of the row
+#pragma unroll
+            for (int cc = 0; cc < CPL; ++cc) {
+              Ar[cc] = 0.0;
+              double sn;
+              pw.eval(fabs(ui[cc]), sn, tn[cc]);
+            }
+            for (int ee = eu; ee < e1; ++ee) {
+              const int64_t j = a.col[ee];
+              const double wv = a.w[ee];
+#pragma unroll
+              for (int cc = 0; cc < CPL; ++cc) {
+                const double ad = fabs(ui[cc] - a.U[j * K + c0 + cc]);
+                Ar[cc] += wv * ((ad != 0.0) ? pow(ad, a.p) : 0.0);
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int cc = 0; cc < CPL; ++cc) {
+          accA[cc] += Ar[cc];
+          accB[cc] = fma(tn[cc], fabs(ui[cc]), accB[cc]);
+        }
+        continue;
+      }
       double L[CPL], HA[CPL];
       unsigned mx = 0;
 #pragma unroll
@@ -367,10 +448,10 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
   }
 }
 
-template <int K, class POW, bool HAS_ETA>
+template <int K, class POW, bool HAS_ETA, bool OBJ>
 plp_status launch_halo_shape(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int* grid_out) {
-  auto kern = edge_halo_kernel<K, POW, HAS_ETA>;
-  const unsigned smem = halo_smem_bytes(K, a.halo_ext_cap, a.halo_nnz_cap, POW::kNeedsTables);
+  auto kern = edge_halo_kernel<K, POW, HAS_ETA, OBJ>;
+  const unsigned smem = halo_smem_bytes(K, a.halo_ext_cap, a.halo_nnz_cap, POW::kNeedsTables, OBJ);
   static unsigned attr_set = 0;
   if (attr_set < smem) {
     PLP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -380,9 +461,10 @@ plp_status launch_halo_shape(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int
   int64_t grid = (int64_t)ctx->num_sms * PLP_HALO_CTAS;
   if (grid > ctx->max_ctas) grid = ctx->max_ctas;
   if (grid > n_tiles) grid = n_tiles > 0 ? n_tiles : 1;
-  kern<<<(int)grid, kHaloThreads, smem, ctx->stream>>>(a, pw);
+  kern<<<(int)grid, kHaloThreads, smem, ctx->stream>>>(pw, a);
   PLP_LAUNCH_CHECK("edge_halo_kernel");
-  note_edge_kernel("edge_halo_kernel", K, halo_cpl<K>(), K / halo_cpl<K>(), 2, POW::kName, HAS_ETA);
+  note_edge_kernel(OBJ ? "edge_halo_kernel[objective]" : "edge_halo_kernel", K, halo_cpl<K>(),
+                   K / halo_cpl<K>(), 2, POW::kName, HAS_ETA);
   *grid_out = (int)grid;
   return PLP_OK;
 }
@@ -400,9 +482,11 @@ plp_status try_launch_halo(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int* 
   if (halo_smem_bytes(k, a.halo_ext_cap, a.halo_nnz_cap, POW::kNeedsTables) > kHaloSmemMax) return PLP_OK;
   *used = true;
   const bool he = a.eta != nullptr;
+  const bool obj = !he && a.G == nullptr && a.upper_ok && a.nlow != nullptr && a.sched_up != nullptr;
 #define PLP_HSHAPE(K)                                                                      \
-  return he ? launch_halo_shape<K, POW, true>(ctx, a, pw, grid)                            \
-            : launch_halo_shape<K, POW, false>(ctx, a, pw, grid)
+  return he ? launch_halo_shape<K, POW, true, false>(ctx, a, pw, grid)                     \
+            : (obj ? launch_halo_shape<K, POW, false, true>(ctx, a, pw, grid)               \
+                   : launch_halo_shape<K, POW, false, false>(ctx, a, pw, grid))
 #ifdef PLP_TUNE_ONLY
   PLP_HSHAPE(8);
 #else

@@ -60,6 +60,11 @@ struct plp_graph {
   int32_t* halo_ext = nullptr;
   int halo_ext_cap = 0;  // max halo rows per tile (rounded up to 4)
   int halo_nnz_cap = 0;  // max stored edges per tile (rounded up to 4)
+  // objective mode (A over the upper triangle): the graph is square, symmetric with bitwise equal
+  // weights and sorted rows; nlow[i] = stored edges of row i with col < i
+  bool upper_ok = false;
+  int32_t* nlow = nullptr;
+  int32_t* sched_up = nullptr;  // rows by decreasing upper-edge count within 32-row windows
 };
 // rows per degree-sorting window: small enough that a CTA's rows per iteration stay contiguous
 // (neighbour rows of a tile-ordered graph then hit L1)
@@ -120,6 +125,9 @@ struct EdgeArgs {
   const int32_t* halo_enc;
   const int32_t* halo_ext;
   int halo_ext_cap, halo_nnz_cap;
+  const int32_t* nlow;  // objective mode (edge_halo.cuh)
+  const int32_t* sched_up;
+  int upper_ok;
 };
 plp_status launch_edge(plp_ctx* ctx, const EdgeArgs& a, int* grid_out);
 // Fixed-order reduction of edge partials: AB_out (2k), dots_out (2k), F (1); any may be null.
