@@ -43,8 +43,11 @@ SYMBOLS = [
     "plp_hessvec", "plp_fgrad_hessvec", "plp_edge_pass", "plp_full_epilogue",
     "plp_objective_from_ab", "plp_gram", "plp_project", "plp_apply_sub", "plp_retract",
     "plp_cholesky", "plp_apply_rinv", "plp_dot", "plp_axpby", "plp_gather_rows", "plp_kmeans",
-    "plp_rcut", "plp_debug_pow", "plp_tile_order", "plp_last_edge_kernel",
+    "plp_rcut", "plp_debug_pow", "plp_tile_order", "plp_last_edge_kernel", "plp_tcg_init",
+    "plp_tcg_run",
 ]
+TCG_STATUS = {0: "running", 1: "boundary", 2: "negative_curvature", 3: "converged", 4: "maxiter",
+              5: "interior"}
 TILE_ROWS = 120  # PLP_TILE_ROWS in include/plp.h
 
 
@@ -306,6 +309,26 @@ def axpby(ctx: Context, a: float, x, b: float, y):
     _ck(_lib.plp_axpby(ctx.h, C_I64(n), k, C_D(a), _dev(x, "x"), C_D(b), _dev(y, "y", shape=(n, k))),
         "plp_axpby")
     return y
+
+
+def tcg_init(ctx: Context, grad, delta: float, kappa: float, theta: float, eta, Heta, r, dlt, scal, status):
+    n, k = grad.shape
+    _ck(_lib.plp_tcg_init(ctx.h, C_I64(n), k, _dev(grad, "grad"), C_D(delta), C_D(kappa), C_D(theta),
+                          _dev(eta, "eta", shape=(n, k)), _dev(Heta, "Heta", shape=(n, k)),
+                          _dev(r, "r", shape=(n, k)), _dev(dlt, "dlt", shape=(n, k)),
+                          _dev(scal, "scal", shape=(16,)), _dev(status, "status", dtype=torch.int32)),
+        "plp_tcg_init")
+
+
+def tcg_run(ctx: Context, g: Graph, U, AB, G_in, S, p: float, eps: float, mode: int, eta, Heta, r, dlt,
+            Hd, scal, status, max_iters: int, iters: int):
+    k = U.shape[1]
+    _ck(_lib.plp_tcg_run(ctx.h, g.h, k, _dev(U, "U", shape=(g.n_cols, k)), _dev(AB, "AB", shape=(2 * k,)),
+                         _dev(G_in, "G_in", shape=(g.n_rows, k), nullable=True), _dev(S, "S", shape=(k, k)),
+                         C_D(p), C_D(eps), int(mode), _dev(eta, "eta"), _dev(Heta, "Heta"), _dev(r, "r"),
+                         _dev(dlt, "dlt"), _dev(Hd, "Hd"), _dev(scal, "scal", shape=(16,)),
+                         _dev(status, "status", dtype=torch.int32), int(max_iters), int(iters)),
+        "plp_tcg_run")
 
 
 def gather_rows(ctx: Context, idx, X, out=None):

@@ -38,6 +38,8 @@ class SolverConfig:
     tcg_max_iters: int | None = None    # default min(2 n k, 1000)
     hessian_mode: int = plp.HESS_SPARSE
     eps: float = 1e-9
+    device_tcg: bool = True            # tCG recurrences on the device (plp_tcg_run), no per-iteration D2H
+    tcg_batch: int = 8                 # iterations launched between two status reads
 
     def resolved(self, n: int, k: int) -> "SolverConfig":
         c = SolverConfig(**self.__dict__)
@@ -112,6 +114,29 @@ class GrassmannTR:
     def _dot(self, x, y) -> float:
         return float(plp.dot(self.ctx, x, y).item())
 
+    # -- truncated CG on the device (plp_tcg_init / plp_tcg_run): same recurrences, no host sync
+    # per iteration; the status is read once per `tcg_batch` iterations -------------------------
+    def tcg_device(self, st: _State, p: float, delta: float):
+        c = self.cfg
+        ctx = self.ctx
+        if not hasattr(self, "_tcg_buf") or self._tcg_buf[0].shape != st.grad.shape:
+            z = lambda: torch.empty_like(st.grad)  # noqa: E731
+            self._tcg_buf = (z(), z(), z(), z(), z(),
+                             torch.zeros(16, dtype=torch.float64, device=st.grad.device),
+                             torch.zeros(2, dtype=torch.int32, device=st.grad.device))
+        eta, Heta, r, dlt, Hd, scal, status = self._tcg_buf
+        plp.tcg_init(ctx, st.grad, delta, c.tcg_kappa, c.tcg_theta, eta, Heta, r, dlt, scal, status)
+        G_in = st.G if c.hessian_mode == plp.HESS_FULL else None
+        done = 0
+        stv = status.cpu().tolist()
+        while stv[0] == 0 and done < c.tcg_max_iters:
+            batch = min(c.tcg_batch, c.tcg_max_iters - done)
+            plp.tcg_run(ctx, self.g, st.U, st.AB, G_in, st.S, p, c.eps, c.hessian_mode, eta, Heta, r, dlt,
+                        Hd, scal, status, c.tcg_max_iters, batch)
+            done += batch
+            stv = status.cpu().tolist()
+        return eta.clone(), Heta.clone(), int(stv[1]), plp.TCG_STATUS[int(stv[0])]
+
     # -- truncated CG (Steihaug-Toint; Absil-Baker-Gallivan 2007, Alg. 2) ------------------------
     def tcg(self, st: _State, p: float, delta: float):
         c = self.cfg
@@ -172,7 +197,10 @@ class GrassmannTR:
                 trace.records.append(IterRecord(p, it, st.Fv, gnorm, delta, 0, "stop", math.nan, False,
                                                 1e3 * (time.perf_counter() - t0)))
                 break
-            eta, Heta, nit, status = self.tcg(st, p, delta)
+            if c.device_tcg:
+                eta, Heta, nit, status = self.tcg_device(st, p, delta)
+            else:
+                eta, Heta, nit, status = self.tcg(st, p, delta)
             model_dec = -self._dot(st.grad, eta) - 0.5 * self._dot(eta, Heta)
             try:
                 U_new = plp.retract(ctx, st.U, eta)

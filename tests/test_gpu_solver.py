@@ -84,3 +84,22 @@ def test_end_to_end_labels_and_rcut_match_oracle(mods, cfg, n, k, sched):
     for p in sched:
         Fs = [r.F for r in tr.records if r.p == p and r.accepted]
         assert all(b <= a + 1e-15 * abs(a) for a, b in zip(Fs, Fs[1:]))
+
+
+@pytest.mark.parametrize("p,delta,mode", [(1.5, 0.3, 0), (1.2, 5.0, 0), (2.0, 0.05, 0), (1.5, 0.3, 1)])
+def test_device_tcg_matches_host_tcg_bitwise(mods, p, delta, mode):
+    """plp_tcg_run keeps the tCG scalars on the device; its recurrences are written in the host
+    loop's order with explicit rounding, so step, H step, iteration count and exit status equal
+    the host-driven tCG bit for bit (boundary, interior-convergence and full-Hessian cases)."""
+    plp, solver, ctx = mods
+    g = make_config("C2", n=5000)
+    k = 2
+    Z = draw_U(g.n, k, 4)
+    Uo, _ = oracle.retract(Z, np.zeros_like(Z))
+    G = plp.Graph(ctx, g.row_ptr, g.col, g.w)
+    tr = solver.GrassmannTR(ctx, G, k, solver.SolverConfig(hessian_mode=mode))
+    st = solver._State(tr, torch.from_numpy(Uo).cuda(), p)
+    a = tr.tcg(st, p, delta)
+    b = tr.tcg_device(st, p, delta)
+    assert a[2:] == b[2:], (a[2:], b[2:])
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
