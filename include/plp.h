@@ -232,25 +232,33 @@ plp_status plp_rcut(plp_ctx* ctx, const plp_graph* g, int clusters, const int32_
 /* Device-resident truncated CG ("truncated conjugate      */
 /* gradient scheme")                                                                */
 /* ---------------------------------------------------------------------------------------------- */
+#define PLP_TCG_SCAL_LEN 4160 /* doubles in the tCG scalar/matrix workspace `scal` */
 enum {
   PLP_TCG_RUNNING = 0, PLP_TCG_BOUNDARY = 1, PLP_TCG_NEGATIVE_CURVATURE = 2, PLP_TCG_CONVERGED = 3,
   PLP_TCG_MAXITER = 4, PLP_TCG_INTERIOR = 5
 };
 /* Steihaug-Toint tCG for min <grad, s> + <s, H s>/2, ||s|| <= delta, with the Riemannian Hessian
  * H(x) = P_U(EucHess[x]) - x S of solver.py (reading #21).  All vectors are device n x k (n =
- * the graph's rows), scal a device double[16] and status a device int[2] = {status, iterations}.
+ * the graph's rows), scal a device double[PLP_TCG_SCAL_LEN] and status a device int[2] =
+ * {status, iterations}.
  * plp_tcg_init: eta = Heta = 0, r = grad, delta_dir = -grad, scalars (stop tolerance
  * ||g|| min(||g||^theta, kappa)); status INTERIOR if grad = 0.
  * plp_tcg_run: `iters` iterations (launches only, no synchronisation; iterations after the exit
- * condition change nothing), Hd a work array; the recurrences are bitwise those of solver.py's
- * host loop.  Read `status` to know when it stopped; eta / Heta are the step and H step. */
+ * condition leave eta, Heta and delta_dir unchanged), Hd a work array.  fused = 0: the
+ * recurrences are bitwise those of solver.py's host loop (projection, curvature term, dots and
+ * axpbys as separate passes).  fused = 1 (k = 8 or 16, 16-byte aligned vectors; else PLP_ERR_ARG):
+ * after the edge pass, three streaming passes on the fp64 tensor cores:
+ * <d, Hd> from the Grams U^T EH, U^T d, d^T d; the eta / Heta / r updates with Hd = EH - U U^T EH
+ * - d S formed in registers, U^T r and ||r||^2; then r's re-projection and the new direction --
+ * the same iteration up to rounding order.  Read `status` to know when it stopped; eta / Heta are
+ * the step and H step. */
 plp_status plp_tcg_init(plp_ctx* ctx, int64_t n, int k, const double* grad, double delta, double kappa,
                         double theta, double* eta, double* Heta, double* r, double* delta_dir,
                         double* scal, int* status);
 plp_status plp_tcg_run(plp_ctx* ctx, const plp_graph* g, int k, const double* U, const double* AB,
                        const double* G_in, const double* S, double p, double eps, int mode, double* eta,
                        double* Heta, double* r, double* delta_dir, double* Hd, double* scal,
-                       int* status, int max_iters, int iters);
+                       int* status, int max_iters, int iters, int fused);
 
 /* ---------------------------------------------------------------------------------------------- */
 /* Diagnostics                                                                                      */

@@ -7,17 +7,24 @@
 // CUDA graph.  The scalar kernels use explicitly rounded fp64 operations in the host code's order
 // (no FMA contraction), so the device recurrence is bitwise that of solver.py's loop; after the
 // exit condition every further iteration is a no-op for eta, Heta, r and delta.
+#include <algorithm>
 #include <cmath>
 
+#include "dense_mma.cuh"
 #include "plp_internal.h"
 
 namespace plp {
 
-// scalar slots (double sc[16]) and status (int st[2] = {status, iterations})
+// scalar slots (double sc[PLP_TCG_SCAL_LEN]) and status (int st[2] = {status, iterations});
+// the fused path also keeps k x k matrices in sc: M1 = U^T EH, M2 = U^T d, Gdd = d^T d,
+// MR = U^T r (slots of PLP_MAX_K^2 from kMat)
 enum {
   kZr = 0, kStopTol = 1, kDelta = 2, kEPe = 3, kEPd = 4, kDPd = 5, kDHd = 6, kAlpha = 7,
-  kZnew = 9, kCEta = 10, kCR = 11, kCA = 12, kCB = 13
+  kZnew = 9, kCEta = 10, kCR = 11, kCA = 12, kCB = 13, kTrDE = 14, kZraw = 15, kMat = 64
 };
+constexpr int kM1 = kMat, kM2 = kMat + PLP_MAX_K * PLP_MAX_K, kGdd = kMat + 2 * PLP_MAX_K * PLP_MAX_K,
+              kMR = kMat + 3 * PLP_MAX_K * PLP_MAX_K;
+static_assert(kMR + PLP_MAX_K * PLP_MAX_K <= PLP_TCG_SCAL_LEN, "scal too short");
 
 __global__ void tcg_init_kernel(double* sc, int* st, double delta, double kappa, double theta) {
   const double zr = sc[kZr];
@@ -33,7 +40,7 @@ __global__ void tcg_init_kernel(double* sc, int* st, double delta, double kappa,
 }
 
 // after <delta, H delta>: step length, trust-boundary / negative-curvature exit
-__global__ void tcg_scalar_a_kernel(double* sc, int* st) {
+__device__ void tcg_scalar_a(double* sc, int* st) {
   if (st[0] != PLP_TCG_RUNNING) {
     sc[kCEta] = 0.0;
     sc[kCR] = 0.0;
@@ -61,19 +68,21 @@ __global__ void tcg_scalar_a_kernel(double* sc, int* st) {
   sc[kCR] = alpha;
 }
 
-// after <r, r>: convergence test, conjugation
-__global__ void tcg_scalar_b_kernel(double* sc, int* st, int max_iters) {
+__global__ void tcg_scalar_a_kernel(double* sc, int* st) { tcg_scalar_a(sc, st); }
+
+// after <r, r>: convergence test, conjugation; returns whether the iteration goes on
+__device__ bool tcg_scalar_b(double* sc, int* st, int max_iters) {
   if (st[0] != PLP_TCG_RUNNING) {
     sc[kCA] = 0.0;
     sc[kCB] = 1.0;
-    return;
+    return false;
   }
   const double znew = sc[kZnew];
   if (sqrt(znew) <= sc[kStopTol]) {
     st[0] = PLP_TCG_CONVERGED;
     sc[kCA] = 0.0;
     sc[kCB] = 1.0;
-    return;
+    return false;
   }
   const double zr = sc[kZr], alpha = sc[kAlpha], ePd = sc[kEPd], dPd = sc[kDPd];
   const double beta = __ddiv_rn(znew, zr);
@@ -83,6 +92,377 @@ __global__ void tcg_scalar_b_kernel(double* sc, int* st, int max_iters) {
   sc[kEPd] = __dmul_rn(beta, __dadd_rn(ePd, __dmul_rn(alpha, dPd)));
   sc[kDPd] = __dadd_rn(znew, __dmul_rn(__dmul_rn(beta, beta), dPd));
   if (st[1] >= max_iters) st[0] = PLP_TCG_MAXITER;
+  return true;
+}
+
+__global__ void tcg_scalar_b_kernel(double* sc, int* st, int max_iters) { tcg_scalar_b(sc, st, max_iters); }
+
+// ---------------------------------------------------------------------------------------------
+// Fused iteration for k = 8 KT: after the edge pass writes EH =
+// EucHess[d], three streaming passes replace the nine tall-skinny launches of the unfused loop.
+// With d horizontal (U^T d = 0 up to rounding) and Hd = EH - U M1 - d S, M1 = U^T EH:
+//   <d, Hd> = tr(d^T EH) - <U^T d, M1>_F - <d^T d, S>_F                    (pass A: Grams only)
+//   eta += c d, Heta += c Hd, r += c' Hd, MR = U^T r, ||r||^2                (pass B: Hd never stored)
+//   r <- r - U MR (the residual's re-projection), ||P r||^2 = ||r||^2 - ||MR||_F^2,
+//   d <- -r + beta d                                                          (pass C)
+// All Grams and the k x k applies run on the fp64 tensor cores (dmma884, as dense_mma.cuh).
+// ---------------------------------------------------------------------------------------------
+constexpr int kTcgThreads = 256, kTcgWarps = kTcgThreads / 32;
+
+// pass A: partials of [M1 | M2 | Gdd | tr(d^T EH)] over 4-row blocks
+template <int KT>
+__global__ void __launch_bounds__(kTcgThreads) tcg_gram_a_kernel(int64_t n, const double* __restrict__ U,
+                                                                 const double* __restrict__ EH,
+                                                                 const double* __restrict__ D,
+                                                                 double* __restrict__ part) {
+  constexpr int K = 8 * KT, KK = K * K, E = 3 * KK + 1;
+  __shared__ double red[E];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  for (int e = threadIdx.x; e < E; e += kTcgThreads) red[e] = 0.0;
+  double m1[KT][KT][2], m2[KT][KT][2], gd[KT][KT][2], tr = 0.0;
+#pragma unroll
+  for (int i = 0; i < KT; ++i)
+#pragma unroll
+    for (int j = 0; j < KT; ++j) m1[i][j][0] = m1[i][j][1] = m2[i][j][0] = m2[i][j][1] = gd[i][j][0] = gd[i][j][1] = 0.0;
+  double de[KT][2];
+#pragma unroll
+  for (int i = 0; i < KT; ++i) de[i][0] = de[i][1] = 0.0;
+  const int64_t blocks = (n + 3) / 4;
+  const int64_t tw = (int64_t)gridDim.x * kTcgWarps, wid = (int64_t)blockIdx.x * kTcgWarps + warp;
+  const int64_t b0 = blocks * wid / tw, b1 = blocks * (wid + 1) / tw;
+  constexpr int UNR = 2;
+  for (int64_t b = b0; b < b1; b += UNR) {
+    double u[UNR][KT], h[UNR][KT], dd[UNR][KT];
+#pragma unroll
+    for (int v = 0; v < UNR; ++v) {
+      const int64_t r = 4 * (b + v) + q;
+      const bool ok = b + v < b1 && r < n;
+#pragma unroll
+      for (int t = 0; t < KT; ++t) {
+        const int64_t o = r * K + 8 * t + g;
+        u[v][t] = ok ? __ldg(U + o) : 0.0;
+        h[v][t] = ok ? __ldg(EH + o) : 0.0;
+        dd[v][t] = ok ? __ldg(D + o) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < UNR; ++v) {
+#pragma unroll
+      for (int i = 0; i < KT; ++i) {
+#pragma unroll
+        for (int j = 0; j < KT; ++j) {
+          dmma884(m1[i][j][0], m1[i][j][1], u[v][i], h[v][j]);
+          dmma884(m2[i][j][0], m2[i][j][1], u[v][i], dd[v][j]);
+          dmma884(gd[i][j][0], gd[i][j][1], dd[v][i], dd[v][j]);
+        }
+        dmma884(de[i][0], de[i][1], dd[v][i], h[v][i]);
+      }
+    }
+  }
+  // diagonal of the d^T EH tiles: element (8i + g, 8i + 2q + h) is diagonal iff g == 2q + h
+#pragma unroll
+  for (int i = 0; i < KT; ++i) tr += (g == 2 * q ? de[i][0] : 0.0) + (g == 2 * q + 1 ? de[i][1] : 0.0);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
+  __syncthreads();
+  for (int w = 0; w < kTcgWarps; ++w) {
+    if (warp == w) {
+#pragma unroll
+      for (int i = 0; i < KT; ++i)
+#pragma unroll
+        for (int j = 0; j < KT; ++j)
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int e = (8 * i + g) * K + 8 * j + 2 * q + hh;
+            red[e] += m1[i][j][hh];
+            red[KK + e] += m2[i][j][hh];
+            red[2 * KK + e] += gd[i][j][hh];
+          }
+      if (lane == 0) red[3 * KK] += tr;
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < E; e += kTcgThreads) part[(int64_t)blockIdx.x * E + e] = red[e];
+}
+
+// sum the pass-A partials (fixed order), then <d, Hd> and the step-length decision
+template <int K>
+__global__ void __launch_bounds__(1024) tcg_fused_a_kernel(int grid, const double* __restrict__ part,
+                                                           const double* __restrict__ S, double* sc, int* st) {
+  constexpr int KK = K * K, E = 3 * KK + 1;
+  __shared__ double tot[E];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int e = warp; e < E; e += 32) {
+    double s = 0.0;
+    for (int b = lane; b < grid; b += 32) s += part[(int64_t)b * E + e];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) tot[e] = s;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < KK; e += blockDim.x) {
+    sc[kM1 + e] = tot[e];
+    sc[kM2 + e] = tot[KK + e];
+    sc[kGdd + e] = tot[2 * KK + e];
+  }
+  if (threadIdx.x == 0) {
+    double c1 = 0.0, c2 = 0.0;
+    for (int e = 0; e < KK; ++e) {
+      c1 = fma(tot[KK + e], tot[e], c1);
+      c2 = fma(tot[2 * KK + e], S[e], c2);
+    }
+    sc[kTrDE] = tot[3 * KK];
+    sc[kDHd] = (tot[3 * KK] - c1) - c2;
+    tcg_scalar_a(sc, st);
+  }
+}
+
+// pass B over 8-row blocks: Hd = EH - U M1 - d S on the tensor cores (accumulator = EH),
+// eta += ce d, Heta += ce Hd, r += cr Hd, then partials of MR = U^T r and ||r||^2.
+template <int KT>
+__global__ void __launch_bounds__(kTcgThreads) tcg_update_kernel(int64_t n, const double* __restrict__ U,
+                                                                 const double* __restrict__ EH,
+                                                                 const double* __restrict__ D,
+                                                                 const double* __restrict__ S,
+                                                                 const double* __restrict__ sc,
+                                                                 double* __restrict__ eta,
+                                                                 double* __restrict__ Heta,
+                                                                 double* __restrict__ r,
+                                                                 double* __restrict__ part) {
+  constexpr int K = 8 * KT, KK = K * K, E = KK + 1;
+  __shared__ double red[E];
+  __shared__ __align__(16) double tile[kTcgWarps][8 * K];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  for (int e = threadIdx.x; e < E; e += kTcgThreads) red[e] = 0.0;
+  // B fragments of -M1 and -S: rows 8 ta + 4 ks + q, column 8 tb + g
+  double bm[KT][2][KT], bs[KT][2][KT];
+#pragma unroll
+  for (int ta = 0; ta < KT; ++ta)
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+      for (int tb = 0; tb < KT; ++tb) {
+        const int e = (8 * ta + 4 * ks + q) * K + 8 * tb + g;
+        bm[ta][ks][tb] = -sc[kM1 + e];
+        bs[ta][ks][tb] = -S[e];
+      }
+  const double ce = sc[kCEta], cr = sc[kCR];
+  double mr[KT][KT][2], zz = 0.0;
+#pragma unroll
+  for (int i = 0; i < KT; ++i)
+#pragma unroll
+    for (int j = 0; j < KT; ++j) mr[i][j][0] = mr[i][j][1] = 0.0;
+  double* tl = tile[warp];
+  const int64_t blocks = (n + 7) / 8;
+  const int64_t tw = (int64_t)gridDim.x * kTcgWarps, wid = (int64_t)blockIdx.x * kTcgWarps + warp;
+  const int64_t b0 = blocks * wid / tw, b1 = blocks * (wid + 1) / tw;
+  for (int64_t b = b0; b < b1; ++b) {
+    const int64_t row = 8 * b + g;
+    const bool ok = row < n;
+    double au[KT][2], ad[KT][2];
+#pragma unroll
+    for (int ta = 0; ta < KT; ++ta)
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        const int64_t o = row * K + 8 * ta + 4 * ks + q;
+        au[ta][ks] = ok ? __ldg(U + o) : 0.0;
+        ad[ta][ks] = ok ? __ldg(D + o) : 0.0;
+      }
+    double hd[KT][2];
+    double2 d2[KT], e2[KT], h2[KT], r2[KT];
+#pragma unroll
+    for (int tb = 0; tb < KT; ++tb) {
+      const int64_t o = row * K + 8 * tb + 2 * q;
+      const double2 z = make_double2(0.0, 0.0);
+      const double2 x = ok ? __ldg(reinterpret_cast<const double2*>(EH + o)) : z;
+      hd[tb][0] = x.x;
+      hd[tb][1] = x.y;
+      d2[tb] = ok ? __ldg(reinterpret_cast<const double2*>(D + o)) : z;
+      e2[tb] = ok ? *reinterpret_cast<const double2*>(eta + o) : z;
+      h2[tb] = ok ? *reinterpret_cast<const double2*>(Heta + o) : z;
+      r2[tb] = ok ? *reinterpret_cast<const double2*>(r + o) : z;
+    }
+#pragma unroll
+    for (int tb = 0; tb < KT; ++tb)
+#pragma unroll
+      for (int ta = 0; ta < KT; ++ta)
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+          dmma884(hd[tb][0], hd[tb][1], au[ta][ks], bm[ta][ks][tb]);
+          dmma884(hd[tb][0], hd[tb][1], ad[ta][ks], bs[ta][ks][tb]);
+        }
+#pragma unroll
+    for (int tb = 0; tb < KT; ++tb) {
+      e2[tb].x = fma(ce, d2[tb].x, e2[tb].x);
+      e2[tb].y = fma(ce, d2[tb].y, e2[tb].y);
+      h2[tb].x = fma(ce, hd[tb][0], h2[tb].x);
+      h2[tb].y = fma(ce, hd[tb][1], h2[tb].y);
+      r2[tb].x = fma(cr, hd[tb][0], r2[tb].x);
+      r2[tb].y = fma(cr, hd[tb][1], r2[tb].y);
+      zz = fma(r2[tb].x, r2[tb].x, zz);
+      zz = fma(r2[tb].y, r2[tb].y, zz);
+      *reinterpret_cast<double2*>(tl + g * K + 8 * tb + 2 * q) = r2[tb];
+      if (ok) {
+        const int64_t o = row * K + 8 * tb + 2 * q;
+        *reinterpret_cast<double2*>(eta + o) = e2[tb];
+        *reinterpret_cast<double2*>(Heta + o) = h2[tb];
+        *reinterpret_cast<double2*>(r + o) = r2[tb];
+      }
+    }
+    __syncwarp();
+    // MR += U^T r over the block's 8 rows: A = U (row 4 ks + q, column 8 t + g), B = r likewise
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const int64_t rr = 8 * b + 4 * ks + q;
+      double bu[KT], br[KT];
+#pragma unroll
+      for (int t = 0; t < KT; ++t) {
+        bu[t] = rr < n ? __ldg(U + rr * K + 8 * t + g) : 0.0;
+        br[t] = tl[(4 * ks + q) * K + 8 * t + g];
+      }
+#pragma unroll
+      for (int i = 0; i < KT; ++i)
+#pragma unroll
+        for (int j = 0; j < KT; ++j) dmma884(mr[i][j][0], mr[i][j][1], bu[i], br[j]);
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) zz += __shfl_xor_sync(0xffffffffu, zz, o);
+  __syncthreads();
+  for (int w = 0; w < kTcgWarps; ++w) {
+    if (warp == w) {
+#pragma unroll
+      for (int i = 0; i < KT; ++i)
+#pragma unroll
+        for (int j = 0; j < KT; ++j)
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) red[(8 * i + g) * K + 8 * j + 2 * q + hh] += mr[i][j][hh];
+      if (lane == 0) red[KK] += zz;
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < E; e += kTcgThreads) part[(int64_t)blockIdx.x * E + e] = red[e];
+}
+
+// sum the pass-B partials, ||P r||^2 = ||r||^2 - ||MR||_F^2, convergence and conjugation;
+// MR is zeroed when the iteration stops so that pass C leaves r as it is
+template <int K>
+__global__ void __launch_bounds__(1024) tcg_fused_b_kernel(int grid, const double* __restrict__ part, double* sc,
+                                                           int* st, int max_iters) {
+  constexpr int KK = K * K, E = KK + 1;
+  __shared__ double tot[E];
+  __shared__ int go;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int e = warp; e < E; e += 32) {
+    double s = 0.0;
+    for (int b = lane; b < grid; b += 32) s += part[(int64_t)b * E + e];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) tot[e] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int e = 0; e < KK; ++e) m = fma(tot[e], tot[e], m);
+    sc[kZraw] = tot[KK];
+    sc[kZnew] = tot[KK] - m;
+    go = tcg_scalar_b(sc, st, max_iters) ? 1 : 0;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < KK; e += blockDim.x) sc[kMR + e] = go ? tot[e] : 0.0;
+}
+
+// pass C over 8-row blocks: r <- r - U MR, d <- ca r + cb d
+template <int KT>
+__global__ void __launch_bounds__(kTcgThreads) tcg_finish_kernel(int64_t n, const double* __restrict__ U,
+                                                                 const double* __restrict__ sc,
+                                                                 double* __restrict__ r,
+                                                                 double* __restrict__ D) {
+  constexpr int K = 8 * KT;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  double bm[KT][2][KT];
+#pragma unroll
+  for (int ta = 0; ta < KT; ++ta)
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+      for (int tb = 0; tb < KT; ++tb) bm[ta][ks][tb] = -sc[kMR + (8 * ta + 4 * ks + q) * K + 8 * tb + g];
+  const double ca = sc[kCA], cb = sc[kCB];
+  const int64_t blocks = (n + 7) / 8;
+  const int64_t tw = (int64_t)gridDim.x * kTcgWarps, wid = (int64_t)blockIdx.x * kTcgWarps + warp;
+  const int64_t b0 = blocks * wid / tw, b1 = blocks * (wid + 1) / tw;
+  for (int64_t b = b0; b < b1; ++b) {
+    const int64_t row = 8 * b + g;
+    const bool ok = row < n;
+    double au[KT][2];
+#pragma unroll
+    for (int ta = 0; ta < KT; ++ta)
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) au[ta][ks] = ok ? __ldg(U + row * K + 8 * ta + 4 * ks + q) : 0.0;
+    double rv[KT][2];
+    double2 d2[KT];
+#pragma unroll
+    for (int tb = 0; tb < KT; ++tb) {
+      const int64_t o = row * K + 8 * tb + 2 * q;
+      const double2 z = make_double2(0.0, 0.0);
+      const double2 x = ok ? *reinterpret_cast<const double2*>(r + o) : z;
+      rv[tb][0] = x.x;
+      rv[tb][1] = x.y;
+      d2[tb] = ok ? *reinterpret_cast<const double2*>(D + o) : z;
+    }
+#pragma unroll
+    for (int tb = 0; tb < KT; ++tb)
+#pragma unroll
+      for (int ta = 0; ta < KT; ++ta)
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) dmma884(rv[tb][0], rv[tb][1], au[ta][ks], bm[ta][ks][tb]);
+    if (ok) {
+#pragma unroll
+      for (int tb = 0; tb < KT; ++tb) {
+        const int64_t o = row * K + 8 * tb + 2 * q;
+        *reinterpret_cast<double2*>(r + o) = make_double2(rv[tb][0], rv[tb][1]);
+        *reinterpret_cast<double2*>(D + o) =
+            make_double2(fma(ca, rv[tb][0], cb * d2[tb].x), fma(ca, rv[tb][1], cb * d2[tb].y));
+      }
+    }
+  }
+}
+
+static int fused_grid(plp_ctx* ctx, int64_t row_blocks, int E) {
+  int64_t g = (int64_t)ctx->num_sms * 4;
+  const int64_t cap = ((int64_t)ctx->max_ctas * 4 * PLP_MAX_K) / E;  // partials capacity
+  if (g > cap) g = cap;
+  const int64_t want = (row_blocks + kTcgWarps * 4 - 1) / (kTcgWarps * 4);  // >= 4 blocks per warp
+  if (g > want) g = want;
+  return (int)(g < 1 ? 1 : g);
+}
+
+template <int KT>
+static plp_status fused_iteration(plp_ctx* ctx, int64_t n, const double* U, const double* S, double* eta,
+                                  double* Heta, double* r, double* dlt, const double* EH, double* scal,
+                                  int* status, int max_iters) {
+  constexpr int K = 8 * KT, KK = K * K;
+  const int ga = fused_grid(ctx, (n + 3) / 4, 3 * KK + 1);
+  tcg_gram_a_kernel<KT><<<ga, kTcgThreads, 0, ctx->stream>>>(n, U, EH, dlt, ctx->partials);
+  PLP_LAUNCH_CHECK("tcg_gram_a_kernel");
+  tcg_fused_a_kernel<K><<<1, 1024, 0, ctx->stream>>>(ga, ctx->partials, S, scal, status);
+  PLP_LAUNCH_CHECK("tcg_fused_a_kernel");
+  const int gb = fused_grid(ctx, (n + 7) / 8, KK + 1);
+  tcg_update_kernel<KT><<<gb, kTcgThreads, 0, ctx->stream>>>(n, U, EH, dlt, S, scal, eta, Heta, r,
+                                                             ctx->partials);
+  PLP_LAUNCH_CHECK("tcg_update_kernel");
+  tcg_fused_b_kernel<K><<<1, 1024, 0, ctx->stream>>>(gb, ctx->partials, scal, status, max_iters);
+  PLP_LAUNCH_CHECK("tcg_fused_b_kernel");
+  int64_t gc = (int64_t)ctx->num_sms * 8;
+  const int64_t bc = (n + 7) / 8;
+  if (bc < gc * kTcgWarps) gc = std::max<int64_t>(1, (bc + kTcgWarps - 1) / kTcgWarps);
+  tcg_finish_kernel<KT><<<(int)gc, kTcgThreads, 0, ctx->stream>>>(n, U, scal, r, dlt);
+  PLP_LAUNCH_CHECK("tcg_finish_kernel");
+  return PLP_OK;
 }
 
 // y = a x + b y with a, b read from the device (the host axpby's formula: fma(a, x, b * y))
@@ -128,14 +508,27 @@ extern "C" plp_status plp_tcg_run(plp_ctx* ctx, const plp_graph* g, int k, const
                                   const double* AB, const double* G_in, const double* S, double p,
                                   double eps, int mode, double* eta, double* Heta, double* r,
                                   double* dlt, double* Hd, double* scal, int* status, int max_iters,
-                                  int iters) {
+                                  int iters, int fused) {
   if (!ctx || !g || !U || !AB || !S || !eta || !Heta || !r || !dlt || !Hd || !scal || !status)
     return set_error(PLP_ERR_ARG, "null argument");
   if (iters < 0 || max_iters < 1) return set_error(PLP_ERR_ARG, "iters >= 0, max_iters >= 1");
   const int64_t n = g->n_rows;
   const int64_t total = n * k;
+  if (fused && k != 8 && k != 16) return set_error(PLP_ERR_ARG, "fused tCG needs k = 8 or 16");
+  auto al16 = [](const void* x) { return ((uintptr_t)x & 15u) == 0; };
+  if (fused && !(al16(U) && al16(eta) && al16(Heta) && al16(r) && al16(dlt) && al16(Hd)))
+    return set_error(PLP_ERR_ARG, "fused tCG needs 16-byte aligned vectors");
   const int grid = axpby_grid(ctx, total);
   plp_status st;
+  if (fused) {
+    for (int it = 0; it < iters; ++it) {
+      if ((st = plp_hessvec(ctx, g, k, U, dlt, p, AB, mode, eps, G_in, Hd))) return st;
+      st = k == 8 ? fused_iteration<1>(ctx, n, U, S, eta, Heta, r, dlt, Hd, scal, status, max_iters)
+                  : fused_iteration<2>(ctx, n, U, S, eta, Heta, r, dlt, Hd, scal, status, max_iters);
+      if (st) return st;
+    }
+    return PLP_OK;
+  }
   for (int it = 0; it < iters; ++it) {
     // H(delta) = P(EucHess[delta]) - delta S
     if ((st = plp_hessvec(ctx, g, k, U, dlt, p, AB, mode, eps, G_in, Hd))) return st;

@@ -49,6 +49,7 @@ SYMBOLS = [
 TCG_STATUS = {0: "running", 1: "boundary", 2: "negative_curvature", 3: "converged", 4: "maxiter",
               5: "interior"}
 TILE_ROWS = 120  # PLP_TILE_ROWS in include/plp.h
+TCG_SCAL_LEN = 4160  # PLP_TCG_SCAL_LEN in include/plp.h
 
 
 def last_edge_kernel() -> str:
@@ -316,18 +317,18 @@ def tcg_init(ctx: Context, grad, delta: float, kappa: float, theta: float, eta, 
     _ck(_lib.plp_tcg_init(ctx.h, C_I64(n), k, _dev(grad, "grad"), C_D(delta), C_D(kappa), C_D(theta),
                           _dev(eta, "eta", shape=(n, k)), _dev(Heta, "Heta", shape=(n, k)),
                           _dev(r, "r", shape=(n, k)), _dev(dlt, "dlt", shape=(n, k)),
-                          _dev(scal, "scal", shape=(16,)), _dev(status, "status", dtype=torch.int32)),
+                          _dev(scal, "scal", shape=(TCG_SCAL_LEN,)), _dev(status, "status", dtype=torch.int32)),
         "plp_tcg_init")
 
 
 def tcg_run(ctx: Context, g: Graph, U, AB, G_in, S, p: float, eps: float, mode: int, eta, Heta, r, dlt,
-            Hd, scal, status, max_iters: int, iters: int):
+            Hd, scal, status, max_iters: int, iters: int, fused: bool = False):
     k = U.shape[1]
     _ck(_lib.plp_tcg_run(ctx.h, g.h, k, _dev(U, "U", shape=(g.n_cols, k)), _dev(AB, "AB", shape=(2 * k,)),
                          _dev(G_in, "G_in", shape=(g.n_rows, k), nullable=True), _dev(S, "S", shape=(k, k)),
                          C_D(p), C_D(eps), int(mode), _dev(eta, "eta"), _dev(Heta, "Heta"), _dev(r, "r"),
-                         _dev(dlt, "dlt"), _dev(Hd, "Hd"), _dev(scal, "scal", shape=(16,)),
-                         _dev(status, "status", dtype=torch.int32), int(max_iters), int(iters)),
+                         _dev(dlt, "dlt"), _dev(Hd, "Hd"), _dev(scal, "scal", shape=(TCG_SCAL_LEN,)),
+                         _dev(status, "status", dtype=torch.int32), int(max_iters), int(iters), int(fused)),
         "plp_tcg_run")
 
 

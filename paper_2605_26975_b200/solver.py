@@ -40,6 +40,7 @@ class SolverConfig:
     eps: float = 1e-9
     device_tcg: bool = True            # tCG recurrences on the device (plp_tcg_run), no per-iteration D2H
     tcg_batch: int = 8                 # iterations launched between two status reads
+    tcg_fused: bool | None = None      # fused tCG passes (NEXT-2); default: when k is 8 or 16
 
     def resolved(self, n: int, k: int) -> "SolverConfig":
         c = SolverConfig(**self.__dict__)
@@ -51,6 +52,8 @@ class SolverConfig:
             c.tr_delta0 = c.tr_delta_max / 8.0
         if c.tcg_max_iters is None:
             c.tcg_max_iters = min(2 * n * k, 1000)
+        if c.tcg_fused is None:
+            c.tcg_fused = c.device_tcg and k in (8, 16)
         if not (0.0 < c.tr_rho_accept < 0.25 and c.grad_tol > 0 and c.tr_delta0 <= c.tr_delta_max):
             raise ValueError("invalid SolverConfig (SPEC.md:303)")
         return c
@@ -122,7 +125,7 @@ class GrassmannTR:
         if not hasattr(self, "_tcg_buf") or self._tcg_buf[0].shape != st.grad.shape:
             z = lambda: torch.empty_like(st.grad)  # noqa: E731
             self._tcg_buf = (z(), z(), z(), z(), z(),
-                             torch.zeros(16, dtype=torch.float64, device=st.grad.device),
+                             torch.zeros(plp.TCG_SCAL_LEN, dtype=torch.float64, device=st.grad.device),
                              torch.zeros(2, dtype=torch.int32, device=st.grad.device))
         eta, Heta, r, dlt, Hd, scal, status = self._tcg_buf
         plp.tcg_init(ctx, st.grad, delta, c.tcg_kappa, c.tcg_theta, eta, Heta, r, dlt, scal, status)
@@ -132,7 +135,7 @@ class GrassmannTR:
         while stv[0] == 0 and done < c.tcg_max_iters:
             batch = min(c.tcg_batch, c.tcg_max_iters - done)
             plp.tcg_run(ctx, self.g, st.U, st.AB, G_in, st.S, p, c.eps, c.hessian_mode, eta, Heta, r, dlt,
-                        Hd, scal, status, c.tcg_max_iters, batch)
+                        Hd, scal, status, c.tcg_max_iters, batch, fused=c.tcg_fused)
             done += batch
             stv = status.cpu().tolist()
         return eta.clone(), Heta.clone(), int(stv[1]), plp.TCG_STATUS[int(stv[0])]

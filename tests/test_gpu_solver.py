@@ -103,3 +103,39 @@ def test_device_tcg_matches_host_tcg_bitwise(mods, p, delta, mode):
     b = tr.tcg_device(st, p, delta)
     assert a[2:] == b[2:], (a[2:], b[2:])
     assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+
+
+@pytest.mark.parametrize("cfg,n,k,p,delta,mode", [("C2", 5003, 8, 1.5, 0.3, 0), ("C2", 5003, 8, 1.2, 50.0, 0),
+                                                  ("C1", None, 16, 1.5, 0.5, 0), ("C2", 4001, 8, 1.8, 2.0, 1),
+                                                  ("C2", 2003, 16, 1.3, 1e3, 0)])
+def test_fused_tcg_matches_oracle(mods, cfg, n, k, p, delta, mode):
+    """NEXT-2 fused tCG (three tensor-core passes after the edge pass; <d, Hd> and ||P r||^2 from
+    Grams) against the oracle's tCG: same iteration count and exit status, step and H step within
+    1e-9 relative (ragged n: 8-row blocks with a tail; boundary, interior and full-Hessian cases)."""
+    plp, solver, ctx = mods
+    g = make_config(cfg, n=n)
+    Z = draw_U(g.n, k, 5)
+    Uo, _ = oracle.retract(Z, np.zeros_like(Z))
+    G = plp.Graph(ctx, g.row_ptr, g.col, g.w)
+    tr = solver.GrassmannTR(ctx, G, k, solver.SolverConfig(hessian_mode=mode, tcg_fused=True))
+    st = solver._State(tr, torch.from_numpy(Uo).cuda(), p)
+    eta, Heta, it, status = tr.tcg_device(st, p, delta)
+    ocfg = osol.default_cfg(g.n, k)
+    hm = "full" if mode == 1 else "sparse"
+    sto = osol._state(g, Uo, p, osol.oracle_fns())
+    eta_o, Heta_o, it_o, status_o = osol.tcg(
+        lambda xi: osol._hess(g, sto, p, xi, ocfg["eps"], hm, osol.oracle_fns()), sto["grad"], Uo, delta, ocfg)
+    assert (it, status) == (it_o, status_o)
+    assert np.max(np.abs(eta.cpu().numpy() - eta_o)) <= 1e-9 * np.max(np.abs(eta_o))
+    assert np.max(np.abs(Heta.cpu().numpy() - Heta_o)) <= 1e-9 * np.max(np.abs(Heta_o))
+
+
+def test_fused_tcg_rejects_unsupported_k(mods):
+    plp, solver, ctx = mods
+    g = make_config("C2", n=500)
+    G = plp.Graph(ctx, g.row_ptr, g.col, g.w)
+    U = torch.from_numpy(oracle.retract(draw_U(g.n, 4, 1), np.zeros((g.n, 4)))[0]).cuda()
+    tr = solver.GrassmannTR(ctx, G, 4, solver.SolverConfig(tcg_fused=True))
+    st = solver._State(tr, U, 1.5)
+    with pytest.raises(plp.PlpError):
+        tr.tcg_device(st, 1.5, 0.3)

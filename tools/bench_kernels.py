@@ -99,6 +99,44 @@ def main():
         row(f"a11 k-means++ seeding + first assignment ({k - 1} D^2 rounds)", ms0, k * (8 * n * k + 8 * n))
         ms = timed(lambda: plp.rcut(ctx, G, k, labels), args.reps, stream)
         row("a12 RCut", ms, csr + 4 * n)
+        tcg_rows(ctx, G, U, k, p, stream, row, csr)
+
+
+def tcg_rows(ctx, G, U, k, p, stream, row, csr):
+    """One truncated-CG iteration (NEXT-1): Hessian-vector product, projection, curvature term,
+    two dots, four axpbys -- device-resident (plp_tcg_run, no host read) and host-driven (two
+    scalar reads per iteration).  kappa = 0 keeps tCG from converging so every iteration runs."""
+    from paper_2605_26975_b200 import solver
+    n = G.n_rows
+    cfg = solver.SolverConfig(tcg_kappa=0.0, tcg_max_iters=10)
+    Uq = plp.retract(ctx, U, torch.zeros_like(U))
+    tr = solver.GrassmannTR(ctx, G, k, cfg)
+    st = solver._State(tr, Uq, p)
+    tr.tcg_device(st, p, 1e6)
+    eta, Heta, r, dlt, Hd, scal, status = tr._tcg_buf
+    iters = 10
+
+    def dev(fused):
+        plp.tcg_init(ctx, st.grad, 1e6, 0.0, 1.0, eta, Heta, r, dlt, scal, status)
+        plp.tcg_run(ctx, G, st.U, st.AB, None, st.S, p, cfg.eps, plp.HESS_SPARSE, eta, Heta, r, dlt, Hd,
+                    scal, status, 1 << 30, iters, fused=fused)
+    ms = timed(lambda: dev(False), 5, stream) / iters
+    # per iteration: edge pass (csr + U, eta, Hd), project (40 n k), apply_sub (24 n k),
+    # dots (2 x 16 n k), axpbys (4 x 24 n k), projection of r (40 n k)
+    byts = csr + 24 * n * k + 40 * n * k + 24 * n * k + 32 * n * k + 96 * n * k + 40 * n * k
+    row("NEXT-1 tCG iteration, device-resident (plp_tcg_run)", ms, byts)
+    if k in (8, 16):
+        # fused: edge pass + pass A (U, EH, d: 24 n k) + pass B (U, EH, d, eta, Heta, r read, three
+        # written: 72 n k) + pass C (U, r, d read, r, d written: 40 n k)
+        ms = timed(lambda: dev(True), 5, stream) / iters
+        row("NEXT-2 tCG iteration, fused passes (plp_tcg_run fused=1)", ms, csr + 24 * n * k + 136 * n * k)
+    res = {}
+
+    def host():
+        res["r"] = tr.tcg(st, p, 1e6)
+    ms = timed(host, 5, stream)
+    nit = res["r"][2]
+    row(f"NEXT-1 tCG iteration, host-driven loop ({res['r'][3]} after {nit})", ms / max(nit, 1), byts)
 
 
 if __name__ == "__main__":
