@@ -9,6 +9,7 @@
 // exit condition every further iteration is a no-op for eta, Heta, r and delta.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "dense_mma.cuh"
 #include "plp_internal.h"
@@ -16,15 +17,15 @@
 namespace plp {
 
 // scalar slots (double sc[PLP_TCG_SCAL_LEN]) and status (int st[2] = {status, iterations});
-// the fused path also keeps k x k matrices in sc: M1 = U^T EH, M2 = U^T d, Gdd = d^T d,
-// MR = U^T r (slots of PLP_MAX_K^2 from kMat)
+// the fused path also keeps its reduction totals in sc (from kMat)
 enum {
   kZr = 0, kStopTol = 1, kDelta = 2, kEPe = 3, kEPd = 4, kDPd = 5, kDHd = 6, kAlpha = 7,
   kZnew = 9, kCEta = 10, kCR = 11, kCA = 12, kCB = 13, kTrDE = 14, kZraw = 15, kMat = 64
 };
-constexpr int kM1 = kMat, kM2 = kMat + PLP_MAX_K * PLP_MAX_K, kGdd = kMat + 2 * PLP_MAX_K * PLP_MAX_K,
-              kMR = kMat + 3 * PLP_MAX_K * PLP_MAX_K;
-static_assert(kMR + PLP_MAX_K * PLP_MAX_K <= PLP_TCG_SCAL_LEN, "scal too short");
+// totals of pass A at kTotA = [M1 | M2 | tr | <Gdd, S>] (M1 first, read by pass B), of pass B at
+// kTotB = [MR | ||r||^2] (MR read by pass C)
+constexpr int kTotA = kMat, kM1 = kTotA, kTotB = kMat + 2 * PLP_MAX_K * PLP_MAX_K + 64, kMR = kTotB;
+static_assert(kTotB + PLP_MAX_K * PLP_MAX_K + 1 <= PLP_TCG_SCAL_LEN, "scal too short");
 
 __global__ void tcg_init_kernel(double* sc, int* st, double delta, double kappa, double theta) {
   const double zr = sc[kZr];
@@ -109,18 +110,22 @@ __global__ void tcg_scalar_b_kernel(double* sc, int* st, int max_iters) { tcg_sc
 // ---------------------------------------------------------------------------------------------
 constexpr int kTcgThreads = 256, kTcgWarps = kTcgThreads / 32;
 
-// pass A: partials of [M1 | M2 | Gdd | tr(d^T EH)] over 4-row blocks
-template <int KT>
+// Grid reductions: each pass CTA writes its E block totals entry-major (part[e * P + cta]); then
+// tcg_reduce_kernel runs one CTA per entry (coalesced fixed-order sum: thread-strided, warp xor
+// tree, warps in order) and its last CTA (ticket) applies the scalar step on the totals.
+// pass A: [M1 | M2 | tr(d^T EH) | <d^T d, S>_F] over 4-row blocks
+template <int KT, int UNR>
 __global__ void __launch_bounds__(kTcgThreads) tcg_gram_a_kernel(int64_t n, const double* __restrict__ U,
                                                                  const double* __restrict__ EH,
                                                                  const double* __restrict__ D,
+                                                                 const double* __restrict__ S,
                                                                  double* __restrict__ part) {
-  constexpr int K = 8 * KT, KK = K * K, E = 3 * KK + 1;
+  constexpr int K = 8 * KT, KK = K * K, E = 2 * KK + 2;
   __shared__ double red[E];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
   for (int e = threadIdx.x; e < E; e += kTcgThreads) red[e] = 0.0;
-  double m1[KT][KT][2], m2[KT][KT][2], gd[KT][KT][2], tr = 0.0;
+  double m1[KT][KT][2], m2[KT][KT][2], gd[KT][KT][2], tr = 0.0, ds = 0.0;
 #pragma unroll
   for (int i = 0; i < KT; ++i)
 #pragma unroll
@@ -131,7 +136,6 @@ __global__ void __launch_bounds__(kTcgThreads) tcg_gram_a_kernel(int64_t n, cons
   const int64_t blocks = (n + 3) / 4;
   const int64_t tw = (int64_t)gridDim.x * kTcgWarps, wid = (int64_t)blockIdx.x * kTcgWarps + warp;
   const int64_t b0 = blocks * wid / tw, b1 = blocks * (wid + 1) / tw;
-  constexpr int UNR = 2;
   for (int64_t b = b0; b < b1; b += UNR) {
     double u[UNR][KT], h[UNR][KT], dd[UNR][KT];
 #pragma unroll
@@ -163,8 +167,18 @@ __global__ void __launch_bounds__(kTcgThreads) tcg_gram_a_kernel(int64_t n, cons
   // diagonal of the d^T EH tiles: element (8i + g, 8i + 2q + h) is diagonal iff g == 2q + h
 #pragma unroll
   for (int i = 0; i < KT; ++i) tr += (g == 2 * q ? de[i][0] : 0.0) + (g == 2 * q + 1 ? de[i][1] : 0.0);
+  // <d^T d, S>_F from this lane's fragment of d^T d (S is known before the pass)
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
+  for (int i = 0; i < KT; ++i)
+#pragma unroll
+    for (int j = 0; j < KT; ++j)
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) ds = fma(gd[i][j][hh], __ldg(S + (8 * i + g) * K + 8 * j + 2 * q + hh), ds);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    tr += __shfl_xor_sync(0xffffffffu, tr, o);
+    ds += __shfl_xor_sync(0xffffffffu, ds, o);
+  }
   __syncthreads();
   for (int w = 0; w < kTcgWarps; ++w) {
     if (warp == w) {
@@ -177,45 +191,15 @@ __global__ void __launch_bounds__(kTcgThreads) tcg_gram_a_kernel(int64_t n, cons
             const int e = (8 * i + g) * K + 8 * j + 2 * q + hh;
             red[e] += m1[i][j][hh];
             red[KK + e] += m2[i][j][hh];
-            red[2 * KK + e] += gd[i][j][hh];
           }
-      if (lane == 0) red[3 * KK] += tr;
+      if (lane == 0) {
+        red[2 * KK] += tr;
+        red[2 * KK + 1] += ds;
+      }
     }
     __syncthreads();
   }
-  for (int e = threadIdx.x; e < E; e += kTcgThreads) part[(int64_t)blockIdx.x * E + e] = red[e];
-}
-
-// sum the pass-A partials (fixed order), then <d, Hd> and the step-length decision
-template <int K>
-__global__ void __launch_bounds__(1024) tcg_fused_a_kernel(int grid, const double* __restrict__ part,
-                                                           const double* __restrict__ S, double* sc, int* st) {
-  constexpr int KK = K * K, E = 3 * KK + 1;
-  __shared__ double tot[E];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int e = warp; e < E; e += 32) {
-    double s = 0.0;
-    for (int b = lane; b < grid; b += 32) s += part[(int64_t)b * E + e];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) tot[e] = s;
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < KK; e += blockDim.x) {
-    sc[kM1 + e] = tot[e];
-    sc[kM2 + e] = tot[KK + e];
-    sc[kGdd + e] = tot[2 * KK + e];
-  }
-  if (threadIdx.x == 0) {
-    double c1 = 0.0, c2 = 0.0;
-    for (int e = 0; e < KK; ++e) {
-      c1 = fma(tot[KK + e], tot[e], c1);
-      c2 = fma(tot[2 * KK + e], S[e], c2);
-    }
-    sc[kTrDE] = tot[3 * KK];
-    sc[kDHd] = (tot[3 * KK] - c1) - c2;
-    tcg_scalar_a(sc, st);
-  }
+  for (int e = threadIdx.x; e < E; e += kTcgThreads) part[(int64_t)e * gridDim.x + blockIdx.x] = red[e];
 }
 
 // pass B over 8-row blocks: Hd = EH - U M1 - d S on the tensor cores (accumulator = EH),
@@ -225,7 +209,7 @@ __global__ void __launch_bounds__(kTcgThreads) tcg_update_kernel(int64_t n, cons
                                                                  const double* __restrict__ EH,
                                                                  const double* __restrict__ D,
                                                                  const double* __restrict__ S,
-                                                                 const double* __restrict__ sc,
+                                                                 const double* sc,
                                                                  double* __restrict__ eta,
                                                                  double* __restrict__ Heta,
                                                                  double* __restrict__ r,
@@ -344,35 +328,7 @@ __global__ void __launch_bounds__(kTcgThreads) tcg_update_kernel(int64_t n, cons
     }
     __syncthreads();
   }
-  for (int e = threadIdx.x; e < E; e += kTcgThreads) part[(int64_t)blockIdx.x * E + e] = red[e];
-}
-
-// sum the pass-B partials, ||P r||^2 = ||r||^2 - ||MR||_F^2, convergence and conjugation;
-// MR is zeroed when the iteration stops so that pass C leaves r as it is
-template <int K>
-__global__ void __launch_bounds__(1024) tcg_fused_b_kernel(int grid, const double* __restrict__ part, double* sc,
-                                                           int* st, int max_iters) {
-  constexpr int KK = K * K, E = KK + 1;
-  __shared__ double tot[E];
-  __shared__ int go;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int e = warp; e < E; e += 32) {
-    double s = 0.0;
-    for (int b = lane; b < grid; b += 32) s += part[(int64_t)b * E + e];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) tot[e] = s;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double m = 0.0;
-    for (int e = 0; e < KK; ++e) m = fma(tot[e], tot[e], m);
-    sc[kZraw] = tot[KK];
-    sc[kZnew] = tot[KK] - m;
-    go = tcg_scalar_b(sc, st, max_iters) ? 1 : 0;
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < KK; e += blockDim.x) sc[kMR + e] = go ? tot[e] : 0.0;
+  for (int e = threadIdx.x; e < E; e += kTcgThreads) part[(int64_t)e * gridDim.x + blockIdx.x] = red[e];
 }
 
 // pass C over 8-row blocks: r <- r - U MR, d <- ca r + cb d
@@ -432,8 +388,66 @@ __global__ void __launch_bounds__(kTcgThreads) tcg_finish_kernel(int64_t n, cons
   }
 }
 
-static int fused_grid(plp_ctx* ctx, int64_t row_blocks, int E) {
-  int64_t g = (int64_t)ctx->num_sms * 4;
+// MODE 0 (after pass A): tot = [M1 | M2 | tr(d^T EH) | <d^T d, S>_F]; <d, Hd>, step length.
+// MODE 1 (after pass B): tot = [MR | ||r||^2]; ||P r||^2 = ||r||^2 - ||MR||_F^2, convergence,
+// conjugation; MR zeroed when the iteration stops (pass C then leaves r as it is).
+template <int K, int MODE>
+__global__ void __launch_bounds__(256) tcg_reduce_kernel(int P, const double* __restrict__ part, double* tot,
+                                                         unsigned* counter, double* sc, int* st, int max_iters) {
+  constexpr int KK = K * K, E = MODE == 0 ? 2 * KK + 2 : KK + 1;
+  __shared__ double ws[8];
+  __shared__ double t[E];
+  __shared__ unsigned ticket;
+  __shared__ int go;
+  const int e = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double v = 0.0;
+  for (int b = threadIdx.x; b < P; b += 256) v += __ldcg(part + (int64_t)e * P + b);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) ws[warp] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < 8; ++w) s += ws[w];
+    tot[e] = s;
+    __threadfence();
+    ticket = atomicAdd(counter, 1u);
+  }
+  __syncthreads();
+  if (ticket != (unsigned)E - 1) return;
+  __threadfence();
+  for (int i = threadIdx.x; i < E; i += 256) t[i] = __ldcg(tot + i);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *counter = 0u;
+    if (MODE == 0) {
+      double c1 = 0.0;
+      for (int i = 0; i < KK; ++i) c1 = fma(t[KK + i], t[i], c1);
+      sc[kTrDE] = t[2 * KK];
+      sc[kDHd] = (t[2 * KK] - c1) - t[2 * KK + 1];
+      tcg_scalar_a(sc, st);
+    } else {
+      double m = 0.0;
+      for (int i = 0; i < KK; ++i) m = fma(t[i], t[i], m);
+      sc[kZraw] = t[KK];
+      sc[kZnew] = t[KK] - m;
+      go = tcg_scalar_b(sc, st, max_iters) ? 1 : 0;
+    }
+  }
+  if (MODE == 1) {
+    __syncthreads();
+    if (!go)
+      for (int i = threadIdx.x; i < KK; i += 256) tot[i] = 0.0;
+  }
+}
+
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
+static int fused_grid(plp_ctx* ctx, int64_t row_blocks, int E, int per_sm) {
+  int64_t g = (int64_t)ctx->num_sms * per_sm;
   const int64_t cap = ((int64_t)ctx->max_ctas * 4 * PLP_MAX_K) / E;  // partials capacity
   if (g > cap) g = cap;
   const int64_t want = (row_blocks + kTcgWarps * 4 - 1) / (kTcgWarps * 4);  // >= 4 blocks per warp
@@ -446,17 +460,26 @@ static plp_status fused_iteration(plp_ctx* ctx, int64_t n, const double* U, cons
                                   double* Heta, double* r, double* dlt, const double* EH, double* scal,
                                   int* status, int max_iters) {
   constexpr int K = 8 * KT, KK = K * K;
-  const int ga = fused_grid(ctx, (n + 3) / 4, 3 * KK + 1);
-  tcg_gram_a_kernel<KT><<<ga, kTcgThreads, 0, ctx->stream>>>(n, U, EH, dlt, ctx->partials);
+  static const int per_sm_a = env_int("PLP_TCG_GRID_A", 4), per_sm_b = env_int("PLP_TCG_GRID_B", 3);
+  unsigned* counter = reinterpret_cast<unsigned*>(ctx->flag + 4);
+  constexpr int EA = 2 * KK + 2, EB = KK + 1;
+  const int ga = fused_grid(ctx, (n + 3) / 4, EA, per_sm_a);
+  static const int unr_a = env_int("PLP_TCG_UNR_A", 4);
+  if (unr_a == 4)
+    tcg_gram_a_kernel<KT, 4><<<ga, kTcgThreads, 0, ctx->stream>>>(n, U, EH, dlt, S, ctx->partials);
+  else
+    tcg_gram_a_kernel<KT, 2><<<ga, kTcgThreads, 0, ctx->stream>>>(n, U, EH, dlt, S, ctx->partials);
   PLP_LAUNCH_CHECK("tcg_gram_a_kernel");
-  tcg_fused_a_kernel<K><<<1, 1024, 0, ctx->stream>>>(ga, ctx->partials, S, scal, status);
-  PLP_LAUNCH_CHECK("tcg_fused_a_kernel");
-  const int gb = fused_grid(ctx, (n + 7) / 8, KK + 1);
+  tcg_reduce_kernel<K, 0><<<EA, 256, 0, ctx->stream>>>(ga, ctx->partials, scal + kTotA, counter, scal, status,
+                                                       max_iters);
+  PLP_LAUNCH_CHECK("tcg_reduce_kernel");
+  const int gb = fused_grid(ctx, (n + 7) / 8, EB, per_sm_b);
   tcg_update_kernel<KT><<<gb, kTcgThreads, 0, ctx->stream>>>(n, U, EH, dlt, S, scal, eta, Heta, r,
                                                              ctx->partials);
   PLP_LAUNCH_CHECK("tcg_update_kernel");
-  tcg_fused_b_kernel<K><<<1, 1024, 0, ctx->stream>>>(gb, ctx->partials, scal, status, max_iters);
-  PLP_LAUNCH_CHECK("tcg_fused_b_kernel");
+  tcg_reduce_kernel<K, 1><<<EB, 256, 0, ctx->stream>>>(gb, ctx->partials, scal + kTotB, counter + 1, scal, status,
+                                                       max_iters);
+  PLP_LAUNCH_CHECK("tcg_reduce_kernel");
   int64_t gc = (int64_t)ctx->num_sms * 8;
   const int64_t bc = (n + 7) / 8;
   if (bc < gc * kTcgWarps) gc = std::max<int64_t>(1, (bc + kTcgWarps - 1) / kTcgWarps);
