@@ -259,6 +259,20 @@ plp_status plp_tcg_run(plp_ctx* ctx, const plp_graph* g, int k, const double* U,
                        const double* G_in, const double* S, double p, double eps, int mode, double* eta,
                        double* Heta, double* r, double* delta_dir, double* Hd, double* scal,
                        int* status, int max_iters, int iters, int fused);
+/* CUDA graph of `iters` plp_tcg_run iterations with exactly these arguments (pointers and scalars
+ * are baked in: refresh the buffers' contents, not the pointers, between launches).  Captured on
+ * ctx's stream, which must be a created stream (not the legacy / per-thread default: PLP_ERR_ARG).
+ * plp_tcg_graph_launch enqueues the whole batch on ctx's stream (one launch); _nodes reports the
+ * captured kernel/memset node count; libplp owns the graph (destroy frees it). */
+typedef struct plp_tcg_graph plp_tcg_graph;
+plp_status plp_tcg_graph_create(plp_ctx* ctx, const plp_graph* g, int k, const double* U, const double* AB,
+                                const double* G_in, const double* S, double p, double eps, int mode,
+                                double* eta, double* Heta, double* r, double* delta_dir, double* Hd,
+                                double* scal, int* status, int max_iters, int iters, int fused,
+                                plp_tcg_graph** out);
+plp_status plp_tcg_graph_launch(plp_tcg_graph* graph);
+plp_status plp_tcg_graph_nodes(const plp_tcg_graph* graph, int* nodes);
+plp_status plp_tcg_graph_destroy(plp_tcg_graph* graph);
 
 /* ---------------------------------------------------------------------------------------------- */
 /* Diagnostics                                                                                      */

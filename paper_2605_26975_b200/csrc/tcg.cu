@@ -573,3 +573,70 @@ extern "C" plp_status plp_tcg_run(plp_ctx* ctx, const plp_graph* g, int k, const
   }
   return PLP_OK;
 }
+
+// ---------------------------------------------------------------------------------------------
+// CUDA-graph capture of a batch of tCG iterations (SURVEY.md §8(f) NEXT-1 "CUDA-Graph the tCG
+// iteration"): one graph launch replaces ~10 kernel launches per iteration.
+// ---------------------------------------------------------------------------------------------
+struct plp_tcg_graph {
+  plp_ctx* ctx = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int nodes = 0;
+};
+
+extern "C" plp_status plp_tcg_graph_create(plp_ctx* ctx, const plp_graph* g, int k, const double* U,
+                                           const double* AB, const double* G_in, const double* S, double p,
+                                           double eps, int mode, double* eta, double* Heta, double* r,
+                                           double* dlt, double* Hd, double* scal, int* status, int max_iters,
+                                           int iters, int fused, plp_tcg_graph** out) {
+  if (!ctx || !out) return set_error(PLP_ERR_ARG, "null argument");
+  *out = nullptr;
+  if (ctx->stream == nullptr || ctx->stream == cudaStreamLegacy || ctx->stream == cudaStreamPerThread)
+    return set_error(PLP_ERR_ARG, "graph capture needs a created (non-default) stream on the context");
+  if (iters < 1) return set_error(PLP_ERR_ARG, "iters >= 1");
+  PLP_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed));
+  const plp_status st = plp_tcg_run(ctx, g, k, U, AB, G_in, S, p, eps, mode, eta, Heta, r, dlt, Hd, scal, status,
+                                    max_iters, iters, fused);
+  cudaGraph_t graph = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+  if (st != PLP_OK || e != cudaSuccess) {
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    return st != PLP_OK ? st : cuda_check(e, "cudaStreamEndCapture");
+  }
+  size_t nodes = 0;
+  cudaGraphGetNodes(graph, nullptr, &nodes);
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t e2 = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e2 != cudaSuccess) return cuda_check(e2, "cudaGraphInstantiate");
+  plp_tcg_graph* gr = new (std::nothrow) plp_tcg_graph();
+  if (!gr) {
+    cudaGraphExecDestroy(exec);
+    return set_error(PLP_ERR_OOM, "host allocation failed");
+  }
+  gr->ctx = ctx;
+  gr->exec = exec;
+  gr->nodes = (int)nodes;
+  *out = gr;
+  return PLP_OK;
+}
+
+extern "C" plp_status plp_tcg_graph_launch(plp_tcg_graph* gr) {
+  if (!gr) return set_error(PLP_ERR_ARG, "graph is null");
+  PLP_CUDA(cudaGraphLaunch(gr->exec, gr->ctx->stream));
+  return PLP_OK;
+}
+
+extern "C" plp_status plp_tcg_graph_nodes(const plp_tcg_graph* gr, int* nodes) {
+  if (!gr || !nodes) return set_error(PLP_ERR_ARG, "null argument");
+  *nodes = gr->nodes;
+  return PLP_OK;
+}
+
+extern "C" plp_status plp_tcg_graph_destroy(plp_tcg_graph* gr) {
+  if (!gr) return PLP_OK;
+  cudaGraphExecDestroy(gr->exec);
+  delete gr;
+  return PLP_OK;
+}

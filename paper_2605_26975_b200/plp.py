@@ -44,7 +44,8 @@ SYMBOLS = [
     "plp_objective_from_ab", "plp_gram", "plp_project", "plp_apply_sub", "plp_retract",
     "plp_cholesky", "plp_apply_rinv", "plp_dot", "plp_axpby", "plp_gather_rows", "plp_kmeans",
     "plp_rcut", "plp_debug_pow", "plp_tile_order", "plp_last_edge_kernel", "plp_tcg_init",
-    "plp_tcg_run",
+    "plp_tcg_run", "plp_tcg_graph_create", "plp_tcg_graph_launch", "plp_tcg_graph_nodes",
+    "plp_tcg_graph_destroy",
 ]
 TCG_STATUS = {0: "running", 1: "boundary", 2: "negative_curvature", 3: "converged", 4: "maxiter",
               5: "interior"}
@@ -330,6 +331,43 @@ def tcg_run(ctx: Context, g: Graph, U, AB, G_in, S, p: float, eps: float, mode: 
                          _dev(dlt, "dlt"), _dev(Hd, "Hd"), _dev(scal, "scal", shape=(TCG_SCAL_LEN,)),
                          _dev(status, "status", dtype=torch.int32), int(max_iters), int(iters), int(fused)),
         "plp_tcg_run")
+
+
+class TcgGraph:
+    """plp_tcg_graph: a captured batch of `iters` tCG iterations (arguments baked in)."""
+
+    def __init__(self, ctx: Context, g: Graph, U, AB, G_in, S, p: float, eps: float, mode: int, eta, Heta, r,
+                 dlt, Hd, scal, status, max_iters: int, iters: int, fused: bool = False):
+        k = U.shape[1]
+        h = VP()
+        self.ctx = ctx
+        self.keep = (U, AB, G_in, S, eta, Heta, r, dlt, Hd, scal, status)  # pointers baked into the graph
+        _ck(_lib.plp_tcg_graph_create(
+            ctx.h, g.h, k, _dev(U, "U", shape=(g.n_cols, k)), _dev(AB, "AB", shape=(2 * k,)),
+            _dev(G_in, "G_in", shape=(g.n_rows, k), nullable=True), _dev(S, "S", shape=(k, k)), C_D(p), C_D(eps),
+            int(mode), _dev(eta, "eta"), _dev(Heta, "Heta"), _dev(r, "r"), _dev(dlt, "dlt"), _dev(Hd, "Hd"),
+            _dev(scal, "scal", shape=(TCG_SCAL_LEN,)), _dev(status, "status", dtype=torch.int32), int(max_iters),
+            int(iters), int(fused), ctypes.byref(h)), "plp_tcg_graph_create")
+        self.h = h
+
+    def launch(self) -> None:
+        _ck(_lib.plp_tcg_graph_launch(self.h), "plp_tcg_graph_launch")
+
+    def nodes(self) -> int:
+        v = ctypes.c_int()
+        _ck(_lib.plp_tcg_graph_nodes(self.h, ctypes.byref(v)), "plp_tcg_graph_nodes")
+        return v.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.plp_tcg_graph_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def gather_rows(ctx: Context, idx, X, out=None):

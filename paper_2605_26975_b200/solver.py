@@ -39,8 +39,9 @@ class SolverConfig:
     hessian_mode: int = plp.HESS_SPARSE
     eps: float = 1e-9
     device_tcg: bool = True            # tCG recurrences on the device (plp_tcg_run), no per-iteration D2H
-    tcg_batch: int = 8                 # iterations launched between two status reads
+    tcg_batch: int = 8                 # most iterations launched between two status reads
     tcg_fused: bool | None = None      # fused tCG passes (NEXT-2); default: when k is 8 or 16
+    tcg_graph: bool = True             # replay each batch as one CUDA graph (needs a non-default stream)
 
     def resolved(self, n: int, k: int) -> "SolverConfig":
         c = SolverConfig(**self.__dict__)
@@ -124,21 +125,58 @@ class GrassmannTR:
         ctx = self.ctx
         if not hasattr(self, "_tcg_buf") or self._tcg_buf[0].shape != st.grad.shape:
             z = lambda: torch.empty_like(st.grad)  # noqa: E731
+            self._graphs, self._gin = {}, None
             self._tcg_buf = (z(), z(), z(), z(), z(),
                              torch.zeros(plp.TCG_SCAL_LEN, dtype=torch.float64, device=st.grad.device),
                              torch.zeros(2, dtype=torch.int32, device=st.grad.device))
         eta, Heta, r, dlt, Hd, scal, status = self._tcg_buf
         plp.tcg_init(ctx, st.grad, delta, c.tcg_kappa, c.tcg_theta, eta, Heta, r, dlt, scal, status)
-        G_in = st.G if c.hessian_mode == plp.HESS_FULL else None
+        full = c.hessian_mode == plp.HESS_FULL
+        use_graph = c.tcg_graph and ctx.stream.cuda_stream != 0
+        if use_graph:
+            self._refresh_graph_inputs(st, p)
+        G_in = st.G if full else None
         done = 0
+        batch = 1  # batches of 1, 2, 4, ... tcg_batch iterations: short solves waste little
         stv = status.cpu().tolist()
         while stv[0] == 0 and done < c.tcg_max_iters:
-            batch = min(c.tcg_batch, c.tcg_max_iters - done)
-            plp.tcg_run(ctx, self.g, st.U, st.AB, G_in, st.S, p, c.eps, c.hessian_mode, eta, Heta, r, dlt,
-                        Hd, scal, status, c.tcg_max_iters, batch, fused=c.tcg_fused)
+            if use_graph:
+                self._graph_for(p, batch).launch()  # iterations past max_iters are no-ops (MAXITER)
+            else:
+                plp.tcg_run(ctx, self.g, st.U, st.AB, G_in, st.S, p, c.eps, c.hessian_mode, eta, Heta, r, dlt,
+                            Hd, scal, status, c.tcg_max_iters, min(batch, c.tcg_max_iters - done),
+                            fused=c.tcg_fused)
             done += batch
+            batch = min(2 * batch, c.tcg_batch)
             stv = status.cpu().tolist()
         return eta.clone(), Heta.clone(), int(stv[1]), plp.TCG_STATUS[int(stv[0])]
+
+    def _refresh_graph_inputs(self, st: _State, p: float) -> None:
+        """Copy the iterate into the persistent buffers the captured graphs read (their pointers
+        are fixed); drop the graphs when p changes (p is baked in)."""
+        full = self.cfg.hessian_mode == plp.HESS_FULL
+        if getattr(self, "_gin", None) is None or self._gin[0].shape != st.U.shape:
+            self._gin = (torch.empty_like(st.U), torch.empty_like(st.AB), torch.empty_like(st.S),
+                         torch.empty_like(st.G) if full else None)
+            self._graphs = {}
+        U, AB, S, G = self._gin
+        U.copy_(st.U)
+        AB.copy_(st.AB)
+        S.copy_(st.S)
+        if full:
+            G.copy_(st.G)
+        if getattr(self, "_graph_p", None) != p:
+            self._graphs, self._graph_p = {}, p
+
+    def _graph_for(self, p: float, batch: int):
+        """The captured batch of `batch` iterations for this p (one CUDA graph per batch size)."""
+        c = self.cfg
+        if batch not in self._graphs:
+            U, AB, S, G = self._gin
+            eta, Heta, r, dlt, Hd, scal, status = self._tcg_buf
+            self._graphs[batch] = plp.TcgGraph(self.ctx, self.g, U, AB, G, S, p, c.eps, c.hessian_mode, eta, Heta,
+                                               r, dlt, Hd, scal, status, c.tcg_max_iters, batch, fused=c.tcg_fused)
+        return self._graphs[batch]
 
     # -- truncated CG (Steihaug-Toint; Absil-Baker-Gallivan 2007, Alg. 2) ------------------------
     def tcg(self, st: _State, p: float, delta: float):
@@ -186,6 +224,12 @@ class GrassmannTR:
 
     # -- outer loop ---------------------------------------------------------------------------------
     def solve(self, U0, p: float, trace: SolveTrace | None = None):
+        """Trust-region solve at fixed p; torch work (buffers, scalar reads) is ordered on the
+        context's stream."""
+        with torch.cuda.stream(self.ctx.stream):
+            return self._solve(U0, p, trace)
+
+    def _solve(self, U0, p: float, trace: SolveTrace | None = None):
         c = self.cfg
         ctx = self.ctx
         trace = trace if trace is not None else SolveTrace()

@@ -139,3 +139,34 @@ def test_fused_tcg_rejects_unsupported_k(mods):
     st = solver._State(tr, U, 1.5)
     with pytest.raises(plp.PlpError):
         tr.tcg_device(st, 1.5, 0.3)
+
+
+@pytest.mark.parametrize("k,fused", [(3, False), (8, True)])
+def test_tcg_graph_replay_is_bitwise_the_direct_launches(k, fused):
+    """plp_tcg_graph_create / _launch: a captured batch of tCG iterations on a side stream gives
+    bitwise the step, H step, iteration count and status of launching the same iterations
+    directly, and the end-to-end solve is unchanged."""
+    from paper_2605_26975_b200 import plp, solver
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        ctx = plp.Context(0, stream)
+        g = make_config("C2", n=3001)
+        G = plp.Graph(ctx, g.row_ptr, g.col, g.w)
+        # near a p = 2 minimiser the Hessian is positive definite: tCG runs many iterations
+        Z = torch.from_numpy(draw_U(g.n, k, 6)).cuda()
+        U, _ = solver.continuation_solve(ctx, G, Z, [2.0], solver.SolverConfig(grad_tol=1e-2, tcg_graph=False))
+        res = []
+        for graph in (False, True):
+            tr = solver.GrassmannTR(ctx, G, k, solver.SolverConfig(tcg_graph=graph, tcg_fused=fused, tcg_batch=4))
+            st = solver._State(tr, U, 2.0)
+            res.append(tr.tcg_device(st, 2.0, 10.0))
+            if graph:
+                assert tr._graphs and all(gr.nodes() >= 5 * b for b, gr in tr._graphs.items())
+        a, b = res
+        assert a[2:] == b[2:] and a[2] > 4
+        assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+        Z = torch.from_numpy(draw_U(g.n, k, 7)).cuda()
+        sols = [solver.continuation_solve(ctx, G, Z, [2.0, 1.5], solver.SolverConfig(tcg_graph=gr, tcg_fused=fused))
+                for gr in (False, True)]
+        assert torch.equal(sols[0][0], sols[1][0])
+        assert [r.tcg_iters for r in sols[0][1].records] == [r.tcg_iters for r in sols[1][1].records]
