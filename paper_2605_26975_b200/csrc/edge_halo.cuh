@@ -74,6 +74,9 @@ constexpr unsigned kHaloSmemMax = 225u * 1024u / PLP_HALO_CTAS;
 #ifndef PLP_HALO_SLEEP_NS
 #define PLP_HALO_SLEEP_NS 64  // producer back-off between polls of the "empty" barrier
 #endif
+#ifndef PLP_HALO_CSLEEP_NS
+#define PLP_HALO_CSLEEP_NS 0  // > 0: consumers poll the "full" barrier with this back-off
+#endif
 #ifndef PLP_HALO_EB
 #define PLP_HALO_EB 2  // edges per straight-line batch in the halo kernel (2 or 4)
 #endif
@@ -227,7 +230,12 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
     const int64_t t = t0 + (int64_t)it * ts;
     if (t >= n_tiles) break;
     const int b = it % kHaloNBuf;
+#if PLP_HALO_CSLEEP_NS > 0
+    if (!mbar_test(&full[b], (unsigned)(it / kHaloNBuf) & 1u))
+      mbar_wait_sleep(&full[b], (unsigned)(it / kHaloNBuf) & 1u, PLP_HALO_CSLEEP_NS);
+#else
     mbar_wait(&full[b], (unsigned)(it / kHaloNBuf) & 1u);  // tile t resident
+#endif
 
     const unsigned char* B = buf0 + (size_t)b * Ly.bytes;
     const int* rp_s = reinterpret_cast<const int*>(B + Ly.rp);

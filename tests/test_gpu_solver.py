@@ -63,7 +63,8 @@ def test_first_trust_region_step_matches_oracle(mods):
 
 @pytest.mark.parametrize("cfg,n,k,sched", [("C1", None, 3, [2.0, 1.8, 1.5, 1.2]),
                                             ("C2", 20000, 2, [2.0, 1.1]),
-                                            ("D16", 8192, 4, [2.0, 1.5])])
+                                            ("D16", 8192, 4, [2.0, 1.5]),
+                                            ("D16", 4096, 8, [2.0, 1.5])])  # k = 8: fused tCG passes
 def test_end_to_end_labels_and_rcut_match_oracle(mods, cfg, n, k, sched):
     """North star: labels agree up to permutation, RCut within 1e-6 relative."""
     plp, solver, ctx = mods

@@ -17,6 +17,14 @@ VDIR = os.path.join(ROOT, "paper_2605_26975_b200", "variants")
 VARIANTS = {
     "h_c2": ["-DPLP_HALO_CPL8=2"],
     "h_c4": ["-DPLP_HALO_CPL8=4"],
+    "t192b3": ["-DPLP_HALO_TILE_ROWS=192", "-DPLP_HALO_NBUF=3"],
+    "t160b3": ["-DPLP_HALO_TILE_ROWS=160", "-DPLP_HALO_NBUF=3"],
+    "t128b4": ["-DPLP_HALO_TILE_ROWS=128", "-DPLP_HALO_NBUF=4"],
+    "t224b3": ["-DPLP_HALO_TILE_ROWS=224", "-DPLP_HALO_NBUF=3"],
+    "t96c2": ["-DPLP_HALO_TILE_ROWS=96", "-DPLP_HALO_CTAS=2"],
+    "t128c2": ["-DPLP_HALO_TILE_ROWS=128", "-DPLP_HALO_CTAS=2"],
+    "cs32": ["-DPLP_HALO_CSLEEP_NS=32"],
+    "cs100": ["-DPLP_HALO_CSLEEP_NS=100"],
 }
 
 
