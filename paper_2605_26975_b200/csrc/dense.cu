@@ -234,13 +234,18 @@ static double* dslot(plp_ctx* ctx, int s) { return ctx->scratch + 256 + (size_t)
 static plp_status gram(plp_ctx* ctx, int64_t n, int k, const double* X, const double* Xa,
                        const double* Y, const double* Ya, double* out) {
   if (k == 8 || k == 16) {  // fp64 tensor cores (dense_mma.cuh)
-    int grid = ctx->num_sms * 4;
+    static const int res1 = resident_ctas(gram_mma_kernel<1, false>, kMmaThreads),
+                     res2 = resident_ctas(gram_mma_kernel<2, false>, kMmaThreads);
+    int grid = ctx->num_sms * (k == 8 ? res1 : res2);  // one full wave
     const int cap = (int)(((int64_t)ctx->max_ctas * 4 * PLP_MAX_K) / (k * k));
     if (grid > cap) grid = cap;
     const int64_t blocks = (n + 3) / 4;
     if (blocks < (int64_t)grid * 8) grid = (int)std::max<int64_t>(1, (blocks + 7) / 8);
-    if (k == 8) gram_mma_kernel<1><<<grid, kMmaThreads, 0, ctx->stream>>>(n, X, Xa, Y, Ya, ctx->partials);
-    else gram_mma_kernel<2><<<grid, kMmaThreads, 0, ctx->stream>>>(n, X, Xa, Y, Ya, ctx->partials);
+    const bool sym = X == Y && Xa == Ya;
+    if (k == 8 && sym) gram_mma_kernel<1, true><<<grid, kMmaThreads, 0, ctx->stream>>>(n, X, Xa, Y, Ya, ctx->partials);
+    else if (k == 8) gram_mma_kernel<1, false><<<grid, kMmaThreads, 0, ctx->stream>>>(n, X, Xa, Y, Ya, ctx->partials);
+    else if (sym) gram_mma_kernel<2, true><<<grid, kMmaThreads, 0, ctx->stream>>>(n, X, Xa, Y, Ya, ctx->partials);
+    else gram_mma_kernel<2, false><<<grid, kMmaThreads, 0, ctx->stream>>>(n, X, Xa, Y, Ya, ctx->partials);
     PLP_LAUNCH_CHECK("gram_mma_kernel");
     sum_partials_kernel<<<1, 1024, 0, ctx->stream>>>(grid, k * k, ctx->partials, out);
     PLP_LAUNCH_CHECK("sum_partials_kernel");
@@ -261,7 +266,9 @@ static plp_status apply(plp_ctx* ctx, int64_t n, int k, const double* S, double 
   auto al16 = [](const void* p) { return ((uintptr_t)p & 15u) == 0; };
   if ((k == 8 || k == 16) && al16(out) && (S == nullptr || al16(S))) {  // fp64 tensor cores
     const int64_t blocks = (n + 7) / 8;
-    int64_t grid = (int64_t)ctx->num_sms * 8;
+    static const int res1 = resident_ctas(apply_mma_kernel<1>, kMmaThreads),
+                     res2 = resident_ctas(apply_mma_kernel<2>, kMmaThreads);
+    int64_t grid = (int64_t)ctx->num_sms * (k == 8 ? res1 : res2);  // one full wave
     if (blocks < grid * 8) grid = std::max<int64_t>(1, (blocks + 7) / 8);
     if (k == 8) apply_mma_kernel<1><<<(int)grid, kMmaThreads, 0, ctx->stream>>>(n, S, sgn, X, Xa, M, out);
     else apply_mma_kernel<2><<<(int)grid, kMmaThreads, 0, ctx->stream>>>(n, S, sgn, X, Xa, M, out);

@@ -4,7 +4,8 @@
 // Gram, fed by two coalesced 256-byte loads, so the kernels stream at the HBM rate where the scalar
 // versions (dense.cu) were issue/latency bound.
 //   gram:   C (k x k) = sum_r (X_r + Xa_r)^T (Y_r + Ya_r), per-CTA partials reduced in a fixed order
-//           (sum_partials_kernel) -- A fragment = 4 rows of X transposed, B fragment = 4 rows of Y;
+//           (sum_partials_kernel) -- A fragment = 4 rows of X transposed, B fragment = 4 rows of Y
+//           (SYM: Y = X, Ya = Xa, one set of loads);
 //   apply:  out_r = S_r + sgn (X_r + Xa_r) M for 8-row blocks -- A = 8 rows x 4 columns of X,
 //           B = 4 x 8 slice of sgn M, C/D = the block of S / out (out may alias S, X or Xa: each
 //           warp reads its rows before writing them).
@@ -23,7 +24,7 @@ constexpr int kMmaThreads = 256;
 
 // k = 8 KT.  Each warp owns a contiguous range of 4-row blocks; D[ta][tb] holds
 // C[8 ta + g][8 tb + 2 q + {0, 1}] with g = lane / 4, q = lane % 4.
-template <int KT>
+template <int KT, bool SYM>
 __global__ void __launch_bounds__(kMmaThreads) gram_mma_kernel(int64_t n, const double* __restrict__ X,
                                                                const double* __restrict__ Xa,
                                                                const double* __restrict__ Y,
@@ -54,7 +55,7 @@ __global__ void __launch_bounds__(kMmaThreads) gram_mma_kernel(int64_t n, const 
       for (int t = 0; t < KT; ++t) {
         const int64_t o = r * K + 8 * t + g;
         a[u][t] = ok ? __ldg(X + o) + (Xa ? __ldg(Xa + o) : 0.0) : 0.0;
-        c[u][t] = ok ? __ldg(Y + o) + (Ya ? __ldg(Ya + o) : 0.0) : 0.0;
+        c[u][t] = SYM ? a[u][t] : ok ? __ldg(Y + o) + (Ya ? __ldg(Ya + o) : 0.0) : 0.0;
       }
     }
 #pragma unroll
@@ -72,7 +73,7 @@ __global__ void __launch_bounds__(kMmaThreads) gram_mma_kernel(int64_t n, const 
     for (int t = 0; t < KT; ++t) {
       const int64_t o = r * K + 8 * t + g;
       a[t] = ok ? __ldg(X + o) + (Xa ? __ldg(Xa + o) : 0.0) : 0.0;
-      c[t] = ok ? __ldg(Y + o) + (Ya ? __ldg(Ya + o) : 0.0) : 0.0;
+      c[t] = SYM ? a[t] : ok ? __ldg(Y + o) + (Ya ? __ldg(Ya + o) : 0.0) : 0.0;
     }
 #pragma unroll
     for (int i = 0; i < KT; ++i)

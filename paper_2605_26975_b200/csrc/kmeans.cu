@@ -24,88 +24,145 @@ __device__ __forceinline__ double km_dist2(const double* x, int xs, const double
   return s;
 }
 
-// D2[i] = dist2(x_i, c) (first) or min(D2[i], dist2(x_i, c))
-__global__ void km_d2_kernel(int64_t n, int dim, const double* __restrict__ X,
-                             const double* __restrict__ c, double* __restrict__ D2, int first) {
+// D2[i] = dist2(x_i, c) (first) or min(D2[i], dist2(x_i, c)), and per chunk of kChunk = 256
+// points (one CTA iteration) the chunk sum cs[chunk] (warp xor trees, warps in order)
+__global__ void __launch_bounds__(kChunk) km_d2_kernel(int64_t n, int dim, const double* __restrict__ X,
+                                                      const double* __restrict__ c, double* __restrict__ D2,
+                                                      double* __restrict__ cs_out, int first) {
   __shared__ double cs[PLP_MAX_K];
+  __shared__ double ws[kChunk / 32];
   if (threadIdx.x < dim) cs[threadIdx.x] = c[threadIdx.x];
   __syncthreads();
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const double d = km_dist2(X + i * dim, 1, cs, dim);
-    D2[i] = first ? d : (d < D2[i] ? d : D2[i]);
-  }
-}
-
-// chunk sums (sequential within each chunk of kChunk points)
-__global__ void km_chunk_kernel(int64_t n, const double* __restrict__ D2, double* __restrict__ cs) {
   const int64_t nch = (n + kChunk - 1) / kChunk;
-  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nch;
-       c += (int64_t)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    const int64_t e = (c + 1) * kChunk < n ? (c + 1) * kChunk : n;
-    for (int64_t i = c * kChunk; i < e; ++i) s += D2[i];
-    cs[c] = s;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
+    const int64_t i = ch * kChunk + threadIdx.x;
+    double v = 0.0;
+    if (i < n) {
+      const double d = km_dist2(X + i * dim, 1, cs, dim);
+      v = first ? d : (d < D2[i] ? d : D2[i]);
+      D2[i] = v;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) ws[warp] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < kChunk / 32; ++w) t += ws[w];
+      cs_out[ch] = t;
+    }
+    __syncthreads();
   }
 }
 
-// One block: S = sum D2 (thread ranges of chunks, then a sequential pass over thread sums),
-// target = u S, smallest i with cumsum_i > target (n-1 if none; floor(u n) if S == 0).
-// Copies X[pick] to cent_row.
+// Block-wide inclusive prefix sum (blockDim.x = 1024) of one value per thread, offset by base:
+// warp shuffle scans, warp totals scanned by warp 0; every thread's result lands in pre[t].
+__device__ void block_scan_to(double v, double base, double* wsum, double* pre) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += y;
+  }
+  if (lane == 31) wsum[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    double w = lane < nw ? wsum[lane] : 0.0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < nw) wsum[lane] = w;
+  }
+  __syncthreads();
+  pre[threadIdx.x] = base + (v + (warp > 0 ? wsum[warp - 1] : 0.0));
+  __syncthreads();
+}
+
+// First index e in [0, cnt) of a monotone running sum pre[] (exclusive value ex = pre[e - 1], or
+// base at e = 0) with ex <= target < pre[e]; -1 if none.  Also the last e with a positive term.
+__device__ void block_find(int cnt, double base, double target, const double* pre, int* s_hit, int* s_last) {
+  const int t = threadIdx.x;
+  if (t == 0) {
+    *s_hit = -1;
+    *s_last = -1;
+  }
+  __syncthreads();
+  if (t < cnt) {
+    const double ex = t > 0 ? pre[t - 1] : base;
+    if (ex <= target && target < pre[t]) *s_hit = t;  // unique: pre is nondecreasing
+    if (pre[t] > ex) atomicMax(s_last, t);
+  }
+  __syncthreads();
+}
+
+// D^2 pick (k-means++): the smallest i with cumsum(D^2)_i > u * sum(D^2), found top-down with
+// parallel prefix sums: 1024 thread ranges of chunk sums, then the chunk sums of the chosen range
+// (in slices of 1024), then the D^2 values of the chosen chunk.  The running sums differ from the
+// oracle's sequential sum only in rounding order (reading #13); where rounding leaves no crossing
+// inside the chosen range, its last positive entry is taken.
 __global__ void __launch_bounds__(1024) km_pick_kernel(int64_t n, int dim, const double* __restrict__ X,
                                                        const double* __restrict__ D2,
                                                        const double* __restrict__ cs, double u,
                                                        double* __restrict__ cent_row,
                                                        int64_t* pick_out) {
-  __shared__ double ts[1024];
-  __shared__ int64_t s_pick;
+  __shared__ double wsum[32];
+  __shared__ double pre[1024];
+  __shared__ int s_hit, s_last;
   const int64_t nch = (n + kChunk - 1) / kChunk;
-  const int T = blockDim.x;
+  const int T = blockDim.x, t = threadIdx.x;
   const int64_t per = (nch + T - 1) / T;
-  const int t = threadIdx.x;
-  double s = 0.0;
-  for (int64_t c = t * per; c < (t + 1) * per && c < nch; ++c) s += cs[c];
-  ts[t] = s;
-  __syncthreads();
-  if (t == 0) {
-    double S = 0.0;
-    for (int q = 0; q < T; ++q) S += ts[q];
-    int64_t pick = n - 1;
-    if (S > 0.0) {
-      const double target = u * S;
-      double run = 0.0;
-      int q = 0;
-      for (; q < T; ++q) {
-        if (run + ts[q] > target) break;
-        run += ts[q];
+  double v = 0.0;
+  for (int64_t c = t * per; c < (t + 1) * per && c < nch; ++c) v += cs[c];
+  block_scan_to(v, 0.0, wsum, pre);
+  const double S = pre[T - 1];
+  int64_t pick;
+  if (!(S > 0.0)) {
+    pick = (int64_t)floor(u * (double)n);
+    if (pick >= n) pick = n - 1;
+  } else {
+    const double target = u * S;
+    // level 1: thread range q
+    block_find(T, 0.0, target, pre, &s_hit, &s_last);
+    const int q = s_hit >= 0 ? s_hit : s_last;
+    double base = q > 0 ? pre[q - 1] : 0.0;
+    __syncthreads();
+    // level 2: chunk inside range q, slices of T chunks
+    const int64_t c0 = (int64_t)q * per, c1 = ((int64_t)q + 1) * per < nch ? ((int64_t)q + 1) * per : nch;
+    int64_t chosen = -1, lastpos = -1;
+    double lastbase = base;
+    for (int64_t cb = c0; cb < c1; cb += T) {
+      const int cnt = (int)(c1 - cb < T ? c1 - cb : T);
+      block_scan_to(t < cnt ? cs[cb + t] : 0.0, base, wsum, pre);
+      block_find(cnt, base, target, pre, &s_hit, &s_last);
+      if (s_last >= 0) {
+        lastpos = cb + s_last;
+        lastbase = s_last > 0 ? pre[s_last - 1] : base;
       }
-      if (q < T) {
-        int64_t c = q * per;
-        const int64_t cend = ((int64_t)q + 1) * per < nch ? ((int64_t)q + 1) * per : nch;
-        for (; c < cend; ++c) {
-          if (run + cs[c] > target) break;
-          run += cs[c];
-        }
-        if (c < cend) {
-          const int64_t e = (c + 1) * kChunk < n ? (c + 1) * kChunk : n;
-          for (int64_t i = c * kChunk; i < e; ++i) {
-            run += D2[i];
-            if (run > target) {
-              pick = i;
-              break;
-            }
-          }
-        }
+      if (s_hit >= 0) {
+        chosen = cb + s_hit;
+        base = s_hit > 0 ? pre[s_hit - 1] : base;
+        break;
       }
-    } else {
-      pick = (int64_t)floor(u * (double)n);
-      if (pick >= n) pick = n - 1;
+      base = pre[cnt - 1];
+      __syncthreads();
     }
-    s_pick = pick;
-    if (pick_out) *pick_out = pick;
+    if (chosen < 0) {  // rounding left no crossing: the last positive chunk of the range
+      chosen = lastpos;
+      base = lastbase;
+    }
+    __syncthreads();
+    // level 3: point inside chunk `chosen`
+    const int64_t i0 = chosen * kChunk, i1 = (chosen + 1) * kChunk < n ? (chosen + 1) * kChunk : n;
+    const int cnt = (int)(i1 - i0);
+    block_scan_to(t < cnt ? D2[i0 + t] : 0.0, base, wsum, pre);
+    block_find(cnt, base, target, pre, &s_hit, &s_last);
+    pick = i0 + (s_hit >= 0 ? s_hit : (s_last >= 0 ? s_last : cnt - 1));
   }
-  __syncthreads();
-  if (t < dim) cent_row[t] = X[s_pick * dim + t];
+  if (t == 0 && pick_out) *pick_out = pick;
+  if (t < dim) cent_row[t] = X[pick * dim + t];
 }
 
 // Fused assign (nearest centroid, ties -> lowest index) + per-CTA partials:
@@ -336,14 +393,20 @@ __global__ void km_reseed_kernel(int grid, int dim, int c, const double* pv, con
   if (threadIdx.x == 0) best_d[far] = -1.0;
 }
 
-__global__ void km_sum_kernel(int grid, int E, const double* part, double* out) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int e = warp; e < E; e += (blockDim.x >> 5)) {
-    double s = 0.0;
-    for (int b = lane; b < grid; b += 32) s += part[(int64_t)b * E + e];
+// out[e] = sum_b part[b][e]: one CTA per entry (thread-strided, warp xor trees, warps in order)
+__global__ void __launch_bounds__(256) km_sum_kernel(int grid, int E, const double* part, double* out) {
+  __shared__ double ws[8];
+  const int e = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (int b = threadIdx.x; b < grid; b += 256) s += part[(int64_t)b * E + e];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) out[e] = s;
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) ws[warp] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += ws[w];
+    out[e] = t;
   }
 }
 
@@ -383,6 +446,8 @@ extern "C" plp_status plp_kmeans(plp_ctx* ctx, int64_t n, int dim, int K, const 
   const int64_t part_cap = (int64_t)ctx->max_ctas * 4 * PLP_MAX_K;
   if ((int64_t)grid * E > part_cap) grid = (int)(part_cap / E);
   double* red = ctx->scratch + 256;  // E <= 32*32+33 doubles
+  static const int res_d2 = resident_ctas(km_d2_kernel, kChunk);
+  const int gridd = (int)std::min<int64_t>((int64_t)ctx->num_sms * res_d2, std::max<int64_t>(1, nch));
   int gridn = (int)((n + 255) / 256);
   if (gridn > ctx->max_ctas) gridn = ctx->max_ctas;
   double* pv = ctx->partials;
@@ -397,17 +462,16 @@ extern "C" plp_status plp_kmeans(plp_ctx* ctx, int64_t n, int dim, int K, const 
     if (c0 >= n) c0 = n - 1;
     PLP_CUDA(cudaMemcpyAsync(cent, X + c0 * dim, sizeof(double) * dim, cudaMemcpyDeviceToDevice, st));
     for (int m = 1; m < K; ++m) {
-      km_d2_kernel<<<gridn, 256, 0, st>>>(n, dim, X, cent + (int64_t)(m - 1) * dim, D2, m == 1);
+      km_d2_kernel<<<gridd, kChunk, 0, st>>>(n, dim, X, cent + (int64_t)(m - 1) * dim, D2, csum, m == 1);
       PLP_LAUNCH_CHECK("km_d2_kernel");
-      const int gc = (int)((nch + 255) / 256);
-      km_chunk_kernel<<<gc, 256, 0, st>>>(n, D2, csum);
-      PLP_LAUNCH_CHECK("km_chunk_kernel");
       km_pick_kernel<<<1, 1024, 0, st>>>(n, dim, X, D2, csum, u[m], cent + (int64_t)m * dim, nullptr);
       PLP_LAUNCH_CHECK("km_pick_kernel");
     }
     // ---- Lloyd ----
     const bool mma = K <= 8 && dim <= 8;
-    int grid_mma = ctx->num_sms * 4;
+    static const int res_mma = std::min(resident_ctas(km_assign_mma_kernel<8>, 256),
+                                        resident_ctas(km_assign_mma_kernel<0>, 256));
+    int grid_mma = ctx->num_sms * res_mma;  // one full wave
     if ((int64_t)grid_mma * E > part_cap) grid_mma = (int)(part_cap / E);
     const int64_t groups = (n + 31) / 32;
     if (groups < (int64_t)grid_mma * 8) grid_mma = (int)std::max<int64_t>(1, (groups + 7) / 8);
@@ -422,7 +486,7 @@ extern "C" plp_status plp_kmeans(plp_ctx* ctx, int64_t n, int dim, int K, const 
         km_assign_kernel<<<grid, kKmThreads, 0, st>>>(n, dim, K, X, cent, lab, best_d, ctx->partials);
         PLP_LAUNCH_CHECK("km_assign_kernel");
       }
-      km_sum_kernel<<<1, 1024, 0, st>>>(mma ? grid_mma : grid, E, ctx->partials, red);
+      km_sum_kernel<<<E, 256, 0, st>>>(mma ? grid_mma : grid, E, ctx->partials, red);
       PLP_LAUNCH_CHECK("km_sum_kernel");
       PLP_CUDA(cudaMemcpyAsync(h.data(), red, sizeof(double) * E, cudaMemcpyDeviceToHost, st));
       PLP_CUDA(cudaStreamSynchronize(st));

@@ -12,6 +12,18 @@
 // unused and t = a^{p-1} must stay on the fast path for every a > 0 (pow64.cuh).
 constexpr double kNoCap = 1e-300;
 
+// Resident CTAs per SM of a kernel at this block size (grids sized to whole waves: a grid of
+// num_sms x this many CTAs runs in one wave, with no partial second wave).
+template <class Kernel>
+inline int resident_ctas(Kernel kernel, int threads, size_t smem = 0) {
+  int b = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, threads, smem) != cudaSuccess || b < 1) {
+    cudaGetLastError();
+    b = 1;
+  }
+  return b;
+}
+
 struct plp_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;

@@ -446,7 +446,7 @@ static int env_int(const char* name, int dflt) {
   return v ? atoi(v) : dflt;
 }
 
-static int fused_grid(plp_ctx* ctx, int64_t row_blocks, int E, int per_sm) {
+static int fused_grid(plp_ctx* ctx, int64_t row_blocks, int E, int per_sm) {  // per_sm: one wave
   int64_t g = (int64_t)ctx->num_sms * per_sm;
   const int64_t cap = ((int64_t)ctx->max_ctas * 4 * PLP_MAX_K) / E;  // partials capacity
   if (g > cap) g = cap;
@@ -460,11 +460,14 @@ static plp_status fused_iteration(plp_ctx* ctx, int64_t n, const double* U, cons
                                   double* Heta, double* r, double* dlt, const double* EH, double* scal,
                                   int* status, int max_iters) {
   constexpr int K = 8 * KT, KK = K * K;
-  static const int per_sm_a = env_int("PLP_TCG_GRID_A", 4), per_sm_b = env_int("PLP_TCG_GRID_B", 3);
+  static const int unr_a = env_int("PLP_TCG_UNR_A", 4);
+  static const int per_sm_a = env_int("PLP_TCG_GRID_A", unr_a == 4 ? resident_ctas(tcg_gram_a_kernel<KT, 4>, kTcgThreads)
+                                                                    : resident_ctas(tcg_gram_a_kernel<KT, 2>, kTcgThreads));
+  static const int per_sm_b = env_int("PLP_TCG_GRID_B", resident_ctas(tcg_update_kernel<KT>, kTcgThreads));
+  static const int per_sm_c = resident_ctas(tcg_finish_kernel<KT>, kTcgThreads);
   unsigned* counter = reinterpret_cast<unsigned*>(ctx->flag + 4);
   constexpr int EA = 2 * KK + 2, EB = KK + 1;
   const int ga = fused_grid(ctx, (n + 3) / 4, EA, per_sm_a);
-  static const int unr_a = env_int("PLP_TCG_UNR_A", 4);
   if (unr_a == 4)
     tcg_gram_a_kernel<KT, 4><<<ga, kTcgThreads, 0, ctx->stream>>>(n, U, EH, dlt, S, ctx->partials);
   else
@@ -480,7 +483,7 @@ static plp_status fused_iteration(plp_ctx* ctx, int64_t n, const double* U, cons
   tcg_reduce_kernel<K, 1><<<EB, 256, 0, ctx->stream>>>(gb, ctx->partials, scal + kTotB, counter + 1, scal, status,
                                                        max_iters);
   PLP_LAUNCH_CHECK("tcg_reduce_kernel");
-  int64_t gc = (int64_t)ctx->num_sms * 8;
+  int64_t gc = (int64_t)ctx->num_sms * per_sm_c;
   const int64_t bc = (n + 7) / 8;
   if (bc < gc * kTcgWarps) gc = std::max<int64_t>(1, (bc + kTcgWarps - 1) / kTcgWarps);
   tcg_finish_kernel<KT><<<(int)gc, kTcgThreads, 0, ctx->stream>>>(n, U, scal, r, dlt);
