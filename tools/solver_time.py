@@ -16,7 +16,7 @@ from plp_inputs import make_config, draw_U  # noqa: E402
 from paper_2605_26975_b200 import plp, solver  # noqa: E402
 
 RUNS = {"C1": (3, [2.0, 1.8, 1.5, 1.2], None), "C2": (2, [2.0, 1.1], None), "D16": (4, [2.0, 1.5], None),
-        "C5": (8, [2.0], 4), "D20": (8, [2.0], 6)}
+        "C5": (8, [2.0], 4), "D20": (8, [2.0, 1.5], None)}
 VARIANTS = {"host": dict(device_tcg=False), "device": dict(tcg_graph=False, tcg_fused=False),
             "graph": dict(tcg_fused=False), "fused": dict(tcg_graph=False, tcg_fused=True),
             "fused+graph": dict(tcg_fused=True)}
