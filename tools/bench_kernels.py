@@ -38,6 +38,8 @@ def main():
     ap.add_argument("--config", default="C5")
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--orders", default="tile,rcm,natural")
+    ap.add_argument("--oracle", action="store_true",
+                    help="also time the CPU oracle for each row (bounded samples, scaled to the full size)")
     args = ap.parse_args()
     k, p = CONFIG_KP[args.config]
     peak, kind = load_peaks()
@@ -45,14 +47,22 @@ def main():
     torch.cuda.set_stream(stream)
     ctx = plp.Context(0, stream)
 
+    orc = {}
+
     def row(name, ms, byts, extra=None):
         gbs = byts / (ms * 1e-3) / 1e9
         d = {"config": args.config, "row": name, "ms": ms, "algorithmic_bytes": int(byts), "GBps": gbs,
              "frac_hbm": gbs / peak, "peak": peak, "peak_kind": kind}
+        tag = name.split()[0] + (" full" if "full mode" in name else "") + (" seed" if "seeding" in name else "")
+        if tag in orc and not any(x in name for x in ("(rcm order)", "(natural order)", "axpby")):
+            o_ms, desc = orc[tag]
+            d.update({"oracle_ms_full_size": o_ms, "oracle_sample": desc, "gpu_speedup_vs_oracle": o_ms / ms})
         if extra:
             d.update(extra)
         print(json.dumps(d), flush=True)
 
+    if args.oracle:
+        orc.update(oracle_rows(get_graph(args.config, "tile"), k, p))
     for order in args.orders.split(","):
         g = get_graph(args.config, order)
         n, nnz = g.n, g.nnz
@@ -100,6 +110,62 @@ def main():
         ms = timed(lambda: plp.rcut(ctx, G, k, labels), args.reps, stream)
         row("a12 RCut", ms, csr + 4 * n)
         tcg_rows(ctx, G, U, k, p, stream, row, csr)
+
+
+def oracle_rows(g, k, p, frac=0.125):
+    """The CPU oracle (as it stands, all host cores) per row: edge rows on the shard of the first
+    frac of the rows (scaled by its share of nnz), dense rows on the full arrays, k-means on the
+    first frac of the points (scaled by n), RCut on the full graph.  Returns {tag: (ms, desc)}."""
+    import time
+    import oracle
+    from oracle import dense as odense
+    from paper_2605_26975_b200 import plp as _plp
+    oracle.set_threads(os.cpu_count() or 1)
+    cores = oracle.get_threads()
+    S = max(1, int(g.n * frac))
+    halo, rp_loc, col_loc = _plp.halo_plan(g.row_ptr, g.col, 0, S)
+    ext = np.concatenate([np.arange(S), halo])
+
+    class Loc:
+        row_ptr, col, w = rp_loc, col_loc, g.w[:g.row_ptr[S]]
+
+    U = draw_U(g.n, k, 0)
+    E = draw_eta(g.n, k, 0)
+    Ul, El = U[ext], E[ext]
+    scale = g.nnz / float(rp_loc[-1])
+    out = {}
+
+    def t(fn, reps=1):
+        t0 = time.time()
+        for _ in range(reps):
+            r = fn()
+        return (time.time() - t0) / reps * 1e3, r
+    desc = f"rows [0,{S}) shard ({int(rp_loc[-1])} nnz), x{scale:.2f}, {cores} threads"
+    ms, (F, A, B) = t(lambda: oracle.objective(Loc, Ul, p))
+    out["a3"] = (ms * scale, desc)
+    ms, _ = t(lambda: oracle.euc_grad(Loc, Ul, p, A, B))
+    out["a4"] = (ms * scale, desc)
+    ms, _ = t(lambda: oracle.hessvec(Loc, Ul, El, p, 1e-9, "sparse", (A, B)))
+    out["a5"] = (ms * scale, desc)
+    ms, _ = t(lambda: oracle.hessvec(Loc, Ul, El, p, 1e-9, "full", (A, B)))
+    out["a5+a6 full"] = (ms * scale, desc)
+    ms, _ = t(lambda: (oracle.objective(Loc, Ul, p), oracle.euc_grad(Loc, Ul, p, A, B),
+                       oracle.hessvec(Loc, Ul, El, p, 1e-9, "sparse", (A, B))))
+    out["a7"] = (ms * scale, desc)
+    dd = f"full {g.n} x {k} arrays (numpy)"
+    out["a8"] = (t(lambda: odense.project(U, E))[0], dd)
+    out["a9"] = (t(lambda: odense.retract(U, E))[0], dd)
+    out["a10"] = (t(lambda: odense.dot(U, E))[0], dd)
+    Xs = U[:S]
+    u = draw_uniforms(1, k)
+    m0, _ = t(lambda: oracle.kmeans(Xs, k, u, restarts=1, max_iters=0))
+    m3, _ = t(lambda: oracle.kmeans(Xs, k, u, restarts=1, max_iters=3, rel_tol=0.0))
+    kd = f"first {S} points, x{g.n / S:.1f}"
+    out["a11"] = ((m3 - m0) / 3 * g.n / S, kd)
+    out["a11 seed"] = (m0 * g.n / S, kd)
+    lab = (np.arange(g.n) * k // g.n).astype(np.int32)
+    out["a12"] = (t(lambda: oracle.rcut(g, lab, k))[0], f"full graph, {cores} threads")
+    return out
 
 
 def tcg_rows(ctx, G, U, k, p, stream, row, csr):
