@@ -130,66 +130,96 @@ __global__ void objective_from_ab_kernel(int k, const double* AB, double* F) {
 }
 
 // ---- RCut (a12): per-CTA cut/size partials by label, fixed-order --------------------------------
-__global__ void __launch_bounds__(256) rcut_kernel(int64_t n, const int32_t* __restrict__ rp,
-                                                   const int32_t* __restrict__ col,
-                                                   const double* __restrict__ w, int K,
-                                                   const int32_t* __restrict__ lab,
-                                                   double* part_cut, int64_t* part_size,
-                                                   int* bad) {
-  __shared__ int s_lab[256];
-  __shared__ double s_cut[256];
-  double acc_cut = 0.0;
-  int64_t acc_size = 0;
-  const int c = threadIdx.x;  // thread c < K owns cluster c's partials
-  const int64_t tiles = (n + 255) / 256;
-  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-    const int64_t i = tile * 256 + threadIdx.x;
+// One thread per row (32 rows in flight per warp: the row_ptr -> col -> label chain is latency-bound);
+// per cluster c the warp sums its rows' cuts with a shuffle tree and counts them with a ballot
+// (lane c keeps cluster c), then the CTA's warps are added in order.  No atomics, fixed order.
+constexpr int kRcutThreads = 256, kRcutLanes = 1;
+__global__ void __launch_bounds__(kRcutThreads) rcut_kernel(int64_t n, const int32_t* __restrict__ rp,
+                                                           const int32_t* __restrict__ col,
+                                                           const double* __restrict__ w, int K,
+                                                           const int32_t* __restrict__ lab,
+                                                           double* part_cut, int64_t* part_size,
+                                                           int* bad) {
+  constexpr int NW = kRcutThreads / 32, RPW = 32 / kRcutLanes;
+  __shared__ double s_cut[NW][PLP_MAX_K];
+  __shared__ int64_t s_cnt[NW][PLP_MAX_K];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = lane / kRcutLanes, gl = lane % kRcutLanes;
+  double acc_cut = 0.0;  // lane c < K: cluster c
+  int64_t acc_cnt = 0;
+  const int64_t steps = (n + RPW - 1) / RPW;
+  const int64_t tw = (int64_t)gridDim.x * NW, wid = (int64_t)blockIdx.x * NW + warp;
+  const int64_t s0 = steps * wid / tw, s1 = steps * (wid + 1) / tw;
+  for (int64_t st = s0; st < s1; ++st) {
+    const int64_t i = st * RPW + grp;
     int li = -1;
     double cut = 0.0;
     if (i < n) {
-      li = lab[i];
-      if (li < 0 || li >= K) atomicExch(bad, 1);
-      for (int e = rp[i]; e < rp[i + 1]; ++e)
-        if (lab[col[e]] != li) cut += w[e];
+      li = __ldg(lab + i);
+      if (gl == 0 && (li < 0 || li >= K)) atomicExch(bad, 1);
+      const int e1 = __ldg(rp + i + 1);
+      for (int e = __ldg(rp + i) + gl; e < e1; e += kRcutLanes)
+        if (__ldg(lab + __ldg(col + e)) != li) cut += __ldg(w + e);
     }
-    s_lab[threadIdx.x] = li;
-    s_cut[threadIdx.x] = cut;
-    __syncthreads();
-    if (c < K) {
-      for (int t = 0; t < 256; ++t)
-        if (s_lab[t] == c) {
-          acc_cut += s_cut[t];
-          acc_size += 1;
-        }
+#pragma unroll
+    for (int o = kRcutLanes / 2; o > 0; o >>= 1) cut += __shfl_xor_sync(0xffffffffu, cut, o);
+    const bool lead = gl == 0 && i < n;
+    for (int c = 0; c < K; ++c) {
+      double v = (lead && li == c) ? cut : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      const int cnt = __popc(__ballot_sync(0xffffffffu, lead && li == c));
+      if (lane == c) {
+        acc_cut += v;
+        acc_cnt += cnt;
+      }
     }
-    __syncthreads();
   }
-  if (c < K) {
-    part_cut[(int64_t)blockIdx.x * K + c] = acc_cut;
-    part_size[(int64_t)blockIdx.x * K + c] = acc_size;
+  if (lane < K) {
+    s_cut[warp][lane] = acc_cut;
+    s_cnt[warp][lane] = acc_cnt;
+  }
+  __syncthreads();
+  if (threadIdx.x < K) {
+    double c = 0.0;
+    int64_t m = 0;
+    for (int q = 0; q < NW; ++q) {
+      c += s_cut[q][threadIdx.x];
+      m += s_cnt[q][threadIdx.x];
+    }
+    part_cut[(int64_t)blockIdx.x * K + threadIdx.x] = c;
+    part_size[(int64_t)blockIdx.x * K + threadIdx.x] = m;
   }
 }
 
-__global__ void rcut_finalize_kernel(int grid, int K, const double* part_cut,
-                                     const int64_t* part_size, double* cut, int64_t* sizes,
-                                     double* rcut) {
+// cut / sizes per cluster (one warp per cluster, lanes over the CTAs, xor tree), then RCut
+__global__ void __launch_bounds__(1024) rcut_finalize_kernel(int grid, int K, const double* part_cut,
+                                                             const int64_t* part_size, double* cut,
+                                                             int64_t* sizes, double* rcut) {
   __shared__ double s_c[PLP_MAX_K];
   __shared__ int64_t s_n[PLP_MAX_K];
-  const int c = threadIdx.x;
+  const int c = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (c < K) {
     double sc = 0.0;
     int64_t sn = 0;
-    for (int b = 0; b < grid; ++b) {
+    for (int b = lane; b < grid; b += 32) {
       sc += part_cut[(int64_t)b * K + c];
       sn += part_size[(int64_t)b * K + c];
     }
-    s_c[c] = sc;
-    s_n[c] = sn;
-    if (cut) cut[c] = sc;
-    if (sizes) sizes[c] = sn;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sc += __shfl_xor_sync(0xffffffffu, sc, o);
+      sn += __shfl_xor_sync(0xffffffffu, sn, o);
+    }
+    if (lane == 0) {
+      s_c[c] = sc;
+      s_n[c] = sn;
+      if (cut) cut[c] = sc;
+      if (sizes) sizes[c] = sn;
+    }
   }
   __syncthreads();
-  if (c == 0 && rcut) {
+  if (threadIdx.x == 0 && rcut) {
     double r = 0.0;
     for (int q = 0; q < K; ++q) r += (s_n[q] > 0) ? s_c[q] / (double)s_n[q] : NAN;
     *rcut = r;
@@ -383,16 +413,18 @@ extern "C" plp_status plp_rcut(plp_ctx* ctx, const plp_graph* g, int clusters,
                                const int32_t* labels, double* cut, int64_t* sizes, double* rcut) {
   if (!ctx || !g || !labels) return set_error(PLP_ERR_ARG, "null argument");
   if (clusters < 1 || clusters > PLP_MAX_K) return set_error(PLP_ERR_DOMAIN, "clusters must be in [1, 32]");
-  int grid = (int)((g->n_rows + 255) / 256);
+  static const int res = resident_ctas(rcut_kernel, kRcutThreads);
+  int grid = ctx->num_sms * res;  // one full wave
+  const int64_t want = (g->n_rows + 255) / 256;
+  if (grid > want) grid = (int)std::max<int64_t>(1, want);
   if (grid > ctx->max_ctas) grid = ctx->max_ctas;
-  if (grid < 1) grid = 1;
   double* pc = ctx->partials;
   int64_t* ps = reinterpret_cast<int64_t*>(ctx->partials + (int64_t)ctx->max_ctas * PLP_MAX_K);
   PLP_CUDA(cudaMemsetAsync(ctx->flag, 0, sizeof(int), ctx->stream));
-  rcut_kernel<<<grid, 256, 0, ctx->stream>>>(g->n_rows, g->rp, g->col, g->w, clusters, labels, pc,
+  rcut_kernel<<<grid, kRcutThreads, 0, ctx->stream>>>(g->n_rows, g->rp, g->col, g->w, clusters, labels, pc,
                                               ps, ctx->flag);
   PLP_LAUNCH_CHECK("rcut_kernel");
-  rcut_finalize_kernel<<<1, 32, 0, ctx->stream>>>(grid, clusters, pc, ps, cut, sizes, rcut);
+  rcut_finalize_kernel<<<1, 1024, 0, ctx->stream>>>(grid, clusters, pc, ps, cut, sizes, rcut);
   PLP_LAUNCH_CHECK("rcut_finalize_kernel");
   return PLP_OK;
 }

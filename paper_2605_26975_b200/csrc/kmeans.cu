@@ -231,93 +231,125 @@ __global__ void __launch_bounds__(kKmThreads) km_assign_kernel(int64_t n, int di
 // m8n8k4: A[c][q] = [label of point q == c], B[q][d] = X[q][d] or 1), 4 points per instruction.
 // Each warp owns a contiguous range of 32-point groups; per-CTA partials in a fixed order, layout
 // [sums K*dim | counts K | sse] like km_assign_kernel.
-template <int DIM>  // DIM = 8: vectorised point loads; DIM = 0: runtime dim <= 8
-__global__ void __launch_bounds__(256) km_assign_mma_kernel(int64_t n, int dim_rt, int K,
+template <int DIM, int KC>  // DIM = 8: vectorised point loads; DIM = 0: runtime dim <= 8;
+                           // KC = 8: K = 8 at compile time (unrolled); KC = 0: runtime K <= 8
+__global__ void __launch_bounds__(256) km_assign_mma_kernel(int64_t n, int dim_rt, int K_rt,
                                                             const double* __restrict__ X,
                                                             const double* __restrict__ cent,
                                                             int32_t* __restrict__ lab,
                                                             double* __restrict__ best_d,
                                                             double* __restrict__ part) {
-  constexpr int NW = 8;
+  constexpr int NW = 8, PPL = 2;  // two points per lane: each centroid load serves both
   const int dim = DIM > 0 ? DIM : dim_rt;
+  const int K = KC > 0 ? KC : K_rt;
   __shared__ __align__(16) double cs[8 * 8];
   __shared__ double red[NW][8 * 8 + 8 + 1];
   for (int i = threadIdx.x; i < K * dim; i += blockDim.x) cs[i] = cent[i];
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
-  const int64_t groups = (n + 31) / 32;
+  const int64_t groups = (n + 32 * PPL - 1) / (32 * PPL);
   const int64_t tw = (int64_t)gridDim.x * NW, wid = (int64_t)blockIdx.x * NW + warp;
   const int64_t g0 = groups * wid / tw, g1 = groups * (wid + 1) / tw;
   double s0 = 0.0, s1 = 0.0, sse = 0.0;
   int cnt = 0;  // lane c < K counts cluster c
   for (int64_t gr = g0; gr < g1; ++gr) {
-    const int64_t p0 = gr * 32, i = p0 + lane;
-    const bool ok = i < n;
-    double x[8];
-    if constexpr (DIM == 8) {
-      if (ok) {
+    const int64_t p0 = gr * 32 * PPL;
+    double x[PPL][8];
+    bool ok[PPL];
 #pragma unroll
-        for (int d = 0; d < 8; d += 2) {
-          const double2 t = __ldg(reinterpret_cast<const double2*>(X + i * 8 + d));
-          x[d] = t.x;
-          x[d + 1] = t.y;
-        }
-      } else {
-#pragma unroll
-        for (int d = 0; d < 8; ++d) x[d] = 0.0;
-      }
-    } else {
-#pragma unroll
-      for (int d = 0; d < 8; ++d) x[d] = (ok && d < dim) ? __ldg(X + i * dim + d) : 0.0;
-    }
-    int bc = -1;
-    double bd = 0.0;
-    if (ok) {
-      bd = INFINITY;
-#pragma unroll 1
-      for (int c = 0; c < K; ++c) {
-        double sd = 0.0;
-        if constexpr (DIM == 8) {
-          // centroid row as four 16-byte broadcasts (LDS.128) instead of eight LDS.64
-          const double2* cr = reinterpret_cast<const double2*>(cs + c * 8);
+    for (int h = 0; h < PPL; ++h) {
+      const int64_t i = p0 + 32 * h + lane;
+      ok[h] = i < n;
+      if constexpr (DIM == 8) {
+        if (ok[h]) {
 #pragma unroll
           for (int d = 0; d < 8; d += 2) {
-            const double2 cc = cr[d / 2];
-            const double t0 = __dsub_rn(x[d], cc.x);
-            sd = __dadd_rn(sd, __dmul_rn(t0, t0));
-            const double t1 = __dsub_rn(x[d + 1], cc.y);
-            sd = __dadd_rn(sd, __dmul_rn(t1, t1));
+            const double2 t = __ldg(reinterpret_cast<const double2*>(X + i * 8 + d));
+            x[h][d] = t.x;
+            x[h][d + 1] = t.y;
           }
         } else {
 #pragma unroll
-          for (int d = 0; d < 8; ++d) {
-            if (d < dim) {
-              const double t = __dsub_rn(x[d], cs[c * dim + d]);
-              sd = __dadd_rn(sd, __dmul_rn(t, t));
+          for (int d = 0; d < 8; ++d) x[h][d] = 0.0;
+        }
+      } else {
+#pragma unroll
+        for (int d = 0; d < 8; ++d) x[h][d] = (ok[h] && d < dim) ? __ldg(X + i * dim + d) : 0.0;
+      }
+    }
+    int bc[PPL];
+    double bd[PPL];
+#pragma unroll
+    for (int h = 0; h < PPL; ++h) {
+      bc[h] = 0;
+      bd[h] = INFINITY;
+    }
+#pragma unroll(KC > 0 ? KC : 1)
+    for (int c = 0; c < K; ++c) {
+      double sd[PPL];
+#pragma unroll
+      for (int h = 0; h < PPL; ++h) sd[h] = 0.0;
+      if constexpr (DIM == 8) {
+        // centroid row as four 16-byte broadcasts (LDS.128), shared by the lane's points
+        const double2* cr = reinterpret_cast<const double2*>(cs + c * 8);
+#pragma unroll
+        for (int d = 0; d < 8; d += 2) {
+          const double2 cc = cr[d / 2];
+#pragma unroll
+          for (int h = 0; h < PPL; ++h) {
+            const double t0 = __dsub_rn(x[h][d], cc.x);
+            sd[h] = __dadd_rn(sd[h], __dmul_rn(t0, t0));
+            const double t1 = __dsub_rn(x[h][d + 1], cc.y);
+            sd[h] = __dadd_rn(sd[h], __dmul_rn(t1, t1));
+          }
+        }
+      } else {
+#pragma unroll
+        for (int d = 0; d < 8; ++d) {
+          if (d < dim) {
+            const double cv = cs[c * dim + d];
+#pragma unroll
+            for (int h = 0; h < PPL; ++h) {
+              const double t = __dsub_rn(x[h][d], cv);
+              sd[h] = __dadd_rn(sd[h], __dmul_rn(t, t));
             }
           }
         }
-        if (sd < bd || c == 0) {
-          bd = sd;
-          bc = c;
-        }
       }
-      lab[i] = bc;
-      best_d[i] = bd;
-      sse += bd;
-    }
-    for (int c = 0; c < K; ++c) {
-      const int m = __popc(__ballot_sync(0xffffffffu, bc == c));
-      if (lane == c) cnt += m;
+#pragma unroll
+      for (int h = 0; h < PPL; ++h)
+        if (sd[h] < bd[h] || c == 0) {  // ties keep the lowest index
+          bd[h] = sd[h];
+          bc[h] = c;
+        }
     }
 #pragma unroll
-    for (int sb = 0; sb < 8; ++sb) {
-      const int lq = __shfl_sync(0xffffffffu, bc, 4 * sb + q);
-      const int64_t pq = p0 + 4 * sb + q;
-      const double a = (lq == g) ? 1.0 : 0.0;
-      const double b = (pq < n && g < dim) ? __ldg(X + pq * dim + g) : 0.0;
-      dmma884(s0, s1, a, b);
+    for (int h = 0; h < PPL; ++h) {
+      const int64_t i = p0 + 32 * h + lane;
+      if (ok[h]) {
+        lab[i] = bc[h];
+        best_d[i] = bd[h];
+        sse += bd[h];
+      } else {
+        bc[h] = -1;
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < PPL; ++h) {
+      for (int c = 0; c < K; ++c) {
+        const int m = __popc(__ballot_sync(0xffffffffu, bc[h] == c));
+        if (lane == c) cnt += m;
+      }
+      const int64_t ph = p0 + 32 * h;
+#pragma unroll
+      for (int sb = 0; sb < 8; ++sb) {
+        const int lq = __shfl_sync(0xffffffffu, bc[h], 4 * sb + q);
+        const int64_t pq = ph + 4 * sb + q;
+        const double a = (lq == g) ? 1.0 : 0.0;
+        const double b = (pq < n && g < dim) ? __ldg(X + pq * dim + g) : 0.0;
+        dmma884(s0, s1, a, b);
+      }
     }
   }
   // per-warp results -> shared, then a fixed-order sum over warps
@@ -469,18 +501,20 @@ extern "C" plp_status plp_kmeans(plp_ctx* ctx, int64_t n, int dim, int K, const 
     }
     // ---- Lloyd ----
     const bool mma = K <= 8 && dim <= 8;
-    static const int res_mma = std::min(resident_ctas(km_assign_mma_kernel<8>, 256),
-                                        resident_ctas(km_assign_mma_kernel<0>, 256));
+    static const int res_mma = std::min(resident_ctas(km_assign_mma_kernel<8, 8>, 256),
+                                        resident_ctas(km_assign_mma_kernel<0, 0>, 256));
     int grid_mma = ctx->num_sms * res_mma;  // one full wave
     if ((int64_t)grid_mma * E > part_cap) grid_mma = (int)(part_cap / E);
-    const int64_t groups = (n + 31) / 32;
+    const int64_t groups = (n + 63) / 64;
     if (groups < (int64_t)grid_mma * 8) grid_mma = (int)std::max<int64_t>(1, (groups + 7) / 8);
     auto assign = [&](double* sse_out, std::vector<double>& h) -> plp_status {
       if (mma) {
-        if (dim == 8 && ((uintptr_t)X & 15u) == 0)
-          km_assign_mma_kernel<8><<<grid_mma, 256, 0, st>>>(n, dim, K, X, cent, lab, best_d, ctx->partials);
+        if (dim == 8 && K == 8 && ((uintptr_t)X & 15u) == 0)
+          km_assign_mma_kernel<8, 8><<<grid_mma, 256, 0, st>>>(n, dim, K, X, cent, lab, best_d, ctx->partials);
+        else if (dim == 8 && ((uintptr_t)X & 15u) == 0)
+          km_assign_mma_kernel<8, 0><<<grid_mma, 256, 0, st>>>(n, dim, K, X, cent, lab, best_d, ctx->partials);
         else
-          km_assign_mma_kernel<0><<<grid_mma, 256, 0, st>>>(n, dim, K, X, cent, lab, best_d, ctx->partials);
+          km_assign_mma_kernel<0, 0><<<grid_mma, 256, 0, st>>>(n, dim, K, X, cent, lab, best_d, ctx->partials);
         PLP_LAUNCH_CHECK("km_assign_mma_kernel");
       } else {
         km_assign_kernel<<<grid, kKmThreads, 0, st>>>(n, dim, K, X, cent, lab, best_d, ctx->partials);
