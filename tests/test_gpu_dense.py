@@ -103,7 +103,10 @@ def test_cholesky_and_apply_rinv(plp, ctx):
 
 # ----------------------------------------------------------------------------------- k-means ---
 @pytest.mark.parametrize("n,dim,K,restarts", [(1000, 3, 3, 10), (100_000, 2, 2, 3), (60_000, 8, 8, 2),
-                                              (4, 1, 2, 10), (20_000, 20, 20, 1), (5000, 5, 7, 4)])
+                                              (4, 1, 2, 10), (20_000, 20, 20, 1), (5000, 5, 7, 4),
+                                              # > 1024 x 256 points: the D^2 pick's per-thread chunk
+                                              # ranges hold several chunks (second scan level)
+                                              (600_077, 8, 8, 2), (300_001, 4, 6, 1)])
 def test_kmeans_parity(plp, ctx, n, dim, K, restarts):
     rng = streams(n + dim)[1]
     if n == 4:

@@ -131,6 +131,25 @@ def test_fused_tcg_matches_oracle(mods, cfg, n, k, p, delta, mode):
     assert np.max(np.abs(Heta.cpu().numpy() - Heta_o)) <= 1e-9 * np.max(np.abs(Heta_o))
 
 
+@pytest.mark.parametrize("n,k", [(37, 8), (70, 16)])
+def test_fused_tcg_tiny_graphs(mods, n, k):
+    """Fused tCG on graphs smaller than one 8-row block per warp (single-CTA grids, ragged tail)."""
+    plp, solver, ctx = mods
+    g = random_graph(streams(n)[0], n, avg_deg=6.0, connected=True)
+    Uo, _ = oracle.retract(draw_U(g.n, k, 8), np.zeros((g.n, k)))
+    G = plp.Graph(ctx, g.row_ptr, g.col, g.w)
+    tr = solver.GrassmannTR(ctx, G, k, solver.SolverConfig(tcg_fused=True))
+    st = solver._State(tr, torch.from_numpy(Uo).cuda(), 1.6)
+    eta, Heta, it, status = tr.tcg_device(st, 1.6, 0.4)
+    ocfg = osol.default_cfg(g.n, k)
+    sto = osol._state(g, Uo, 1.6, osol.oracle_fns())
+    eta_o, Heta_o, it_o, status_o = osol.tcg(
+        lambda xi: osol._hess(g, sto, 1.6, xi, ocfg["eps"], "sparse", osol.oracle_fns()), sto["grad"], Uo, 0.4, ocfg)
+    assert (it, status) == (it_o, status_o)
+    assert np.max(np.abs(eta.cpu().numpy() - eta_o)) <= 1e-9 * np.max(np.abs(eta_o))
+    assert np.max(np.abs(Heta.cpu().numpy() - Heta_o)) <= 1e-9 * np.max(np.abs(Heta_o))
+
+
 def test_fused_tcg_rejects_unsupported_k(mods):
     plp, solver, ctx = mods
     g = make_config("C2", n=500)
