@@ -246,7 +246,9 @@ enum {
  * plp_tcg_run: `iters` iterations (launches only, no synchronisation; iterations after the exit
  * condition leave eta, Heta and delta_dir unchanged), Hd a work array.  fused = 0: the
  * recurrences are bitwise those of solver.py's host loop (projection, curvature term, dots and
- * axpbys as separate passes).  fused = 1 (k = 8 or 16, 16-byte aligned vectors; else PLP_ERR_ARG):
+ * axpbys as separate passes).  fused = 1 (k = 8 or 16, or k = 1, 2, 4 with n k divisible by 8 --
+ * the arrays then read as n k / 8 rows of 8 with block-diagonal k x k matrices --, 16-byte aligned
+ * vectors; else PLP_ERR_ARG):
  * after the edge pass, three streaming passes on the fp64 tensor cores:
  * <d, Hd> from the Grams U^T EH, U^T d, d^T d; the eta / Heta / r updates with Hd = EH - U U^T EH
  * - d S formed in registers, U^T r and ||r||^2; then r's re-projection and the new direction --

@@ -25,7 +25,8 @@ enum {
 // totals of pass A at kTotA = [M1 | M2 | tr | <Gdd, S>] (M1 first, read by pass B), of pass B at
 // kTotB = [MR | ||r||^2] (MR read by pass C)
 constexpr int kTotA = kMat, kM1 = kTotA, kTotB = kMat + 2 * PLP_MAX_K * PLP_MAX_K + 64, kMR = kTotB;
-static_assert(kTotB + PLP_MAX_K * PLP_MAX_K + 1 <= PLP_TCG_SCAL_LEN, "scal too short");
+constexpr int kSx = kTotB + PLP_MAX_K * PLP_MAX_K + 64;  // S expanded block-diagonally (folded k < 8)
+static_assert(kSx + 64 <= PLP_TCG_SCAL_LEN, "scal too short");
 
 __global__ void tcg_init_kernel(double* sc, int* st, double delta, double kappa, double theta) {
   const double zr = sc[kZr];
@@ -391,12 +392,33 @@ __global__ void __launch_bounds__(kTcgThreads) tcg_finish_kernel(int64_t n, cons
 // MODE 0 (after pass A): tot = [M1 | M2 | tr(d^T EH) | <d^T d, S>_F]; <d, Hd>, step length.
 // MODE 1 (after pass B): tot = [MR | ||r||^2]; ||P r||^2 = ||r||^2 - ||MR||_F^2, convergence,
 // conjugation; MR zeroed when the iteration stops (pass C then leaves r as it is).
+// Folded k (kr = 1, 2, 4 < K = 8): the n x kr arrays are read as n kr / 8 rows of 8, so every 8 x 8
+// Gram holds 8 / kr diagonal kr x kr blocks whose sum is the true Gram (off-diagonal blocks pair
+// different nodes and are dropped); the k x k matrices the passes apply (M1, MR, S) are expanded
+// block-diagonally.  kr = K: no folding.
+__device__ void fold_blocks(const double* t, int K, int kr, double* f) {
+  for (int i = threadIdx.x; i < kr * kr; i += blockDim.x) {
+    const int a = i / kr, b = i % kr;
+    double v = 0.0;
+    for (int blk = 0; blk < K / kr; ++blk) v += t[(blk * kr + a) * K + blk * kr + b];
+    f[i] = v;
+  }
+}
+__device__ void expand_blocks(const double* f, int K, int kr, double* out) {
+  for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
+    const int row = e / K, col = e % K;
+    out[e] = row / kr == col / kr ? f[(row % kr) * kr + col % kr] : 0.0;
+  }
+}
+
 template <int K, int MODE>
 __global__ void __launch_bounds__(256) tcg_reduce_kernel(int P, const double* __restrict__ part, double* tot,
-                                                         unsigned* counter, double* sc, int* st, int max_iters) {
+                                                         unsigned* counter, double* sc, int* st, int max_iters,
+                                                         int kr) {
   constexpr int KK = K * K, E = MODE == 0 ? 2 * KK + 2 : KK + 1;
   __shared__ double ws[8];
   __shared__ double t[E];
+  __shared__ double f1[KK], f2[KK];
   __shared__ unsigned ticket;
   __shared__ int go;
   const int e = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -418,27 +440,45 @@ __global__ void __launch_bounds__(256) tcg_reduce_kernel(int P, const double* __
   __threadfence();
   for (int i = threadIdx.x; i < E; i += 256) t[i] = __ldcg(tot + i);
   __syncthreads();
+  const bool fold = kr < K;
+  const int kk = kr * kr;
+  if (fold) {  // the true kr x kr Grams
+    fold_blocks(t, K, kr, f1);
+    if (MODE == 0) fold_blocks(t + KK, K, kr, f2);
+  } else {
+    for (int i = threadIdx.x; i < KK; i += 256) {
+      f1[i] = t[i];
+      if (MODE == 0) f2[i] = t[KK + i];
+    }
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
     *counter = 0u;
     if (MODE == 0) {
       double c1 = 0.0;
-      for (int i = 0; i < KK; ++i) c1 = fma(t[KK + i], t[i], c1);
+      for (int i = 0; i < kk; ++i) c1 = fma(f2[i], f1[i], c1);
       sc[kTrDE] = t[2 * KK];
       sc[kDHd] = (t[2 * KK] - c1) - t[2 * KK + 1];
       tcg_scalar_a(sc, st);
     } else {
       double m = 0.0;
-      for (int i = 0; i < KK; ++i) m = fma(t[i], t[i], m);
+      for (int i = 0; i < kk; ++i) m = fma(f1[i], f1[i], m);
       sc[kZraw] = t[KK];
       sc[kZnew] = t[KK] - m;
       go = tcg_scalar_b(sc, st, max_iters) ? 1 : 0;
     }
   }
-  if (MODE == 1) {
-    __syncthreads();
-    if (!go)
-      for (int i = threadIdx.x; i < KK; i += 256) tot[i] = 0.0;
+  __syncthreads();
+  // the matrix the next pass applies (M1 for pass B, MR for pass C), block-diagonal when folded
+  if (MODE == 1 && !go) {
+    for (int i = threadIdx.x; i < KK; i += 256) tot[i] = 0.0;
+  } else if (fold) {
+    expand_blocks(f1, K, kr, tot);
   }
+}
+
+__global__ void tcg_expand_s_kernel(const double* __restrict__ S, int kr, double* __restrict__ out) {
+  expand_blocks(S, 8, kr, out);
 }
 
 static int env_int(const char* name, int dflt) {
@@ -458,7 +498,7 @@ static int fused_grid(plp_ctx* ctx, int64_t row_blocks, int E, int per_sm) {  //
 template <int KT>
 static plp_status fused_iteration(plp_ctx* ctx, int64_t n, const double* U, const double* S, double* eta,
                                   double* Heta, double* r, double* dlt, const double* EH, double* scal,
-                                  int* status, int max_iters) {
+                                  int* status, int max_iters, int kr) {
   constexpr int K = 8 * KT, KK = K * K;
   static const int unr_a = env_int("PLP_TCG_UNR_A", 4);
   static const int per_sm_a = env_int("PLP_TCG_GRID_A", unr_a == 4 ? resident_ctas(tcg_gram_a_kernel<KT, 4>, kTcgThreads)
@@ -474,14 +514,14 @@ static plp_status fused_iteration(plp_ctx* ctx, int64_t n, const double* U, cons
     tcg_gram_a_kernel<KT, 2><<<ga, kTcgThreads, 0, ctx->stream>>>(n, U, EH, dlt, S, ctx->partials);
   PLP_LAUNCH_CHECK("tcg_gram_a_kernel");
   tcg_reduce_kernel<K, 0><<<EA, 256, 0, ctx->stream>>>(ga, ctx->partials, scal + kTotA, counter, scal, status,
-                                                       max_iters);
+                                                       max_iters, kr);
   PLP_LAUNCH_CHECK("tcg_reduce_kernel");
   const int gb = fused_grid(ctx, (n + 7) / 8, EB, per_sm_b);
   tcg_update_kernel<KT><<<gb, kTcgThreads, 0, ctx->stream>>>(n, U, EH, dlt, S, scal, eta, Heta, r,
                                                              ctx->partials);
   PLP_LAUNCH_CHECK("tcg_update_kernel");
   tcg_reduce_kernel<K, 1><<<EB, 256, 0, ctx->stream>>>(gb, ctx->partials, scal + kTotB, counter + 1, scal, status,
-                                                       max_iters);
+                                                       max_iters, kr);
   PLP_LAUNCH_CHECK("tcg_reduce_kernel");
   int64_t gc = (int64_t)ctx->num_sms * per_sm_c;
   const int64_t bc = (n + 7) / 8;
@@ -540,17 +580,27 @@ extern "C" plp_status plp_tcg_run(plp_ctx* ctx, const plp_graph* g, int k, const
   if (iters < 0 || max_iters < 1) return set_error(PLP_ERR_ARG, "iters >= 0, max_iters >= 1");
   const int64_t n = g->n_rows;
   const int64_t total = n * k;
-  if (fused && k != 8 && k != 16) return set_error(PLP_ERR_ARG, "fused tCG needs k = 8 or 16");
+  const bool foldable = (k == 1 || k == 2 || k == 4) && (n * k) % 8 == 0;
+  if (fused && k != 8 && k != 16 && !foldable)
+    return set_error(PLP_ERR_ARG, "fused tCG needs k = 8 or 16, or k = 1, 2, 4 with n k divisible by 8");
   auto al16 = [](const void* x) { return ((uintptr_t)x & 15u) == 0; };
   if (fused && !(al16(U) && al16(eta) && al16(Heta) && al16(r) && al16(dlt) && al16(Hd)))
     return set_error(PLP_ERR_ARG, "fused tCG needs 16-byte aligned vectors");
   const int grid = axpby_grid(ctx, total);
   plp_status st;
   if (fused) {
+    if (k < 8) {
+      tcg_expand_s_kernel<<<1, 64, 0, ctx->stream>>>(S, k, scal + kSx);
+      PLP_LAUNCH_CHECK("tcg_expand_s_kernel");
+    }
     for (int it = 0; it < iters; ++it) {
       if ((st = plp_hessvec(ctx, g, k, U, dlt, p, AB, mode, eps, G_in, Hd))) return st;
-      st = k == 8 ? fused_iteration<1>(ctx, n, U, S, eta, Heta, r, dlt, Hd, scal, status, max_iters)
-                  : fused_iteration<2>(ctx, n, U, S, eta, Heta, r, dlt, Hd, scal, status, max_iters);
+      if (k == 16)
+        st = fused_iteration<2>(ctx, n, U, S, eta, Heta, r, dlt, Hd, scal, status, max_iters, 16);
+      else if (k == 8)
+        st = fused_iteration<1>(ctx, n, U, S, eta, Heta, r, dlt, Hd, scal, status, max_iters, 8);
+      else  // k = 1, 2, 4: the n x k arrays as n k / 8 rows of 8, S block-diagonal
+        st = fused_iteration<1>(ctx, n * k / 8, U, scal + kSx, eta, Heta, r, dlt, Hd, scal, status, max_iters, k);
       if (st) return st;
     }
     return PLP_OK;

@@ -40,7 +40,10 @@ class SolverConfig:
     eps: float = 1e-9
     device_tcg: bool = True            # tCG recurrences on the device (plp_tcg_run), no per-iteration D2H
     tcg_batch: int = 8                 # most iterations launched between two status reads
-    tcg_fused: bool | None = None      # fused tCG passes (NEXT-2); default: when k is 8 or 16
+    # fused tCG passes (NEXT-2); default on for k = 8, 16.  k = 1, 2, 4 with n k % 8 = 0 (folded) on
+    # request: same iteration up to rounding, but over a long continuation solve the trajectory
+    # drifts from the oracle's far enough to move k-means boundary points
+    tcg_fused: bool | None = None
     tcg_graph: bool = True             # replay each batch as one CUDA graph (needs a non-default stream)
 
     def resolved(self, n: int, k: int) -> "SolverConfig":

@@ -108,7 +108,10 @@ def test_device_tcg_matches_host_tcg_bitwise(mods, p, delta, mode):
 
 @pytest.mark.parametrize("cfg,n,k,p,delta,mode", [("C2", 5003, 8, 1.5, 0.3, 0), ("C2", 5003, 8, 1.2, 50.0, 0),
                                                   ("C1", None, 16, 1.5, 0.5, 0), ("C2", 4001, 8, 1.8, 2.0, 1),
-                                                  ("C2", 2003, 16, 1.3, 1e3, 0)])
+                                                  ("C2", 2003, 16, 1.3, 1e3, 0),
+                                                  # folded k (n k / 8 rows of 8, block-diagonal k x k)
+                                                  ("C2", 5002, 4, 1.5, 0.3, 0), ("C2", 5004, 2, 1.2, 50.0, 0),
+                                                  ("C2", 4000, 1, 1.6, 1e3, 0), ("C2", 3002, 4, 1.8, 2.0, 1)])
 def test_fused_tcg_matches_oracle(mods, cfg, n, k, p, delta, mode):
     """NEXT-2 fused tCG (three tensor-core passes after the edge pass; <d, Hd> and ||P r||^2 from
     Grams) against the oracle's tCG: same iteration count and exit status, step and H step within
@@ -152,7 +155,7 @@ def test_fused_tcg_tiny_graphs(mods, n, k):
 
 def test_fused_tcg_rejects_unsupported_k(mods):
     plp, solver, ctx = mods
-    g = make_config("C2", n=500)
+    g = make_config("C2", n=501)  # k = 4: n k not divisible by 8
     G = plp.Graph(ctx, g.row_ptr, g.col, g.w)
     U = torch.from_numpy(oracle.retract(draw_U(g.n, 4, 1), np.zeros((g.n, 4)))[0]).cuda()
     tr = solver.GrassmannTR(ctx, G, 4, solver.SolverConfig(tcg_fused=True))

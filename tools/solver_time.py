@@ -38,7 +38,7 @@ def main():
         G = plp.Graph(ctx, g.row_ptr, g.col, g.w)
         Z = torch.from_numpy(draw_U(g.n, k, 0)).cuda()
         for vname, kw in VARIANTS.items():
-            if "fused" in vname and k not in (8, 16):
+            if "fused" in vname and not (k in (8, 16) or (k in (1, 2, 4) and g.n * k % 8 == 0)):
                 continue
             cfg = solver.SolverConfig(**kw)
             if max_outer:
