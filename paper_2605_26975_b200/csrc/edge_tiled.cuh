@@ -428,6 +428,10 @@ plp_status launch_edge_any(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int* 
   if (!staged) {
     st = try_launch_halo(ctx, a, pw, grid, &used);
     if (st || used) return st;
+    // wide rows without a halo tiling (C4: k = 20 on a random block graph): the gathers are
+    // latency-bound and the row kernel, without the staged kernel's shared-memory ring, keeps more
+    // warps resident (C4: 2.04 against 2.41 ms)
+    if (a.k > 16) return launch_edge_pow(ctx, a, pw, grid);
   }
   return launch_staged_pow(ctx, a, pw, grid);
 #endif

@@ -25,6 +25,10 @@ VARIANTS = {
     "t128c2": ["-DPLP_HALO_TILE_ROWS=128", "-DPLP_HALO_CTAS=2"],
     "cs32": ["-DPLP_HALO_CSLEEP_NS=32"],
     "cs100": ["-DPLP_HALO_CSLEEP_NS=100"],
+    # full builds (all k): staged-kernel occupancy for the random-graph configs (C4, k = 20)
+    "full_minb2": ["FULL"],
+    "full_minb3": ["FULL", "-DPLP_EDGE_MINB=3"],
+    "full_minb4": ["FULL", "-DPLP_EDGE_MINB=4"],
 }
 
 
@@ -35,7 +39,10 @@ def build(names):
         shutil.rmtree(d, ignore_errors=True)
         os.makedirs(d, exist_ok=True)
         try:
-            b(obj_dir=os.path.join(d, "obj"), lib=os.path.join(d, "libplp.so"), extra=VARIANTS[name] + ["-DPLP_TUNE_ONLY"])
+            flags = [f for f in VARIANTS[name] if f != "FULL"]
+            if "FULL" not in VARIANTS[name]:
+                flags.append("-DPLP_TUNE_ONLY")
+            b(obj_dir=os.path.join(d, "obj"), lib=os.path.join(d, "libplp.so"), extra=flags)
         except RuntimeError as e:
             print("FAILED", name, str(e)[-600:], flush=True)
         shutil.rmtree(os.path.join(d, "obj"), ignore_errors=True)
