@@ -70,6 +70,25 @@ __global__ void k_cvt(double* out, int iters) {
   if (y == 12345.678f) out[0] = y;
 }
 
+// fp64 tensor cores: mma.sync m8n8k4 f64 (DMMA), CH independent accumulators per warp
+template <int CH>
+__global__ void k_dmma(double* out, int iters) {
+  double d[CH][2];
+  const double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) d[c][0] = d[c][1] = c;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(d[c][0]), "+d"(d[c][1]) : "d"(a), "d"(b));
+  }
+  double s = 0;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) s += d[c][0] + d[c][1];
+  if (s == 12345.678) out[0] = s;
+}
+
 __global__ void k_copy(const double4* __restrict__ a, double4* __restrict__ b, size_t n) {
   size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   size_t st = (size_t)gridDim.x * blockDim.x;
@@ -98,6 +117,17 @@ int main() {
   double nf = (double)blocks * threads * iters * 8;
   printf("DFMA: %.3f ms, %.2f T DFMA/s, block0 cycles %lld -> eff clock %.0f MHz, DFMA/clk/SM %.1f\n", ms, nf / ms / 1e9, c,
          c / (ms * 1e3), nf / sms / (c * 1.0));
+  k_dmma<8><<<blocks, threads>>>(dout, 16);
+  CK(cudaDeviceSynchronize());
+  cudaEventRecord(e0);
+  k_dmma<8><<<blocks, threads>>>(dout, iters);
+  cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
+  cudaEventElapsedTime(&ms, e0, e1);
+  {
+    const double nm = (double)blocks * (threads / 32) * iters * 8;  // warp-level DMMA instructions
+    printf("DMMA m8n8k4 f64: %.3f ms, %.2f T DMMA/s, %.2f TFLOP/s (512 flop each)\n", ms, nm / ms / 1e9,
+           nm * 512.0 / ms / 1e9);
+  }
   k_ffma<8><<<blocks, threads>>>(fout, 16, 1.0000001f, 1e-9f);
   cudaEventRecord(e0);
   k_ffma<8><<<blocks, threads>>>(fout, iters, 1.0000001f, 1e-9f);
