@@ -26,7 +26,7 @@ ncu --set full --clock-control none --import-source on -k "regex:edge_(halo_|sta
     -o $OUT/prof_edge_$TAG python tools/prof_edge.py --reps 3 > $OUT/ncu_full_$TAG.log 2>&1
 echo "NCU_FULL_RC=$?" >> $OUT/ncu_full_$TAG.log
 # per-row table (every §8 row + the tCG iteration variants) and solver wall times
-timeout 900 python tools/bench_kernels.py --config C5 > $OUT/kernel_table_$TAG.jsonl 2>&1
+timeout 1200 python tools/bench_kernels.py --config C5 --oracle > $OUT/kernel_table_$TAG.jsonl 2>&1
 timeout 900 python tools/solver_time.py C1 C2:20000 D16:8192 D20 > $OUT/solver_time_$TAG.jsonl 2>&1
 # launch list + one full capture of the fused tCG passes (NEXT-2)
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
