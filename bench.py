@@ -213,7 +213,7 @@ def run_reference(args, rank, world):
     val = float(np.median(vals))
     out = {"metric": "fused grad+Hv GNNZ*k/s", "value": val, "unit": "GNNZ*k/s", "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.median(dts)),
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic", "impl": "reference",
            "config": {"workload": args.config, "desc": CONFIG_DESC.get(args.config, args.config),
                       "n": g.n, "nnz": g.nnz, "k": k, "p": p, "order": args.order},
