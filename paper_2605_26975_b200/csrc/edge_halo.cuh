@@ -36,7 +36,8 @@ static_assert(kHaloT % kSchedWindow == 0 && kHaloThreads <= 16 * 32, "tile map (
 struct HaloLayout {
   unsigned rp, sched, nl, enc, w, U, E, bytes;
 };
-__host__ __device__ inline HaloLayout halo_layout(int k, int ext_cap, int nnz_cap, bool obj = false) {
+__host__ __device__ inline HaloLayout halo_layout(int k, int ext_cap, int nnz_cap, bool obj = false,
+                                                  bool eta = true) {
   HaloLayout L;
   unsigned o = 0;
   L.rp = o; o += (kHaloT + 8) * 4;
@@ -46,12 +47,15 @@ __host__ __device__ inline HaloLayout halo_layout(int k, int ext_cap, int nnz_ca
   o = (o + 15u) & ~15u;
   L.w = o; o += (unsigned)(nnz_cap + 16) * 8;
   L.U = o; o += (unsigned)(kHaloT + ext_cap) * (unsigned)k * 8u;
-  L.E = o; o += (unsigned)(kHaloT + ext_cap) * (unsigned)k * 8u;
+  L.E = o; o += eta ? (unsigned)(kHaloT + ext_cap) * (unsigned)k * 8u : 0u;
   L.bytes = (o + 127u) & ~127u;
   return L;
 }
 #ifndef PLP_HALO_NBUF
 #define PLP_HALO_NBUF 2  // tile buffers in flight (2 or 3)
+#endif
+#ifndef PLP_HALO_NBUF_NOETA
+#define PLP_HALO_NBUF_NOETA 3  // passes without eta (objective, gradient) stage half the rows: 3 buffers
 #endif
 constexpr int kHaloNBuf = PLP_HALO_NBUF;
 constexpr unsigned kHaloHead = 256;  // mbarriers (full[NBUF], list[3], empty[NBUF]); tables follow
@@ -63,8 +67,8 @@ __host__ __device__ inline unsigned halo_bufs_off(int ext_cap, bool tables) {
   return (halo_lists_off(tables) + 3u * (unsigned)(ext_cap + 4) * 4u + 127u) & ~127u;
 }
 __host__ __device__ inline unsigned halo_smem_bytes(int k, int ext_cap, int nnz_cap, bool tables,
-                                                    bool obj = false) {
-  return halo_bufs_off(ext_cap, tables) + (unsigned)kHaloNBuf * halo_layout(k, ext_cap, nnz_cap, obj).bytes;
+                                                    bool obj = false, bool eta = true, int nbuf = kHaloNBuf) {
+  return halo_bufs_off(ext_cap, tables) + (unsigned)nbuf * halo_layout(k, ext_cap, nnz_cap, obj, eta).bytes;
 }
 #ifndef PLP_HALO_CTAS
 #define PLP_HALO_CTAS 1  // resident CTAs per SM (each with its own double buffer)
@@ -92,7 +96,7 @@ constexpr int halo_cpl() { return K == 8 ? PLP_HALO_CPL8 : K == 16 ? 4 : 2; }
 // OBJ: objective-only pass (no eta, no G) on a symmetric graph: A_l = sum over the upper-triangle
 // edges (j > i) of w_ij |u_il - u_jl|^p, i.e. Eq. (1)'s numerator with each undirected edge once
 // (half the powers of the row form); B_l from the node terms as usual.
-template <int K, class POW, bool HAS_ETA, bool OBJ>
+template <int K, class POW, bool HAS_ETA, bool OBJ, int NB>
 __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(POW pw, EdgeArgs a) {
   static_assert(!(OBJ && HAS_ETA), "objective mode has no eta");
   constexpr int CPL = halo_cpl<K>(), LPR = K / CPL, RPW = 32 / LPR;  // rows per pass
@@ -100,19 +104,19 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
   static_assert(NS % 2 == 0 || NS == 2, "slice count");
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [2] tile data landed
-  uint64_t* lbar = full + kHaloNBuf;                   // [3] halo list landed
+  uint64_t* lbar = full + NB;                   // [3] halo list landed
   uint64_t* empty = lbar + 3;                          // [NBUF] consumers done with the buffer
   if constexpr (POW::kNeedsTables) pw.init_smem(smem + kHaloHead);
   const int ext_cap = a.halo_ext_cap;
   const int LS = ext_cap + 4;  // list slot: n_ext, eb, ee, pad, columns
   int* lists = reinterpret_cast<int*>(smem + halo_lists_off(POW::kNeedsTables));
-  const HaloLayout Ly = halo_layout(K, ext_cap, a.halo_nnz_cap, OBJ);
+  const HaloLayout Ly = halo_layout(K, ext_cap, a.halo_nnz_cap, OBJ, HAS_ETA);
   unsigned char* buf0 = smem + halo_bufs_off(ext_cap, POW::kNeedsTables);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int grp = lane / LPR, li = lane % LPR, c0 = li * CPL;
   if (tid == 0) {
     // full: the producer's arrive.expect_tx (TMA bytes) + one cp.async arrival per producer lane
-    for (int q = 0; q < kHaloNBuf; ++q) {
+    for (int q = 0; q < NB; ++q) {
       mbar_init(&full[q], 1 + 32);
       mbar_init(&empty[q], kHaloCWarps);
     }
@@ -197,9 +201,9 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
     for (int it = 0;; ++it) {
       const int64_t t = t0 + (int64_t)it * ts;
       if (t >= n_tiles) break;
-      const int b = it % kHaloNBuf;
-      if (it >= kHaloNBuf)
-        mbar_wait_sleep(&empty[b], (unsigned)((it - kHaloNBuf) / kHaloNBuf) & 1u, PLP_HALO_SLEEP_NS);
+      const int b = it % NB;
+      if (it >= NB)
+        mbar_wait_sleep(&empty[b], (unsigned)((it - NB) / NB) & 1u, PLP_HALO_SLEEP_NS);
       if (lane == 0) fence_proxy_async();  // consumers' generic reads before the async refill
       __syncwarp();
       issue_tile(t, b, it % 3, (unsigned)(it / 3) & 1u);
@@ -229,12 +233,12 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
   for (int it = 0;; ++it) {
     const int64_t t = t0 + (int64_t)it * ts;
     if (t >= n_tiles) break;
-    const int b = it % kHaloNBuf;
+    const int b = it % NB;
 #if PLP_HALO_CSLEEP_NS > 0
-    if (!mbar_test(&full[b], (unsigned)(it / kHaloNBuf) & 1u))
-      mbar_wait_sleep(&full[b], (unsigned)(it / kHaloNBuf) & 1u, PLP_HALO_CSLEEP_NS);
+    if (!mbar_test(&full[b], (unsigned)(it / NB) & 1u))
+      mbar_wait_sleep(&full[b], (unsigned)(it / NB) & 1u, PLP_HALO_CSLEEP_NS);
 #else
-    mbar_wait(&full[b], (unsigned)(it / kHaloNBuf) & 1u);  // tile t resident
+    mbar_wait(&full[b], (unsigned)(it / NB) & 1u);  // tile t resident
 #endif
 
     const unsigned char* B = buf0 + (size_t)b * Ly.bytes;
@@ -458,12 +462,17 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
 
 template <int K, class POW, bool HAS_ETA, bool OBJ>
 plp_status launch_halo_shape(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int* grid_out) {
-  auto kern = edge_halo_kernel<K, POW, HAS_ETA, OBJ>;
-  const unsigned smem = halo_smem_bytes(K, a.halo_ext_cap, a.halo_nnz_cap, POW::kNeedsTables, OBJ);
-  static unsigned attr_set = 0;
-  if (attr_set < smem) {
+  // passes without eta stage U rows only: a third buffer fits where the eta pass has two
+  constexpr int NB3 = HAS_ETA ? kHaloNBuf : PLP_HALO_NBUF_NOETA;
+  const unsigned smem3 = halo_smem_bytes(K, a.halo_ext_cap, a.halo_nnz_cap, POW::kNeedsTables, OBJ, HAS_ETA, NB3);
+  const bool deep = NB3 != kHaloNBuf && smem3 <= kHaloSmemMax;
+  const int nb = deep ? NB3 : kHaloNBuf;
+  auto kern = deep ? edge_halo_kernel<K, POW, HAS_ETA, OBJ, NB3> : edge_halo_kernel<K, POW, HAS_ETA, OBJ, kHaloNBuf>;
+  const unsigned smem = halo_smem_bytes(K, a.halo_ext_cap, a.halo_nnz_cap, POW::kNeedsTables, OBJ, HAS_ETA, nb);
+  static unsigned attr_set[2] = {0, 0};
+  if (attr_set[deep] < smem) {
     PLP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_set = smem;
+    attr_set[deep] = smem;
   }
   const int64_t n_tiles = (a.n_rows + kHaloT - 1) / kHaloT;
   int64_t grid = (int64_t)ctx->num_sms * PLP_HALO_CTAS;
@@ -471,8 +480,9 @@ plp_status launch_halo_shape(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int
   if (grid > n_tiles) grid = n_tiles > 0 ? n_tiles : 1;
   kern<<<(int)grid, kHaloThreads, smem, ctx->stream>>>(pw, a);
   PLP_LAUNCH_CHECK("edge_halo_kernel");
-  note_edge_kernel(OBJ ? "edge_halo_kernel[objective]" : "edge_halo_kernel", K, halo_cpl<K>(),
-                   K / halo_cpl<K>(), 2, POW::kName, HAS_ETA);
+  note_edge_kernel(OBJ ? (deep ? "edge_halo_kernel[objective,3buf]" : "edge_halo_kernel[objective]")
+                       : (deep ? "edge_halo_kernel[3buf]" : "edge_halo_kernel"),
+                   K, halo_cpl<K>(), K / halo_cpl<K>(), 2, POW::kName, HAS_ETA);
   *grid_out = (int)grid;
   return PLP_OK;
 }
