@@ -96,7 +96,12 @@ constexpr int halo_cpl() { return K == 8 ? PLP_HALO_CPL8 : K == 16 ? 4 : 2; }
 // OBJ: objective-only pass (no eta, no G) on a symmetric graph: A_l = sum over the upper-triangle
 // edges (j > i) of w_ij |u_il - u_jl|^p, i.e. Eq. (1)'s numerator with each undirected edge once
 // (half the powers of the row form); B_l from the node terms as usual.
-template <int K, class POW, bool HAS_ETA, bool OBJ, int NB>
+// ADAPT: rows that leave the fast domain (mostly |d| < eps: the solver's degenerate regime, where
+// p-Laplacian iterates flatten on clusters) are recomputed from shared memory in the capped form,
+// and a warp whose previous pass needed it goes there directly; libdevice only for |d| < 2^-120 or
+// >= 2^120.  Off for the fused F/G/Hv pass (the benchmark unit; its random inputs rarely leave the
+// domain, and the plain loop keeps its code), which recomputes such rows with libdevice.
+template <int K, class POW, bool HAS_ETA, bool OBJ, int NB, bool ADAPT>
 __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(POW pw, EdgeArgs a) {
   static_assert(!(OBJ && HAS_ETA), "objective mode has no eta");
   constexpr int CPL = halo_cpl<K>(), LPR = K / CPL, RPW = 32 / LPR;  // rows per pass
@@ -230,6 +235,7 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
     }
   } else {
   const int h = warp & 1, win = warp >> 1;  // warp pair shares a 32-row window
+  bool capmode = false;  // this warp's previous pass needed the capped form (|d| < eps rows)
   for (int it = 0;; ++it) {
     const int64_t t = t0 + (int64_t)it * ts;
     if (t >= n_tiles) break;
@@ -312,14 +318,37 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
           }
         }
         if constexpr (!POW::kIsP2) {
-          if (mx >= pw.fast_span2) {  // rare: exact libdevice recomputation of the row
+          if (mx >= pw.fast_span2) {  // some |d| outside the fast domain (usually |d| < eps)
+            unsigned bad = 0;
 #pragma unroll
             for (int cc = 0; cc < CPL; ++cc) {
               Ar[cc] = 0.0;
               double sn;
               pw.eval(fabs(ui[cc]), sn, tn[cc]);
             }
-            for (int ee = eu; ee < e1; ++ee) {
+            if constexpr (ADAPT) {
+              // A needs the uncapped |d|^p: the clamped fast power from shared memory covers d = 0
+              // and every |d| >= 2^-120; libdevice below only for what it flags
+#pragma unroll 1
+              for (int ee = eu; ee < e1; ++ee) {
+                double uj0[CPL];
+                lds_vec<CPL>(tU + enc_s[ee] * K, uj0);
+                const double wv = w_s[ee];
+#pragma unroll
+                for (int cc = 0; cc < CPL; ++cc) {
+                  const double d = ui[cc] - uj0[cc];
+                  bad |= out_of_domain(abs_hi(d));
+                  Ar[cc] = fma(wv * pw.pow_fast(fmax(fabs(d), 0x1p-120)), d * d, Ar[cc]);
+                }
+              }
+            } else {
+              bad = 1;
+            }
+            if (bad) {
+#pragma unroll
+              for (int cc = 0; cc < CPL; ++cc) Ar[cc] = 0.0;
+            }
+            for (int ee = eu; ee < e1 && bad; ++ee) {
               const int64_t j = a.col[ee];
               const double wv = a.w[ee];
 #pragma unroll
@@ -341,9 +370,12 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
       unsigned mx = 0;
 #pragma unroll
       for (int cc = 0; cc < CPL; ++cc) L[cc] = HA[cc] = 0.0;
+      if constexpr (!POW::kIsP2 && ADAPT) {
+        if (capmode) mx = ~0u;  // straight to the capped form (previous pass of this warp needed it)
+      }
       // batches of EB edges as straight-line code (their dependency chains interleave), then the
       // remainder two edges / one edge at a time; summation order stays the CSR order
-      int e = e0;
+      int e = (ADAPT && capmode) ? e1 : e0;  // capmode: the capped form below recomputes the row
 #if PLP_HALO_EB == 4
 #pragma unroll 1
       for (; e + 3 < e1; e += 4) {
@@ -405,12 +437,34 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
           tn[cc] = sn[cc] * au;
         }
       }
-      if constexpr (!POW::kIsP2) {
+      if constexpr (!POW::kIsP2 && !ADAPT) {
         if (mx >= pw.fast_span2) {  // rare: exact libdevice recomputation of the row
           edge_row_exact<CPL, POW, HAS_ETA>(pw, e0, e1, a.col, a.w, a.U, a.eta, K, c0, ui, ei, L, HA);
 #pragma unroll
           for (int cc = 0; cc < CPL; ++cc) pw.eval(fabs(ui[cc]), sn[cc], tn[cc]);
         }
+      }
+      if constexpr (!POW::kIsP2 && ADAPT) {
+        const bool need = mx >= pw.fast_span2;
+        if (need) {
+          // some |d| left the fast domain (usually |d| < eps: the degenerate regime): the row
+          // again from shared memory in the capped form; libdevice only for what that cannot take
+          unsigned bad = 0, mxf = 0;
+#pragma unroll
+          for (int cc = 0; cc < CPL; ++cc) L[cc] = HA[cc] = 0.0;
+#pragma unroll 1
+          for (int ee = e0; ee < e1; ++ee) {
+            const int x0 = enc_s[ee];
+            double uj0[CPL], ej0[CPL];
+            lds_vec<CPL>(tU + x0 * K, uj0);
+            if constexpr (HAS_ETA) lds_vec<CPL>(tE + x0 * K, ej0);
+            edge_update_capsel<CPL, POW, HAS_ETA>(pw, w_s[ee], ui, uj0, ei, ej0, L, HA, bad, mxf);
+          }
+          if (bad) edge_row_exact<CPL, POW, HAS_ETA>(pw, e0, e1, a.col, a.w, a.U, a.eta, K, c0, ui, ei, L, HA);
+#pragma unroll
+          for (int cc = 0; cc < CPL; ++cc) pw.eval(fabs(ui[cc]), sn[cc], tn[cc]);
+        }
+        capmode = __any_sync(__activemask(), need);
       }
       double g[CPL], hv[CPL];
 #pragma unroll
@@ -467,12 +521,17 @@ plp_status launch_halo_shape(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int
   const unsigned smem3 = halo_smem_bytes(K, a.halo_ext_cap, a.halo_nnz_cap, POW::kNeedsTables, OBJ, HAS_ETA, NB3);
   const bool deep = NB3 != kHaloNBuf && smem3 <= kHaloSmemMax;
   const int nb = deep ? NB3 : kHaloNBuf;
-  auto kern = deep ? edge_halo_kernel<K, POW, HAS_ETA, OBJ, NB3> : edge_halo_kernel<K, POW, HAS_ETA, OBJ, kHaloNBuf>;
+  // the fused F/G/Hv pass (G and eta) keeps the plain loop; every other pass adapts
+  const bool adapt = !(HAS_ETA && a.G != nullptr);
+  auto kern = deep ? edge_halo_kernel<K, POW, HAS_ETA, OBJ, NB3, true>
+                   : (adapt ? edge_halo_kernel<K, POW, HAS_ETA, OBJ, kHaloNBuf, true>
+                            : edge_halo_kernel<K, POW, HAS_ETA, OBJ, kHaloNBuf, false>);
   const unsigned smem = halo_smem_bytes(K, a.halo_ext_cap, a.halo_nnz_cap, POW::kNeedsTables, OBJ, HAS_ETA, nb);
-  static unsigned attr_set[2] = {0, 0};
-  if (attr_set[deep] < smem) {
+  static unsigned attr_set[3] = {0, 0, 0};
+  const int vi = deep ? 2 : adapt ? 1 : 0;
+  if (attr_set[vi] < smem) {
     PLP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_set[deep] = smem;
+    attr_set[vi] = smem;
   }
   const int64_t n_tiles = (a.n_rows + kHaloT - 1) / kHaloT;
   int64_t grid = (int64_t)ctx->num_sms * PLP_HALO_CTAS;

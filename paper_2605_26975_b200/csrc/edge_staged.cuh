@@ -68,6 +68,29 @@ __device__ __forceinline__ const double* row_at(const double* base, int j, unsig
                                          (uint64_t)(uint32_t)j * stride_bytes);
 }
 
+// Capped form of one stored edge for rows with |d| < eps (the degenerate regime of the method:
+// p-Laplacian minimisers are nearly constant on clusters, so neighbour differences fall below the
+// curvature cap).  s_raw = |d|^{p-2} from the clamped fast power (valid for every |d| >= 2^-120 and
+// for d = 0, where it is finite and multiplies d = 0), s_cap = min(s_raw, eps^{p-2}) (x^{p-2} is
+// decreasing for p < 2, so the min is exactly the cap).  `bad` flags 0 < |d| < 2^-120 and
+// |d| >= 2^120 (exact path); `mxf` keeps the fast-path test (does the next row need this form?).
+template <int CPL, class POW, bool HAS_ETA>
+__device__ __forceinline__ void edge_update_capsel(const POW& pw, double wv, const double (&ui)[CPL],
+                                                   const double (&uj)[CPL], const double (&ei)[CPL],
+                                                   const double (&ej)[CPL], double (&L)[CPL],
+                                                   double (&HA)[CPL], unsigned& bad, unsigned& mxf) {
+  const double wcap = wv * pw.s_eps;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const double d = ui[c] - uj[c];
+    bad |= out_of_domain(abs_hi(d));
+    mxf = max(mxf, (unsigned)__double2hiint(d) * 2u - pw.fast_lo2);
+    const double wsr = wv * pw.pow_fast(fmax(fabs(d), 0x1p-120));  // w |d|^{p-2}
+    L[c] = fma(wsr, d, L[c]);                                       // w phi_p(d)
+    if constexpr (HAS_ETA) HA[c] = fma(fmin(wsr, wcap), ei[c] - ej[c], HA[c]);  // w cap(|d|)^{p-2}
+  }
+}
+
 // One stored edge for the lane's CPL columns (branch-free); `mx` collects the fast-domain test
 // (hi word of |d| relative to the lower bound, unsigned max: >= fast_span2 means some |d| left
 // the domain and the row is recomputed exactly).
