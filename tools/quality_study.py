@@ -23,6 +23,7 @@ def main():
     ap.add_argument("configs", nargs="*", default=["D16", "D20"])
     ap.add_argument("--k", type=int, default=4)
     ap.add_argument("--pfinal", type=float, default=1.2)
+    ap.add_argument("--fused", action="store_true", help="fused tCG passes also for k = 1, 2, 4 (folded)")
     args = ap.parse_args()
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)  # a created stream: the solver replays tCG batches as CUDA graphs
@@ -34,7 +35,8 @@ def main():
         u = draw_uniforms(10, args.k)
         for sched in ([2.0], [2.0, 1.6, args.pfinal]):
             t = time.time()
-            U, tr = solver.continuation_solve(ctx, G, Z, sched)
+            U, tr = solver.continuation_solve(ctx, G, Z, sched,
+                                              solver.SolverConfig(tcg_fused=True if args.fused else None))
             torch.cuda.synchronize()
             ts = time.time() - t
             t = time.time()
@@ -44,7 +46,7 @@ def main():
             print(json.dumps({"graph": cfg, "n": g.n, "nnz": g.nnz, "k": args.k, "schedule": sched,
                               "rcut": rc, "cluster_sizes": sizes, "F_final": tr.records[-1].F,
                               "outer_iters": len(tr.records),
-                              "tcg_iters": sum(r.tcg_iters for r in tr.records), "solve_s": ts,
+                              "tcg_iters": sum(r.tcg_iters for r in tr.records), "solve_s": ts, "fused": args.fused,
                               "cluster_s": tc}),
                   flush=True)
 

@@ -41,6 +41,7 @@ def main():
     ap.add_argument("--k", type=int, default=8)
     ap.add_argument("--sched", default="2.0,1.5")
     ap.add_argument("--graphs", action="store_true", help="replay tCG batches as CUDA graphs")
+    ap.add_argument("--fused", action="store_true", help="fused tCG passes also for k = 1, 2, 4 (folded)")
     a = ap.parse_args()
     sched = [float(x) for x in a.sched.split(",")]
     g = get_graph(a.config, "tile")
@@ -50,7 +51,7 @@ def main():
     G = plp.Graph(ctx, g.row_ptr, g.col, g.w)
     Z = torch.from_numpy(draw_U(g.n, a.k, 0)).cuda()
     u = draw_uniforms(10, a.k)
-    cfg = solver.SolverConfig(tcg_graph=a.graphs)
+    cfg = solver.SolverConfig(tcg_graph=a.graphs, tcg_fused=True if a.fused else None)
     solver.continuation_solve(ctx, G, Z, sched[:1], solver.SolverConfig(tcg_graph=a.graphs, max_outer=2))
     torch.cuda.synchronize()
     from torch.profiler import profile, ProfilerActivity
@@ -73,7 +74,7 @@ def main():
             per[ev.name][1] += 1
     gpu = sum(agg.values())
     out = {"config": a.config, "n": g.n, "nnz": g.nnz, "k": a.k, "schedule": sched, "graphs": a.graphs,
-           "fused_tcg": solver.SolverConfig().resolved(g.n, a.k).tcg_fused, "wall_s": wall,
+           "fused_tcg": cfg.resolved(g.n, a.k).tcg_fused, "wall_s": wall,
            "gpu_busy_s": gpu / 1e3, "outer": len(tr.records), "tcg_iters": sum(r.tcg_iters for r in tr.records),
            "rcut": rc, "components_ms": {k: round(v, 3) for k, v in sorted(agg.items(), key=lambda x: -x[1])},
            "launches": dict(cnt),
