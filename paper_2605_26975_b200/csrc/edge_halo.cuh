@@ -452,8 +452,21 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
           unsigned bad = 0, mxf = 0;
 #pragma unroll
           for (int cc = 0; cc < CPL; ++cc) L[cc] = HA[cc] = 0.0;
+          int ee = e0;
 #pragma unroll 1
-          for (int ee = e0; ee < e1; ++ee) {
+          for (; ee + 1 < e1; ee += 2) {  // edge pairs: two dependency chains interleave
+            const int x0 = enc_s[ee], x1 = enc_s[ee + 1];
+            double uj0[CPL], ej0[CPL], uj1[CPL], ej1[CPL];
+            lds_vec<CPL>(tU + x0 * K, uj0);
+            lds_vec<CPL>(tU + x1 * K, uj1);
+            if constexpr (HAS_ETA) {
+              lds_vec<CPL>(tE + x0 * K, ej0);
+              lds_vec<CPL>(tE + x1 * K, ej1);
+            }
+            edge_update_capsel<CPL, POW, HAS_ETA>(pw, w_s[ee], ui, uj0, ei, ej0, L, HA, bad, mxf);
+            edge_update_capsel<CPL, POW, HAS_ETA>(pw, w_s[ee + 1], ui, uj1, ei, ej1, L, HA, bad, mxf);
+          }
+          if (ee < e1) {
             const int x0 = enc_s[ee];
             double uj0[CPL], ej0[CPL];
             lds_vec<CPL>(tU + x0 * K, uj0);
