@@ -1,4 +1,5 @@
-"""Wall time of the GPU solver (continuation solve) under the tCG variants: host-driven loop,
+"""Wall time of the GPU solver (continuation solve, graphs in the library's tile order) under the
+tCG variants: host-driven loop,
 device-resident launches, CUDA-graph replay, fused passes (k = 8, 16).  Prints one JSON line per
 (config, variant): seconds, outer and tCG iterations, ms per tCG iteration, final F.
 
@@ -29,11 +30,14 @@ def main():
     ctx = plp.Context(0, stream)
     for spec in specs:
         name, _, nn = spec.partition(":")
-        if name == "C5":
+        if not nn:
             from bench import get_graph
-            g = get_graph("C5", "tile")
-        else:
-            g = make_config(name, n=int(nn) if nn else None)
+            g = get_graph(name, "tile")
+        else:  # the library's tile order (RCM + BFS tiles), as the product path uses
+            from plp_inputs import Graph
+            g0 = make_config(name, n=int(nn))
+            rp, col, w = plp.permute_csr(g0.row_ptr, g0.col, g0.w, plp.tile_order(g0.row_ptr, g0.col))
+            g = Graph(name, g0.n, rp, col, w)
         k, sched, max_outer = RUNS[name]
         G = plp.Graph(ctx, g.row_ptr, g.col, g.w)
         Z = torch.from_numpy(draw_U(g.n, k, 0)).cuda()
