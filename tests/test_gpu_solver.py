@@ -193,3 +193,20 @@ def test_tcg_graph_replay_is_bitwise_the_direct_launches(k, fused):
                 for gr in (False, True)]
         assert torch.equal(sols[0][0], sols[1][0])
         assert [r.tcg_iters for r in sols[0][1].records] == [r.tcg_iters for r in sols[1][1].records]
+
+
+def test_tcg_graph_needs_created_stream(mods):
+    """plp_tcg_graph_create on the legacy default stream is refused (PLP_ERR_ARG), not captured."""
+    plp, solver, ctx = mods
+    if ctx.stream.cuda_stream != 0:
+        pytest.skip("context not on the default stream")
+    g = make_config("C2", n=400)
+    G = plp.Graph(ctx, g.row_ptr, g.col, g.w)
+    Uo, _ = oracle.retract(draw_U(g.n, 2, 2), np.zeros((g.n, 2)))
+    tr = solver.GrassmannTR(ctx, G, 2, solver.SolverConfig(tcg_graph=False))
+    st = solver._State(tr, torch.from_numpy(Uo).cuda(), 1.5)
+    tr.tcg_device(st, 1.5, 0.3)
+    eta, Heta, r, dlt, Hd, scal, status = tr._tcg_buf
+    with pytest.raises(plp.PlpError):
+        plp.TcgGraph(ctx, G, st.U, st.AB, None, st.S, 1.5, 1e-9, plp.HESS_SPARSE, eta, Heta, r, dlt, Hd, scal,
+                     status, 100, 4)
