@@ -370,9 +370,7 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
       unsigned mx = 0;
 #pragma unroll
       for (int cc = 0; cc < CPL; ++cc) L[cc] = HA[cc] = 0.0;
-      if constexpr (!POW::kIsP2 && ADAPT) {
-        if (capmode) mx = ~0u;  // straight to the capped form (previous pass of this warp needed it)
-      }
+
       // batches of EB edges as straight-line code (their dependency chains interleave), then the
       // remainder two edges / one edge at a time; summation order stays the CSR order
       int e = (ADAPT && capmode) ? e1 : e0;  // capmode: the capped form below recomputes the row
@@ -445,7 +443,9 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
         }
       }
       if constexpr (!POW::kIsP2 && ADAPT) {
-        const bool need = mx >= pw.fast_span2;
+        // capmode skipped the fast loop (mx then holds the node tests only)
+        const bool need = capmode || mx >= pw.fast_span2;
+        bool fast_fails = mx >= pw.fast_span2;
         if (need) {
           // some |d| left the fast domain (usually |d| < eps: the degenerate regime): the row
           // again from shared memory in the capped form; libdevice only for what that cannot take
@@ -476,8 +476,10 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
           if (bad) edge_row_exact<CPL, POW, HAS_ETA>(pw, e0, e1, a.col, a.w, a.U, a.eta, K, c0, ui, ei, L, HA);
 #pragma unroll
           for (int cc = 0; cc < CPL; ++cc) pw.eval(fabs(ui[cc]), sn[cc], tn[cc]);
+          fast_fails = fast_fails || mxf >= pw.fast_span2;
         }
-        capmode = __any_sync(__activemask(), need);
+        // the warp's next pass goes straight to the capped form iff the fast form failed here
+        capmode = __any_sync(__activemask(), fast_fails);
       }
       double g[CPL], hv[CPL];
 #pragma unroll

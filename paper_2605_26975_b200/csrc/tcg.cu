@@ -115,6 +115,9 @@ constexpr int kTcgThreads = 256, kTcgWarps = kTcgThreads / 32;
 // tcg_reduce_kernel runs one CTA per entry (coalesced fixed-order sum: thread-strided, warp xor
 // tree, warps in order) and its last CTA (ticket) applies the scalar step on the totals.
 // pass A: [M1 | M2 | tr(d^T EH) | <d^T d, S>_F] over 4-row blocks
+#ifndef PLP_TCG_DHD_ROWWISE
+#define PLP_TCG_DHD_ROWWISE 1  // <d, EH - d S> element by element (cancellation before the sum)
+#endif
 template <int KT, int UNR>
 __global__ void __launch_bounds__(kTcgThreads) tcg_gram_a_kernel(int64_t n, const double* __restrict__ U,
                                                                  const double* __restrict__ EH,
@@ -123,9 +126,15 @@ __global__ void __launch_bounds__(kTcgThreads) tcg_gram_a_kernel(int64_t n, cons
                                                                  double* __restrict__ part) {
   constexpr int K = 8 * KT, KK = K * K, E = 2 * KK + 2;
   __shared__ double red[E];
+  __shared__ double sS[KK];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
   for (int e = threadIdx.x; e < E; e += kTcgThreads) red[e] = 0.0;
+  for (int e = threadIdx.x; e < KK; e += kTcgThreads) sS[e] = S[e];
+  __syncthreads();
+  double sc1[8];  // k = 8: the lane's column g of S in registers
+#pragma unroll
+  for (int a = 0; a < 8; ++a) sc1[a] = KT == 1 ? sS[a * K + g] : 0.0;
   double m1[KT][KT][2], m2[KT][KT][2], gd[KT][KT][2], tr = 0.0, ds = 0.0;
 #pragma unroll
   for (int i = 0; i < KT; ++i)
@@ -159,12 +168,32 @@ __global__ void __launch_bounds__(kTcgThreads) tcg_gram_a_kernel(int64_t n, cons
         for (int j = 0; j < KT; ++j) {
           dmma884(m1[i][j][0], m1[i][j][1], u[v][i], h[v][j]);
           dmma884(m2[i][j][0], m2[i][j][1], u[v][i], dd[v][j]);
+#if !PLP_TCG_DHD_ROWWISE
           dmma884(gd[i][j][0], gd[i][j][1], dd[v][i], dd[v][j]);
+#endif
         }
+#if !PLP_TCG_DHD_ROWWISE
         dmma884(de[i][0], de[i][1], dd[v][i], h[v][i]);
+#endif
       }
+#if PLP_TCG_DHD_ROWWISE
+      // d (EH - d S) per element; (d S)[r][c] = sum_a d[r][a] S[a][c], the row's d values from the
+      // lanes with the same q (a = 8 t2 + g2 ascending)
+#pragma unroll
+      for (int t = 0; t < KT; ++t) {
+        double dS = 0.0;
+#pragma unroll
+        for (int t2 = 0; t2 < KT; ++t2)
+#pragma unroll
+          for (int g2 = 0; g2 < 8; ++g2)
+            dS = fma(__shfl_sync(0xffffffffu, dd[v][t2], g2 * 4 + q),
+                     KT == 1 ? sc1[g2] : sS[(8 * t2 + g2) * K + 8 * t + g], dS);
+        tr = fma(dd[v][t], h[v][t] - dS, tr);
+      }
+#endif
     }
   }
+#if !PLP_TCG_DHD_ROWWISE
   // diagonal of the d^T EH tiles: element (8i + g, 8i + 2q + h) is diagonal iff g == 2q + h
 #pragma unroll
   for (int i = 0; i < KT; ++i) tr += (g == 2 * q ? de[i][0] : 0.0) + (g == 2 * q + 1 ? de[i][1] : 0.0);
@@ -174,7 +203,10 @@ __global__ void __launch_bounds__(kTcgThreads) tcg_gram_a_kernel(int64_t n, cons
 #pragma unroll
     for (int j = 0; j < KT; ++j)
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) ds = fma(gd[i][j][hh], __ldg(S + (8 * i + g) * K + 8 * j + 2 * q + hh), ds);
+      for (int hh = 0; hh < 2; ++hh) ds = fma(gd[i][j][hh], sS[(8 * i + g) * K + 8 * j + 2 * q + hh], ds);
+#endif
+  (void)gd;
+  (void)de;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     tr += __shfl_xor_sync(0xffffffffu, tr, o);

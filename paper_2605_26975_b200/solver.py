@@ -40,9 +40,7 @@ class SolverConfig:
     eps: float = 1e-9
     device_tcg: bool = True            # tCG recurrences on the device (plp_tcg_run), no per-iteration D2H
     tcg_batch: int = 8                 # most iterations launched between two status reads
-    # fused tCG passes (NEXT-2); default on for k = 8, 16.  k = 1, 2, 4 with n k % 8 = 0 (folded) on
-    # request: same iteration up to rounding, but over a long continuation solve the trajectory
-    # drifts from the oracle's far enough to move k-means boundary points
+    # fused tCG passes (NEXT-2); default on for k = 8, 16 and (folded) k = 1, 2, 4 with n k % 8 = 0
     tcg_fused: bool | None = None
     tcg_graph: bool = True             # replay each batch as one CUDA graph (needs a non-default stream)
 
@@ -57,7 +55,7 @@ class SolverConfig:
         if c.tcg_max_iters is None:
             c.tcg_max_iters = min(2 * n * k, 1000)
         if c.tcg_fused is None:
-            c.tcg_fused = c.device_tcg and k in (8, 16)
+            c.tcg_fused = c.device_tcg and (k in (8, 16) or (k in (1, 2, 4) and (n * k) % 8 == 0))
         if not (0.0 < c.tr_rho_accept < 0.25 and c.grad_tol > 0 and c.tr_delta0 <= c.tr_delta_max):
             raise ValueError("invalid SolverConfig (SPEC.md:303)")
         return c

@@ -63,8 +63,9 @@ def test_first_trust_region_step_matches_oracle(mods):
 
 @pytest.mark.parametrize("cfg,n,k,sched", [("C1", None, 3, [2.0, 1.8, 1.5, 1.2]),
                                             ("C2", 20000, 2, [2.0, 1.1]),
-                                            ("D16", 8192, 4, [2.0, 1.5]),
-                                            ("D16", 4096, 8, [2.0, 1.5])])  # k = 8: fused tCG passes
+                                            ("D16", 8192, 4, [2.0, 1.5]),  # k = 2, 4: folded fused tCG
+                                            ("D16", 4096, 8, [2.0, 1.5]),  # k = 8: fused tCG passes
+                                            ("C1", None, 3, [2.0, 1.5])])  # k = 3: unfused device tCG
 def test_end_to_end_labels_and_rcut_match_oracle(mods, cfg, n, k, sched):
     """North star: labels agree up to permutation, RCut within 1e-6 relative."""
     plp, solver, ctx = mods
@@ -98,7 +99,7 @@ def test_device_tcg_matches_host_tcg_bitwise(mods, p, delta, mode):
     Z = draw_U(g.n, k, 4)
     Uo, _ = oracle.retract(Z, np.zeros_like(Z))
     G = plp.Graph(ctx, g.row_ptr, g.col, g.w)
-    tr = solver.GrassmannTR(ctx, G, k, solver.SolverConfig(hessian_mode=mode))
+    tr = solver.GrassmannTR(ctx, G, k, solver.SolverConfig(hessian_mode=mode, tcg_fused=False))
     st = solver._State(tr, torch.from_numpy(Uo).cuda(), p)
     a = tr.tcg(st, p, delta)
     b = tr.tcg_device(st, p, delta)
