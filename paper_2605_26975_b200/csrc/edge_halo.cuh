@@ -235,7 +235,10 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
     }
   } else {
   const int h = warp & 1, win = warp >> 1;  // warp pair shares a 32-row window
-  bool capmode = false;  // this warp's previous pass needed the capped form (|d| < eps rows)
+#ifndef PLP_HALO_CAPSEL_ONLY
+#define PLP_HALO_CAPSEL_ONLY 0  // 1: adaptive passes always use the capped form (experiment)
+#endif
+  bool capmode = PLP_HALO_CAPSEL_ONLY;  // this warp's previous pass needed the capped form
   for (int it = 0;; ++it) {
     const int64_t t = t0 + (int64_t)it * ts;
     if (t >= n_tiles) break;
@@ -479,7 +482,7 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
           fast_fails = fast_fails || mxf >= pw.fast_span2;
         }
         // the warp's next pass goes straight to the capped form iff the fast form failed here
-        capmode = __any_sync(__activemask(), fast_fails);
+        if (!PLP_HALO_CAPSEL_ONLY) capmode = __any_sync(__activemask(), fast_fails);
       }
       double g[CPL], hv[CPL];
 #pragma unroll

@@ -30,6 +30,7 @@ VARIANTS = {
     "full_minb3": ["FULL", "-DPLP_EDGE_MINB=3"],
     "full_minb4": ["FULL", "-DPLP_EDGE_MINB=4"],
     "full_nbuf3": ["FULL", "-DPLP_HALO_NBUF=3"],
+    "full_capsel": ["FULL", "-DPLP_HALO_CAPSEL_ONLY=1"],
 }
 
 
