@@ -96,6 +96,29 @@ constexpr int halo_cpl() { return K == 8 ? PLP_HALO_CPL8 : K == 16 ? 4 : 2; }
 // OBJ: objective-only pass (no eta, no G) on a symmetric graph: A_l = sum over the upper-triangle
 // edges (j > i) of w_ij |u_il - u_jl|^p, i.e. Eq. (1)'s numerator with each undirected edge once
 // (half the powers of the row form); B_l from the node terms as usual.
+// Out-of-line row fallback of the plain (fused-pass) variant: the capped form from shared memory,
+// libdevice only for what it flags.  Not inlined, so the hot loop's code and registers are those of
+// the kernel without it; the call only happens for rows that left the fast domain.
+template <int CPL, int K, class POW, bool HAS_ETA>
+__device__ __noinline__ void halo_row_fallback(const POW& pw, const EdgeArgs& a, int e0, int e1, const int* enc_s,
+                                               const double* w_s, const double* tU, const double* tE, int c0,
+                                               const double (&ui)[CPL], const double (&ei)[CPL], double (&L)[CPL],
+                                               double (&HA)[CPL], double (&sn)[CPL], double (&tn)[CPL]) {
+  unsigned bad = 0, mxf = 0;
+#pragma unroll
+  for (int cc = 0; cc < CPL; ++cc) L[cc] = HA[cc] = 0.0;
+  for (int ee = e0; ee < e1; ++ee) {
+    const int x0 = enc_s[ee];
+    double uj0[CPL], ej0[CPL];
+    lds_vec<CPL>(tU + x0 * K, uj0);
+    if constexpr (HAS_ETA) lds_vec<CPL>(tE + x0 * K, ej0);
+    edge_update_capsel<CPL, POW, HAS_ETA>(pw, w_s[ee], ui, uj0, ei, ej0, L, HA, bad, mxf);
+  }
+  if (bad) edge_row_exact<CPL, POW, HAS_ETA>(pw, e0, e1, a.col, a.w, a.U, a.eta, K, c0, ui, ei, L, HA);
+#pragma unroll
+  for (int cc = 0; cc < CPL; ++cc) pw.eval(fabs(ui[cc]), sn[cc], tn[cc]);
+}
+
 // ADAPT: rows that leave the fast domain (mostly |d| < eps: the solver's degenerate regime, where
 // p-Laplacian iterates flatten on clusters) are recomputed from shared memory in the capped form,
 // and a warp whose previous pass needed it goes there directly; libdevice only for |d| < 2^-120 or
@@ -235,6 +258,9 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
     }
   } else {
   const int h = warp & 1, win = warp >> 1;  // warp pair shares a 32-row window
+#ifndef PLP_HALO_PLAIN_FALLBACK_CAPPED
+#define PLP_HALO_PLAIN_FALLBACK_CAPPED 0  // 1: fused pass calls an out-of-line capped-form row fallback (measured: the call costs the hot loop 20 %)
+#endif
 #ifndef PLP_HALO_CAPSEL_ONLY
 #define PLP_HALO_CAPSEL_ONLY 0  // 1: adaptive passes always use the capped form (experiment)
 #endif
@@ -439,11 +465,16 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
         }
       }
       if constexpr (!POW::kIsP2 && !ADAPT) {
+#if PLP_HALO_PLAIN_FALLBACK_CAPPED
+        if (mx >= pw.fast_span2)  // rare: out of line, capped form, libdevice for what it flags
+          halo_row_fallback<CPL, K, POW, HAS_ETA>(pw, a, e0, e1, enc_s, w_s, tU, tE, c0, ui, ei, L, HA, sn, tn);
+#else
         if (mx >= pw.fast_span2) {  // rare: exact libdevice recomputation of the row
           edge_row_exact<CPL, POW, HAS_ETA>(pw, e0, e1, a.col, a.w, a.U, a.eta, K, c0, ui, ei, L, HA);
 #pragma unroll
           for (int cc = 0; cc < CPL; ++cc) pw.eval(fabs(ui[cc]), sn[cc], tn[cc]);
         }
+#endif
       }
       if constexpr (!POW::kIsP2 && ADAPT) {
         // capmode skipped the fast loop (mx then holds the node tests only)
