@@ -31,6 +31,10 @@ VARIANTS = {
     "full_minb4": ["FULL", "-DPLP_EDGE_MINB=4"],
     "full_nbuf3": ["FULL", "-DPLP_HALO_NBUF=3"],
     "full_capsel": ["FULL", "-DPLP_HALO_CAPSEL_ONLY=1"],
+    "eb4": ["-DPLP_HALO_EB=4"],
+    "sleep0": ["-DPLP_HALO_SLEEP_NS=0"],
+    "sleep256": ["-DPLP_HALO_SLEEP_NS=256"],
+    "nol2pf": ["-DPLP_HALO_L2PF=0"],
 }
 
 
