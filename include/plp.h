@@ -253,7 +253,9 @@ enum {
  * <d, Hd> from the Grams U^T EH, U^T d, d^T d; the eta / Heta / r updates with Hd = EH - U U^T EH
  * - d S formed in registers, U^T r and ||r||^2; then r's re-projection and the new direction --
  * the same iteration up to rounding order.  Read `status` to know when it stopped; eta / Heta are
- * the step and H step. */
+ * the step and H step.  With fused = 1, Heta may be NULL (plp_tcg_init likewise): the update pass
+ * then neither reads nor writes an H step (16 n k bytes less per iteration) and the caller forms
+ * H(eta) once at the end (by linearity the same vector up to rounding). */
 plp_status plp_tcg_init(plp_ctx* ctx, int64_t n, int k, const double* grad, double delta, double kappa,
                         double theta, double* eta, double* Heta, double* r, double* delta_dir,
                         double* scal, int* status);

@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(kTcgThreads) tcg_gram_a_kernel(int64_t n, cons
 
 // pass B over 8-row blocks: Hd = EH - U M1 - d S on the tensor cores (accumulator = EH),
 // eta += ce d, Heta += ce Hd, r += cr Hd, then partials of MR = U^T r and ||r||^2.
-template <int KT>
+template <int KT, bool HETA>
 __global__ void __launch_bounds__(kTcgThreads) tcg_update_kernel(int64_t n, const double* __restrict__ U,
                                                                  const double* __restrict__ EH,
                                                                  const double* __restrict__ D,
@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(kTcgThreads) tcg_update_kernel(int64_t n, cons
       hd[tb][1] = x.y;
       d2[tb] = ok ? __ldg(reinterpret_cast<const double2*>(D + o)) : z;
       e2[tb] = ok ? *reinterpret_cast<const double2*>(eta + o) : z;
-      h2[tb] = ok ? *reinterpret_cast<const double2*>(Heta + o) : z;
+      h2[tb] = (HETA && ok) ? *reinterpret_cast<const double2*>(Heta + o) : z;
       r2[tb] = ok ? *reinterpret_cast<const double2*>(r + o) : z;
     }
 #pragma unroll
@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(kTcgThreads) tcg_update_kernel(int64_t n, cons
       if (ok) {
         const int64_t o = row * K + 8 * tb + 2 * q;
         *reinterpret_cast<double2*>(eta + o) = e2[tb];
-        *reinterpret_cast<double2*>(Heta + o) = h2[tb];
+        if constexpr (HETA) *reinterpret_cast<double2*>(Heta + o) = h2[tb];
         *reinterpret_cast<double2*>(r + o) = r2[tb];
       }
     }
@@ -535,7 +535,7 @@ static plp_status fused_iteration(plp_ctx* ctx, int64_t n, const double* U, cons
   static const int unr_a = env_int("PLP_TCG_UNR_A", 4);
   static const int per_sm_a = env_int("PLP_TCG_GRID_A", unr_a == 4 ? resident_ctas(tcg_gram_a_kernel<KT, 4>, kTcgThreads)
                                                                     : resident_ctas(tcg_gram_a_kernel<KT, 2>, kTcgThreads));
-  static const int per_sm_b = env_int("PLP_TCG_GRID_B", resident_ctas(tcg_update_kernel<KT>, kTcgThreads));
+  static const int per_sm_b = env_int("PLP_TCG_GRID_B", resident_ctas(tcg_update_kernel<KT, true>, kTcgThreads));
   static const int per_sm_c = resident_ctas(tcg_finish_kernel<KT>, kTcgThreads);
   unsigned* counter = reinterpret_cast<unsigned*>(ctx->flag + 4);
   constexpr int EA = 2 * KK + 2, EB = KK + 1;
@@ -549,7 +549,8 @@ static plp_status fused_iteration(plp_ctx* ctx, int64_t n, const double* U, cons
                                                        max_iters, kr);
   PLP_LAUNCH_CHECK("tcg_reduce_kernel");
   const int gb = fused_grid(ctx, (n + 7) / 8, EB, per_sm_b);
-  tcg_update_kernel<KT><<<gb, kTcgThreads, 0, ctx->stream>>>(n, U, EH, dlt, S, scal, eta, Heta, r,
+  auto upd = Heta ? tcg_update_kernel<KT, true> : tcg_update_kernel<KT, false>;
+  upd<<<gb, kTcgThreads, 0, ctx->stream>>>(n, U, EH, dlt, S, scal, eta, Heta, r,
                                                              ctx->partials);
   PLP_LAUNCH_CHECK("tcg_update_kernel");
   tcg_reduce_kernel<K, 1><<<EB, 256, 0, ctx->stream>>>(gb, ctx->partials, scal + kTotB, counter + 1, scal, status,
@@ -585,7 +586,7 @@ using namespace plp;
 extern "C" plp_status plp_tcg_init(plp_ctx* ctx, int64_t n, int k, const double* grad, double delta,
                                    double kappa, double theta, double* eta, double* Heta, double* r,
                                    double* dlt, double* scal, int* status) {
-  if (!ctx || !grad || !eta || !Heta || !r || !dlt || !scal || !status || n < 0)
+  if (!ctx || !grad || !eta || !r || !dlt || !scal || !status || n < 0)
     return set_error(PLP_ERR_ARG, "null argument");
   plp_status st = check_k(k);
   if (st) return st;
@@ -593,7 +594,7 @@ extern "C" plp_status plp_tcg_init(plp_ctx* ctx, int64_t n, int k, const double*
   const size_t bytes = sizeof(double) * (size_t)n * k;
   PLP_CUDA(cudaMemcpyAsync(r, grad, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
   PLP_CUDA(cudaMemsetAsync(eta, 0, bytes, ctx->stream));
-  PLP_CUDA(cudaMemsetAsync(Heta, 0, bytes, ctx->stream));
+  if (Heta) PLP_CUDA(cudaMemsetAsync(Heta, 0, bytes, ctx->stream));
   PLP_CUDA(cudaMemsetAsync(dlt, 0, bytes, ctx->stream));
   if ((st = plp_axpby(ctx, n, k, -1.0, r, 0.0, dlt))) return st;  // delta = -r
   if ((st = plp_dot(ctx, n, k, r, r, scal + kZr))) return st;
@@ -607,7 +608,7 @@ extern "C" plp_status plp_tcg_run(plp_ctx* ctx, const plp_graph* g, int k, const
                                   double eps, int mode, double* eta, double* Heta, double* r,
                                   double* dlt, double* Hd, double* scal, int* status, int max_iters,
                                   int iters, int fused) {
-  if (!ctx || !g || !U || !AB || !S || !eta || !Heta || !r || !dlt || !Hd || !scal || !status)
+  if (!ctx || !g || !U || !AB || !S || !eta || !r || !dlt || !Hd || !scal || !status)
     return set_error(PLP_ERR_ARG, "null argument");
   if (iters < 0 || max_iters < 1) return set_error(PLP_ERR_ARG, "iters >= 0, max_iters >= 1");
   const int64_t n = g->n_rows;
@@ -616,7 +617,8 @@ extern "C" plp_status plp_tcg_run(plp_ctx* ctx, const plp_graph* g, int k, const
   if (fused && k != 8 && k != 16 && !foldable)
     return set_error(PLP_ERR_ARG, "fused tCG needs k = 8 or 16, or k = 1, 2, 4 with n k divisible by 8");
   auto al16 = [](const void* x) { return ((uintptr_t)x & 15u) == 0; };
-  if (fused && !(al16(U) && al16(eta) && al16(Heta) && al16(r) && al16(dlt) && al16(Hd)))
+  if (!fused && !Heta) return set_error(PLP_ERR_ARG, "Heta may be NULL only with fused = 1");
+  if (fused && !(al16(U) && al16(eta) && (!Heta || al16(Heta)) && al16(r) && al16(dlt) && al16(Hd)))
     return set_error(PLP_ERR_ARG, "fused tCG needs 16-byte aligned vectors");
   const int grid = axpby_grid(ctx, total);
   plp_status st;

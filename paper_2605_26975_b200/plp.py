@@ -316,7 +316,7 @@ def axpby(ctx: Context, a: float, x, b: float, y):
 def tcg_init(ctx: Context, grad, delta: float, kappa: float, theta: float, eta, Heta, r, dlt, scal, status):
     n, k = grad.shape
     _ck(_lib.plp_tcg_init(ctx.h, C_I64(n), k, _dev(grad, "grad"), C_D(delta), C_D(kappa), C_D(theta),
-                          _dev(eta, "eta", shape=(n, k)), _dev(Heta, "Heta", shape=(n, k)),
+                          _dev(eta, "eta", shape=(n, k)), _dev(Heta, "Heta", shape=(n, k), nullable=True),
                           _dev(r, "r", shape=(n, k)), _dev(dlt, "dlt", shape=(n, k)),
                           _dev(scal, "scal", shape=(TCG_SCAL_LEN,)), _dev(status, "status", dtype=torch.int32)),
         "plp_tcg_init")
@@ -327,7 +327,7 @@ def tcg_run(ctx: Context, g: Graph, U, AB, G_in, S, p: float, eps: float, mode: 
     k = U.shape[1]
     _ck(_lib.plp_tcg_run(ctx.h, g.h, k, _dev(U, "U", shape=(g.n_cols, k)), _dev(AB, "AB", shape=(2 * k,)),
                          _dev(G_in, "G_in", shape=(g.n_rows, k), nullable=True), _dev(S, "S", shape=(k, k)),
-                         C_D(p), C_D(eps), int(mode), _dev(eta, "eta"), _dev(Heta, "Heta"), _dev(r, "r"),
+                         C_D(p), C_D(eps), int(mode), _dev(eta, "eta"), _dev(Heta, "Heta", nullable=True), _dev(r, "r"),
                          _dev(dlt, "dlt"), _dev(Hd, "Hd"), _dev(scal, "scal", shape=(TCG_SCAL_LEN,)),
                          _dev(status, "status", dtype=torch.int32), int(max_iters), int(iters), int(fused)),
         "plp_tcg_run")
@@ -345,7 +345,7 @@ class TcgGraph:
         _ck(_lib.plp_tcg_graph_create(
             ctx.h, g.h, k, _dev(U, "U", shape=(g.n_cols, k)), _dev(AB, "AB", shape=(2 * k,)),
             _dev(G_in, "G_in", shape=(g.n_rows, k), nullable=True), _dev(S, "S", shape=(k, k)), C_D(p), C_D(eps),
-            int(mode), _dev(eta, "eta"), _dev(Heta, "Heta"), _dev(r, "r"), _dev(dlt, "dlt"), _dev(Hd, "Hd"),
+            int(mode), _dev(eta, "eta"), _dev(Heta, "Heta", nullable=True), _dev(r, "r"), _dev(dlt, "dlt"), _dev(Hd, "Hd"),
             _dev(scal, "scal", shape=(TCG_SCAL_LEN,)), _dev(status, "status", dtype=torch.int32), int(max_iters),
             int(iters), int(fused), ctypes.byref(h)), "plp_tcg_graph_create")
         self.h = h

@@ -131,7 +131,9 @@ class GrassmannTR:
                              torch.zeros(plp.TCG_SCAL_LEN, dtype=torch.float64, device=st.grad.device),
                              torch.zeros(2, dtype=torch.int32, device=st.grad.device))
         eta, Heta, r, dlt, Hd, scal, status = self._tcg_buf
-        plp.tcg_init(ctx, st.grad, delta, c.tcg_kappa, c.tcg_theta, eta, Heta, r, dlt, scal, status)
+        # fused: no H step accumulated per iteration (16 n k bytes less per pass); H(eta) once at the end
+        Hacc = None if c.tcg_fused else Heta
+        plp.tcg_init(ctx, st.grad, delta, c.tcg_kappa, c.tcg_theta, eta, Hacc, r, dlt, scal, status)
         full = c.hessian_mode == plp.HESS_FULL
         use_graph = c.tcg_graph and ctx.stream.cuda_stream != 0
         if use_graph:
@@ -144,12 +146,14 @@ class GrassmannTR:
             if use_graph:
                 self._graph_for(p, batch).launch()  # iterations past max_iters are no-ops (MAXITER)
             else:
-                plp.tcg_run(ctx, self.g, st.U, st.AB, G_in, st.S, p, c.eps, c.hessian_mode, eta, Heta, r, dlt,
+                plp.tcg_run(ctx, self.g, st.U, st.AB, G_in, st.S, p, c.eps, c.hessian_mode, eta, Hacc, r, dlt,
                             Hd, scal, status, c.tcg_max_iters, min(batch, c.tcg_max_iters - done),
                             fused=c.tcg_fused)
             done += batch
             batch = min(2 * batch, c.tcg_batch)
             stv = status.cpu().tolist()
+        if c.tcg_fused:
+            return eta.clone(), self._hess(st, p, eta), int(stv[1]), plp.TCG_STATUS[int(stv[0])]
         return eta.clone(), Heta.clone(), int(stv[1]), plp.TCG_STATUS[int(stv[0])]
 
     def _refresh_graph_inputs(self, st: _State, p: float) -> None:
@@ -175,8 +179,9 @@ class GrassmannTR:
         if batch not in self._graphs:
             U, AB, S, G = self._gin
             eta, Heta, r, dlt, Hd, scal, status = self._tcg_buf
-            self._graphs[batch] = plp.TcgGraph(self.ctx, self.g, U, AB, G, S, p, c.eps, c.hessian_mode, eta, Heta,
-                                               r, dlt, Hd, scal, status, c.tcg_max_iters, batch, fused=c.tcg_fused)
+            self._graphs[batch] = plp.TcgGraph(self.ctx, self.g, U, AB, G, S, p, c.eps, c.hessian_mode, eta,
+                                               None if c.tcg_fused else Heta, r, dlt, Hd, scal, status,
+                                               c.tcg_max_iters, batch, fused=c.tcg_fused)
         return self._graphs[batch]
 
     # -- truncated CG (Steihaug-Toint; Absil-Baker-Gallivan 2007, Alg. 2) ------------------------

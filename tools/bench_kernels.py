@@ -183,8 +183,9 @@ def tcg_rows(ctx, G, U, k, p, stream, row, csr):
     iters = 10
 
     def dev(fused):
-        plp.tcg_init(ctx, st.grad, 1e6, 0.0, 1.0, eta, Heta, r, dlt, scal, status)
-        plp.tcg_run(ctx, G, st.U, st.AB, None, st.S, p, cfg.eps, plp.HESS_SPARSE, eta, Heta, r, dlt, Hd,
+        Hacc = None if fused else Heta  # the solver's fused path accumulates no H step
+        plp.tcg_init(ctx, st.grad, 1e6, 0.0, 1.0, eta, Hacc, r, dlt, scal, status)
+        plp.tcg_run(ctx, G, st.U, st.AB, None, st.S, p, cfg.eps, plp.HESS_SPARSE, eta, Hacc, r, dlt, Hd,
                     scal, status, 1 << 30, iters, fused=fused)
     ms = timed(lambda: dev(False), 5, stream) / iters
     # per iteration: edge pass (csr + U, eta, Hd), project (40 n k), apply_sub (24 n k),
@@ -192,10 +193,10 @@ def tcg_rows(ctx, G, U, k, p, stream, row, csr):
     byts = csr + 24 * n * k + 40 * n * k + 24 * n * k + 32 * n * k + 96 * n * k + 40 * n * k
     row("NEXT-1 tCG iteration, device-resident (plp_tcg_run)", ms, byts)
     if k in (8, 16):
-        # fused: edge pass + pass A (U, EH, d: 24 n k) + pass B (U, EH, d, eta, Heta, r read, three
-        # written: 72 n k) + pass C (U, r, d read, r, d written: 40 n k)
+        # fused: edge pass + pass A (U, EH, d: 24 n k) + pass B (U, EH, d, eta, r read, two written:
+        # 56 n k; no H step) + pass C (U, r, d read, r, d written: 40 n k)
         ms = timed(lambda: dev(True), 5, stream) / iters
-        row("NEXT-2 tCG iteration, fused passes (plp_tcg_run fused=1)", ms, csr + 24 * n * k + 136 * n * k)
+        row("NEXT-2 tCG iteration, fused passes (plp_tcg_run fused=1, no H step)", ms, csr + 24 * n * k + 120 * n * k)
     res = {}
 
     def host():

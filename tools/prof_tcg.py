@@ -32,8 +32,9 @@ def main():
     st = solver._State(tr, U, p)
     tr.tcg_device(st, p, 1e6)
     eta, Heta, r, dlt, Hd, scal, status = tr._tcg_buf
-    plp.tcg_init(ctx, st.grad, 1e6, 0.0, 1.0, eta, Heta, r, dlt, scal, status)
-    plp.tcg_run(ctx, G, st.U, st.AB, None, st.S, p, cfg.eps, plp.HESS_SPARSE, eta, Heta, r, dlt, Hd, scal, status,
+    Hacc = Heta if a.unfused else None  # the solver's fused path accumulates no H step
+    plp.tcg_init(ctx, st.grad, 1e6, 0.0, 1.0, eta, Hacc, r, dlt, scal, status)
+    plp.tcg_run(ctx, G, st.U, st.AB, None, st.S, p, cfg.eps, plp.HESS_SPARSE, eta, Hacc, r, dlt, Hd, scal, status,
                 1 << 30, a.iters, fused=not a.unfused)
     torch.cuda.synchronize()
     print("ok", status.cpu().tolist())
@@ -41,7 +42,7 @@ def main():
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record()
         for _ in range(a.time):
-            plp.tcg_run(ctx, G, st.U, st.AB, None, st.S, p, cfg.eps, plp.HESS_SPARSE, eta, Heta, r, dlt, Hd,
+            plp.tcg_run(ctx, G, st.U, st.AB, None, st.S, p, cfg.eps, plp.HESS_SPARSE, eta, Hacc, r, dlt, Hd,
                         scal, status, 1 << 30, a.iters, fused=not a.unfused)
         s1.record()
         torch.cuda.synchronize()
