@@ -118,8 +118,11 @@ constexpr int kTcgThreads = 256, kTcgWarps = kTcgThreads / 32;
 #ifndef PLP_TCG_DHD_ROWWISE
 #define PLP_TCG_DHD_ROWWISE 1  // <d, EH - d S> element by element (cancellation before the sum)
 #endif
+#ifndef PLP_TCG_MINB_A
+#define PLP_TCG_MINB_A 1
+#endif
 template <int KT, int UNR>
-__global__ void __launch_bounds__(kTcgThreads) tcg_gram_a_kernel(int64_t n, const double* __restrict__ U,
+__global__ void __launch_bounds__(kTcgThreads, KT == 1 ? PLP_TCG_MINB_A : 1) tcg_gram_a_kernel(int64_t n, const double* __restrict__ U,
                                                                  const double* __restrict__ EH,
                                                                  const double* __restrict__ D,
                                                                  const double* __restrict__ S,
@@ -237,8 +240,11 @@ __global__ void __launch_bounds__(kTcgThreads) tcg_gram_a_kernel(int64_t n, cons
 
 // pass B over 8-row blocks: Hd = EH - U M1 - d S on the tensor cores (accumulator = EH),
 // eta += ce d, Heta += ce Hd, r += cr Hd, then partials of MR = U^T r and ||r||^2.
+#ifndef PLP_TCG_MINB_B
+#define PLP_TCG_MINB_B 4  // k = 8: 4 CTAs (32 warps) per SM at <= 64 registers, no spills
+#endif
 template <int KT, bool HETA>
-__global__ void __launch_bounds__(kTcgThreads) tcg_update_kernel(int64_t n, const double* __restrict__ U,
+__global__ void __launch_bounds__(kTcgThreads, KT == 1 ? PLP_TCG_MINB_B : 1) tcg_update_kernel(int64_t n, const double* __restrict__ U,
                                                                  const double* __restrict__ EH,
                                                                  const double* __restrict__ D,
                                                                  const double* __restrict__ S,
@@ -365,8 +371,11 @@ __global__ void __launch_bounds__(kTcgThreads) tcg_update_kernel(int64_t n, cons
 }
 
 // pass C over 8-row blocks: r <- r - U MR, d <- ca r + cb d
+#ifndef PLP_TCG_MINB_C
+#define PLP_TCG_MINB_C 1
+#endif
 template <int KT>
-__global__ void __launch_bounds__(kTcgThreads) tcg_finish_kernel(int64_t n, const double* __restrict__ U,
+__global__ void __launch_bounds__(kTcgThreads, KT == 1 ? PLP_TCG_MINB_C : 1) tcg_finish_kernel(int64_t n, const double* __restrict__ U,
                                                                  const double* __restrict__ sc,
                                                                  double* __restrict__ r,
                                                                  double* __restrict__ D) {
