@@ -231,9 +231,12 @@ __global__ void __launch_bounds__(kKmThreads) km_assign_kernel(int64_t n, int di
 // m8n8k4: A[c][q] = [label of point q == c], B[q][d] = X[q][d] or 1), 4 points per instruction.
 // Each warp owns a contiguous range of 32-point groups; per-CTA partials in a fixed order, layout
 // [sums K*dim | counts K | sse] like km_assign_kernel.
+#ifndef PLP_KM_MINB
+#define PLP_KM_MINB 1  // 3 (80 registers, small spill) measured slower: Lloyd 0.223 vs 0.211 ms
+#endif
 template <int DIM, int KC>  // DIM = 8: vectorised point loads; DIM = 0: runtime dim <= 8;
                            // KC = 8: K = 8 at compile time (unrolled); KC = 0: runtime K <= 8
-__global__ void __launch_bounds__(256) km_assign_mma_kernel(int64_t n, int dim_rt, int K_rt,
+__global__ void __launch_bounds__(256, KC == 8 ? PLP_KM_MINB : 1) km_assign_mma_kernel(int64_t n, int dim_rt, int K_rt,
                                                             const double* __restrict__ X,
                                                             const double* __restrict__ cent,
                                                             int32_t* __restrict__ lab,
