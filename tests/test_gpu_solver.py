@@ -211,3 +211,30 @@ def test_tcg_graph_needs_created_stream(mods):
     with pytest.raises(plp.PlpError):
         plp.TcgGraph(ctx, G, st.U, st.AB, None, st.S, 1.5, 1e-9, plp.HESS_SPARSE, eta, Heta, r, dlt, Hd, scal,
                      status, 100, 4)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_fused_tcg_randomised_against_oracle(mods, seed):
+    """Randomised fused-tCG cases (k, p, trust radius, iteration cap, graph size drawn from the
+    seed): same iteration count and exit status as the oracle's tCG (boundary, negative curvature,
+    convergence and the iteration cap all occur), step and H step within 1e-9."""
+    plp, solver, ctx = mods
+    rng = np.random.default_rng(1000 + seed)
+    k = int(rng.choice([2, 4, 8]))
+    n = int(rng.choice([600, 1200, 2400])) // 8 * 8 + 8
+    p = float(rng.choice([1.1, 1.3, 1.6, 1.9, 2.0]))
+    delta = float(rng.choice([1e-3, 0.3, 50.0]))
+    cap = int(rng.choice([2, 7, 200]))
+    g = random_graph(streams(seed + 50)[0], n, avg_deg=7.0, connected=True)
+    Uo, _ = oracle.retract(draw_U(g.n, k, seed + 60), np.zeros((g.n, k)))
+    G = plp.Graph(ctx, g.row_ptr, g.col, g.w)
+    tr = solver.GrassmannTR(ctx, G, k, solver.SolverConfig(tcg_fused=True, tcg_max_iters=cap))
+    st = solver._State(tr, torch.from_numpy(Uo).cuda(), p)
+    eta, Heta, it, status = tr.tcg_device(st, p, delta)
+    ocfg = osol.default_cfg(g.n, k, tcg_max_iters=cap)
+    sto = osol._state(g, Uo, p, osol.oracle_fns())
+    eta_o, Heta_o, it_o, status_o = osol.tcg(
+        lambda xi: osol._hess(g, sto, p, xi, ocfg["eps"], "sparse", osol.oracle_fns()), sto["grad"], Uo, delta, ocfg)
+    assert (it, status) == (it_o, status_o), (k, n, p, delta, cap)
+    assert np.max(np.abs(eta.cpu().numpy() - eta_o)) <= 1e-9 * np.max(np.abs(eta_o))
+    assert np.max(np.abs(Heta.cpu().numpy() - Heta_o)) <= 1e-9 * np.max(np.abs(Heta_o))
