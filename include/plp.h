@@ -250,9 +250,10 @@ enum {
  * the arrays then read as n k / 8 rows of 8 with block-diagonal k x k matrices --, 16-byte aligned
  * vectors; else PLP_ERR_ARG):
  * after the edge pass, three streaming passes on the fp64 tensor cores:
- * <d, Hd> from the Grams U^T EH, U^T d, d^T d; the eta / Heta / r updates with Hd = EH - U U^T EH
- * - d S formed in registers, U^T r and ||r||^2; then r's re-projection and the new direction --
- * the same iteration up to rounding order.  Read `status` to know when it stopped; eta / Heta are
+ * <d, Hd> = sum d (EH - d S) - <U^T d, U^T EH>_F element by element; the eta / Heta / r updates
+ * with Hd = EH - U U^T EH - d S formed in registers, U^T r and ||r||^2; then r's re-projection and
+ * the new direction -- the same iteration up to rounding order.  Errors: PLP_ERR_ARG for null
+ * pointers (Heta only as below), iters < 0, max_iters < 1; CUDA errors as PLP_ERR_CUDA.  Read `status` to know when it stopped; eta / Heta are
  * the step and H step.  With fused = 1, Heta may be NULL (plp_tcg_init likewise): the update pass
  * then neither reads nor writes an H step (16 n k bytes less per iteration) and the caller forms
  * H(eta) once at the end (by linearity the same vector up to rounding). */
