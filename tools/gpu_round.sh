@@ -33,4 +33,9 @@ timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
     --csv --log-file $OUT/tcg_launches_$TAG.csv python tools/prof_tcg.py --iters 2 > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k "regex:tcg_update_kernel" -s 1 -c 1 \
     -o $OUT/prof_tcg_update_$TAG python tools/prof_tcg.py --iters 2 > $OUT/ncu_tcg_$TAG.log 2>&1
+# optional (QUALITY=1): the NEXT-3 quality study up to D23 and the D23 per-component breakdown
+if [ "${QUALITY:-0}" = "1" ]; then
+  timeout 1800 python tools/quality_study.py D16 D20 D21 D22 D23 > $OUT/quality_$TAG.jsonl 2> $OUT/quality_$TAG.err
+  timeout 900 python tools/solver_breakdown.py D23 --k 4 --sched 2.0,1.6,1.2 --graphs > $OUT/breakdown_d23_$TAG.json 2>/dev/null
+fi
 echo "DONE" > $OUT/round_done_$TAG.txt
