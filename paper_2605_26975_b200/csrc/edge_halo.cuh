@@ -104,7 +104,7 @@ __device__ __noinline__ void halo_row_fallback(const POW& pw, const EdgeArgs& a,
                                                const double* w_s, const double* tU, const double* tE, int c0,
                                                const double (&ui)[CPL], const double (&ei)[CPL], double (&L)[CPL],
                                                double (&HA)[CPL], double (&sn)[CPL], double (&tn)[CPL]) {
-  unsigned bad = 0, mxf = 0;
+  CapRange rg;
 #pragma unroll
   for (int cc = 0; cc < CPL; ++cc) L[cc] = HA[cc] = 0.0;
   for (int ee = e0; ee < e1; ++ee) {
@@ -112,9 +112,9 @@ __device__ __noinline__ void halo_row_fallback(const POW& pw, const EdgeArgs& a,
     double uj0[CPL], ej0[CPL];
     lds_vec<CPL>(tU + x0 * K, uj0);
     if constexpr (HAS_ETA) lds_vec<CPL>(tE + x0 * K, ej0);
-    edge_update_capsel<CPL, POW, HAS_ETA>(pw, w_s[ee], ui, uj0, ei, ej0, L, HA, bad, mxf);
+    edge_update_capsel<CPL, POW, HAS_ETA>(pw, w_s[ee], ui, uj0, ei, ej0, L, HA, rg);
   }
-  if (bad) edge_row_exact<CPL, POW, HAS_ETA>(pw, e0, e1, a.col, a.w, a.U, a.eta, K, c0, ui, ei, L, HA);
+  if (rg.bad()) edge_row_exact<CPL, POW, HAS_ETA>(pw, e0, e1, a.col, a.w, a.U, a.eta, K, c0, ui, ei, L, HA);
 #pragma unroll
   for (int cc = 0; cc < CPL; ++cc) pw.eval(fabs(ui[cc]), sn[cc], tn[cc]);
 }
@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
         if (need) {
           // some |d| left the fast domain (usually |d| < eps: the degenerate regime): the row
           // again from shared memory in the capped form; libdevice only for what that cannot take
-          unsigned bad = 0, mxf = 0;
+          CapRange rg;
 #pragma unroll
           for (int cc = 0; cc < CPL; ++cc) L[cc] = HA[cc] = 0.0;
           int ee = e0;
@@ -497,20 +497,20 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
               lds_vec<CPL>(tE + x0 * K, ej0);
               lds_vec<CPL>(tE + x1 * K, ej1);
             }
-            edge_update_capsel<CPL, POW, HAS_ETA>(pw, w_s[ee], ui, uj0, ei, ej0, L, HA, bad, mxf);
-            edge_update_capsel<CPL, POW, HAS_ETA>(pw, w_s[ee + 1], ui, uj1, ei, ej1, L, HA, bad, mxf);
+            edge_update_capsel<CPL, POW, HAS_ETA>(pw, w_s[ee], ui, uj0, ei, ej0, L, HA, rg);
+            edge_update_capsel<CPL, POW, HAS_ETA>(pw, w_s[ee + 1], ui, uj1, ei, ej1, L, HA, rg);
           }
           if (ee < e1) {
             const int x0 = enc_s[ee];
             double uj0[CPL], ej0[CPL];
             lds_vec<CPL>(tU + x0 * K, uj0);
             if constexpr (HAS_ETA) lds_vec<CPL>(tE + x0 * K, ej0);
-            edge_update_capsel<CPL, POW, HAS_ETA>(pw, w_s[ee], ui, uj0, ei, ej0, L, HA, bad, mxf);
+            edge_update_capsel<CPL, POW, HAS_ETA>(pw, w_s[ee], ui, uj0, ei, ej0, L, HA, rg);
           }
-          if (bad) edge_row_exact<CPL, POW, HAS_ETA>(pw, e0, e1, a.col, a.w, a.U, a.eta, K, c0, ui, ei, L, HA);
+          if (rg.bad()) edge_row_exact<CPL, POW, HAS_ETA>(pw, e0, e1, a.col, a.w, a.U, a.eta, K, c0, ui, ei, L, HA);
 #pragma unroll
           for (int cc = 0; cc < CPL; ++cc) pw.eval(fabs(ui[cc]), sn[cc], tn[cc]);
-          fast_fails = fast_fails || mxf >= pw.fast_span2;
+          fast_fails = fast_fails || rg.fast_fails(pw);
         }
         // the warp's next pass goes straight to the capped form iff the fast form failed here
         if (!PLP_HALO_CAPSEL_ONLY) capmode = __any_sync(__activemask(), fast_fails);

@@ -72,19 +72,32 @@ __device__ __forceinline__ const double* row_at(const double* base, int j, unsig
 // p-Laplacian minimisers are nearly constant on clusters, so neighbour differences fall below the
 // curvature cap).  s_raw = |d|^{p-2} from the clamped fast power (valid for every |d| >= 2^-120 and
 // for d = 0, where it is finite and multiplies d = 0), s_cap = min(s_raw, eps^{p-2}) (x^{p-2} is
-// decreasing for p < 2, so the min is exactly the cap).  `bad` flags 0 < |d| < 2^-120 and
-// |d| >= 2^120 (exact path); `mxf` keeps the fast-path test (does the next row need this form?).
+// decreasing for p < 2, so the min is exactly the cap).  The CapRange flags 0 < |d| < 2^-120 and
+// |d| >= 2^120 (exact path) and tells whether the fast form would have failed (next row's choice).
+// Range tracker of the capped form: min |hi word|, min (|hi word| - 1) (zeros wrap to the top, so it
+// is the minimum over nonzero differences) and max |hi word| over the row's differences.
+struct CapRange {
+  unsigned mn = ~0u, mnz = ~0u, mx = 0u;
+  __device__ __forceinline__ bool bad() const { return (mnz < kHiMin - 1u) | (mx >= kHiMax); }
+  // would the fast form (edge_update_mx) have failed on these differences?
+  template <class POW>
+  __device__ __forceinline__ bool fast_fails(const POW& pw) const {
+    return (mn * 2u < pw.fast_lo2) | (mx * 2u - pw.fast_lo2 >= pw.fast_span2);
+  }
+};
 template <int CPL, class POW, bool HAS_ETA>
 __device__ __forceinline__ void edge_update_capsel(const POW& pw, double wv, const double (&ui)[CPL],
                                                    const double (&uj)[CPL], const double (&ei)[CPL],
                                                    const double (&ej)[CPL], double (&L)[CPL],
-                                                   double (&HA)[CPL], unsigned& bad, unsigned& mxf) {
+                                                   double (&HA)[CPL], CapRange& rg) {
   const double wcap = wv * pw.s_eps;
 #pragma unroll
   for (int c = 0; c < CPL; ++c) {
     const double d = ui[c] - uj[c];
-    bad |= out_of_domain(abs_hi(d));
-    mxf = max(mxf, (unsigned)__double2hiint(d) * 2u - pw.fast_lo2);
+    const unsigned ahi = abs_hi(d);
+    rg.mn = min(rg.mn, ahi);
+    rg.mnz = min(rg.mnz, ahi - 1u);
+    rg.mx = max(rg.mx, ahi);
     const double wsr = wv * pw.pow_fast(fmax(fabs(d), 0x1p-120));  // w |d|^{p-2}
     L[c] = fma(wsr, d, L[c]);                                       // w phi_p(d)
     if constexpr (HAS_ETA) HA[c] = fma(fmin(wsr, wcap), ei[c] - ej[c], HA[c]);  // w cap(|d|)^{p-2}
