@@ -115,6 +115,9 @@ constexpr int kTcgThreads = 256, kTcgWarps = kTcgThreads / 32;
 // tcg_reduce_kernel runs one CTA per entry (coalesced fixed-order sum: thread-strided, warp xor
 // tree, warps in order) and its last CTA (ticket) applies the scalar step on the totals.
 // pass A: [M1 | M2 | tr(d^T EH) | <d^T d, S>_F] over 4-row blocks
+#ifndef PLP_TCG_DS_LDG
+#define PLP_TCG_DS_LDG 0  // 1: k = 8 reads the row of d for d S from L1 instead of 8 shuffles
+#endif
 #ifndef PLP_TCG_DHD_ROWWISE
 #define PLP_TCG_DHD_ROWWISE 1  // <d, EH - d S> element by element (cancellation before the sum)
 #endif
@@ -182,6 +185,29 @@ __global__ void __launch_bounds__(kTcgThreads, KT == 1 ? PLP_TCG_MINB_A : 1) tcg
 #if PLP_TCG_DHD_ROWWISE
       // d (EH - d S) per element; (d S)[r][c] = sum_a d[r][a] S[a][c], the row's d values from the
       // lanes with the same q (a = 8 t2 + g2 ascending)
+#if PLP_TCG_DS_LDG
+      if constexpr (KT == 1) {
+        // the row's d values straight from L1 (the 8 lanes of a row read the same 64 bytes)
+        const int64_t rr = 4 * (b + v) + q;
+        double drow[8];
+        if (b + v < b1 && rr < n) {
+#pragma unroll
+          for (int a2 = 0; a2 < 8; a2 += 2) {
+            const double2 x = __ldg(reinterpret_cast<const double2*>(D + rr * K + a2));
+            drow[a2] = x.x;
+            drow[a2 + 1] = x.y;
+          }
+        } else {
+#pragma unroll
+          for (int a2 = 0; a2 < 8; ++a2) drow[a2] = 0.0;
+        }
+        double dS = 0.0;
+#pragma unroll
+        for (int g2 = 0; g2 < 8; ++g2) dS = fma(drow[g2], sc1[g2], dS);
+        tr = fma(dd[v][0], h[v][0] - dS, tr);
+      } else
+#endif
+      {
 #pragma unroll
       for (int t = 0; t < KT; ++t) {
         double dS = 0.0;
@@ -192,6 +218,7 @@ __global__ void __launch_bounds__(kTcgThreads, KT == 1 ? PLP_TCG_MINB_A : 1) tcg
             dS = fma(__shfl_sync(0xffffffffu, dd[v][t2], g2 * 4 + q),
                      KT == 1 ? sc1[g2] : sS[(8 * t2 + g2) * K + 8 * t + g], dS);
         tr = fma(dd[v][t], h[v][t] - dS, tr);
+      }
       }
 #endif
     }
