@@ -357,3 +357,16 @@ def test_delaunay_generator_is_a_triangulation():
     und = g.nnz // 2
     assert und <= 3 * g.n - 6 and 5.5 * g.n < g.nnz < 6.0 * g.n
     assert np.all(g.w == 1.0)
+
+
+@pytest.mark.parametrize("p", [1.05, 1.2, 1.5, 1.8, 1.99])
+def test_capped_weight_is_min_of_raw_and_cap(p):
+    """The edge passes' capped form uses cap(|d|)^{p-2} = min(|d|^{p-2}, eps^{p-2}):
+    exact because x^{p-2} is decreasing for p < 2 (checked on values spanning the cap, in the
+    oracle's own arithmetic)."""
+    eps = 1e-9
+    rng = np.random.default_rng(int(p * 100))
+    x = np.concatenate([10.0 ** rng.uniform(-14, 1, 2000), [eps, eps * (1 - 1e-15), eps * (1 + 1e-15)]])
+    capped = np.maximum(x, eps) ** (p - 2.0)
+    via_min = np.minimum(x ** (p - 2.0), eps ** (p - 2.0))
+    assert np.max(np.abs(capped - via_min) / capped) <= 4e-16
