@@ -370,3 +370,22 @@ def test_capped_weight_is_min_of_raw_and_cap(p):
     capped = np.maximum(x, eps) ** (p - 2.0)
     via_min = np.minimum(x ** (p - 2.0), eps ** (p - 2.0))
     assert np.max(np.abs(capped - via_min) / capped) <= 4e-16
+
+
+@pytest.mark.parametrize("k", [1, 2, 4])
+def test_folded_gram_and_apply_identities(k):
+    """The folded fused tCG (k = 1, 2, 4) reads n x k arrays as n k / 8 rows of 8:
+    the sum of the 8 / k diagonal k x k blocks of the 8 x 8 Gram is the true Gram, and applying the
+    block-diagonal expansion of M equals X M row by row."""
+    rng = np.random.default_rng(k)
+    n = 8 * 37
+    X, Y = rng.standard_normal((n, k)), rng.standard_normal((n, k))
+    M = rng.standard_normal((k, k))
+    Xf, Yf = X.reshape(n * k // 8, 8), Y.reshape(n * k // 8, 8)
+    G8 = Xf.T @ Yf
+    folded = sum(G8[b * k:(b + 1) * k, b * k:(b + 1) * k] for b in range(8 // k))
+    assert np.allclose(folded, X.T @ Y, rtol=1e-13, atol=1e-12)
+    Mbd = np.kron(np.eye(8 // k), M)
+    assert np.allclose((Xf @ Mbd).reshape(n, k), X @ M, rtol=1e-13, atol=1e-12)
+    # the Frobenius norm of the folded Gram is what ||P r||^2 subtracts
+    assert np.isclose(np.sum(folded * folded), np.sum((X.T @ Y) ** 2), rtol=1e-12)
