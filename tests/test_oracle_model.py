@@ -389,3 +389,23 @@ def test_folded_gram_and_apply_identities(k):
     assert np.allclose((Xf @ Mbd).reshape(n, k), X @ M, rtol=1e-13, atol=1e-12)
     # the Frobenius norm of the folded Gram is what ||P r||^2 subtracts
     assert np.isclose(np.sum(folded * folded), np.sum((X.T @ Y) ** 2), rtol=1e-12)
+
+
+def test_fused_tcg_reformulations():
+    """The fused tCG's reformulations against the definitions on random data:
+    <d, P(EH) - d S> = sum d (EH - d S) - <U^T d, U^T EH>_F, and with U^T U = I,
+    ||P r||^2 = ||r||^2 - ||U^T r||_F^2 and P(r + c Hd') = P(r + c Hd) for Hd' = EH - d S."""
+    rng = np.random.default_rng(7)
+    n, k = 500, 4
+    U, _ = np.linalg.qr(rng.standard_normal((n, k)))
+    A = rng.standard_normal((k, k))
+    S = (A + A.T) / 2
+    d, EH, r = (rng.standard_normal((n, k)) for _ in range(3))
+    P = lambda X: X - U @ (U.T @ X)  # noqa: E731
+    Hd = P(EH) - d @ S
+    lhs = np.sum(d * Hd)
+    rhs = np.sum(d * (EH - d @ S)) - np.sum((U.T @ d) * (U.T @ EH))
+    assert abs(lhs - rhs) <= 1e-12 * max(1.0, abs(lhs))
+    assert np.isclose(np.sum(P(r) ** 2), np.sum(r ** 2) - np.sum((U.T @ r) ** 2), rtol=1e-12)
+    c = 0.37
+    assert np.allclose(P(r + c * (EH - d @ S)), P(r + c * Hd), rtol=1e-12, atol=1e-12)
