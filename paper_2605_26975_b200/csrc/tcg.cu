@@ -122,7 +122,7 @@ constexpr int kTcgThreads = 256, kTcgWarps = kTcgThreads / 32;
 #define PLP_TCG_DHD_ROWWISE 1  // <d, EH - d S> element by element (cancellation before the sum)
 #endif
 #ifndef PLP_TCG_MINB_A
-#define PLP_TCG_MINB_A 1
+#define PLP_TCG_MINB_A 3
 #endif
 template <int KT, int UNR>
 __global__ void __launch_bounds__(kTcgThreads, KT == 1 ? PLP_TCG_MINB_A : 1) tcg_gram_a_kernel(int64_t n, const double* __restrict__ U,
