@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(kTcgThreads, KT == 1 ? PLP_TCG_MINB_B : 1) tcg
 
 // pass C over 8-row blocks: r <- r - U MR, d <- ca r + cb d
 #ifndef PLP_TCG_MINB_C
-#define PLP_TCG_MINB_C 1
+#define PLP_TCG_MINB_C 5
 #endif
 template <int KT>
 __global__ void __launch_bounds__(kTcgThreads, KT == 1 ? PLP_TCG_MINB_C : 1) tcg_finish_kernel(int64_t n, const double* __restrict__ U,
