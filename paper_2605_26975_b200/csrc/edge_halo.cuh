@@ -588,8 +588,9 @@ plp_status launch_halo_shape(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int
   if (grid > n_tiles) grid = n_tiles > 0 ? n_tiles : 1;
   kern<<<(int)grid, kHaloThreads, smem, ctx->stream>>>(pw, a);
   PLP_LAUNCH_CHECK("edge_halo_kernel");
-  note_edge_kernel(OBJ ? (deep ? "edge_halo_kernel[objective,3buf]" : "edge_halo_kernel[objective]")
-                       : (deep ? "edge_halo_kernel[3buf]" : "edge_halo_kernel"),
+  // [adapt]: the capped-form row recompute (every pass but the fused F/G/Hv benchmark pass)
+  note_edge_kernel(OBJ ? (deep ? "edge_halo_kernel[objective,3buf,adapt]" : "edge_halo_kernel[objective,adapt]")
+                       : (deep ? "edge_halo_kernel[3buf,adapt]" : adapt ? "edge_halo_kernel[adapt]" : "edge_halo_kernel"),
                    K, halo_cpl<K>(), K / halo_cpl<K>(), 2, POW::kName, HAS_ETA);
   *grid_out = (int)grid;
   return PLP_OK;

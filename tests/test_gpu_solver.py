@@ -238,3 +238,72 @@ def test_fused_tcg_randomised_against_oracle(mods, seed):
     assert (it, status) == (it_o, status_o), (k, n, p, delta, cap)
     assert np.max(np.abs(eta.cpu().numpy() - eta_o)) <= 1e-9 * np.max(np.abs(eta_o))
     assert np.max(np.abs(Heta.cpu().numpy() - Heta_o)) <= 1e-9 * np.max(np.abs(Heta_o))
+
+
+def _tile_ordered(plp, cfg, n):
+    from plp_inputs import permute_graph
+    g0 = make_config(cfg, n=n)
+    return permute_graph(g0, plp.tile_order(g0.row_ptr, g0.col))
+
+
+@pytest.mark.parametrize("cfg,n,k,sched", [("D16", 8192, 4, [2.0, 1.5]),
+                                            ("D16", 8192, 8, [2.0, 1.2]),
+                                            ("C2", 20000, 4, [2.0, 1.1]),
+                                            ("C5", 50000, 8, [2.0, 1.2])])
+def test_end_to_end_tile_ordered_matches_oracle(mods, cfg, n, k, sched):
+    """The ordering the solver runs on (plp_tile_order): every Hessian-vector product of the solve
+    goes through the halo kernel's adaptive capped-form variant (k = 4, 8).  Labels equal up to
+    permutation, RCut within 1e-6 relative, against the oracle solver on the same permuted graph."""
+    plp, solver, ctx = mods
+    g = _tile_ordered(plp, cfg, n)
+    Z = draw_U(g.n, k, 0)
+    u = draw_uniforms(10, k)
+    G = plp.Graph(ctx, g.row_ptr, g.col, g.w)
+    U, tr = solver.continuation_solve(ctx, G, torch.from_numpy(Z).cuda(), sched)
+    assert plp.last_edge_kernel().startswith("edge_halo_kernel"), plp.last_edge_kernel()
+    lab, rc, sse = solver.cluster(ctx, G, U, k, u)
+    Uo, tro = osol.continuation_solve(g, Z, sched)
+    lab_o, _, sse_o, _ = oracle.kmeans(Uo, k, u, restarts=10)
+    rc_o = oracle.rcut(g, lab_o, k)[0]
+    assert same_partition(lab.cpu().numpy(), lab_o, k)
+    assert abs(rc - rc_o) <= 1e-6 * max(abs(rc_o), 1e-300)
+
+
+@pytest.mark.slow
+def test_end_to_end_c2_full_size_matches_oracle(mods):
+    """North star acceptance at config 2's own size (two moons, n = 100,000, k = 2, p 2 -> 1.1)."""
+    plp, solver, ctx = mods
+    g = make_config("C2")
+    k, sched = 2, [2.0, 1.1]
+    Z = draw_U(g.n, k, 0)
+    u = draw_uniforms(10, k)
+    G = plp.Graph(ctx, g.row_ptr, g.col, g.w)
+    U, tr = solver.continuation_solve(ctx, G, torch.from_numpy(Z).cuda(), sched)
+    lab, rc, sse = solver.cluster(ctx, G, U, k, u)
+    Uo, tro = osol.continuation_solve(g, Z, sched)
+    lab_o, _, sse_o, _ = oracle.kmeans(Uo, k, u, restarts=10)
+    rc_o = oracle.rcut(g, lab_o, k)[0]
+    assert same_partition(lab.cpu().numpy(), lab_o, k)
+    assert abs(rc - rc_o) <= 1e-6 * max(abs(rc_o), 1e-300)
+
+
+@pytest.mark.parametrize("cfg,n,k,p,delta", [("D16", 8192, 8, 1.2, 0.3), ("D16", 8192, 4, 1.5, 50.0),
+                                              ("C5", 30000, 8, 1.2, 1e3), ("C5", 30000, 16, 1.8, 0.3)])
+def test_fused_tcg_tile_ordered_matches_oracle(mods, cfg, n, k, p, delta):
+    """Fused tCG on tile-ordered graphs (its Hessian-vector products run the adaptive halo kernel):
+    same iteration count and status as the oracle's tCG, step and H step within 1e-9."""
+    plp, solver, ctx = mods
+    g = _tile_ordered(plp, cfg, n)
+    Uo, _ = oracle.retract(draw_U(g.n, k, 5), np.zeros((g.n, k)))
+    G = plp.Graph(ctx, g.row_ptr, g.col, g.w)
+    tr = solver.GrassmannTR(ctx, G, k, solver.SolverConfig(tcg_fused=True))
+    st = solver._State(tr, torch.from_numpy(Uo).cuda(), p)
+    eta, Heta, it, status = tr.tcg_device(st, p, delta)
+    assert plp.last_edge_kernel().startswith("edge_halo_kernel[adapt]"), plp.last_edge_kernel()
+    ocfg = osol.default_cfg(g.n, k)
+    sto = osol._state(g, Uo, p, osol.oracle_fns())
+    eta_o, Heta_o, it_o, status_o = osol.tcg(
+        lambda xi: osol._hess(g, sto, p, xi, ocfg["eps"], "sparse", osol.oracle_fns()), sto["grad"], Uo, delta, ocfg)
+    assert (it, status) == (it_o, status_o)
+    assert np.max(np.abs(eta.cpu().numpy() - eta_o)) <= 1e-9 * np.max(np.abs(eta_o))
+    assert np.max(np.abs(Heta.cpu().numpy() - Heta_o)) <= 1e-9 * np.max(np.abs(Heta_o))

@@ -409,3 +409,51 @@ def test_fused_tcg_reformulations():
     assert np.isclose(np.sum(P(r) ** 2), np.sum(r ** 2) - np.sum((U.T @ r) ** 2), rtol=1e-12)
     c = 0.37
     assert np.allclose(P(r + c * (EH - d @ S)), P(r + c * Hd), rtol=1e-12, atol=1e-12)
+
+
+def test_node_cap_exact_zero_worked_example():
+    """Exact zero node u_0 = 0 (reading #6, the node cap): single edge, u = (0, 1), p = 1.5.
+    By hand: A = w |0 - 1|^p = w, B = |0|^p + |1|^p = 1, the edge weight w~ = w |1|^{p-2} = w, so
+    HA eta = p(p-1) w (eta_0 - eta_1, eta_1 - eta_0) and HB eta = p(p-1)(eps^{p-2} eta_0, eta_1);
+    Hv = HA eta / B - (A/B^2) HB eta."""
+    w, p, eps = 0.7, 1.5, 1e-4
+    g = single_edge(w)
+    U = np.array([[0.0], [1.0]])
+    eta = np.array([[0.3], [-0.2]])
+    c = p * (p - 1)
+    ref = np.array([c * w * (0.3 + 0.2) - w * c * eps ** (p - 2) * 0.3,
+                    c * w * (-0.2 - 0.3) - w * c * (-0.2)])
+    Hv = oracle.hessvec(g, U, eta, p, eps=eps)
+    assert relerr(Hv[:, 0], ref) < 1e-14
+
+
+@pytest.mark.parametrize("p", [1.8, 1.5, 1.2, 1.1])
+@pytest.mark.parametrize("eps", [1e-9, 1e-2])
+def test_hessvec_dense_assembly_with_zero_nodes_and_ties(p, eps):
+    """Exact zero rows u_i = 0 and exact ties u_i = u_j in several columns: the oracle's sparse
+    Hessian-vector product equals the dense operator HessA/B - (A/B^2) HessB assembled from the
+    matrix definitions (SURVEY.md §8(c) formula 3; Alg. 1), column by column,
+    with A, B from Eq. (1) written as dense sums."""
+    g = small_graph(41, 14)
+    rng = streams(41)[1]
+    k = 3
+    U = np.round(rng.standard_normal((g.n, k)) * 2.0) / 2.0  # ties and zeros
+    U[3, :] = 0.0
+    U[7, :] = 0.0  # two exact zero rows
+    U[:, 0] += np.arange(g.n) * 1e-3  # keep column 0 tie-free as a control
+    eta = rng.standard_normal((g.n, k))
+    W = g.to_scipy().toarray()
+    ref = np.zeros_like(eta)
+    for l in range(k):
+        u = U[:, l]
+        Dm = np.abs(u[:, None] - u[None, :])
+        A = 0.5 * np.sum(W * Dm ** p)
+        B = np.sum(np.abs(u) ** p)
+        Wt = W * np.maximum(Dm, eps) ** (p - 2.0)
+        HA = p * (p - 1) * (np.diag(Wt.sum(1)) - Wt)
+        HB = p * (p - 1) * np.diag(np.maximum(np.abs(u), eps) ** (p - 2.0))
+        ref[:, l] = (HA / B - (A / B ** 2) * HB) @ eta[:, l]
+    assert np.sum(U == 0.0) >= 2 * k
+    got = oracle.hessvec(g, U, eta, p, eps=eps)
+    for l in range(k):
+        assert relerr(got[:, l], ref[:, l]) < 1e-12, l
