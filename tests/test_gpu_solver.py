@@ -249,7 +249,7 @@ def _tile_ordered(plp, cfg, n):
 @pytest.mark.parametrize("cfg,n,k,sched", [("D16", 8192, 4, [2.0, 1.5]),
                                             ("D16", 8192, 8, [2.0, 1.2]),
                                             ("C2", 20000, 4, [2.0, 1.1]),
-                                            ("C5", 50000, 8, [2.0, 1.2])])
+                                            ("C5", 20000, 8, [2.0, 1.2])])
 def test_end_to_end_tile_ordered_matches_oracle(mods, cfg, n, k, sched):
     """The ordering the solver runs on (plp_tile_order): every Hessian-vector product of the solve
     goes through the halo kernel's adaptive capped-form variant (k = 4, 8).  Labels equal up to
