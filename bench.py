@@ -2,17 +2,18 @@
 
 A step = one plp_fgrad_hessvec call (SURVEY.md §8(a) a7 = a2..a5 fused, sparse-mode Hessian) on
 the workload config (default C5: 8,388,608 uniform points in [0,1]^2, symmetrised 6-NN graph,
-Gaussian weights, k = 8, p = 1.2, tile order = RCM + BFS-grown 120-row tiles), with A, B at U
+Gaussian weights, k = 8, p = 1.2, tile order = RCM + BFS-grown tiles of the halo kernel's 224 rows), with A, B at U
 supplied from a preceding plp_fgrad
 (the trust-region rho-test always has them).  Inputs (CSR 0.71 GB + U, eta 1.07 GB)
 exceed the 126 MB L2, so no flush is needed between steps.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl plp|reference] [--config C5]
 
-N > 1: launched by torchrun; rows are split in contiguous blocks (RCM order), each step exchanges
+N > 1: launched by torchrun (or, without WORLD_SIZE in the environment, bench.py re-executes itself
+under torch.distributed.run with N ranks); rows are split in contiguous blocks (RCM order), each step exchanges
 the U and eta halos with NCCL and all-reduces A, B; time = max over ranks.
-`--impl reference` times the fp64 CPU oracle (oracle/) on a bounded row sample of the same
-workload on this host's cores (the tier's reference arm).
+`--impl reference` times the fp64 CPU oracle (oracle/) on the same workload (generator order, from
+plp_inputs alone) on this host's cores (the tier's reference arm); no product code runs on that arm.
 """
 from __future__ import annotations
 
@@ -60,8 +61,9 @@ def get_graph(name: str, order: str):
     to save generation time between runs (regenerated when absent)."""
     from plp_inputs import make_config, Graph
     from paper_2605_26975_b200 import plp
-    from paper_2605_26975_b200.plp import TILE_ROWS
-    key = hashlib.sha1(f"{name}-{order}-{TILE_ROWS}-v2".encode()).hexdigest()[:12]
+    from paper_2605_26975_b200.plp import HALO_TILE
+    tile = int(os.environ.get("PLP_ORDER_TILE", HALO_TILE))  # BFS tile of the ordering (experiments)
+    key = hashlib.sha1(f"{name}-{order}-{tile}-v5".encode()).hexdigest()[:12]
     cache = f"/tmp/plp_cache/{name}_{order}_{key}.npz"
     if os.path.exists(cache):
         try:
@@ -74,7 +76,7 @@ def get_graph(name: str, order: str):
     log(f"[bench] generated {name}: n={g.n} nnz={g.nnz} in {time.time() - t0:.1f}s")
     if order in ("rcm", "tile"):
         t0 = time.time()
-        perm = plp.rcm_order(g.row_ptr, g.col) if order == "rcm" else plp.tile_order(g.row_ptr, g.col)
+        perm = plp.rcm_order(g.row_ptr, g.col) if order == "rcm" else plp.tile_order(g.row_ptr, g.col, tile)
         rp, col, w = plp.permute_csr(g.row_ptr, g.col, g.w, perm)
         g = Graph(name, g.n, rp, col, w)
         log(f"[bench] {order} reorder in {time.time() - t0:.1f}s")
@@ -142,14 +144,26 @@ def algorithmic_bytes(n: int, nnz: int, k: int) -> int:
 
 
 # ------------------------------------------------------------------------------------------------
+def row_block_sample(g, S: int):
+    """Rows [0, S) of a CSR as a local CSR whose columns index an extended array [rows 0..S-1;
+    halo] (the sorted distinct columns >= S), like one rank's shard.  numpy only: the oracle legs
+    of this file execute no product code."""
+    rp = np.ascontiguousarray(g.row_ptr[:S + 1], np.int64)
+    cols = np.asarray(g.col[:rp[S]], np.int64)
+    out = cols >= S
+    halo = np.unique(cols[out])
+    col_loc = cols.copy()
+    col_loc[out] = S + np.searchsorted(halo, cols[out])
+    return halo, rp, col_loc.astype(np.int32)
+
+
 def cpu_oracle_sample(g, k, p, eps, rows_frac=0.25, reps=1, threads=None):
     """Time the fp64 oracle (as it stands) on rows [0, S) of the workload (a local CSR whose
     columns index an extended U, like one rank's shard).  Returns (GNNZ*k/s, seconds, desc, cores)."""
     import oracle
-    from paper_2605_26975_b200 import plp
     from plp_inputs import draw_U, draw_eta
-    S = max(1, int(g.n * rows_frac))
-    halo, rp_loc, col_loc = plp.halo_plan(g.row_ptr, g.col, 0, S)
+    S = max(1, min(g.n, int(round(g.n * rows_frac))))
+    halo, rp_loc, col_loc = row_block_sample(g, S)
     ext = np.concatenate([np.arange(S), halo])
 
     class Loc:
@@ -169,10 +183,33 @@ def cpu_oracle_sample(g, k, p, eps, rows_frac=0.25, reps=1, threads=None):
         Gr = oracle.euc_grad(Loc, U, p, A, B)
         Hv = oracle.hessvec(Loc, U, eta, p, eps, "sparse", (A, B))
     dt = (time.time() - t0) / reps
-    desc = (f"oracle F+grad+Hv (sparse) on rows [0,{S}) of the workload = {nnz_s} stored nonzeros "
-            f"x k={k} (fraction {rows_frac} of nnz), {cores} OpenMP threads on {cpu_model()}")
+    what = "all rows" if S == g.n else f"rows [0,{S})"
+    desc = (f"oracle F+grad+Hv (sparse) on {what} of the workload = {nnz_s} stored nonzeros "
+            f"x k={k} (fraction {nnz_s / g.nnz:.3f} of nnz), {cores} OpenMP threads on {cpu_model()}")
     del Gr, Hv
     return nnz_s * k / dt / 1e9, dt, desc, cores
+
+
+def get_graph_generator_order(name: str):
+    """The workload in generator order from plp_inputs alone (no libplp): the reference arm's input.
+    Same graph as get_graph's up to a node relabelling."""
+    from plp_inputs import make_config, Graph
+    cache = f"/tmp/plp_cache/{name}_gen_oracle.npz"
+    if os.path.exists(cache):
+        try:
+            z = np.load(cache)
+            return Graph(name, int(z["n"]), z["rp"], z["col"], z["w"])
+        except Exception:
+            pass
+    g = make_config(name)
+    try:
+        os.makedirs(os.path.dirname(cache), exist_ok=True)
+        tmp = f"{cache}.{os.getpid()}.tmp.npz"
+        np.savez(tmp, n=g.n, rp=g.row_ptr, col=g.col, w=g.w)
+        os.replace(tmp, cache)
+    except Exception:
+        pass
+    return g
 
 
 def cpu_model() -> str:
@@ -202,7 +239,7 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     k, p = CONFIG_KP[args.config]
-    g = get_graph(args.config, args.order)
+    g = get_graph_generator_order(args.config)  # plp_inputs only: no product code on this arm
     vals, dts = [], []
     desc, cores = "", 0
     for s in range(args.warmup + args.steps):
@@ -211,12 +248,14 @@ def run_reference(args, rank, world):
             vals.append(v)
             dts.append(dt)
     val = float(np.median(vals))
-    out = {"metric": "fused grad+Hv GNNZ*k/s", "value": val, "unit": "GNNZ*k/s", "n_gpus": args.gpus,
+    out = {"metric": "fused grad+Hv GNNZ*k/s", "value": val, "unit": "GNNZ*k/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.median(dts)),
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic", "impl": "reference",
            "config": {"workload": args.config, "desc": CONFIG_DESC.get(args.config, args.config),
-                      "n": g.n, "nnz": g.nnz, "k": k, "p": p, "order": args.order},
+                      "n": g.n, "nnz": g.nnz, "k": k, "p": p,
+                      "order": "generator (the same graph as the plp arm's up to a relabelling)",
+                      "rows": "all" if args.ref_frac >= 1.0 else f"fraction {args.ref_frac} of the rows"},
            "cpu_baseline": {"value": val, "unit": "GNNZ*k/s", "cores": cores, "kind": "oracle",
                             "sample": desc},
            "e2e": {"value": val, "unit": "GNNZ*k/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -479,11 +518,23 @@ def main():
                          "rank: exercises dist.ShardedProblem on a single GPU")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-frac", type=float, default=0.25)
-    ap.add_argument("--ref-frac", type=float, default=0.1)
+    ap.add_argument("--ref-frac", type=float, default=1.0,
+                    help="reference arm: fraction of the workload's rows per step (1.0: the whole workload)")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # launched without torchrun: start the N ranks ourselves (one process per GPU), rank 0 prints
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     args.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        log(f"[bench] --gpus {args.gpus} but WORLD_SIZE={world}: reporting n_gpus={world}")
     if args.impl == "reference":
         run_reference(args, rank, world)
         return

@@ -18,9 +18,11 @@
  *    device pointers too, so no hot call synchronises with the host.  Exceptions are stated.
  *  - libplp owns plp_ctx and plp_graph and everything inside them (device CSR, workspaces).
  *    Hot calls never allocate; all workspace is sized at plp_ctx_create / plp_create_graph.
- *  - Work is enqueued on the ctx's CUDA stream (plp_ctx_set_stream).  Calls are rank-local: on P
- *    ranks each rank passes its own rows (plus halo rows of U/eta, see plp_create_graph) and the
- *    caller all-reduces the small partial outputs (AB, dots, Grams) -- DESIGN.md §7.
+ *  - Work is enqueued on the ctx's CUDA stream (plp_ctx_set_stream).  On P ranks (a ctx with an
+ *    NCCL communicator, plp_ctx_create) each call is collective: every rank passes its own rows
+ *    (dense arrays of a plp_create_graph_dist graph carry halo slots the calls fill), and scalar /
+ *    k x k outputs (F, AB, dots, Grams) are global -- DESIGN.md §7.  plp_edge_pass and
+ *    plp_full_epilogue stay rank-local building blocks.
  *  - 1 <= k <= 32.  p in (1, 2].  eps > 0 when p < 2 (curvature cap, reading #6).
  *  - Every call returns a plp_status; plp_last_error() gives a thread-local message.  No C++
  *    exception crosses the ABI.  Results are deterministic: every reduction runs in a fixed order
@@ -47,10 +49,16 @@ typedef enum {
   PLP_ERR_NONFINITE = 7,  /* non-finite input or result detected                                    */
   PLP_ERR_CUDA = 8,       /* CUDA runtime error (message in plp_last_error)                        */
   PLP_ERR_OOM = 9,        /* device allocation failed                                               */
-  PLP_ERR_EMPTY = 10      /* empty cluster where the metric needs |C| > 0    */
+  PLP_ERR_EMPTY = 10,     /* empty cluster where the metric needs |C| > 0    */
+  PLP_ERR_NCCL = 11       /* NCCL missing or an NCCL call failed (message in plp_last_error)       */
 } plp_status;
 
 enum { PLP_HESS_SPARSE = 0, PLP_HESS_FULL = 1 };          /* reading #5 */
+/* OR-ed into `mode` of plp_hessvec / plp_fgrad_hessvec on a multi-rank graph: the halo rows of U
+ * are already current (exchanged by an earlier call at the same U, e.g. plp_fgrad), so only the
+ * eta halo is exchanged -- the tCG's Hessian-vector products at a fixed iterate.  Ignored on a
+ * single-rank graph. */
+enum { PLP_U_HALO_CURRENT = 16 };
 enum { PLP_VALIDATE = 1u, PLP_VALIDATE_SYMMETRIC = 2u };  /* plp_create_graph flags */
 enum { PLP_TILE_ROWS = 120 };  /* rows per tile of the tiled edge kernel (plp_tile_order) */
 #ifndef PLP_HALO_TILE_ROWS
@@ -63,13 +71,31 @@ typedef struct plp_graph plp_graph;
 
 const char* plp_last_error(void);
 const char* plp_version(void);
+/* Rows per tile of the halo-tile edge kernel (PLP_HALO_TILE).  Pass it as plp_tile_order's `tile`
+ * so that the BFS-grown tiles of the ordering coincide with the kernel's tiles (smallest halos). */
+int plp_halo_tile_rows(void);
 
 /* ---------------------------------------------------------------------------------------------- */
 /* Context                                                                                          */
 /* ---------------------------------------------------------------------------------------------- */
 /* device: CUDA ordinal.  stream: a cudaStream_t (NULL = legacy default stream).  Allocates the
- * ctx workspaces (CTA partials, k x k scratch) on the device. */
-plp_status plp_ctx_create(int device, void* stream, plp_ctx** out);
+ * ctx workspaces (CTA partials, k x k scratch) on the device.
+ * rank, world, nccl_id: one process per GPU.  nccl_id = the 128-byte id from
+ * plp_get_nccl_unique_id on rank 0, broadcast by the caller (e.g. torch.distributed); the call is
+ * then collective over the `world` ranks and the ctx owns an NCCL communicator: every call below
+ * on a graph from plp_create_graph_dist, and every Gram / dot / projection / retraction, is then
+ * collective (each rank passes its own rows; scalar and k x k outputs are global).  nccl_id NULL
+ * requires world == 1 (single GPU, no communicator).  world == 1 with an id creates a one-rank
+ * communicator (the collective code path on one GPU).  PLP_ERR_NCCL if NCCL cannot be loaded. */
+plp_status plp_ctx_create(int device, void* stream, int rank, int world, const void* nccl_id,
+                          plp_ctx** out);
+/* Rank 0: a fresh NCCL unique id (128 bytes) for plp_ctx_create.  Loads NCCL (libnccl.so.2). */
+plp_status plp_get_nccl_unique_id(void* out128);
+/* rank, world, and whether the ctx holds a communicator. */
+plp_status plp_ctx_comm_info(const plp_ctx* ctx, int* rank, int* world, int* has_comm);
+/* In-place sum over the ranks of `count` device doubles, on the ctx stream (collective; no-op
+ * without a communicator). */
+plp_status plp_allreduce_sum(plp_ctx* ctx, double* buf, int64_t count);
 plp_status plp_ctx_set_stream(plp_ctx* ctx, void* stream);
 plp_status plp_ctx_destroy(plp_ctx* ctx);
 /* Number of CTAs the edge kernel launches (the fixed reduction grid); informational. */
@@ -90,8 +116,9 @@ plp_status plp_validate_csr(int64_t n_rows, int64_t n_cols, const int64_t* row_p
  * pseudo-peripheral node with neighbours visited in (degree, id) order; the whole order is then
  * reversed.  Deterministic.  Used so that U_j gathers hit L2. */
 plp_status plp_rcm_order(int64_t n, const int64_t* row_ptr, const int32_t* col, int64_t* perm);
-/* Tile ordering for the tiled edge kernel: RCM sweep, then tiles of `tile` nodes
- * (pass PLP_TILE_ROWS) grown by BFS along the sweep, nodes within a tile by decreasing degree.
+/* Tile ordering for the halo-tile edge kernel: RCM sweep, then tiles of `tile`
+ * nodes (pass plp_halo_tile_rows()) grown by BFS along the sweep, the nodes of a tile sorted by
+ * decreasing degree.
  * perm[new] = old.  Relabel with plp_permute_csr; U and eta must then use the new order. */
 plp_status plp_tile_order(int64_t n, const int64_t* row_ptr, const int32_t* col, int tile,
                           int64_t* perm);
@@ -123,6 +150,34 @@ plp_status plp_halo_plan(const int64_t* row_ptr, const int32_t* col, int64_t r0,
 plp_status plp_create_graph(plp_ctx* ctx, int64_t n_rows, int64_t n_cols, const int64_t* row_ptr,
                             const int32_t* col, const double* w, uint32_t flags, plp_graph** out);
 plp_status plp_graph_info(const plp_graph* g, int64_t* n_rows, int64_t* n_cols, int64_t* nnz);
+/* Collective graph creation on a ctx with a communicator: this rank owns the
+ * global rows [row_begin, row_end) of an n_global-node graph; the ranks' ranges must be contiguous
+ * in rank order and cover [0, n_global).  row_ptr (n_own + 1 entries, any base), col (GLOBAL
+ * column ids) and w are the host CSR of the owned rows.  The call finds this rank's halo (the
+ * sorted distinct columns outside the owned range), relabels columns locally (owned j ->
+ * j - row_begin, halo h -> n_own + index of h), exchanges the request lists with the peers (NCCL)
+ * and keeps the send/recv plan.  Dense arrays of this graph then have n_cols = n_own + n_halo rows:
+ * rows [0, n_own) are the caller's, rows [n_own, n_cols) are halo slots that the collective calls
+ * (plp_fgrad, plp_hessvec, plp_fgrad_hessvec, plp_rcut) fill from the peers before their edge
+ * pass (grouped NCCL send/recv; a peer's rows land in place).  Outputs (G, Hv, labels) have n_own
+ * rows.  flags: PLP_VALIDATE checks the local CSR (symmetry needs the whole graph: not checked).
+ * Without a communicator (world == 1, no id) the graph must have no column outside the range. */
+plp_status plp_create_graph_dist(plp_ctx* ctx, int64_t n_global, int64_t row_begin, int64_t row_end,
+                                 const int64_t* row_ptr, const int32_t* col, const double* w,
+                                 uint32_t flags, plp_graph** out);
+/* n_own, n_halo (the dense arrays' n_cols = n_own + n_halo), row_begin, and the number of rows this
+ * rank sends per exchange.  A graph from plp_create_graph reports n_own = n_rows, send_rows = 0. */
+plp_status plp_graph_dist_info(const plp_graph* g, int64_t* n_own, int64_t* n_halo, int64_t* row_begin,
+                               int64_t* send_rows);
+/* Halo exchange of an n_cols x row_bytes device array (row_bytes % 4 == 0): one gather launch packs
+ * the rows the peers need, grouped NCCL send/recv fill rows [n_own, n_cols).  Collective; no-op on a
+ * single-rank graph.  The edge calls run it themselves; exposed for other per-node arrays. */
+plp_status plp_halo_exchange(plp_ctx* ctx, const plp_graph* g, int row_bytes, void* X);
+/* Host part of the plan (no GPU): the slice of a sorted halo owned by each of `world` ranks with
+ * row bounds bounds[0..world] -- recv_off[q], recv_cnt[q].  PLP_ERR_ARG if a halo column lies
+ * outside [bounds[0], bounds[world]). */
+plp_status plp_dist_recv_plan(int world, const int64_t* bounds, int64_t n_halo, const int64_t* halo,
+                              int64_t* recv_off, int64_t* recv_cnt);
 plp_status plp_destroy_graph(plp_graph* g);
 
 /* ---------------------------------------------------------------------------------------------- */

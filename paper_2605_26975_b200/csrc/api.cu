@@ -56,7 +56,8 @@ static void fill_pow_tables(PowTables* t) {
 using namespace plp;
 
 extern "C" const char* plp_last_error(void) { return g_err; }
-extern "C" const char* plp_version(void) { return "libplp 0.2 (sm_100a)"; }
+extern "C" const char* plp_version(void) { return "libplp 0.3 (sm_100a)"; }
+extern "C" int plp_halo_tile_rows(void) { return PLP_HALO_TILE; }
 
 static char g_last_edge_kernel[160] = "";
 void plp::note_edge_kernel(const char* family, int kc, int cpl, int lpr, int unr, const char* pow,
@@ -66,9 +67,12 @@ void plp::note_edge_kernel(const char* family, int kc, int cpl, int lpr, int unr
 }
 extern "C" const char* plp_last_edge_kernel(void) { return g_last_edge_kernel; }
 
-extern "C" plp_status plp_ctx_create(int device, void* stream, plp_ctx** out) {
+extern "C" plp_status plp_ctx_create(int device, void* stream, int rank, int world,
+                                     const void* nccl_id, plp_ctx** out) {
   if (!out) return set_error(PLP_ERR_ARG, "out is null");
   *out = nullptr;
+  if (world < 1 || rank < 0 || rank >= world) return set_error(PLP_ERR_ARG, "bad rank/world");
+  if (world > 1 && !nccl_id) return set_error(PLP_ERR_ARG, "world > 1 needs an NCCL unique id");
   PLP_CUDA(cudaSetDevice(device));
   plp_ctx* c = new (std::nothrow) plp_ctx();
   if (!c) return set_error(PLP_ERR_OOM, "host allocation failed");
@@ -97,6 +101,11 @@ extern "C" plp_status plp_ctx_create(int device, void* stream, plp_ctx** out) {
     plp_ctx_destroy(c);
     return cuda_check(e, "ctx init");
   }
+  plp_status st = comm_init(c, rank, world, nccl_id);  // collective when an id is given
+  if (st) {
+    plp_ctx_destroy(c);
+    return st;
+  }
   *out = c;
   return PLP_OK;
 }
@@ -109,6 +118,7 @@ extern "C" plp_status plp_ctx_set_stream(plp_ctx* ctx, void* stream) {
 
 extern "C" plp_status plp_ctx_destroy(plp_ctx* ctx) {
   if (!ctx) return PLP_OK;
+  comm_destroy(ctx);
   cudaFree(ctx->partials);
   cudaFree(ctx->scratch);
   cudaFree(ctx->flag);
@@ -423,6 +433,7 @@ extern "C" plp_status plp_destroy_graph(plp_graph* g) {
   cudaFree(g->ext_col);
   cudaFree(g->tile_meta);
   cudaFree(g->tile_row);
+  dist_destroy(g->dist);
   delete g;
   return PLP_OK;
 }

@@ -307,7 +307,9 @@ extern "C" plp_status plp_gram(plp_ctx* ctx, int64_t n, int k, const double* X, 
   PLP_REQ(ctx && X && Y && out && n >= 0, "bad argument");
   plp_status st = check_k(k);
   if (st) return st;
-  return gram(ctx, n, k, X, nullptr, Y, nullptr, out);
+  st = gram(ctx, n, k, X, nullptr, Y, nullptr, out);
+  if (st) return st;
+  return comm_allreduce(ctx, out, (size_t)k * k);  // collective on a multi-rank ctx
 }
 
 extern "C" plp_status plp_apply_sub(plp_ctx* ctx, int64_t n, int k, const double* U,
@@ -326,6 +328,7 @@ extern "C" plp_status plp_project(plp_ctx* ctx, int64_t n, int k, const double* 
   double* M = dslot(ctx, 0);
   st = gram(ctx, n, k, U, nullptr, G, nullptr, M);  // M = U^T G
   if (st) return st;
+  if ((st = comm_allreduce(ctx, M, (size_t)k * k))) return st;  // global Gram (multi-rank ctx)
   return apply(ctx, n, k, G, -1.0, U, nullptr, M, out);  // G - U M
 }
 
@@ -359,10 +362,12 @@ extern "C" plp_status plp_retract(plp_ctx* ctx, int64_t n, int k, const double* 
   PLP_CUDA(cudaMemsetAsync(ctx->flag, 0, 2 * sizeof(int), ctx->stream));
   // Cholesky-QR2: Y = U + xi; Q1 = Y R1^-1; Q = Q1 R2^-1; R = R2 R1
   if ((st = gram(ctx, n, k, U, xi, U, xi, C1))) return st;
+  if ((st = comm_allreduce(ctx, C1, (size_t)k * k))) return st;  // global Grams (multi-rank ctx)
   chol_kernel<<<1, 32, 0, ctx->stream>>>(k, C1, R1, R1i, ctx->flag);
   PLP_LAUNCH_CHECK("chol_kernel");
   if ((st = apply(ctx, n, k, nullptr, 1.0, U, xi, R1i, Q))) return st;
   if ((st = gram(ctx, n, k, Q, nullptr, Q, nullptr, C2))) return st;
+  if ((st = comm_allreduce(ctx, C2, (size_t)k * k))) return st;
   chol_kernel<<<1, 32, 0, ctx->stream>>>(k, C2, R2, R2i, ctx->flag + 1);
   PLP_LAUNCH_CHECK("chol_kernel");
   if ((st = apply(ctx, n, k, nullptr, 1.0, Q, nullptr, R2i, Q))) return st;
@@ -388,7 +393,7 @@ extern "C" plp_status plp_dot(plp_ctx* ctx, int64_t n, int k, const double* x, c
   PLP_LAUNCH_CHECK("dot_kernel");
   sum_partials_kernel<<<1, 32, 0, ctx->stream>>>(grid, 1, ctx->partials, out);
   PLP_LAUNCH_CHECK("sum_partials_kernel");
-  return PLP_OK;
+  return comm_allreduce(ctx, out, 1);  // collective on a multi-rank ctx
 }
 
 extern "C" plp_status plp_axpby(plp_ctx* ctx, int64_t n, int k, double a, const double* x, double b,

@@ -268,6 +268,14 @@ static plp_status check_graph_call(plp_ctx* ctx, const plp_graph* g, int k, cons
   return check_p(p, eps);
 }
 
+// Multi-rank graph on a ctx with a communicator: the calls below exchange halo rows and
+// all-reduce their partial sums (on P ranks each call is collective).
+static bool collective(const plp_ctx* ctx, const plp_graph* g) { return ctx->comm && g->dist; }
+static plp_status exchange(plp_ctx* ctx, const plp_graph* g, const double* X, int k) {
+  // the halo rows [n_own, n_cols) of X are library-written slots (plp_create_graph_dist)
+  return halo_exchange_bytes(ctx, g, const_cast<double*>(X), k * (int)sizeof(double));
+}
+
 extern "C" plp_status plp_edge_pass(plp_ctx* ctx, const plp_graph* g, int k, const double* U,
                                     const double* eta, double p, double eps, const double* AB_in,
                                     double* AB_out, double* dots_out, double* G, double* Hv) {
@@ -327,6 +335,8 @@ extern "C" plp_status plp_fgrad(plp_ctx* ctx, const plp_graph* g, int k, const d
                                 double* F, double* AB_out, double* G) {
   plp_status st = check_graph_call(ctx, g, k, U, p, 1.0);
   if (st) return st;
+  const bool coll = collective(ctx, g);
+  if (coll && (st = exchange(ctx, g, U, k))) return st;  // U halo (a new iterate)
   double* ab = AB_out ? AB_out : scratch_ab(ctx);
   EdgeArgs a = graph_args(g);
   a.k = k;
@@ -335,8 +345,12 @@ extern "C" plp_status plp_fgrad(plp_ctx* ctx, const plp_graph* g, int k, const d
   int grid = 0;
   st = launch_edge(ctx, a, &grid);  // objective pass
   if (st) return st;
-  st = launch_edge_finalize(ctx, grid, k, ctx->partials, ab, nullptr, F);
+  st = launch_edge_finalize(ctx, grid, k, ctx->partials, ab, nullptr, coll ? nullptr : F);
   if (st) return st;
+  if (coll) {  // global A, B, then F = sum A / B
+    if ((st = comm_allreduce(ctx, ab, 2 * (size_t)k))) return st;
+    if (F && (st = plp_objective_from_ab(ctx, k, ab, F))) return st;
+  }
   if (G) {
     EdgeArgs b = a;
     b.AB = ab;
@@ -352,14 +366,20 @@ extern "C" plp_status plp_hessvec(plp_ctx* ctx, const plp_graph* g, int k, const
                                   double eps, const double* G_in, double* Hv) {
   plp_status st = check_graph_call(ctx, g, k, U, p, eps);
   if (st) return st;
+  const bool u_current = (mode & PLP_U_HALO_CURRENT) != 0;
+  mode &= ~PLP_U_HALO_CURRENT;
   if (!eta || !AB_in || !Hv) return set_error(PLP_ERR_ARG, "hessvec needs eta, AB_in and Hv");
   if (mode != PLP_HESS_SPARSE && mode != PLP_HESS_FULL) return set_error(PLP_ERR_ARG, "bad mode");
   if (mode == PLP_HESS_FULL && !G_in)
     return set_error(PLP_ERR_ARG, "full mode needs G_in (the Euclidean gradient at U)");
   const bool full = mode == PLP_HESS_FULL;
+  const bool coll = collective(ctx, g);
+  if (coll && !u_current && (st = exchange(ctx, g, U, k))) return st;
+  if (coll && (st = exchange(ctx, g, eta, k))) return st;
   st = plp_edge_pass(ctx, g, k, U, eta, p, eps, AB_in, nullptr, full ? scratch_dots(ctx) : nullptr,
                      nullptr, Hv);
   if (st || !full) return st;
+  if (coll && (st = comm_allreduce(ctx, scratch_dots(ctx), 2 * (size_t)k))) return st;
   return plp_full_epilogue(ctx, g->n_rows, k, U, p, AB_in, scratch_dots(ctx), G_in, Hv);
 }
 
@@ -369,14 +389,20 @@ extern "C" plp_status plp_fgrad_hessvec(plp_ctx* ctx, const plp_graph* g, int k,
                                         double* Hv) {
   plp_status st = check_graph_call(ctx, g, k, U, p, eps);
   if (st) return st;
+  const bool u_current = (mode & PLP_U_HALO_CURRENT) != 0;
+  mode &= ~PLP_U_HALO_CURRENT;
   if (mode != PLP_HESS_SPARSE && mode != PLP_HESS_FULL) return set_error(PLP_ERR_ARG, "bad mode");
   if (Hv && !eta) return set_error(PLP_ERR_ARG, "Hv needs eta");
   const bool full = mode == PLP_HESS_FULL && Hv != nullptr;
   if (full && !G) return set_error(PLP_ERR_ARG, "full mode needs the G output buffer");
+  const bool coll = collective(ctx, g);
+  if (coll && !u_current && (st = exchange(ctx, g, U, k))) return st;
+  if (coll && Hv && (st = exchange(ctx, g, eta, k))) return st;
   if (!AB_in) {  // objective pass first (two edge passes)
     st = plp_edge_pass(ctx, g, k, U, nullptr, p, eps, nullptr, scratch_ab(ctx), nullptr, nullptr,
                        nullptr);
     if (st) return st;
+    if (coll && (st = comm_allreduce(ctx, scratch_ab(ctx), 2 * (size_t)k))) return st;
     AB_in = scratch_ab(ctx);
   }
   EdgeArgs a = graph_args(g);
@@ -389,10 +415,16 @@ extern "C" plp_status plp_fgrad_hessvec(plp_ctx* ctx, const plp_graph* g, int k,
   st = launch_edge(ctx, a, &grid);
   if (st) return st;
   if (AB_out || full || F) {
-    // F and AB_out come from the fused pass's own A', B' (single rank: the global values)
-    st = launch_edge_finalize(ctx, grid, k, ctx->partials, AB_out ? AB_out : scratch_ab2(ctx),
-                              full ? scratch_dots(ctx) : nullptr, F);
+    // F and AB_out come from the fused pass's own A', B' (all-reduced over the ranks)
+    double* abo = AB_out ? AB_out : scratch_ab2(ctx);
+    st = launch_edge_finalize(ctx, grid, k, ctx->partials, abo, full ? scratch_dots(ctx) : nullptr,
+                              coll ? nullptr : F);
     if (st) return st;
+    if (coll) {
+      if ((st = comm_allreduce(ctx, abo, 2 * (size_t)k))) return st;
+      if (full && (st = comm_allreduce(ctx, scratch_dots(ctx), 2 * (size_t)k))) return st;
+      if (F && (st = plp_objective_from_ab(ctx, k, abo, F))) return st;
+    }
   }
   if (full) return plp_full_epilogue(ctx, g->n_rows, k, U, p, AB_in, scratch_dots(ctx), G, Hv);
   return PLP_OK;
@@ -409,10 +441,22 @@ extern "C" plp_status plp_debug_pow(plp_ctx* ctx, int64_t n, const double* a, do
   });
 }
 
+__global__ void rcut_ratio_kernel(int K, const double* cut, const int64_t* sizes, double* rcut) {
+  if (threadIdx.x == 0) {
+    double r = 0.0;
+    for (int q = 0; q < K; ++q) r += (sizes[q] > 0) ? cut[q] / (double)sizes[q] : NAN;
+    *rcut = r;
+  }
+}
+
 extern "C" plp_status plp_rcut(plp_ctx* ctx, const plp_graph* g, int clusters,
                                const int32_t* labels, double* cut, int64_t* sizes, double* rcut) {
   if (!ctx || !g || !labels) return set_error(PLP_ERR_ARG, "null argument");
   if (clusters < 1 || clusters > PLP_MAX_K) return set_error(PLP_ERR_DOMAIN, "clusters must be in [1, 32]");
+  const bool coll = collective(ctx, g);
+  plp_status st;
+  // multi-rank: the halo rows' labels come from their owners (labels has n_cols entries)
+  if (coll && (st = halo_exchange_bytes(ctx, g, const_cast<int32_t*>(labels), (int)sizeof(int32_t)))) return st;
   static const int res = resident_ctas(rcut_kernel, kRcutThreads);
   int grid = ctx->num_sms * res;  // one full wave
   const int64_t want = (g->n_rows + 255) / 256;
@@ -424,7 +468,21 @@ extern "C" plp_status plp_rcut(plp_ctx* ctx, const plp_graph* g, int clusters,
   rcut_kernel<<<grid, kRcutThreads, 0, ctx->stream>>>(g->n_rows, g->rp, g->col, g->w, clusters, labels, pc,
                                               ps, ctx->flag);
   PLP_LAUNCH_CHECK("rcut_kernel");
-  rcut_finalize_kernel<<<1, 1024, 0, ctx->stream>>>(grid, clusters, pc, ps, cut, sizes, rcut);
+  if (!coll) {
+    rcut_finalize_kernel<<<1, 1024, 0, ctx->stream>>>(grid, clusters, pc, ps, cut, sizes, rcut);
+    PLP_LAUNCH_CHECK("rcut_finalize_kernel");
+    return PLP_OK;
+  }
+  // rank-local cut / sizes, summed over the ranks, then the ratio
+  double* c = cut ? cut : ctx->scratch + 8 * PLP_MAX_K;
+  int64_t* m = sizes ? sizes : ctx->iscratch + 16;
+  rcut_finalize_kernel<<<1, 1024, 0, ctx->stream>>>(grid, clusters, pc, ps, c, m, nullptr);
   PLP_LAUNCH_CHECK("rcut_finalize_kernel");
+  if ((st = comm_allreduce(ctx, c, clusters))) return st;
+  if ((st = comm_allreduce_i64(ctx, m, clusters))) return st;
+  if (rcut) {
+    rcut_ratio_kernel<<<1, 32, 0, ctx->stream>>>(clusters, c, m, rcut);
+    PLP_LAUNCH_CHECK("rcut_ratio_kernel");
+  }
   return PLP_OK;
 }

@@ -128,8 +128,6 @@ template <int K, class POW, bool HAS_ETA, bool OBJ, int NB, bool ADAPT>
 __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(POW pw, EdgeArgs a) {
   static_assert(!(OBJ && HAS_ETA), "objective mode has no eta");
   constexpr int CPL = halo_cpl<K>(), LPR = K / CPL, RPW = 32 / LPR;  // rows per pass
-  constexpr int NS = kSchedWindow / RPW;               // rank slices per 32-row window
-  static_assert(NS % 2 == 0 || NS == 2, "slice count");
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [2] tile data landed
   uint64_t* lbar = full + NB;                   // [3] halo list landed
@@ -257,7 +255,10 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
       __syncwarp();
     }
   } else {
-  const int h = warp & 1, win = warp >> 1;  // warp pair shares a 32-row window
+  // The tile's rows are split into NSL slices of RPW schedule-consecutive rows (rows of similar
+  // degree: the schedule sorts by degree); slices go to the consumer warps in snake order (warp w
+  // takes slices w, 2C - 1 - w, 2C + w, ...), so every warp gets a heavy and a light slice.
+  constexpr int NSL = kHaloT / RPW, C = kHaloCWarps;
 #ifndef PLP_HALO_PLAIN_FALLBACK_CAPPED
 #define PLP_HALO_PLAIN_FALLBACK_CAPPED 0  // 1: fused pass calls an out-of-line capped-form row fallback (measured: the call costs the hot loop 20 %)
 #endif
@@ -288,9 +289,10 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
     const double* tE = reinterpret_cast<const double*>(B + Ly.E) + c0;
 
 #pragma unroll 1
-    for (int sl = 0; sl < NS; ++sl) {
-      if ((NS == 2 ? sl : ((sl & 1) ^ ((sl >> 1) & 1))) != h) continue;
-      const int lr = win * kSchedWindow + sl * RPW + grp;  // position in the tile's schedule
+    for (int rd = 0; rd * C < NSL; ++rd) {
+      const int sl = rd * C + ((rd & 1) ? C - 1 - warp : warp);
+      if (sl >= NSL) continue;
+      const int lr = sl * RPW + grp;  // position in the tile's schedule
       if (lr >= nr) continue;
       const int row = sc_s[lr];
       const int lrow = row - r0;

@@ -120,7 +120,8 @@ extern "C" plp_status plp_rcm_order(int64_t n, const int64_t* rp, const int32_t*
 
 // Tile ordering: RCM sweep, then tiles of T nodes grown by BFS from the first unassigned node of
 // the sweep (restarting from the next unassigned sweep node when a BFS runs dry), nodes of a tile
-// sorted by decreasing degree.  Consecutive T-row ranges of the relabelled graph are then compact
+// sorted by decreasing degree (the halo kernel deals the tile's 8-row slices to its warps in
+// snake order, so every warp gets heavy and light rows while the rows of a slice stay alike).  Consecutive T-row ranges of the relabelled graph are then compact
 // graph regions: most edges have both ends in one tile (C5: ~91% at T = 256), so the tiled edge
 // kernel reads them from shared memory and evaluates each such undirected edge once.
 extern "C" plp_status plp_tile_order(int64_t n, const int64_t* rp, const int32_t* col, int tile,

@@ -4,6 +4,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <string>
+#include <vector>
 
 #include "plp.h"
 
@@ -37,6 +38,25 @@ struct plp_ctx {
   // k-means workspace (grown at plp_kmeans entry if needed; not a hot edge call)
   double* km_best = nullptr;
   size_t km_cap = 0;
+  // collective layer (comm.cu): rank / world and the NCCL communicator (ncclComm_t; nullptr on a
+  // single-rank context created without an id)
+  int rank = 0, world = 1;
+  void* comm = nullptr;
+  // kernel attributes set on this ctx's device (cudaFuncSetAttribute is per device)
+  unsigned halo_smem_attr[3] = {0, 0, 0};
+};
+
+// Halo plan of a graph created by plp_create_graph_dist (comm.cu): this rank owns global rows
+// [row_begin, row_end); its dense arrays hold those rows followed by the n_halo halo rows (sorted
+// global ids, local ids n_own + h).  Per peer q: recv slice [recv_off[q], + recv_cnt[q]) of the
+// halo; send_cnt[q] rows listed from send_idx[send_off[q]] (local row ids, in q's halo order).
+struct plp_dist {
+  int64_t n_global = 0, row_begin = 0, row_end = 0, n_own = 0, n_halo = 0;
+  std::vector<int64_t> bounds, send_off, send_cnt, recv_off, recv_cnt;
+  int64_t total_send = 0;
+  int32_t* send_idx = nullptr;  // device
+  void* sendbuf = nullptr;      // device, grown to total_send x the widest row exchanged
+  size_t sendbuf_bytes = 0;
 };
 
 struct plp_graph {
@@ -77,6 +97,7 @@ struct plp_graph {
   bool upper_ok = false;
   int32_t* nlow = nullptr;
   int32_t* sched_up = nullptr;  // rows by decreasing upper-edge count within 32-row windows
+  plp_dist* dist = nullptr;     // multi-rank halo plan (plp_create_graph_dist), else nullptr
 };
 // rows per degree-sorting window: small enough that a CTA's rows per iteration stay contiguous
 // (neighbour rows of a tile-ordered graph then hit L1)
@@ -103,6 +124,13 @@ plp_status cuda_check(cudaError_t e, const char* what);
   } while (0)
 
 plp_status check_p(double p, double eps);
+// collective layer (comm.cu)
+plp_status comm_init(plp_ctx* ctx, int rank, int world, const void* nccl_id);
+void comm_destroy(plp_ctx* ctx);
+plp_status comm_allreduce(plp_ctx* ctx, double* buf, size_t count);  // in place, no-op on one rank
+plp_status comm_allreduce_i64(plp_ctx* ctx, int64_t* buf, size_t count);
+plp_status halo_exchange_bytes(plp_ctx* ctx, const plp_graph* g, void* X, int row_bytes);
+void dist_destroy(plp_dist* d);
 // records the last launched edge kernel's name (plp_last_edge_kernel)
 void note_edge_kernel(const char* family, int kc, int cpl, int lpr, int unr, const char* pow, int eta);
 plp_status check_k(int k);

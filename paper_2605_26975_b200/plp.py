@@ -23,8 +23,9 @@ _lib = ctypes.CDLL(LIB_PATH)
 PLP_OK = 0
 STATUS = {0: "PLP_OK", 1: "PLP_ERR_ARG", 2: "PLP_ERR_SHAPE", 3: "PLP_ERR_DOMAIN", 4: "PLP_ERR_GRAPH",
           5: "PLP_ERR_DEGENERATE", 6: "PLP_ERR_RANK", 7: "PLP_ERR_NONFINITE", 8: "PLP_ERR_CUDA",
-          9: "PLP_ERR_OOM", 10: "PLP_ERR_EMPTY"}
+          9: "PLP_ERR_OOM", 10: "PLP_ERR_EMPTY", 11: "PLP_ERR_NCCL"}
 HESS_SPARSE, HESS_FULL = 0, 1
+U_HALO_CURRENT = 16  # PLP_U_HALO_CURRENT: OR into mode when U's halo rows are already exchanged
 VALIDATE, VALIDATE_SYMMETRIC = 1, 2
 
 _lib.plp_last_error.restype = ctypes.c_char_p
@@ -43,13 +44,15 @@ SYMBOLS = [
     "plp_hessvec", "plp_fgrad_hessvec", "plp_edge_pass", "plp_full_epilogue",
     "plp_objective_from_ab", "plp_gram", "plp_project", "plp_apply_sub", "plp_retract",
     "plp_cholesky", "plp_apply_rinv", "plp_dot", "plp_axpby", "plp_gather_rows", "plp_kmeans",
-    "plp_rcut", "plp_debug_pow", "plp_tile_order", "plp_last_edge_kernel", "plp_tcg_init",
+    "plp_rcut", "plp_debug_pow", "plp_tile_order", "plp_last_edge_kernel", "plp_halo_tile_rows", "plp_tcg_init",
     "plp_tcg_run", "plp_tcg_graph_create", "plp_tcg_graph_launch", "plp_tcg_graph_nodes",
-    "plp_tcg_graph_destroy",
+    "plp_tcg_graph_destroy", "plp_get_nccl_unique_id", "plp_ctx_comm_info", "plp_allreduce_sum",
+    "plp_create_graph_dist", "plp_graph_dist_info", "plp_halo_exchange", "plp_dist_recv_plan",
 ]
 TCG_STATUS = {0: "running", 1: "boundary", 2: "negative_curvature", 3: "converged", 4: "maxiter",
               5: "interior"}
-TILE_ROWS = 120  # PLP_TILE_ROWS in include/plp.h
+TILE_ROWS = 120  # PLP_TILE_ROWS in include/plp.h (tiled kernel)
+HALO_TILE = int(_lib.plp_halo_tile_rows())  # PLP_HALO_TILE: tile_order's default tile size
 TCG_SCAL_LEN = 4160  # PLP_TCG_SCAL_LEN in include/plp.h
 
 
@@ -100,17 +103,38 @@ def _host(a, dtype):
 
 class Context:
     """plp_ctx: device workspaces + the CUDA stream work is enqueued on (torch's current stream
-    unless given)."""
+    unless given).  rank / world / nccl_id: a collective context (one process per GPU; nccl_id =
+    plp_get_nccl_unique_id() from rank 0, broadcast by the caller -- see `Context.distributed`)."""
 
-    def __init__(self, device: int = 0, stream: torch.cuda.Stream | None = None):
+    def __init__(self, device: int = 0, stream: torch.cuda.Stream | None = None, rank: int = 0,
+                 world: int = 1, nccl_id: bytes | None = None):
         self.device = device
         torch.cuda.set_device(device)
         s = stream if stream is not None else torch.cuda.current_stream(device)
         self.stream = s
+        self.rank, self.world = rank, world
         h = VP()
-        _ck(_lib.plp_ctx_create(device, VP(s.cuda_stream), ctypes.byref(h)), "plp_ctx_create")
+        idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
+        _ck(_lib.plp_ctx_create(device, VP(s.cuda_stream), int(rank), int(world),
+                                idbuf if idbuf is not None else VP(0), ctypes.byref(h)), "plp_ctx_create")
         self.h = h
         self.scratch = {}
+
+    @classmethod
+    def distributed(cls, device: int, stream=None, group=None):
+        """Collective context over torch.distributed's default group: rank 0 draws the NCCL id,
+        torch broadcasts it (the only use of torch.distributed: plumbing), every rank creates its
+        communicator inside libplp."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [get_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return cls(device, stream, rank, world, obj[0])
+
+    def comm_info(self):
+        r, w, c = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        _ck(_lib.plp_ctx_comm_info(self.h, ctypes.byref(r), ctypes.byref(w), ctypes.byref(c)), "plp_ctx_comm_info")
+        return r.value, w.value, bool(c.value)
 
     def set_stream(self, stream: torch.cuda.Stream) -> None:
         self.stream = stream
@@ -159,6 +183,63 @@ class Graph:
             self.close()
         except Exception:
             pass
+
+
+class DistGraph(Graph):
+    """plp_create_graph_dist: this rank's rows [row_begin, row_end) of an n_global-node graph (host
+    CSR of the owned rows, GLOBAL column ids).  Dense arrays of the graph have n_cols = n_own +
+    n_halo rows (halo slots filled by the collective calls); outputs have n_own rows."""
+
+    def __init__(self, ctx: Context, n_global: int, row_begin: int, row_end: int, row_ptr, col, w,
+                 flags: int = VALIDATE):
+        rp, rpp = _host(row_ptr, np.int64)
+        c, cp = _host(col, np.int32)
+        ww, wp = _host(w, np.float64)
+        self.ctx = ctx
+        h = VP()
+        _ck(_lib.plp_create_graph_dist(ctx.h, C_I64(n_global), C_I64(row_begin), C_I64(row_end), rpp, cp, wp,
+                                       ctypes.c_uint32(flags), ctypes.byref(h)), "plp_create_graph_dist")
+        self.h = h
+        a, b, c2, d = C_I64(), C_I64(), C_I64(), C_I64()
+        _ck(_lib.plp_graph_dist_info(h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c2), ctypes.byref(d)),
+            "plp_graph_dist_info")
+        self.n_rows, self.n_halo, self.row_begin, self.send_rows = a.value, b.value, c2.value, d.value
+        self.n_cols = self.n_rows + self.n_halo
+        self.row_end = self.row_begin + self.n_rows
+        self.n_global = int(n_global)
+        self.nnz = int(rp[-1] - rp[0])
+
+
+def get_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _ck(_lib.plp_get_nccl_unique_id(buf), "plp_get_nccl_unique_id")
+    return buf.raw
+
+
+def allreduce_sum(ctx: Context, x):
+    """In-place sum over the ranks of a device fp64 tensor (plp_allreduce_sum)."""
+    _ck(_lib.plp_allreduce_sum(ctx.h, _dev(x, "x"), C_I64(x.numel())), "plp_allreduce_sum")
+    return x
+
+
+def halo_exchange(ctx: Context, g: Graph, X):
+    """Fill the halo rows [n_own, n_cols) of X (n_cols x ..., any dtype with rows of 4k bytes)."""
+    rb = X[0].numel() * X.element_size() if X.dim() > 1 else X.element_size()
+    _ck(_lib.plp_halo_exchange(ctx.h, g.h, int(rb), VP(X.data_ptr())), "plp_halo_exchange")
+    return X
+
+
+def dist_recv_plan(bounds, halo):
+    """Host part of the halo plan (no GPU): per rank q the (offset, count) slice of the sorted halo
+    it owns, from the ranks' row bounds."""
+    b, bp = _host(bounds, np.int64)
+    h, hp = _host(halo, np.int64)
+    world = b.size - 1
+    off = np.zeros(world, np.int64)
+    cnt = np.zeros(world, np.int64)
+    _ck(_lib.plp_dist_recv_plan(int(world), bp, C_I64(h.size), hp, VP(off.ctypes.data), VP(cnt.ctypes.data)),
+        "plp_dist_recv_plan")
+    return off, cnt
 
 
 def _empty(ctx, *shape):
@@ -427,8 +508,11 @@ def rcm_order(row_ptr, col):
     return perm
 
 
-def tile_order(row_ptr, col, tile: int = TILE_ROWS):
-    """RCM sweep + BFS-grown tiles of `tile` nodes (perm[new] = old) for the tiled edge kernel."""
+def tile_order(row_ptr, col, tile: int = HALO_TILE):
+    """RCM sweep + BFS-grown tiles of `tile` nodes (perm[new] = old).  The default equals the halo
+    kernel's tile, so the ordering's tiles are the kernel's tiles: at C5 a 224-row tile then has
+    ~71 halo rows and 90 % of its stored edges internal (120-row BFS tiles cut into 224-row kernel
+    tiles: ~181 halo rows, 73 %)."""
     rp, rpp = _host(row_ptr, np.int64)
     c, cp = _host(col, np.int32)
     perm = np.empty(rp.size - 1, dtype=np.int64)

@@ -1,0 +1,128 @@
+"""The collective C ABI on one GPU ("on P ranks each call is collective"): a
+context holding a one-rank NCCL communicator (plp_ctx_create with an id from
+plp_get_nccl_unique_id) and a graph from plp_create_graph_dist run the multi-rank code path --
+halo exchange (no peers at world = 1), in-library all-reduce of A, B, dots, Grams and dots, F from
+the reduced A, B -- and must give bitwise the single-GPU results.  The multi-rank exchange logic is
+covered by the gloo tests (tests/test_dist_gloo.py) on CPU."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from plp_inputs import make_config, draw_U, draw_eta, draw_uniforms, permute_graph
+from helpers import TOL, colwise_relerr, scalar_relerr, to_np
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def plp():
+    from paper_2605_26975_b200 import plp as mod
+    return mod
+
+
+@pytest.fixture(scope="module")
+def ctxs(plp):
+    plain = plp.Context(0)
+    coll = plp.Context(0, rank=0, world=1, nccl_id=plp.get_nccl_unique_id())
+    return plain, coll
+
+
+@pytest.fixture(scope="module")
+def graph(plp):
+    g0 = make_config("C5", n=60_000)
+    return permute_graph(g0, plp.tile_order(g0.row_ptr, g0.col))
+
+
+def test_comm_info(plp, ctxs):
+    plain, coll = ctxs
+    assert plain.comm_info() == (0, 1, False)
+    assert coll.comm_info() == (0, 1, True)
+
+
+def test_world_gt_one_needs_id(plp):
+    with pytest.raises(plp.PlpError, match="PLP_ERR_ARG"):
+        plp.Context(0, rank=0, world=2, nccl_id=None)
+
+
+@pytest.mark.parametrize("k,p,mode", [(8, 1.2, 0), (4, 1.5, 1), (3, 1.8, 0), (8, 2.0, 1)])
+def test_edge_calls_bitwise_equal_to_single_gpu(plp, ctxs, graph, k, p, mode):
+    plain, coll = ctxs
+    g = graph
+    Gp = plp.Graph(plain, g.row_ptr, g.col, g.w)
+    Gc = plp.DistGraph(coll, g.n, 0, g.n, g.row_ptr, g.col, g.w)
+    assert Gc.n_halo == 0 and Gc.send_rows == 0 and Gc.n_cols == g.n
+    U = torch.from_numpy(draw_U(g.n, k, 2)).cuda()
+    eta = torch.from_numpy(draw_eta(g.n, k, 2)).cuda()
+    res = []
+    for ctx, G in ((plain, Gp), (coll, Gc)):
+        F0, AB, Gr = plp.fgrad(ctx, G, U, p)
+        Hv = plp.hessvec(ctx, G, U, eta, p, AB, mode=mode, G_in=Gr)
+        Hv2 = plp.hessvec(ctx, G, U, eta, p, AB, mode=mode | plp.U_HALO_CURRENT, G_in=Gr)
+        F, ABo, G2, Hv3 = plp.fgrad_hessvec(ctx, G, U, eta, p, AB_in=AB, mode=mode)
+        Fn, ABn, G3, Hv4 = plp.fgrad_hessvec(ctx, G, U, eta, p, AB_in=None, mode=mode)
+        torch.cuda.synchronize()
+        res.append([F0, AB, Gr, Hv, Hv2, F, ABo, G2, Hv3, Fn, ABn, G3, Hv4])
+    for a, b in zip(*res):
+        assert torch.equal(a, b)
+    # and the collective results are the oracle's
+    F, A, B, Gro, Hvo = oracle.fgrad_hessvec(g, U.cpu().numpy(), eta.cpu().numpy(), p, 1e-9,
+                                             "full" if mode else "sparse")
+    assert scalar_relerr(to_np(res[1][5])[0], F) < TOL
+    assert colwise_relerr(to_np(res[1][7]), Gro) < TOL and colwise_relerr(to_np(res[1][8]), Hvo) < TOL
+
+
+def test_dense_calls_bitwise_equal_to_single_gpu(plp, ctxs):
+    plain, coll = ctxs
+    n, k = 50_001, 8
+    rng = np.random.default_rng(3)
+    U = torch.from_numpy(np.linalg.qr(rng.standard_normal((n, k)))[0]).cuda()
+    X = torch.from_numpy(rng.standard_normal((n, k))).cuda()
+    out = []
+    for ctx in (plain, coll):
+        out.append([plp.gram(ctx, U, X), plp.project(ctx, U, X), plp.retract(ctx, U, 0.1 * X),
+                    plp.dot(ctx, U, X)])
+    torch.cuda.synchronize()
+    for a, b in zip(*out):
+        assert torch.equal(a, b)
+
+
+def test_rcut_and_allreduce(plp, ctxs, graph):
+    plain, coll = ctxs
+    g = graph
+    k = 5
+    lab = torch.from_numpy((np.arange(g.n) * 7 // g.n % k).astype(np.int32)).cuda()
+    Gp = plp.Graph(plain, g.row_ptr, g.col, g.w)
+    Gc = plp.DistGraph(coll, g.n, 0, g.n, g.row_ptr, g.col, g.w)
+    a = plp.rcut(plain, Gp, k, lab)
+    b = plp.rcut(coll, Gc, k, lab)
+    torch.cuda.synchronize()
+    for x, y in zip(a, b):
+        assert torch.equal(x, y)
+    rc_o = oracle.rcut(g, lab.cpu().numpy(), k)[0]
+    assert abs(float(b[0].item()) - rc_o) <= 1e-12 * rc_o
+    x = torch.arange(10, dtype=torch.float64, device="cuda")
+    y = x.clone()
+    plp.allreduce_sum(coll, y)
+    torch.cuda.synchronize()
+    assert torch.equal(x, y)
+
+
+def test_device_tcg_on_collective_context(plp, ctxs):
+    """The unfused device tCG calls the collective entry points (plp_hessvec, plp_project, plp_dot):
+    on the one-rank communicator it gives bitwise the plain context's iterates."""
+    from paper_2605_26975_b200 import solver
+    plain, coll = ctxs
+    g = make_config("C2", n=4000)
+    k = 2
+    Z = torch.from_numpy(draw_U(g.n, k, 4)).cuda()
+    outs = []
+    for ctx, mk in ((plain, lambda c: plp.Graph(c, g.row_ptr, g.col, g.w)),
+                    (coll, lambda c: plp.DistGraph(c, g.n, 0, g.n, g.row_ptr, g.col, g.w))):
+        G = mk(ctx)
+        with torch.cuda.stream(ctx.stream):
+            U, tr = solver.continuation_solve(ctx, G, Z, [2.0, 1.5],
+                                              solver.SolverConfig(tcg_fused=False, tcg_graph=False))
+        outs.append((U, [r.tcg_iters for r in tr.records]))
+    assert outs[0][1] == outs[1][1]
+    assert torch.equal(outs[0][0], outs[1][0])

@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+for T in 224 120; do PLP_ORDER_TILE=$T python tools/prof_edge.py --reps 20 --events > gpurun_out/prof_r02g_T$T.log 2>&1; done
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_hessvec.py -q -x -p no:cacheprovider -k "C5t or D16t or C3t or hessvec" > gpurun_out/par_r02g.log 2>&1
+python tools/prof_edge.py --reps 3 > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k "regex:edge_halo_kernel" -s 1 -c 1 -o gpurun_out/prof_edge_r02g python tools/prof_edge.py --reps 3 > gpurun_out/ncu_full_r02g.log 2>&1
