@@ -2,7 +2,7 @@
 
 A step = one plp_fgrad_hessvec call (SURVEY.md §8(a) a7 = a2..a5 fused, sparse-mode Hessian) on
 the workload config (default C5: 8,388,608 uniform points in [0,1]^2, symmetrised 6-NN graph,
-Gaussian weights, k = 8, p = 1.2, tile order = RCM + BFS-grown tiles of the halo kernel's 224 rows), with A, B at U
+Gaussian weights, k = 8, p = 1.2, tile order = RCM + BFS-grown 120-row tiles), with A, B at U
 supplied from a preceding plp_fgrad
 (the trust-region rho-test always has them).  Inputs (CSR 0.71 GB + U, eta 1.07 GB)
 exceed the 126 MB L2, so no flush is needed between steps.
@@ -61,8 +61,8 @@ def get_graph(name: str, order: str):
     to save generation time between runs (regenerated when absent)."""
     from plp_inputs import make_config, Graph
     from paper_2605_26975_b200 import plp
-    from paper_2605_26975_b200.plp import HALO_TILE
-    tile = int(os.environ.get("PLP_ORDER_TILE", HALO_TILE))  # BFS tile of the ordering (experiments)
+    from paper_2605_26975_b200.plp import TILE_ROWS
+    tile = int(os.environ.get("PLP_ORDER_TILE", TILE_ROWS))  # BFS tile of the ordering (experiments)
     key = hashlib.sha1(f"{name}-{order}-{tile}-v5".encode()).hexdigest()[:12]
     cache = f"/tmp/plp_cache/{name}_{order}_{key}.npz"
     if os.path.exists(cache):
@@ -277,11 +277,12 @@ def run_plp(args, rank, world):
     n, nnz = g.n, g.nnz
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
-    ctx = plp.Context(args.local_rank, stream)
+    sharded = world > 1 or args.sharded
+    # multi-rank: the collective ABI (libplp's own NCCL communicator; torch broadcasts its id)
+    ctx = plp.Context.distributed(args.local_rank, stream) if sharded else plp.Context(args.local_rank, stream)
     U_h = draw_U(n, k, 0)
     eta_h = draw_eta(n, k, 0)
 
-    sharded = world > 1 or args.sharded
     if sharded:
         from paper_2605_26975_b200 import dist
         prob = dist.ShardedProblem(ctx, g, k, rank, world, device=dev)
@@ -442,17 +443,17 @@ def run_plp(args, rank, world):
 
     if sharded and not args.no_e2e:
         # each rank: its own rows of U, eta from pinned host memory in, its rows of G, Hv and F out
-        pl = prob.plan
-        U_p = torch.from_numpy(np.ascontiguousarray(U_h[pl.r0:pl.r1])).pin_memory()
-        E_p = torch.from_numpy(np.ascontiguousarray(eta_h[pl.r0:pl.r1])).pin_memory()
-        G_p = torch.empty(pl.n_loc, k, dtype=torch.float64).pin_memory()
-        H_p = torch.empty(pl.n_loc, k, dtype=torch.float64).pin_memory()
+        n_loc = prob.graph.n_rows
+        U_p = torch.from_numpy(np.ascontiguousarray(U_h[prob.r0:prob.r1])).pin_memory()
+        E_p = torch.from_numpy(np.ascontiguousarray(eta_h[prob.r0:prob.r1])).pin_memory()
+        G_p = torch.empty(n_loc, k, dtype=torch.float64).pin_memory()
+        H_p = torch.empty(n_loc, k, dtype=torch.float64).pin_memory()
         F_p = torch.empty(1, dtype=torch.float64).pin_memory()
         e_steps = max(3, min(args.steps, 10))
 
         def e2e_step():
-            prob.U_ext[:pl.n_loc].copy_(U_p, non_blocking=True)
-            prob.eta_ext[:pl.n_loc].copy_(E_p, non_blocking=True)
+            prob.U_ext[:n_loc].copy_(U_p, non_blocking=True)
+            prob.eta_ext[:n_loc].copy_(E_p, non_blocking=True)
             step()
             G_p.copy_(prob.G, non_blocking=True)
             H_p.copy_(prob.Hv, non_blocking=True)
@@ -476,9 +477,13 @@ def run_plp(args, rank, world):
                "ms_per_step": ems, "note": "bytes summed over ranks; time = max over ranks"}
 
     # ---- consistency: AB recomputed by the fused pass vs AB_in ----
+    variants = None
     if not sharded:
         d = (AB_out - AB_in).abs().max().item() / AB_in.abs().max().item()
         log(f"[bench] AB_out vs AB_in max rel diff {d:.2e}")
+        if not args.no_variants:
+            variants = measure_variants(args, ctx, stream, plp, G, U, eta, Fb, AB_out, Gr, Hv, n, nnz, k, p,
+                                        mode, eps, U_h, eta_h)
 
     if rank != 0:
         return
@@ -498,9 +503,47 @@ def run_plp(args, rank, world):
                       "l2": "inputs (1.8 GB) larger than the 126 MB L2; no flush",
                       "parallelism": f"row-blocks x{world}", "nnz_local_rank0": nnz_local},
            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
-           # per step: edge pass + finalize; sharded: + 2 halo packs (when a peer needs rows) + F
+           "variants": variants,
+           # per step: edge pass + finalize; collective: + F from the reduced A, B (+ 2 halo packs
+           # when a peer needs rows; NCCL's own kernels are not counted)
            "gpu_launches": args.steps * (2 if not sharded else 3 + (2 if world > 1 else 0))}
     print(json.dumps(out), flush=True)
+
+
+def measure_variants(args, ctx, stream, plp, G, U, eta, Fb, AB_out, Gr, Hv, n, nnz, k, p, mode, eps, U_h, eta_h):
+    """the same call with AB_in == NULL (objective pass first: two edge passes),
+    and the fused call on the generator-order numbering of the same graph (no locality ordering)."""
+    import torch
+
+    def timed(fn, reps):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    reps = max(3, min(args.steps, 10))
+    out = {}
+    ms = timed(lambda: plp.fgrad_hessvec_raw(ctx, G, k, U, eta, p, None, mode, eps, Fb, AB_out, Gr, Hv), reps)
+    out["ab_in_null"] = {"ms_per_step": ms, "value": nnz * k / (ms * 1e-3) / 1e9, "unit": "GNNZ*k/s",
+                         "note": "plp_fgrad_hessvec with AB_in == NULL: objective pass + fused pass"}
+    try:
+        g0 = get_graph_generator_order(args.config)
+        G0 = plp.Graph(ctx, g0.row_ptr, g0.col, g0.w, flags=0)
+        # the same random draws on the generator numbering (U, eta are iid: any labelling)
+        ms = timed(lambda: plp.fgrad_hessvec_raw(ctx, G0, k, U, eta, p, AB_out, mode, eps, Fb, AB_out, Gr, Hv), reps)
+        out["generator_order"] = {"ms_per_step": ms, "value": nnz * k / (ms * 1e-3) / 1e9, "unit": "GNNZ*k/s",
+                                  "kernel": plp.last_edge_kernel(),
+                                  "note": "the fused call on the graph in generator order (no RCM / tile ordering)"}
+        del G0
+    except Exception as e:  # pragma: no cover - informational only
+        out["generator_order"] = {"error": repr(e)[:200]}
+    return out
 
 
 def main():
@@ -514,9 +557,10 @@ def main():
     ap.add_argument("--mode", default="sparse", choices=["sparse", "full"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sharded", action="store_true",
-                    help="use the multi-GPU path (row blocks, halo exchange, NCCL all-reduce) even at one "
-                         "rank: exercises dist.ShardedProblem on a single GPU")
+                    help="use the collective path (plp_create_graph_dist, in-library NCCL halo exchange and "
+                         "all-reduce) even at one rank: exercises it on a single GPU")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-variants", action="store_true", help="skip the AB_in == NULL and generator-order timings")
     ap.add_argument("--cpu-frac", type=float, default=0.25)
     ap.add_argument("--ref-frac", type=float, default=1.0,
                     help="reference arm: fraction of the workload's rows per step (1.0: the whole workload)")

@@ -60,7 +60,7 @@ enum { PLP_HESS_SPARSE = 0, PLP_HESS_FULL = 1 };          /* reading #5 */
  * single-rank graph. */
 enum { PLP_U_HALO_CURRENT = 16 };
 enum { PLP_VALIDATE = 1u, PLP_VALIDATE_SYMMETRIC = 2u };  /* plp_create_graph flags */
-enum { PLP_TILE_ROWS = 120 };  /* rows per tile of the tiled edge kernel (plp_tile_order) */
+enum { PLP_TILE_ROWS = 120 };  /* default BFS tile of plp_tile_order */
 #ifndef PLP_HALO_TILE_ROWS
 #define PLP_HALO_TILE_ROWS 224
 #endif
@@ -71,8 +71,8 @@ typedef struct plp_graph plp_graph;
 
 const char* plp_last_error(void);
 const char* plp_version(void);
-/* Rows per tile of the halo-tile edge kernel (PLP_HALO_TILE).  Pass it as plp_tile_order's `tile`
- * so that the BFS-grown tiles of the ordering coincide with the kernel's tiles (smallest halos). */
+/* Rows per tile of the halo-tile edge kernel (PLP_HALO_TILE); multi-rank row blocks are aligned to
+ * it (paper_2605_26975_b200/dist.py).  plp_tile_order takes its own BFS tile size. */
 int plp_halo_tile_rows(void);
 
 /* ---------------------------------------------------------------------------------------------- */
@@ -117,8 +117,8 @@ plp_status plp_validate_csr(int64_t n_rows, int64_t n_cols, const int64_t* row_p
  * reversed.  Deterministic.  Used so that U_j gathers hit L2. */
 plp_status plp_rcm_order(int64_t n, const int64_t* row_ptr, const int32_t* col, int64_t* perm);
 /* Tile ordering for the halo-tile edge kernel: RCM sweep, then tiles of `tile`
- * nodes (pass plp_halo_tile_rows()) grown by BFS along the sweep, the nodes of a tile sorted by
- * decreasing degree.
+ * nodes (PLP_TILE_ROWS = 120 measured best with the 224-row halo-kernel tiles) grown by BFS along
+ * the sweep, the nodes of a tile sorted by decreasing degree.
  * perm[new] = old.  Relabel with plp_permute_csr; U and eta must then use the new order. */
 plp_status plp_tile_order(int64_t n, const int64_t* row_ptr, const int32_t* col, int tile,
                           int64_t* perm);

@@ -136,104 +136,6 @@ extern "C" plp_status plp_ctx_info(const plp_ctx* ctx, int* num_sms, int* max_ct
   return PLP_OK;
 }
 
-// Tiled representation for edge_tiled.cuh (see plp_graph): per tile of PLP_TILE_ROWS rows, every
-// internal undirected edge gets one slot (assigned at its upper row, shared by both directions)
-// and every external edge its own slot.  Tiling is skipped (the row kernel is used) if a tile
-// would overflow the 16-bit slot / offset fields.
-static plp_status build_tiles(plp_graph* g, const int64_t* rp, const int32_t* col) {
-  const int64_t n = g->n_rows;
-  const int T = PLP_TILE_ROWS;
-  // Tile boundaries: T rows, halved while the tile would exceed the slot / external / nnz caps
-  // that keep two CTAs per SM for k = 8 (kTileMax* in plp_internal.h).
-  std::vector<int32_t> trow{0};
-  for (int64_t r0 = 0; r0 < n;) {
-    int64_t r1 = std::min<int64_t>(n, r0 + T);
-    for (;;) {
-      int64_t ni = 0, ne = 0;
-      for (int64_t i = r0; i < r1; ++i)
-        for (int64_t e = rp[i]; e < rp[i + 1]; ++e) {
-          const int64_t j = col[e];
-          if (j >= r0 && j < r1) ni += (j > i);
-          else ++ne;
-        }
-      const int64_t nz = rp[r1] - rp[r0];
-      if ((ni + ne <= kTileMaxSlots && ne <= kTileMaxExt && nz <= kTileMaxNnz) || r1 - r0 == 1) break;
-      r1 = r0 + (r1 - r0) / 2;
-    }
-    trow.push_back((int32_t)r1);
-    r0 = r1;
-  }
-  const int64_t nt = (int64_t)trow.size() - 1;
-  std::vector<int32_t> enc((size_t)g->nnz + 16, 0);
-  std::vector<int32_t> slot_of((size_t)g->nnz, -1);
-  std::vector<int32_t> ext;
-  std::vector<int4> meta((size_t)nt + 1);
-  int max_slots = 0, max_nnz = 0, max_ext = 0;
-  for (int64_t t = 0; t < nt; ++t) {
-    const int64_t r0 = trow[t], r1 = trow[t + 1];
-    const int64_t e0 = rp[r0], e1 = rp[r1];
-    int n_int = 0, n_ext = 0;
-    const int ext_off = (int)ext.size();
-    for (int64_t i = r0; i < r1; ++i) {
-      for (int64_t e = rp[i]; e < rp[i + 1]; ++e) {
-        const int64_t j = col[e];
-        if (j >= r0 && j < r1) {
-          int s;
-          uint32_t lower = 0;
-          if (j > i) {
-            s = slot_of[e] = n_int++;
-          } else {  // partner (j, i) sits in the earlier row j
-            int64_t f = rp[j];
-            while (f < rp[j + 1] && col[f] != i) ++f;
-            if (f == rp[j + 1] || slot_of[f] < 0) return PLP_OK;  // not symmetric: no tiling
-            s = slot_of[f];
-            lower = 1;
-          }
-          enc[e] = (int32_t)((lower << 31) | ((uint32_t)(j - r0) << 16) | (uint32_t)s);
-        } else {
-          enc[e] = -1 - n_ext++;  // external: finalised below, once n_int is known
-          ext.push_back((int32_t)j);
-        }
-      }
-    }
-    if (n_int + n_ext >= 65536 || T + n_ext >= 32768 || e1 - e0 >= 65536) return PLP_OK;
-    for (int64_t e = e0; e < e1; ++e) {
-      const int64_t j = col[e];
-      if (!(j >= r0 && j < r1)) {  // external: eta row T + x of the tile table, slot n_int + x
-        const int x = -1 - enc[e];
-        enc[e] = (int32_t)(((uint32_t)(T + x) << 16) | (uint32_t)(n_int + x));
-      }
-    }
-    meta[t] = make_int4((int)e0, ext_off, n_int, n_ext);
-    max_slots = std::max(max_slots, n_int + n_ext);
-    max_ext = std::max(max_ext, n_ext);
-    max_nnz = std::max(max_nnz, (int)(e1 - e0));
-  }
-  meta[nt] = make_int4((int)g->nnz, (int)ext.size(), 0, 0);
-  ext.resize(ext.size() + 16, 0);
-  cudaError_t e;
-  if ((e = cudaMalloc(&g->enc, sizeof(int32_t) * enc.size())) != cudaSuccess ||
-      (e = cudaMalloc(&g->ext_col, sizeof(int32_t) * ext.size())) != cudaSuccess ||
-      (e = cudaMalloc(&g->tile_meta, sizeof(int4) * meta.size())) != cudaSuccess ||
-      (e = cudaMalloc(&g->tile_row, sizeof(int32_t) * trow.size())) != cudaSuccess ||
-      (e = cudaMemcpy(g->tile_row, trow.data(), sizeof(int32_t) * trow.size(), cudaMemcpyHostToDevice)) !=
-          cudaSuccess)
-    return cuda_check(e, "cudaMalloc(tiles)");
-  if ((e = cudaMemcpy(g->enc, enc.data(), sizeof(int32_t) * enc.size(), cudaMemcpyHostToDevice)) !=
-          cudaSuccess ||
-      (e = cudaMemcpy(g->ext_col, ext.data(), sizeof(int32_t) * ext.size(), cudaMemcpyHostToDevice)) !=
-          cudaSuccess ||
-      (e = cudaMemcpy(g->tile_meta, meta.data(), sizeof(int4) * meta.size(), cudaMemcpyHostToDevice)) !=
-          cudaSuccess)
-    return cuda_check(e, "cudaMemcpy(tiles)");
-  g->tiled = true;
-  g->n_tiles = nt;
-  g->max_slots = max_slots;
-  g->max_nnz = max_nnz;
-  g->max_ext = max_ext;
-  return PLP_OK;
-}
-
 // Halo tiles for edge_halo.cuh (see plp_graph): per tile of PLP_HALO_TILE consecutive rows its
 // sorted distinct outside columns, and per stored edge the tile-local neighbour index.  Skipped
 // (nullptr halo_enc) when a tile's buffers could not fit in shared memory even at k = 8.
@@ -400,8 +302,7 @@ extern "C" plp_status plp_create_graph(plp_ctx* ctx, int64_t n_rows, int64_t n_c
     plp_destroy_graph(g);
     return cuda_check(e, "cudaMemcpy(graph)");
   }
-  plp_status st = build_tiles(g, row_ptr, col);
-  if (!st) st = build_halo_tiles(g, row_ptr, col, w);
+  plp_status st = build_halo_tiles(g, row_ptr, col, w);
   if (st) {
     plp_destroy_graph(g);
     return st;
@@ -429,10 +330,6 @@ extern "C" plp_status plp_destroy_graph(plp_graph* g) {
   cudaFree(g->halo_ext);
   cudaFree(g->nlow);
   cudaFree(g->sched_up);
-  cudaFree(g->enc);
-  cudaFree(g->ext_col);
-  cudaFree(g->tile_meta);
-  cudaFree(g->tile_row);
   dist_destroy(g->dist);
   delete g;
   return PLP_OK;

@@ -245,17 +245,9 @@ static EdgeArgs graph_args(const plp_graph* g) {
   a.nlow = g->nlow;
   a.sched_up = g->sched_up;
   a.upper_ok = g->upper_ok ? 1 : 0;
-  if (const char* v = getenv("PLP_DEBUG_LDX")) a.ldx = atoi(v);  // layout experiments only
-  if (g->tiled) {
-    a.enc = g->enc;
-    a.ext_col = g->ext_col;
-    a.tile_meta = g->tile_meta;
-    a.tile_row = g->tile_row;
-    a.n_tiles = g->n_tiles;
-    a.max_slots = g->max_slots;
-    a.max_nnz = g->max_nnz;
-    a.max_ext = g->max_ext;
-  }
+#ifdef PLP_DEBUG_LDX
+  a.ldx = PLP_DEBUG_LDX;  // layout experiments only (compile-time)
+#endif
   return a;
 }
 

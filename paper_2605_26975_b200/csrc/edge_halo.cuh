@@ -78,53 +78,20 @@ constexpr unsigned kHaloSmemMax = 225u * 1024u / PLP_HALO_CTAS;
 #ifndef PLP_HALO_SLEEP_NS
 #define PLP_HALO_SLEEP_NS 64  // producer back-off between polls of the "empty" barrier
 #endif
-#ifndef PLP_HALO_CSLEEP_NS
-#define PLP_HALO_CSLEEP_NS 0  // > 0: consumers poll the "full" barrier with this back-off
-#endif
-#ifndef PLP_HALO_EB
-#define PLP_HALO_EB 2  // edges per straight-line batch in the halo kernel (2 or 4)
-#endif
-#ifndef PLP_HALO_L2PF
-#define PLP_HALO_L2PF 1  // producer L2-prefetches the next tile's streamed parts
-#endif
-#ifndef PLP_HALO_CPL8
-#define PLP_HALO_CPL8 2  // columns per lane at k = 8 (2 or 4)
-#endif
 template <int K>
-constexpr int halo_cpl() { return K == 8 ? PLP_HALO_CPL8 : K == 16 ? 4 : 2; }
+constexpr int halo_cpl() { return K == 16 ? 4 : 2; }  // columns per lane (k = 8: 4 measured slower)
 
 // OBJ: objective-only pass (no eta, no G) on a symmetric graph: A_l = sum over the upper-triangle
 // edges (j > i) of w_ij |u_il - u_jl|^p, i.e. Eq. (1)'s numerator with each undirected edge once
 // (half the powers of the row form); B_l from the node terms as usual.
-// Out-of-line row fallback of the plain (fused-pass) variant: the capped form from shared memory,
-// libdevice only for what it flags.  Not inlined, so the hot loop's code and registers are those of
-// the kernel without it; the call only happens for rows that left the fast domain.
-template <int CPL, int K, class POW, bool HAS_ETA>
-__device__ __noinline__ void halo_row_fallback(const POW& pw, const EdgeArgs& a, int e0, int e1, const int* enc_s,
-                                               const double* w_s, const double* tU, const double* tE, int c0,
-                                               const double (&ui)[CPL], const double (&ei)[CPL], double (&L)[CPL],
-                                               double (&HA)[CPL], double (&sn)[CPL], double (&tn)[CPL]) {
-  CapRange rg;
-#pragma unroll
-  for (int cc = 0; cc < CPL; ++cc) L[cc] = HA[cc] = 0.0;
-  for (int ee = e0; ee < e1; ++ee) {
-    const int x0 = enc_s[ee];
-    double uj0[CPL], ej0[CPL];
-    lds_vec<CPL>(tU + x0 * K, uj0);
-    if constexpr (HAS_ETA) lds_vec<CPL>(tE + x0 * K, ej0);
-    edge_update_capsel<CPL, POW, HAS_ETA>(pw, w_s[ee], ui, uj0, ei, ej0, L, HA, rg);
-  }
-  if (rg.bad()) edge_row_exact<CPL, POW, HAS_ETA>(pw, e0, e1, a.col, a.w, a.U, a.eta, K, c0, ui, ei, L, HA);
-#pragma unroll
-  for (int cc = 0; cc < CPL; ++cc) pw.eval(fabs(ui[cc]), sn[cc], tn[cc]);
-}
-
 // ADAPT: rows that leave the fast domain (mostly |d| < eps: the solver's degenerate regime, where
 // p-Laplacian iterates flatten on clusters) are recomputed from shared memory in the capped form,
 // and a warp whose previous pass needed it goes there directly; libdevice only for |d| < 2^-120 or
 // >= 2^120.  Off for the fused F/G/Hv pass (the benchmark unit; its random inputs rarely leave the
 // domain, and the plain loop keeps its code), which recomputes such rows with libdevice.
-template <int K, class POW, bool HAS_ETA, bool OBJ, int NB, bool ADAPT>
+// DOTS: also accumulate the full-mode dots alpha, gamma (a.want_dots; a template flag so that the
+// sparse passes carry no code for them).
+template <int K, class POW, bool HAS_ETA, bool OBJ, int NB, bool ADAPT, bool DOTS>
 __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(POW pw, EdgeArgs a) {
   static_assert(!(OBJ && HAS_ETA), "objective mode has no eta");
   constexpr int CPL = halo_cpl<K>(), LPR = K / CPL, RPW = 32 / LPR;  // rows per pass
@@ -233,11 +200,11 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
       if (lane == 0) fence_proxy_async();  // consumers' generic reads before the async refill
       __syncwarp();
       issue_tile(t, b, it % 3, (unsigned)(it / 3) & 1u);
+      if (lane == 0) issue_list(t + 2 * ts, (it + 2) % 3);
+      // warm L2 with the next tile's streamed parts (own rows, enc, w), so that its TMA copies,
+      // issued only once the consumers release a buffer, are L2 hits (per-row bulk prefetches of
+      // the halo rows too measured 1.6x slower: tiny bulk operations)
       if (lane == 0) {
-        issue_list(t + 2 * ts, (it + 2) % 3);
-#if PLP_HALO_L2PF
-        // warm L2 with the next tile's streamed parts (own rows, enc, w), so that its TMA copies,
-        // issued only once the consumers release a buffer, are L2 hits
         const int64_t tn = t + ts;
         if (tn < n_tiles) {
           const int qn = (it + 1) % 3;
@@ -250,7 +217,6 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
           l2_prefetch_range(a.halo_enc + Ln[1], (size_t)(Ln[2] - Ln[1]) * 4u);
           l2_prefetch_range(a.w + Ln[1], (size_t)(Ln[2] - Ln[1]) * 8u);
         }
-#endif
       }
       __syncwarp();
     }
@@ -259,23 +225,12 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
   // degree: the schedule sorts by degree); slices go to the consumer warps in snake order (warp w
   // takes slices w, 2C - 1 - w, 2C + w, ...), so every warp gets a heavy and a light slice.
   constexpr int NSL = kHaloT / RPW, C = kHaloCWarps;
-#ifndef PLP_HALO_PLAIN_FALLBACK_CAPPED
-#define PLP_HALO_PLAIN_FALLBACK_CAPPED 0  // 1: fused pass calls an out-of-line capped-form row fallback (measured: the call costs the hot loop 20 %)
-#endif
-#ifndef PLP_HALO_CAPSEL_ONLY
-#define PLP_HALO_CAPSEL_ONLY 0  // 1: adaptive passes always use the capped form (experiment)
-#endif
-  bool capmode = PLP_HALO_CAPSEL_ONLY;  // this warp's previous pass needed the capped form
+  bool capmode = false;  // this warp's previous row needed the capped form
   for (int it = 0;; ++it) {
     const int64_t t = t0 + (int64_t)it * ts;
     if (t >= n_tiles) break;
     const int b = it % NB;
-#if PLP_HALO_CSLEEP_NS > 0
-    if (!mbar_test(&full[b], (unsigned)(it / NB) & 1u))
-      mbar_wait_sleep(&full[b], (unsigned)(it / NB) & 1u, PLP_HALO_CSLEEP_NS);
-#else
     mbar_wait(&full[b], (unsigned)(it / NB) & 1u);  // tile t resident
-#endif
 
     const unsigned char* B = buf0 + (size_t)b * Ly.bytes;
     const int* rp_s = reinterpret_cast<const int*>(B + Ly.rp);
@@ -402,32 +357,11 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
 #pragma unroll
       for (int cc = 0; cc < CPL; ++cc) L[cc] = HA[cc] = 0.0;
 
-      // batches of EB edges as straight-line code (their dependency chains interleave), then the
-      // remainder two edges / one edge at a time; summation order stays the CSR order
+      // edge pairs as straight-line code (their dependency chains interleave), then the
+      // remaining edge; summation order stays the CSR order
       int e = (ADAPT && capmode) ? e1 : e0;  // capmode: the capped form below recomputes the row
-#if PLP_HALO_EB == 4
-#pragma unroll 1
-      for (; e + 3 < e1; e += 4) {
-        int x[4];
-        double wv[4], uj[4][CPL], ej[4][CPL];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          x[u] = enc_s[e + u];
-          wv[u] = w_s[e + u];
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          lds_vec<CPL>(tU + x[u] * K, uj[u]);
-          if constexpr (HAS_ETA) lds_vec<CPL>(tE + x[u] * K, ej[u]);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) edge_update_mx<CPL, POW, HAS_ETA>(pw, wv[u], ui, uj[u], ei, ej[u], L, HA, mx);
-      }
-      if (e + 1 < e1) {
-#else
 #pragma unroll 1
       for (; e + 1 < e1; e += 2) {
-#endif
         const int x0 = enc_s[e], x1 = enc_s[e + 1];
         const double w0 = w_s[e], w1 = w_s[e + 1];
         double uj0[CPL], ej0[CPL], uj1[CPL], ej1[CPL];
@@ -439,9 +373,6 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
         }
         edge_update_mx<CPL, POW, HAS_ETA>(pw, w0, ui, uj0, ei, ej0, L, HA, mx);
         edge_update_mx<CPL, POW, HAS_ETA>(pw, w1, ui, uj1, ei, ej1, L, HA, mx);
-#if PLP_HALO_EB == 4
-        e += 2;
-#endif
       }
       if (e < e1) {
         const int x0 = enc_s[e];
@@ -467,16 +398,11 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
         }
       }
       if constexpr (!POW::kIsP2 && !ADAPT) {
-#if PLP_HALO_PLAIN_FALLBACK_CAPPED
-        if (mx >= pw.fast_span2)  // rare: out of line, capped form, libdevice for what it flags
-          halo_row_fallback<CPL, K, POW, HAS_ETA>(pw, a, e0, e1, enc_s, w_s, tU, tE, c0, ui, ei, L, HA, sn, tn);
-#else
         if (mx >= pw.fast_span2) {  // rare: exact libdevice recomputation of the row
           edge_row_exact<CPL, POW, HAS_ETA>(pw, e0, e1, a.col, a.w, a.U, a.eta, K, c0, ui, ei, L, HA);
 #pragma unroll
           for (int cc = 0; cc < CPL; ++cc) pw.eval(fabs(ui[cc]), sn[cc], tn[cc]);
         }
-#endif
       }
       if constexpr (!POW::kIsP2 && ADAPT) {
         // capmode skipped the fast loop (mx then holds the node tests only)
@@ -515,7 +441,7 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
           fast_fails = fast_fails || rg.fast_fails(pw);
         }
         // the warp's next pass goes straight to the capped form iff the fast form failed here
-        if (!PLP_HALO_CAPSEL_ONLY) capmode = __any_sync(__activemask(), fast_fails);
+        capmode = __any_sync(__activemask(), fast_fails);
       }
       double g[CPL], hv[CPL];
 #pragma unroll
@@ -526,7 +452,7 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
         g[cc] = cG[cc] * (L[cc] - cAB[cc] * phi);
         if constexpr (HAS_ETA) {
           hv[cc] = cHA[cc] * HA[cc] - cHB[cc] * sn[cc] * ei[cc];
-          if (a.want_dots) {
+          if constexpr (DOTS) {
             accAl[cc] = fma(p * phi, ei[cc], accAl[cc]);
             accGa[cc] = fma(g[cc], ei[cc], accGa[cc]);
           }
@@ -574,15 +500,21 @@ plp_status launch_halo_shape(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int
   const int nb = deep ? NB3 : kHaloNBuf;
   // the fused F/G/Hv pass (G and eta) keeps the plain loop; every other pass adapts
   const bool adapt = !(HAS_ETA && a.G != nullptr);
-  auto kern = deep ? edge_halo_kernel<K, POW, HAS_ETA, OBJ, NB3, true>
-                   : (adapt ? edge_halo_kernel<K, POW, HAS_ETA, OBJ, kHaloNBuf, true>
-                            : edge_halo_kernel<K, POW, HAS_ETA, OBJ, kHaloNBuf, false>);
+  const bool dots = HAS_ETA && a.want_dots;
+  auto kern = deep ? edge_halo_kernel<K, POW, HAS_ETA, OBJ, NB3, true, false>
+                   : (adapt ? (dots ? edge_halo_kernel<K, POW, HAS_ETA, OBJ, kHaloNBuf, true, HAS_ETA>
+                                    : edge_halo_kernel<K, POW, HAS_ETA, OBJ, kHaloNBuf, true, false>)
+                            : (dots ? edge_halo_kernel<K, POW, HAS_ETA, OBJ, kHaloNBuf, false, HAS_ETA>
+                                    : edge_halo_kernel<K, POW, HAS_ETA, OBJ, kHaloNBuf, false, false>));
   const unsigned smem = halo_smem_bytes(K, a.halo_ext_cap, a.halo_nnz_cap, POW::kNeedsTables, OBJ, HAS_ETA, nb);
-  static unsigned attr_set[3] = {0, 0, 0};
-  const int vi = deep ? 2 : adapt ? 1 : 0;
-  if (attr_set[vi] < smem) {
+  // the dynamic shared-memory opt-in is a per-device function attribute: set it on this ctx's
+  // device whenever a launch needs more than the value set so far (per template instance)
+  static unsigned attr_set[64][5] = {};
+  const int vi = deep ? 4 : (adapt ? 1 : 0) + (dots ? 2 : 0);
+  unsigned& set_to = attr_set[ctx->device & 63][vi];
+  if (set_to < smem) {
     PLP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_set[vi] = smem;
+    set_to = smem;
   }
   const int64_t n_tiles = (a.n_rows + kHaloT - 1) / kHaloT;
   int64_t grid = (int64_t)ctx->num_sms * PLP_HALO_CTAS;

@@ -1,7 +1,7 @@
 // Instantiation unit of the fused edge kernel, full-mode epilogue and power diagnostic for the
 // power policy PowR10M3 (see pow64.cuh, edge_kernel.cuh, edge_inst.cuh).
 #include "edge_inst.cuh"
-#include "edge_tiled.cuh"
+#include "edge_dispatch.cuh"
 
 namespace plp {
 plp_status launch_edge_pol(plp_ctx* ctx, const EdgeArgs& a, const PowR10M3& pw, int* grid) {

@@ -424,8 +424,10 @@ plp_status launch_staged_shape(plp_ctx* ctx, const EdgeArgs& a0, const POW& pw, 
   if (a.ldx == 0) a.ldx = a.k;
   a.chunk_cap = staged_cap(a.max_chunk_nnz, POW::kNeedsTables, CPL);
   const unsigned smem = staged_smem_bytes(a.chunk_cap, POW::kNeedsTables, CPL);
-  static unsigned attr_set = 0;  // per instantiation
-  static int occ = 1;
+  static unsigned attr_set_d[64] = {};  // per instantiation and device (the opt-in is per device)
+  static int occ_d[64] = {};
+  unsigned& attr_set = attr_set_d[ctx->device & 63];
+  int& occ = occ_d[ctx->device & 63];
   if (attr_set < smem) {
     PLP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_set = smem;

@@ -42,8 +42,6 @@ struct plp_ctx {
   // single-rank context created without an id)
   int rank = 0, world = 1;
   void* comm = nullptr;
-  // kernel attributes set on this ctx's device (cudaFuncSetAttribute is per device)
-  unsigned halo_smem_attr[3] = {0, 0, 0};
 };
 
 // Halo plan of a graph created by plp_create_graph_dist (comm.cu): this rank owns global rows
@@ -66,23 +64,6 @@ struct plp_graph {
   int32_t* col = nullptr;    // device int32 col[nnz]
   double* w = nullptr;       // device fp64 w[nnz]
   int32_t* sched = nullptr;  // device row schedule: rows sorted by degree within windows
-  // Tiled representation (edge_tiled.cuh): tiles of PLP_TILE_ROWS consecutive rows.
-  //   enc[e] = flip << 31 | erow << 16 | slot, with
-  //     internal edge (both ends in the tile): erow = j - r0, slot = the undirected edge's slot,
-  //                                           flip = 1 at the lower row (j < i)
-  //     external edge:                         erow = T + x, slot = n_int + x (x-th external
-  //                                           edge of the tile), flip = 0
-  //   ext_col[ext_off + x]: global column of the tile's x-th external edge;
-  //   tile_meta = (e0, ext_off, n_int, n_ext), one sentinel entry at n_tiles
-  bool tiled = false;
-  int32_t* enc = nullptr;
-  int32_t* ext_col = nullptr;
-  int4* tile_meta = nullptr;
-  int32_t* tile_row = nullptr;  // first row of each tile (n_tiles + 1 entries)
-  int64_t n_tiles = 0;
-  int max_slots = 0;  // max over tiles of n_int + n_ext
-  int max_nnz = 0;    // max over tiles of the tile's nnz
-  int max_ext = 0;    // max over tiles of n_ext
   int max_chunk_nnz = 0;  // max nnz over chunks of kSchedWindow rows (staged kernel ring slots)
   // Halo tiles (edge_halo.cuh): tiles of PLP_HALO_TILE rows; per stored edge the tile-local index
   // (j - r0 inside the tile, PLP_HALO_TILE + x for the x-th halo row); per tile a slot of
@@ -102,10 +83,6 @@ struct plp_graph {
 // rows per degree-sorting window: small enough that a CTA's rows per iteration stay contiguous
 // (neighbour rows of a tile-ordered graph then hit L1)
 constexpr int kSchedWindow = 32;
-// Per-tile caps of the tiled kernel (a tile of PLP_TILE_ROWS rows is halved until it fits): with
-// k = 8 they keep the tile's shared memory under ~110 KB, i.e. two CTAs per SM.
-constexpr int kTileMaxSlots = 536, kTileMaxExt = 192, kTileMaxNnz = 992;
-
 namespace plp {
 
 plp_status set_error(plp_status st, const char* fmt, ...);
@@ -151,13 +128,6 @@ struct EdgeArgs {
   double p, eps;
   double* partials;     // [grid][4][k]: A, B, alpha, gamma partial sums
   int want_dots;
-  // tiled representation (nullptr enc: use the row kernel)
-  const int32_t* enc;
-  const int32_t* ext_col;
-  const int4* tile_meta;
-  const int32_t* tile_row;
-  int64_t n_tiles;
-  int max_slots, max_nnz, max_ext;
   // staged kernel (edge_staged.cuh): largest chunk nnz of the graph, ring slot capacity
   int max_chunk_nnz, chunk_cap;
   int ldx;  // row stride (elements) of U and eta in the staged kernel; 0 = k (contiguous)

@@ -20,9 +20,6 @@
 // libdevice (edge_kernel.cuh), so every input follows the definitions.  The cap test runs on the
 // integer pipe: for non-negative doubles the bit patterns order like the values.
 #pragma once
-#ifndef PLP_POW_F2F
-#define PLP_POW_F2F 0  // seed float -> double by F2F instead of integer bit assembly
-#endif
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -182,11 +179,7 @@ struct PowRoot : PowCapped<PowRoot<D, M>> {
     float yf;
     if constexpr (D == 2) yf = rsqrt_approx(xf);
     else yf = ex2_approx(lg2_approx(xf) * (-1.0f / (float)D));
-#if PLP_POW_F2F
-    const double y0 = (double)yf;  // F2F.F64.F32 (one instruction on the conversion path)
-#else
-    const double y0 = f2d_exact(yf);  // two integer instructions
-#endif
+    const double y0 = f2d_exact(yf);  // two integer instructions (F2F measured slower)
     double yD, yM;
     root_powers<D, M>(y0, yD, yM);
     const double e = fma(-fabs(d), yD, 1.0);  // 1 - x y0^D

@@ -656,6 +656,11 @@ extern "C" plp_status plp_tcg_run(plp_ctx* ctx, const plp_graph* g, int k, const
   if (!fused && !Heta) return set_error(PLP_ERR_ARG, "Heta may be NULL only with fused = 1");
   if (fused && !(al16(U) && al16(eta) && (!Heta || al16(Heta)) && al16(r) && al16(dlt) && al16(Hd)))
     return set_error(PLP_ERR_ARG, "fused tCG needs 16-byte aligned vectors");
+  if (fused && ctx->comm && g->dist && ctx->world > 1)
+    return set_error(PLP_ERR_ARG, "fused tCG is single-rank (its reductions are CTA tickets): use fused = 0");
+  // on a multi-rank graph U's halo rows are current (the plp_fgrad at this iterate exchanged them):
+  // each Hessian-vector product exchanges only the direction's halo
+  if (ctx->comm && g->dist) mode |= PLP_U_HALO_CURRENT;
   const int grid = axpby_grid(ctx, total);
   plp_status st;
   if (fused) {

@@ -87,16 +87,21 @@ class SolveTrace:
 
 
 class _State:
-    """Device state at the current iterate: U, F, AB, G, grad = P(G), S = sym(U^T G)."""
+    """Device state at the current iterate: U, F, AB, G, grad = P(G), S = sym(U^T G).
+
+    On a multi-rank graph (plp.DistGraph) U has n_cols = n_own + n_halo rows (plp_fgrad fills the
+    halo rows); every other vector has the n_own owned rows, and the Grams / dots / projections are
+    collective (global) in libplp."""
 
     def __init__(self, solver: "GrassmannTR", U, p: float):
         s = solver
         self.U = U
+        Uo = s.own(U)
         self.F, self.AB, self.G = plp.fgrad(s.ctx, s.g, U, p)
-        self.grad = plp.project(s.ctx, U, self.G)
+        self.grad = plp.project(s.ctx, Uo, self.G)
         # S = sym(U^T G) = (U^T G + G^T U) / 2, two Grams and an axpby in libplp
-        self.S = plp.gram(s.ctx, U, self.G)
-        plp.axpby(s.ctx, 0.5, plp.gram(s.ctx, self.G, U), 0.5, self.S)
+        self.S = plp.gram(s.ctx, Uo, self.G)
+        plp.axpby(s.ctx, 0.5, plp.gram(s.ctx, self.G, Uo), 0.5, self.S)
         self.Fv = float(self.F.item())
 
 
@@ -105,16 +110,38 @@ class GrassmannTR:
 
     def __init__(self, ctx: plp.Context, g: plp.Graph, k: int, cfg: SolverConfig | None = None):
         self.ctx, self.g, self.k = ctx, g, k
-        self.cfg = (cfg or SolverConfig()).resolved(g.n_rows, k)
+        # multi-rank (a DistGraph on a context with peers): global sizes for the defaults, the
+        # unfused device tCG (its reductions go through the collective plp_dot / plp_project),
+        # no CUDA-graph capture of the NCCL calls
+        self.n_own, self.n_cols = g.n_rows, g.n_cols
+        self.multi = isinstance(g, plp.DistGraph) and ctx.world > 1
+        n_glob = g.n_global if isinstance(g, plp.DistGraph) else g.n_rows
+        cfg = cfg or SolverConfig()
+        if self.multi:
+            cfg = SolverConfig(**{**cfg.__dict__, "tcg_fused": False, "tcg_graph": False})
+        self.cfg = cfg.resolved(n_glob, k)
+        self.hmode = self.cfg.hessian_mode | (plp.U_HALO_CURRENT if isinstance(g, plp.DistGraph) else 0)
+
+    def own(self, X):
+        """The owned rows of an n_cols-row array (a view)."""
+        return X[:self.n_own] if X.shape[0] != self.n_own else X
+
+    def ext(self, X):
+        """An n_cols-row copy of an owned-row array (halo rows to be filled by libplp)."""
+        if X.shape[0] == self.n_cols:
+            return X
+        Y = torch.zeros(self.n_cols, X.shape[1], dtype=X.dtype, device=X.device)
+        Y[:self.n_own] = X
+        return Y
 
     # -- operators --------------------------------------------------------------------------------
     def _hess(self, st: _State, p: float, xi):
         """H(xi) = P(EucHess[xi]) - xi S."""
         c = self.cfg
-        EH = plp.hessvec(self.ctx, self.g, st.U, xi, p, st.AB, mode=c.hessian_mode, eps=c.eps,
+        EH = plp.hessvec(self.ctx, self.g, st.U, self.ext(xi), p, st.AB, mode=self.hmode, eps=c.eps,
                          G_in=st.G if c.hessian_mode == plp.HESS_FULL else None)
-        PEH = plp.project(self.ctx, st.U, EH, out=EH)
-        return plp.apply_sub(self.ctx, xi, st.S, PEH, out=PEH)
+        PEH = plp.project(self.ctx, self.own(st.U), EH, out=EH)
+        return plp.apply_sub(self.ctx, self.own(xi), st.S, PEH, out=PEH)
 
     def _dot(self, x, y) -> float:
         return float(plp.dot(self.ctx, x, y).item())
@@ -127,13 +154,15 @@ class GrassmannTR:
         if not hasattr(self, "_tcg_buf") or self._tcg_buf[0].shape != st.grad.shape:
             z = lambda: torch.empty_like(st.grad)  # noqa: E731
             self._graphs, self._gin = {}, None
-            self._tcg_buf = (z(), z(), z(), z(), z(),
+            # the direction is a Hessian-vector input: n_cols rows (halo slots on a DistGraph)
+            dl = torch.zeros(self.n_cols, st.grad.shape[1], dtype=st.grad.dtype, device=st.grad.device)
+            self._tcg_buf = (z(), z(), z(), dl, z(),
                              torch.zeros(plp.TCG_SCAL_LEN, dtype=torch.float64, device=st.grad.device),
                              torch.zeros(2, dtype=torch.int32, device=st.grad.device))
         eta, Heta, r, dlt, Hd, scal, status = self._tcg_buf
         # fused: no H step accumulated per iteration (16 n k bytes less per pass); H(eta) once at the end
         Hacc = None if c.tcg_fused else Heta
-        plp.tcg_init(ctx, st.grad, delta, c.tcg_kappa, c.tcg_theta, eta, Hacc, r, dlt, scal, status)
+        plp.tcg_init(ctx, st.grad, delta, c.tcg_kappa, c.tcg_theta, eta, Hacc, r, self.own(dlt), scal, status)
         full = c.hessian_mode == plp.HESS_FULL
         use_graph = c.tcg_graph and ctx.stream.cuda_stream != 0
         if use_graph:
@@ -195,14 +224,15 @@ class GrassmannTR:
         r0 = math.sqrt(z_r)
         if r0 == 0.0:
             return eta, Heta, 0, "interior"
-        dlt = torch.zeros_like(r)
+        dlt_ext = torch.zeros(self.n_cols, r.shape[1], dtype=r.dtype, device=r.device)
+        dlt = self.own(dlt_ext)  # view: the owned rows of the Hessian-vector input
         plp.axpby(ctx, -1.0, r, 0.0, dlt)  # dlt = -r
         e_Pe, e_Pd, d_Pd = 0.0, 0.0, z_r
         stop_tol = r0 * min(r0 ** c.tcg_theta, c.tcg_kappa)
         status = "maxiter"
         j = 0
         for j in range(1, c.tcg_max_iters + 1):
-            Hd = self._hess(st, p, dlt)
+            Hd = self._hess(st, p, dlt_ext)
             d_Hd = self._dot(dlt, Hd)
             alpha = z_r / d_Hd if d_Hd != 0.0 else math.inf
             e_Pe_new = e_Pe + 2.0 * alpha * e_Pd + alpha * alpha * d_Pd
@@ -216,7 +246,7 @@ class GrassmannTR:
             plp.axpby(ctx, alpha, dlt, 1.0, eta)
             plp.axpby(ctx, alpha, Hd, 1.0, Heta)
             plp.axpby(ctx, alpha, Hd, 1.0, r)
-            r = plp.project(ctx, st.U, r, out=r)  # keep the residual horizontal
+            r = plp.project(ctx, self.own(st.U), r, out=r)  # keep the residual horizontal
             z_new = self._dot(r, r)
             if math.sqrt(z_new) <= stop_tol:
                 status = "converged"
@@ -256,7 +286,7 @@ class GrassmannTR:
                 eta, Heta, nit, status = self.tcg(st, p, delta)
             model_dec = -self._dot(st.grad, eta) - 0.5 * self._dot(eta, Heta)
             try:
-                U_new = plp.retract(ctx, st.U, eta)
+                U_new = self.ext(plp.retract(ctx, self.own(st.U), eta))
                 cand = _State(self, U_new, p)
                 F_new = cand.Fv
             except plp.PlpError:  # rank-deficient U + eta: a rejected step
@@ -284,20 +314,49 @@ def init_embedding(ctx: plp.Context, Z) -> torch.Tensor:
 
 def continuation_solve(ctx: plp.Context, g: plp.Graph, Z, schedule, cfg: SolverConfig | None = None):
     """Solve at p = schedule[0] (= 2) from QR(Z), then warm-start each smaller p from the previous
-    solution after QR re-orthonormalisation (reading #23)."""
+    solution after QR re-orthonormalisation (reading #23).  On a multi-rank graph
+    every rank passes its own rows of Z and gets its own rows of U back (the QR is collective)."""
     k = Z.shape[1]
     tr = GrassmannTR(ctx, g, k, cfg)
     trace = SolveTrace()
-    U = init_embedding(ctx, Z)
+    U = tr.ext(init_embedding(ctx, tr.own(Z)))
     for j, p in enumerate(schedule):
         if j > 0:
-            U = plp.retract(ctx, U, torch.zeros_like(U))
+            Uo = tr.own(U)
+            U = tr.ext(plp.retract(ctx, Uo, torch.zeros_like(Uo)))
         U, trace = tr.solve(U, float(p), trace)
-    return U, trace
+    return tr.own(U), trace
+
+
+def _allgather_rows(X, group=None):
+    """All ranks' owned rows of X, in rank order (= global row order of the contiguous blocks)."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    n = torch.tensor([X.shape[0]], dtype=torch.int64, device=X.device)
+    ns = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(ns, n, group=group)
+    m = int(max(int(v.item()) for v in ns))
+    pad = torch.zeros(m, *X.shape[1:], dtype=X.dtype, device=X.device)
+    pad[:X.shape[0]] = X
+    parts = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad, group=group)
+    return torch.cat([pt[:int(v.item())] for pt, v in zip(parts, ns)])
 
 
 def cluster(ctx: plp.Context, g: plp.Graph, U, k: int, uniforms, restarts: int = 10):
-    """Discretisation: k-means on the rows of U, then RCut of the labels."""
+    """Discretisation: k-means on the rows of U, then RCut of the labels.
+
+    Multi-rank: the n x k embedding is gathered on every rank (NCCL all-gather; 0.5 GB at C5, a
+    millisecond over NVLink) and k-means runs on the whole embedding on each GPU (identical input,
+    identical labels: the same seeding uniforms and deterministic kernels); each rank keeps its
+    own rows' labels (+ halo slots) and RCut is collective (plp_rcut)."""
+    if isinstance(g, plp.DistGraph) and ctx.world > 1:
+        Ua = _allgather_rows(U[:g.n_rows].contiguous())
+        lab_all, centroids, sse, _ = plp.kmeans(ctx, Ua, k, uniforms, restarts=restarts)
+        labels = torch.zeros(g.n_cols, dtype=torch.int32, device=U.device)
+        labels[:g.n_rows] = lab_all[g.row_begin:g.row_end]
+        rc, cut, sizes = plp.rcut(ctx, g, k, labels)
+        return labels[:g.n_rows], float(rc.item()), sse
     labels, centroids, sse, _ = plp.kmeans(ctx, U, k, uniforms, restarts=restarts)
     rc, cut, sizes = plp.rcut(ctx, g, k, labels)
     return labels, float(rc.item()), sse

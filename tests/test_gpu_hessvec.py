@@ -59,10 +59,12 @@ def degenerate_U(g, k, seed, noise=1e-12, zero_rows=True, half=True):
     return U
 
 
-def assert_adaptive_path(kern, k):
-    """k = 4, 8: the halo kernel's adaptive variant; k = 16 tiles of these graphs may not fit in
-    shared memory, then the staged kernel (libdevice row recompute) runs."""
-    ok = kern.startswith("edge_halo_kernel[adapt]") or (k == 16 and kern.startswith("edge_staged_kernel"))
+def assert_adaptive_path(kern, k, name=""):
+    """k = 4, 8: the halo kernel's adaptive variant.  Where a tile's halo does not fit in shared
+    memory (k = 16 tiles; C3's 3-D grid with random long-range edges has tiles with ~1000 halo
+    rows) the staged kernel (libdevice row recompute) runs instead."""
+    ok = kern.startswith("edge_halo_kernel[adapt]") or \
+        ((k == 16 or name.startswith("C3")) and kern.startswith("edge_staged_kernel"))
     assert ok, kern
 
 
@@ -93,7 +95,7 @@ def test_hessvec_tile_ordered_random(plp, ctx, name, k, p, mode):
     g = tgraph(name)
     U, eta = draw_U(g.n, k, 12), draw_eta(g.n, k, 12)
     Hv, AB, kern = gpu_hessvec(plp, ctx, g, U, eta, p, mode, 1e-9)
-    assert_adaptive_path(kern, k)
+    assert_adaptive_path(kern, k, name)
     ref, A, B = oracle_hessvec(g, U, eta, p, mode, 1e-9)
     assert colwise_relerr(AB[:k], A) < TOL and colwise_relerr(AB[k:], B) < TOL
     e = colwise_relerr(Hv, ref)
@@ -112,7 +114,7 @@ def test_hessvec_degenerate_regime(plp, ctx, name, k, p, mode, eps):
     U = degenerate_U(g, k, 5)
     eta = draw_eta(g.n, k, 5)
     Hv, AB, kern = gpu_hessvec(plp, ctx, g, U, eta, p, mode, eps)
-    assert_adaptive_path(kern, k)
+    assert_adaptive_path(kern, k, name)
     ref, A, B = oracle_hessvec(g, U, eta, p, mode, eps)
     assert colwise_relerr(AB[:k], A) < TOL and colwise_relerr(AB[k:], B) < TOL
     e = colwise_relerr(Hv, ref)

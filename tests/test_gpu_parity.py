@@ -102,7 +102,7 @@ CASES = [
     # odd and extreme k
     ("C1", 1, 1.5), ("C1", 5, 1.2), ("C1", 7, 1.1), ("C1", 16, 1.5), ("C1", 32, 1.2),
     ("C1", 31, 2.0), ("C1", 12, 1.8), ("P5", 2, 1.5), ("K2", 1, 1.2), ("iso", 3, 1.5),
-    # tile-ordered graphs (tiled kernel: internal edges from shared memory, one power each)
+    # tile-ordered graphs (halo kernel: every neighbour row from shared memory)
     ("C5t", 8, 1.2), ("C5t", 8, 2.0), ("C5t", 8, 1.37), ("C5t", 8, 1.5), ("C5t", 4, 1.1),
     ("C5t", 16, 1.8), ("C3t", 8, 1.5), ("C2t", 2, 1.1), ("iso", 4, 1.2), ("C1", 20, 1.2),
     # the paper's workload shape: Delaunay graph of 2^16 uniform points (NEXT-3), tile order
@@ -143,7 +143,7 @@ def test_ab_in_null_runs_objective_first(plp, ctx):
 def test_ties_zeros_and_cap(plp, ctx, p, eps, name, k):
     """Exact ties u_i = u_j and exact zeros u_i = 0 (reading #6): the cap decision is taken on the
     same IEEE |u_i - u_j| on both sides; eps = 0.3 puts many edges below the cap.  k = 3 runs the
-    row kernel, k = 4 on a tile-ordered graph the tiled kernel."""
+    row kernel, k = 4 on a tile-ordered graph the halo kernel."""
     g = graph(name)
     rng = streams(8)[1]
     U = np.round(rng.standard_normal((g.n, k)) * 2.0) / 4.0  # many ties and zeros
@@ -167,15 +167,14 @@ def test_out_of_fast_domain_differences(plp, ctx):
         check(res, g, U, eta, 1.5, 0, 1e-300)
 
 
-ALT_KERNELS = {"tiled": "PLP_EDGE_TILED", "rows": "PLP_EDGE_ROWS", "staged": "PLP_EDGE_STAGED"}
+ALT_KERNELS = {"rows": "PLP_EDGE_ROWS", "staged": "PLP_EDGE_STAGED"}
 
 
 @pytest.mark.parametrize("kernel", sorted(ALT_KERNELS))
 def test_parity_suite_with_alternative_kernel(kernel):
-    """Re-runs this module's oracle-parity cases in a subprocess with the tiled kernel
-    (PLP_EDGE_TILED=1, edge_tiled.cuh) or the unstaged row kernel (PLP_EDGE_ROWS=1,
-    edge_kernel.cuh), so every edge kernel, not only the default staged one, is held to the
-    oracle."""
+    """Re-runs this module's oracle-parity cases in a subprocess with the staged kernel forced
+    (PLP_EDGE_STAGED=1, edge_staged.cuh) or the unstaged row kernel (PLP_EDGE_ROWS=1,
+    edge_kernel.cuh), so every edge kernel, not only the default one, is held to the oracle."""
     if any(os.environ.get(v) for v in ALT_KERNELS.values()):
         pytest.skip("already an alternative-kernel run")
     env = dict(os.environ, **{ALT_KERNELS[kernel]: "1"})
@@ -189,8 +188,8 @@ def test_parity_suite_with_alternative_kernel(kernel):
 
 @pytest.mark.parametrize("kernel", sorted(ALT_KERNELS))
 def test_default_and_alternative_kernels_agree(plp, ctx, tmp_path, kernel):
-    """The same call with the default (staged) kernel and, in a subprocess, with the tiled or
-    the unstaged row kernel: within 1e-12 of each other (summation association only)."""
+    """The same call with the default (halo) kernel and, in a subprocess, with the staged or the
+    unstaged row kernel: within 1e-12 of each other (summation association only)."""
     if any(os.environ.get(v) for v in ALT_KERNELS.values()):
         pytest.skip("already an alternative-kernel run")
     g = graph("C5t")

@@ -15,26 +15,15 @@ sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "paper_2605_26975_b200", "variants")
 
 VARIANTS = {
-    "h_c2": ["-DPLP_HALO_CPL8=2"],
-    "h_c4": ["-DPLP_HALO_CPL8=4"],
+    "t224b3": ["-DPLP_HALO_TILE_ROWS=224", "-DPLP_HALO_NBUF=3"],
     "t192b3": ["-DPLP_HALO_TILE_ROWS=192", "-DPLP_HALO_NBUF=3"],
     "t160b3": ["-DPLP_HALO_TILE_ROWS=160", "-DPLP_HALO_NBUF=3"],
     "t128b4": ["-DPLP_HALO_TILE_ROWS=128", "-DPLP_HALO_NBUF=4"],
-    "t224b3": ["-DPLP_HALO_TILE_ROWS=224", "-DPLP_HALO_NBUF=3"],
-    "t96c2": ["-DPLP_HALO_TILE_ROWS=96", "-DPLP_HALO_CTAS=2"],
     "t128c2": ["-DPLP_HALO_TILE_ROWS=128", "-DPLP_HALO_CTAS=2"],
-    "cs32": ["-DPLP_HALO_CSLEEP_NS=32"],
-    "cs100": ["-DPLP_HALO_CSLEEP_NS=100"],
-    # full builds (all k): staged-kernel occupancy for the random-graph configs (C4, k = 20)
-    "full_minb2": ["FULL"],
-    "full_minb3": ["FULL", "-DPLP_EDGE_MINB=3"],
-    "full_minb4": ["FULL", "-DPLP_EDGE_MINB=4"],
-    "full_nbuf3": ["FULL", "-DPLP_HALO_NBUF=3"],
-    "full_capsel": ["FULL", "-DPLP_HALO_CAPSEL_ONLY=1"],
-    "eb4": ["-DPLP_HALO_EB=4"],
     "sleep0": ["-DPLP_HALO_SLEEP_NS=0"],
     "sleep256": ["-DPLP_HALO_SLEEP_NS=256"],
-    "nol2pf": ["-DPLP_HALO_L2PF=0"],
+    # full builds (all k): staged-kernel occupancy for the random-graph configs (C4, k = 20)
+    "full_minb3": ["FULL", "-DPLP_EDGE_MINB=3"],
 }
 
 
