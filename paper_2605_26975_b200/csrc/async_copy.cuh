@@ -1,6 +1,22 @@
 // Shared-memory / asynchronous-copy helpers for sm_100a: mbarriers, TMA bulk copies
 // (cp.async.bulk, SASS UBLKCP), L2 bulk prefetch and Ampere-style cp.async (LDGSTS).
 #pragma once
+#include <cstdio>
+// Device-side bounds / protocol checks of a debug build (-DPLP_DEBUG_CHECKS; tools/tune_edge.py
+// variant `checked`): compute-sanitizer is unavailable on the GPU pool, so the kernels' shared-
+// memory indexing and copy sizes are asserted in-kernel instead.  Free in the product build.
+#ifdef PLP_DEBUG_CHECKS
+#define PLP_DCHECK(cond, what)                                                                  \
+  do {                                                                                          \
+    if (!(cond)) {                                                                              \
+      printf("PLP_DCHECK failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, __LINE__,     \
+             (int)blockIdx.x, (int)threadIdx.x);                                                \
+      __trap();                                                                                 \
+    }                                                                                           \
+  } while (0)
+#else
+#define PLP_DCHECK(cond, what) do {} while (0)
+#endif
 #include <cstdint>
 
 namespace plp {

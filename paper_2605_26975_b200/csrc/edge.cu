@@ -233,6 +233,7 @@ using namespace plp;
 static EdgeArgs graph_args(const plp_graph* g) {
   EdgeArgs a{};
   a.n_rows = g->n_rows;
+  a.n_cols = g->n_cols;
   a.rp = g->rp;
   a.sched = g->sched;
   a.col = g->col;

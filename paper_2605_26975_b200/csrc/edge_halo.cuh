@@ -89,6 +89,21 @@ constexpr int halo_cpl() { return K == 16 ? 4 : 2; }  // columns per lane (k = 8
 // and a warp whose previous pass needed it goes there directly; libdevice only for |d| < 2^-120 or
 // >= 2^120.  Off for the fused F/G/Hv pass (the benchmark unit; its random inputs rarely leave the
 // domain, and the plain loop keeps its code), which recomputes such rows with libdevice.
+#ifdef PLP_HALO_TRACE
+// Pipeline trace (tools/trace_halo.py; a build flag, never in the product build): clock64 per tile
+// iteration: [0] producer past the "empty" wait, [1] producer done issuing, [2 + w] consumer warp w
+// past the "full" wait, [16 + w] consumer warp w released the buffer.
+constexpr int kTraceTiles = 320, kTraceSlots = 32;
+static __device__ long long g_halo_trace[160 * kTraceTiles * kTraceSlots];
+#define PLP_TRACE(it, slot)                                                                         \
+  do {                                                                                              \
+    if ((it) < kTraceTiles && blockIdx.x < 160)                                                     \
+      g_halo_trace[((int64_t)blockIdx.x * kTraceTiles + (it)) * kTraceSlots + (slot)] = clock64();  \
+  } while (0)
+#else
+#define PLP_TRACE(it, slot) do {} while (0)
+#endif
+
 // DOTS: also accumulate the full-mode dots alpha, gamma (a.want_dots; a template flag so that the
 // sparse passes carry no code for them).
 template <int K, class POW, bool HAS_ETA, bool OBJ, int NB, bool ADAPT, bool DOTS>
@@ -151,8 +166,11 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
     mbar_wait(&lbar[q], lph);
     const int* Lq = lists + q * LS;
     const int nx = Lq[0];
+    PLP_DCHECK(nx >= 0 && nx <= ext_cap, "halo count within the tile's list slot");
     if (lane == 0) {
       const int eb = Lq[1], ee = Lq[2];
+      PLP_DCHECK(ee - eb >= 0 && ee - eb <= a.halo_nnz_cap, "tile nnz within the buffer");
+      PLP_DCHECK(eb == (int)a.rp[r0] && ee == (int)a.rp[r1], "tile CSR bounds match row_ptr");
       const unsigned rp_b = (unsigned)(((r1 + 1 + 3) & ~3) - r0) * 4u;
       const unsigned sc_b = (unsigned)(((r1 + 3) & ~3) - r0) * 4u;
       const int cb = eb & ~3, ce = (ee + 3) & ~3, wb = eb & ~1, we = (ee + 1) & ~1;
@@ -175,6 +193,7 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
 #pragma unroll 4
     for (int x = rl; x < nx; x += RPI) {
       const int j = Lq[4 + x];
+      PLP_DCHECK(j >= 0 && (int64_t)j < a.n_cols && (j < r0 || j >= r1), "halo column outside the tile, inside U");
       const unsigned off = ((unsigned)(kHaloT + x) * K + 2 * pc) * 8u;
       cp_async16(B + Ly.U + off, a.U + (int64_t)j * K + 2 * pc);
       if constexpr (HAS_ETA) cp_async16(B + Ly.E + off, a.eta + (int64_t)j * K + 2 * pc);
@@ -197,9 +216,11 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
       const int b = it % NB;
       if (it >= NB)
         mbar_wait_sleep(&empty[b], (unsigned)((it - NB) / NB) & 1u, PLP_HALO_SLEEP_NS);
+      if (lane == 0) PLP_TRACE(it, 0);
       if (lane == 0) fence_proxy_async();  // consumers' generic reads before the async refill
       __syncwarp();
       issue_tile(t, b, it % 3, (unsigned)(it / 3) & 1u);
+      if (lane == 0) PLP_TRACE(it, 1);
       if (lane == 0) issue_list(t + 2 * ts, (it + 2) % 3);
       // warm L2 with the next tile's streamed parts (own rows, enc, w), so that its TMA copies,
       // issued only once the consumers release a buffer, are L2 hits (per-row bulk prefetches of
@@ -231,6 +252,7 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
     if (t >= n_tiles) break;
     const int b = it % NB;
     mbar_wait(&full[b], (unsigned)(it / NB) & 1u);  // tile t resident
+    if (lane == 0) PLP_TRACE(it, 2 + warp);
 
     const unsigned char* B = buf0 + (size_t)b * Ly.bytes;
     const int* rp_s = reinterpret_cast<const int*>(B + Ly.rp);
@@ -363,6 +385,8 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
 #pragma unroll 1
       for (; e + 1 < e1; e += 2) {
         const int x0 = enc_s[e], x1 = enc_s[e + 1];
+        PLP_DCHECK(x0 >= 0 && x1 >= 0 && x0 < kHaloT + ext_cap && x1 < kHaloT + ext_cap && (x0 < nr || x0 >= kHaloT) &&
+                       (x1 < nr || x1 >= kHaloT), "edge's tile-local neighbour index");
         const double w0 = w_s[e], w1 = w_s[e + 1];
         double uj0[CPL], ej0[CPL], uj1[CPL], ej1[CPL];
         lds_vec<CPL>(tU + x0 * K, uj0);
@@ -466,6 +490,7 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
       }
     }
     __syncwarp();
+    if (lane == 0) PLP_TRACE(it, 16 + warp);
     if (lane == 0) mbar_arrive(&empty[b]);  // this warp is done with buffer b
   }
   }

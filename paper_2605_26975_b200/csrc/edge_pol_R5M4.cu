@@ -15,3 +15,9 @@ plp_status launch_dbg_pol(plp_ctx* ctx, int64_t n, const double* a, double* s, d
   return launch_dbg(ctx, n, a, s, t, pw);
 }
 }  // namespace plp
+
+#ifdef PLP_HALO_TRACE
+extern "C" int plp_debug_halo_trace(long long* host, long long n) {
+  return (int)cudaMemcpyFromSymbol(host, plp::g_halo_trace, sizeof(long long) * n);
+}
+#endif

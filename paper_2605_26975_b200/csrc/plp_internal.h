@@ -115,6 +115,7 @@ plp_status check_k(int k);
 // Edge kernel launcher (edge.cu).
 struct EdgeArgs {
   int64_t n_rows;
+  int64_t n_cols;  // rows of U / eta (owned + halo)
   const int32_t* rp;
   const int32_t* sched;
   const int32_t* col;
