@@ -1,5 +1,6 @@
 // Context, graph handle, error reporting and argument checks of libplp (plp.h).
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdarg>
 #include <cstring>
@@ -149,13 +150,25 @@ static plp_status build_halo_tiles(plp_graph* g, const int64_t* rp, const int32_
   std::vector<int32_t> xs;
   int max_ext = 0, max_nnz = 0;
   std::vector<int32_t> tmp;
+  std::vector<std::pair<int32_t, int32_t>> cnt;  // (-references, column)
   for (int64_t t = 0; t < nt; ++t) {
     const int64_t r0 = t * T, r1 = std::min<int64_t>(n, r0 + T);
     tmp.clear();
     for (int64_t e = rp[r0]; e < rp[r1]; ++e)
       if (col[e] < r0 || col[e] >= r1) tmp.push_back(col[e]);
     std::sort(tmp.begin(), tmp.end());
-    tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+    // halo rows by decreasing number of references (ties: column order), so that when a tile's
+    // halo overflows shared memory (overflow mode) the rows left in L2 are the least used ones
+    cnt.clear();
+    for (size_t q = 0; q < tmp.size();) {
+      size_t r = q;
+      while (r < tmp.size() && tmp[r] == tmp[q]) ++r;
+      cnt.emplace_back(-(int32_t)(r - q), tmp[q]);
+      q = r;
+    }
+    std::sort(cnt.begin(), cnt.end());
+    tmp.resize(cnt.size());
+    for (size_t q = 0; q < cnt.size(); ++q) tmp[q] = cnt[q].second;
     xs.insert(xs.end(), tmp.begin(), tmp.end());
     xoff[t + 1] = (int64_t)xs.size();
     max_ext = std::max<int>(max_ext, (int)tmp.size());
@@ -165,7 +178,9 @@ static plp_status build_halo_tiles(plp_graph* g, const int64_t* rp, const int32_
 #ifndef PLP_HALO_NBUF
 #define PLP_HALO_NBUF 2
 #endif
-  const double bytes_k8 = PLP_HALO_NBUF * ((T + ext_cap) * 128.0 + nnz_cap * 12.0 + 4096.0);
+  // skipped only if not even 64 halo rows per tile fit next to the tile's own data at k = 8 (the
+  // launcher stages what fits and reads the rest from L2: overflow mode)
+  const double bytes_k8 = PLP_HALO_NBUF * ((T + 64) * 128.0 + nnz_cap * 12.0 + 4096.0);
 #ifndef PLP_HALO_CTAS
 #define PLP_HALO_CTAS 1
 #endif
@@ -183,10 +198,16 @@ static plp_status build_halo_tiles(plp_graph* g, const int64_t* rp, const int32_
     ext[t * LS + 2] = (int32_t)rp[r1];
     ext[t * LS + 3] = 0;
     std::copy(xb, xe, ext.begin() + t * LS + 4);
+    // tile-local index of each halo column (the list is ordered by references, not by column)
+    std::vector<std::pair<int32_t, int32_t>> pos;
+    pos.reserve(xe - xb);
+    for (const int32_t* q = xb; q < xe; ++q) pos.emplace_back(*q, (int32_t)(q - xb));
+    std::sort(pos.begin(), pos.end());
     for (int64_t e = rp[r0]; e < rp[r1]; ++e) {
       const int32_t j = col[e];
-      enc[e] = (j >= r0 && j < r1) ? (int32_t)(j - r0)
-                                   : (int32_t)(T + (std::lower_bound(xb, xe, j) - xb));
+      enc[e] = (j >= r0 && j < r1)
+                   ? (int32_t)(j - r0)
+                   : (int32_t)(T + std::lower_bound(pos.begin(), pos.end(), std::make_pair(j, INT32_MIN))->second);
     }
   }
   cudaError_t e;

@@ -82,6 +82,17 @@ __device__ __forceinline__ void l2_prefetch_range(const void* src, size_t bytes)
   const uintptr_t e = ((uintptr_t)src + bytes + 15) & ~(uintptr_t)15;
   if (e > a) l2_prefetch(reinterpret_cast<const void*>(a), (unsigned)(e - a));
 }
+// TMA row gather (sm_100 tile::gather4): rows r0..r3, columns [c0, c0 + box width) of the 2-D
+// tensor described by `tmap` (a __grid_constant__ CUtensorMap) land densely at dst (128-byte
+// aligned); completion counts bytes on `bar`.  One instruction, one thread, no LSU traffic.
+__device__ __forceinline__ void tma_gather4(void* dst, const void* tmap, int c0, int r0, int r1, int r2, int r3,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }

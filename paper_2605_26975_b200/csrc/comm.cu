@@ -13,6 +13,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -102,12 +103,21 @@ plp_status comm_init(plp_ctx* ctx, int rank, int world, const void* id) {
   ncclComm_t c = nullptr;
   PLP_NCCL(api->CommInitRank(&c, world, uid, rank));
   ctx->comm = c;
+  // side stream + events: halo exchanges run there while the interior tiles compute
+  PLP_CUDA(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+  PLP_CUDA(cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming));
+  PLP_CUDA(cudaEventCreateWithFlags(&ctx->ev_halo, cudaEventDisableTiming));
   return PLP_OK;
 }
 
 void comm_destroy(plp_ctx* ctx) {
   if (ctx->comm && nccl()) nccl()->CommDestroy(comm_of(ctx));
   ctx->comm = nullptr;
+  if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
+  if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
+  if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
+  ctx->comm_stream = nullptr;
+  ctx->ev_in = ctx->ev_halo = nullptr;
 }
 
 // In-place sum over the ranks of `count` doubles (device), on the ctx stream.  No-op without a
@@ -138,9 +148,10 @@ __global__ void gather_rows_bytes_kernel(int64_t m, int row_words, const int32_t
 // pack the rows each peer needs (one gather launch), then grouped NCCL send/recv; a received
 // peer slice lands in place in X's halo rows (the halo is sorted and ownership ranges are
 // contiguous, so each peer's rows form one slice).
-plp_status halo_exchange_bytes(plp_ctx* ctx, const plp_graph* g, void* X, int row_bytes) {
+plp_status halo_exchange_bytes(plp_ctx* ctx, const plp_graph* g, void* X, int row_bytes, cudaStream_t stream) {
   const plp_dist* d = g->dist;
   if (!d || !ctx->comm) return PLP_OK;
+  if (!stream) stream = ctx->stream;
   if (row_bytes % 4) return set_error(PLP_ERR_ARG, "halo rows must be a multiple of 4 bytes");
   const size_t need = (size_t)d->total_send * (size_t)row_bytes;
   if (need > d->sendbuf_bytes)
@@ -149,7 +160,7 @@ plp_status halo_exchange_bytes(plp_ctx* ctx, const plp_graph* g, void* X, int ro
   if (d->total_send > 0) {
     const int64_t total = d->total_send * words;
     const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)ctx->num_sms * 8);
-    gather_rows_bytes_kernel<<<grid, 256, 0, ctx->stream>>>(d->total_send, words, d->send_idx,
+    gather_rows_bytes_kernel<<<grid, 256, 0, stream>>>(d->total_send, words, d->send_idx,
                                                             static_cast<const uint32_t*>(X),
                                                             static_cast<uint32_t*>(d->sendbuf));
     PLP_LAUNCH_CHECK("gather_rows_bytes_kernel");
@@ -161,10 +172,10 @@ plp_status halo_exchange_bytes(plp_ctx* ctx, const plp_graph* g, void* X, int ro
   for (int q = 0; q < ctx->world; ++q) {
     if (d->send_cnt[q] > 0)
       PLP_NCCL(api->Send(sb + (size_t)d->send_off[q] * row_bytes, (size_t)d->send_cnt[q] * words,
-                         ncclUint32, q, comm_of(ctx), ctx->stream));
+                         ncclUint32, q, comm_of(ctx), stream));
     if (d->recv_cnt[q] > 0)
       PLP_NCCL(api->Recv(xb + (size_t)(d->n_own + d->recv_off[q]) * row_bytes,
-                         (size_t)d->recv_cnt[q] * words, ncclUint32, q, comm_of(ctx), ctx->stream));
+                         (size_t)d->recv_cnt[q] * words, ncclUint32, q, comm_of(ctx), stream));
   }
   PLP_NCCL(api->GroupEnd());
   return PLP_OK;
@@ -363,7 +374,32 @@ extern "C" plp_status plp_create_graph_dist(plp_ctx* ctx, int64_t n_global, int6
     cudaFree(d->send_idx);
     return fail(st);
   }
+  // interior tiles (no column in the halo) first, then the boundary tiles (SURVEY.md §8(e):
+  // interior rows compute while the halo is in flight).  PLP_DEBUG_SPLIT=1 also lists every third
+  // interior tile as a boundary tile (exercises the two-launch path on one GPU; tests).
   g->dist = d;
+  if (g->halo_enc) {
+    const int64_t T = PLP_HALO_TILE, nt = (n_own + T - 1) / T;
+    std::vector<int32_t> inter, bnd;
+    static const bool dbg = getenv("PLP_DEBUG_SPLIT") != nullptr;
+    for (int64_t t = 0; t < nt; ++t) {
+      const int64_t r0 = t * T, r1 = std::min<int64_t>(n_own, r0 + T);
+      bool b = false;
+      for (int64_t e = rp[r0]; e < rp[r1] && !b; ++e) b = col_loc[e] >= n_own;
+      if (dbg && t % 3 == 1) b = true;
+      (b ? bnd : inter).push_back((int32_t)t);
+    }
+    d->n_interior = (int64_t)inter.size();
+    d->n_boundary = (int64_t)bnd.size();
+    inter.insert(inter.end(), bnd.begin(), bnd.end());
+    if (!inter.empty() &&
+        (cudaMalloc(&d->tile_order, sizeof(int32_t) * inter.size()) != cudaSuccess ||
+         cudaMemcpy(d->tile_order, inter.data(), sizeof(int32_t) * inter.size(), cudaMemcpyHostToDevice) !=
+             cudaSuccess)) {
+      plp_destroy_graph(g);
+      return set_error(PLP_ERR_OOM, "cudaMalloc(tile order)");
+    }
+  }
   *out = g;
   return PLP_OK;
 }
@@ -382,6 +418,7 @@ extern "C" plp_status plp_graph_dist_info(const plp_graph* g, int64_t* n_own, in
 namespace plp {
 void dist_destroy(plp_dist* d) {
   if (!d) return;
+  cudaFree(d->tile_order);
   cudaFree(d->send_idx);
   cudaFree(d->sendbuf);
   delete d;

@@ -269,6 +269,48 @@ static plp_status exchange(plp_ctx* ctx, const plp_graph* g, const double* X, in
   return halo_exchange_bytes(ctx, g, const_cast<double*>(X), k * (int)sizeof(double));
 }
 
+// One edge pass of a collective call with its halo exchange (arrays xU, xE: nullptr = not needed).
+// With interior and boundary tiles (plp_dist::tile_order) and the halo kernel, the exchange runs on
+// the context's comm stream while the interior tiles compute; the boundary tiles follow once the
+// halo has landed.  Partial sums of the two launches are consecutive CTA blocks (*grid = both).
+static plp_status overlapped_pass(plp_ctx* ctx, const plp_graph* g, const EdgeArgs& a, const double* xU,
+                                  const double* xE, int* grid) {
+  const plp_dist* d = g->dist;
+  const int k = a.k;
+  plp_status st;
+  const bool split = d && ctx->comm && ctx->comm_stream && d->tile_order && d->n_interior > 0 &&
+                     d->n_boundary > 0 && (xU || xE);
+  if (!split) {
+    if (xU && (st = exchange(ctx, g, xU, k))) return st;
+    if (xE && (st = exchange(ctx, g, xE, k))) return st;
+    return launch_edge(ctx, a, grid);
+  }
+  PLP_CUDA(cudaEventRecord(ctx->ev_in, ctx->stream));  // U / eta written by the caller's stream
+  PLP_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_in, 0));
+  if (xU && (st = halo_exchange_bytes(ctx, g, const_cast<double*>(xU), k * 8, ctx->comm_stream))) return st;
+  if (xE && (st = halo_exchange_bytes(ctx, g, const_cast<double*>(xE), k * 8, ctx->comm_stream))) return st;
+  PLP_CUDA(cudaEventRecord(ctx->ev_halo, ctx->comm_stream));
+  EdgeArgs ai = a;
+  ai.tile_list = d->tile_order;
+  ai.tile_begin = 0;
+  ai.tile_count = d->n_interior;
+  int g1 = 0, g2 = 0;
+  st = launch_edge(ctx, ai, &g1);
+  if (st == PLP_ERR_SHAPE) {  // the halo kernel does not apply (k, alignment): exchange, then one pass
+    PLP_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_halo, 0));
+    return launch_edge(ctx, a, grid);
+  }
+  if (st) return st;
+  PLP_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_halo, 0));
+  EdgeArgs ab = ai;
+  ab.tile_begin = d->n_interior;
+  ab.tile_count = d->n_boundary;
+  ab.partials = a.partials + (int64_t)g1 * 4 * k;
+  if ((st = launch_edge(ctx, ab, &g2))) return st;
+  *grid = g1 + g2;
+  return PLP_OK;
+}
+
 extern "C" plp_status plp_edge_pass(plp_ctx* ctx, const plp_graph* g, int k, const double* U,
                                     const double* eta, double p, double eps, const double* AB_in,
                                     double* AB_out, double* dots_out, double* G, double* Hv) {
@@ -367,12 +409,21 @@ extern "C" plp_status plp_hessvec(plp_ctx* ctx, const plp_graph* g, int k, const
     return set_error(PLP_ERR_ARG, "full mode needs G_in (the Euclidean gradient at U)");
   const bool full = mode == PLP_HESS_FULL;
   const bool coll = collective(ctx, g);
-  if (coll && !u_current && (st = exchange(ctx, g, U, k))) return st;
-  if (coll && (st = exchange(ctx, g, eta, k))) return st;
-  st = plp_edge_pass(ctx, g, k, U, eta, p, eps, AB_in, nullptr, full ? scratch_dots(ctx) : nullptr,
-                     nullptr, Hv);
-  if (st || !full) return st;
-  if (coll && (st = comm_allreduce(ctx, scratch_dots(ctx), 2 * (size_t)k))) return st;
+  if (!coll) {
+    st = plp_edge_pass(ctx, g, k, U, eta, p, eps, AB_in, nullptr, full ? scratch_dots(ctx) : nullptr,
+                       nullptr, Hv);
+    if (st || !full) return st;
+  } else {
+    EdgeArgs a = graph_args(g);
+    a.k = k; a.U = U; a.eta = eta; a.AB = AB_in; a.Hv = Hv; a.p = p; a.eps = eps;
+    a.partials = ctx->partials;
+    a.want_dots = full;
+    int grid = 0;
+    if ((st = overlapped_pass(ctx, g, a, u_current ? nullptr : U, eta, &grid))) return st;
+    if (!full) return PLP_OK;
+    if ((st = launch_edge_finalize(ctx, grid, k, ctx->partials, nullptr, scratch_dots(ctx), nullptr))) return st;
+    if ((st = comm_allreduce(ctx, scratch_dots(ctx), 2 * (size_t)k))) return st;
+  }
   return plp_full_epilogue(ctx, g->n_rows, k, U, p, AB_in, scratch_dots(ctx), G_in, Hv);
 }
 
@@ -389,9 +440,11 @@ extern "C" plp_status plp_fgrad_hessvec(plp_ctx* ctx, const plp_graph* g, int k,
   const bool full = mode == PLP_HESS_FULL && Hv != nullptr;
   if (full && !G) return set_error(PLP_ERR_ARG, "full mode needs the G output buffer");
   const bool coll = collective(ctx, g);
-  if (coll && !u_current && (st = exchange(ctx, g, U, k))) return st;
-  if (coll && Hv && (st = exchange(ctx, g, eta, k))) return st;
+  const double* xU = coll && !u_current ? U : nullptr;  // halo exchanges this call still owes
+  const double* xE = coll && Hv ? eta : nullptr;
   if (!AB_in) {  // objective pass first (two edge passes)
+    if (xU && (st = exchange(ctx, g, U, k))) return st;
+    xU = nullptr;
     st = plp_edge_pass(ctx, g, k, U, nullptr, p, eps, nullptr, scratch_ab(ctx), nullptr, nullptr,
                        nullptr);
     if (st) return st;
@@ -405,7 +458,7 @@ extern "C" plp_status plp_fgrad_hessvec(plp_ctx* ctx, const plp_graph* g, int k,
   a.AB = AB_in; a.G = G; a.Hv = Hv; a.p = p; a.eps = eps; a.partials = ctx->partials;
   a.want_dots = full;
   int grid = 0;
-  st = launch_edge(ctx, a, &grid);
+  st = coll ? overlapped_pass(ctx, g, a, xU, xE, &grid) : launch_edge(ctx, a, &grid);
   if (st) return st;
   if (AB_out || full || F) {
     // F and AB_out come from the fused pass's own A', B' (all-reduced over the ranks)

@@ -12,6 +12,10 @@ plp_status launch_edge_any(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int* 
 #ifdef PLP_TUNE_ONLY  // tuning builds (tools/tune_edge.py): k = 8 halo or staged shapes only
   if (a.k != 8) return set_error(PLP_ERR_ARG, "tuning build: k = 8 only");
   bool used_h = false;
+  if (a.tile_list) {
+    plp_status sh = try_launch_halo(ctx, a, pw, grid, &used_h);
+    return sh ? sh : used_h ? PLP_OK : set_error(PLP_ERR_SHAPE, "tile list needs the halo kernel");
+  }
   if (getenv("PLP_EDGE_STAGED") == nullptr) {
     plp_status sh = try_launch_halo(ctx, a, pw, grid, &used_h);
     if (sh || used_h) return sh;
@@ -20,6 +24,11 @@ plp_status launch_edge_any(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int* 
 #else
   bool used = false;
   plp_status st = PLP_OK;
+  if (a.tile_list) {  // a tile work list: the halo kernel or nothing (the caller falls back)
+    st = try_launch_halo(ctx, a, pw, grid, &used);
+    if (st) return st;
+    return used ? PLP_OK : set_error(PLP_ERR_SHAPE, "tile list needs the halo kernel");
+  }
   static const bool rows = getenv("PLP_EDGE_ROWS") != nullptr;
   if (rows) return launch_edge_pow(ctx, a, pw, grid);
   static const bool staged = getenv("PLP_EDGE_STAGED") != nullptr;

@@ -28,9 +28,13 @@
 namespace plp {
 
 constexpr int kHaloT = PLP_HALO_TILE;  // rows per tile (plp.h)
+#ifndef PLP_HALO_PROD
+#define PLP_HALO_PROD 1  // producer warps (the halo-row gathers are split between them)
+#endif
+constexpr int kHaloProd = PLP_HALO_PROD;
 constexpr int kHaloCWarps = 2 * (kHaloT / kSchedWindow);  // consumers: a warp pair per window
-constexpr int kHaloThreads = (kHaloCWarps + 1) * 32;       // + one producer warp
-static_assert(kHaloT % kSchedWindow == 0 && kHaloThreads <= 16 * 32, "tile map (<= 4 warps per SMSP)");
+constexpr int kHaloThreads = (kHaloCWarps + kHaloProd) * 32;  // + the producer warp(s)
+static_assert(kHaloT % kSchedWindow == 0 && kHaloThreads <= 1024, "tile map");
 
 // Per-buffer shared-memory layout (bytes), identical on host and device.
 struct HaloLayout {
@@ -106,7 +110,10 @@ static __device__ long long g_halo_trace[160 * kTraceTiles * kTraceSlots];
 
 // DOTS: also accumulate the full-mode dots alpha, gamma (a.want_dots; a template flag so that the
 // sparse passes carry no code for them).
-template <int K, class POW, bool HAS_ETA, bool OBJ, int NB, bool ADAPT, bool DOTS>
+// OVF: some tile's halo exceeds what fits in shared memory (a.halo_stage rows are staged, the rest
+// -- the tile's least referenced halo rows, the list being ordered by reference count -- are read
+// from global memory / L2 by the consumers; C3's random long-range edges).
+template <int K, class POW, bool HAS_ETA, bool OBJ, int NB, bool ADAPT, bool DOTS, bool OVF>
 __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(POW pw, EdgeArgs a) {
   static_assert(!(OBJ && HAS_ETA), "objective mode has no eta");
   constexpr int CPL = halo_cpl<K>(), LPR = K / CPL, RPW = 32 / LPR;  // rows per pass
@@ -115,24 +122,29 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
   uint64_t* lbar = full + NB;                   // [3] halo list landed
   uint64_t* empty = lbar + 3;                          // [NBUF] consumers done with the buffer
   if constexpr (POW::kNeedsTables) pw.init_smem(smem + kHaloHead);
-  const int ext_cap = a.halo_ext_cap;
-  const int LS = ext_cap + 4;  // list slot: n_ext, eb, ee, pad, columns
+  const int ext_cap = OVF ? a.halo_stage : a.halo_ext_cap;  // halo rows staged per tile
+  const int LS = ext_cap + 4;                  // shared list slot: n_ext, eb, ee, pad, columns
+  const int LSG = a.halo_ext_cap + 4;          // global list stride
   int* lists = reinterpret_cast<int*>(smem + halo_lists_off(POW::kNeedsTables));
   const HaloLayout Ly = halo_layout(K, ext_cap, a.halo_nnz_cap, OBJ, HAS_ETA);
   unsigned char* buf0 = smem + halo_bufs_off(ext_cap, POW::kNeedsTables);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int grp = lane / LPR, li = lane % LPR, c0 = li * CPL;
+  const int pw_id = warp - kHaloCWarps;  // producer index (>= 0): 0 stages the streamed parts and lists
   if (tid == 0) {
     // full: the producer's arrive.expect_tx (TMA bytes) + one cp.async arrival per producer lane
     for (int q = 0; q < NB; ++q) {
-      mbar_init(&full[q], 1 + 32);
+      mbar_init(&full[q], 1 + 32 * kHaloProd);
       mbar_init(&empty[q], kHaloCWarps);
     }
     for (int q = 0; q < 3; ++q) mbar_init(&lbar[q], 1);
     fence_mbar_init();
   }
   const int n_rows = (int)a.n_rows;
-  const int64_t n_tiles = (a.n_rows + kHaloT - 1) / kHaloT;
+  // work items: the tiles, or (a.tile_list) the listed tiles [tile_begin, + tile_count) -- the
+  // interior / boundary launches of the multi-rank overlap (edge.cu)
+  const int64_t n_tiles = a.tile_list ? a.tile_count : (a.n_rows + kHaloT - 1) / kHaloT;
+  auto tile_of = [&](int64_t li) -> int64_t { return a.tile_list ? (int64_t)a.tile_list[a.tile_begin + li] : li; };
   const double p = a.p, pp1 = p * (p - 1.0);
   double cG[CPL], cAB[CPL], cHA[CPL], cHB[CPL];
 #pragma unroll
@@ -155,19 +167,19 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
   auto issue_list = [&](int64_t t, int q) {
     if (t >= n_tiles) return;
     mbar_expect_tx(&lbar[q], (unsigned)LS * 4u);
-    tma_bulk_g2s(lists + q * LS, a.halo_ext + t * LS, (unsigned)LS * 4u, &lbar[q]);
+    tma_bulk_g2s(lists + q * LS, a.halo_ext + tile_of(t) * LSG, (unsigned)LS * 4u, &lbar[q]);
   };
   // (producer warp) stage tile t into buffer b; its halo list is in slot q (use parity lph)
   auto issue_tile = [&](int64_t t, int b, int q, unsigned lph) {
     if (t >= n_tiles) return;
     unsigned char* B = buf0 + (size_t)b * Ly.bytes;
-    const int r0 = (int)(t * kHaloT), r1 = min(r0 + kHaloT, n_rows);
+    const int r0 = (int)(tile_of(t) * kHaloT), r1 = min(r0 + kHaloT, n_rows);
     constexpr unsigned RB = K * 8u;  // bytes per row
     mbar_wait(&lbar[q], lph);
     const int* Lq = lists + q * LS;
-    const int nx = Lq[0];
+    const int nx = OVF ? min(Lq[0], ext_cap) : Lq[0];  // rows staged (OVF: the first ext_cap)
     PLP_DCHECK(nx >= 0 && nx <= ext_cap, "halo count within the tile's list slot");
-    if (lane == 0) {
+    if (lane == 0 && pw_id == 0) {
       const int eb = Lq[1], ee = Lq[2];
       PLP_DCHECK(ee - eb >= 0 && ee - eb <= a.halo_nnz_cap, "tile nnz within the buffer");
       PLP_DCHECK(eb == (int)a.rp[r0] && ee == (int)a.rp[r1], "tile CSR bounds match row_ptr");
@@ -189,9 +201,9 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
     }
     // halo rows: PPR lanes per row, 32 / PPR rows per warp instruction
     constexpr int PPR = K / 2, RPI = 32 / PPR;
-    const int rl = lane / PPR, pc = lane % PPR;
+    const int rl = lane / PPR + pw_id * RPI, pc = lane % PPR;
 #pragma unroll 4
-    for (int x = rl; x < nx; x += RPI) {
+    for (int x = rl; x < nx; x += RPI * kHaloProd) {
       const int j = Lq[4 + x];
       PLP_DCHECK(j >= 0 && (int64_t)j < a.n_cols && (j < r0 || j >= r1), "halo column outside the tile, inside U");
       const unsigned off = ((unsigned)(kHaloT + x) * K + 2 * pc) * 8u;
@@ -202,10 +214,10 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
   };
 
   const int64_t t0 = blockIdx.x, ts = gridDim.x;
-  if (warp == kHaloCWarps) {
+  if (warp >= kHaloCWarps) {
     // ---- producer warp: stages tile it into buffer it & 1 once the consumers released it, and
     // the halo list of tile it + 2 into list slot (it + 2) % 3 (freed by tile it - 1) ----
-    if (lane == 0) {
+    if (lane == 0 && pw_id == 0) {
       issue_list(t0, 0);
       issue_list(t0 + ts, 1);
     }
@@ -216,22 +228,24 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
       const int b = it % NB;
       if (it >= NB)
         mbar_wait_sleep(&empty[b], (unsigned)((it - NB) / NB) & 1u, PLP_HALO_SLEEP_NS);
-      if (lane == 0) PLP_TRACE(it, 0);
+      if (lane == 0 && pw_id == 0) PLP_TRACE(it, 0);
       if (lane == 0) fence_proxy_async();  // consumers' generic reads before the async refill
       __syncwarp();
       issue_tile(t, b, it % 3, (unsigned)(it / 3) & 1u);
-      if (lane == 0) PLP_TRACE(it, 1);
-      if (lane == 0) issue_list(t + 2 * ts, (it + 2) % 3);
+      // every producer warp is done with list slot it % 3 before producer 0 reuses slot (it + 2) % 3
+      if constexpr (kHaloProd > 1) asm volatile("bar.sync 1, %0;" ::"n"(32 * kHaloProd) : "memory");
+      if (lane == 0 && pw_id == 0) PLP_TRACE(it, 1);
+      if (lane == 0 && pw_id == 0) issue_list(t + 2 * ts, (it + 2) % 3);
       // warm L2 with the next tile's streamed parts (own rows, enc, w), so that its TMA copies,
       // issued only once the consumers release a buffer, are L2 hits (per-row bulk prefetches of
       // the halo rows too measured 1.6x slower: tiny bulk operations)
-      if (lane == 0) {
+      if (lane == 0 && pw_id == 0) {
         const int64_t tn = t + ts;
         if (tn < n_tiles) {
           const int qn = (it + 1) % 3;
           mbar_wait(&lbar[qn], (unsigned)((it + 1) / 3) & 1u);
           const int* Ln = lists + qn * LS;
-          const int r0 = (int)(tn * kHaloT), r1 = min(r0 + kHaloT, n_rows);
+          const int r0 = (int)(tile_of(tn) * kHaloT), r1 = min(r0 + kHaloT, n_rows);
           const size_t rows_b = (size_t)(r1 - r0) * K * 8u;
           l2_prefetch_range(a.U + (int64_t)r0 * K, rows_b);
           if constexpr (HAS_ETA) l2_prefetch_range(a.eta + (int64_t)r0 * K, rows_b);
@@ -257,13 +271,35 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
     const unsigned char* B = buf0 + (size_t)b * Ly.bytes;
     const int* rp_s = reinterpret_cast<const int*>(B + Ly.rp);
     const int* sc_s = reinterpret_cast<const int*>(B + Ly.sched);
-    const int r0 = (int)(t * kHaloT);
+    const int64_t tt = tile_of(t);
+    const int r0 = (int)(tt * kHaloT);
     const int nr = min(kHaloT, n_rows - r0);
     const int eb = rp_s[0];
     const int* enc_s = reinterpret_cast<const int*>(B + Ly.enc) - (eb & ~3);
     const double* w_s = reinterpret_cast<const double*>(B + Ly.w) - (eb & ~1);
     const double* tU = reinterpret_cast<const double*>(B + Ly.U) + c0;
     const double* tE = reinterpret_cast<const double*>(B + Ly.E) + c0;
+    // neighbour rows: tile-local index x; OVF: x >= kHaloT + ext_cap is an unstaged halo row, read
+    // through its global id in the tile's (global) halo list
+    const int* glist = a.halo_ext + tt * LSG + 4 - kHaloT;
+    auto ldU = [&](int x, double (&v)[CPL]) {
+      if constexpr (OVF) {
+        if (x >= kHaloT + ext_cap) {
+          lds_vec<CPL>(a.U + (int64_t)__ldg(glist + x) * K + c0, v);
+          return;
+        }
+      }
+      lds_vec<CPL>(tU + x * K, v);
+    };
+    auto ldE = [&](int x, double (&v)[CPL]) {
+      if constexpr (OVF) {
+        if (x >= kHaloT + ext_cap) {
+          lds_vec<CPL>(a.eta + (int64_t)__ldg(glist + x) * K + c0, v);
+          return;
+        }
+      }
+      lds_vec<CPL>(tE + x * K, v);
+    };
 
 #pragma unroll 1
     for (int rd = 0; rd * C < NSL; ++rd) {
@@ -304,14 +340,14 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
           const int x0 = enc_s[e], x1 = enc_s[e + 1];
           const double w0 = w_s[e], w1 = w_s[e + 1];
           double uj0[CPL], uj1[CPL];
-          lds_vec<CPL>(tU + x0 * K, uj0);
-          lds_vec<CPL>(tU + x1 * K, uj1);
+          ldU(x0, uj0);
+          ldU(x1, uj1);
           obj_edge(w0, uj0);
           obj_edge(w1, uj1);
         }
         if (e < e1) {
           double uj0[CPL];
-          lds_vec<CPL>(tU + enc_s[e] * K, uj0);
+          ldU(enc_s[e], uj0);
           obj_edge(w_s[e], uj0);
         }
         double tn[CPL];
@@ -340,7 +376,7 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
 #pragma unroll 1
               for (int ee = eu; ee < e1; ++ee) {
                 double uj0[CPL];
-                lds_vec<CPL>(tU + enc_s[ee] * K, uj0);
+                ldU(enc_s[ee], uj0);
                 const double wv = w_s[ee];
 #pragma unroll
                 for (int cc = 0; cc < CPL; ++cc) {
@@ -385,15 +421,15 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
 #pragma unroll 1
       for (; e + 1 < e1; e += 2) {
         const int x0 = enc_s[e], x1 = enc_s[e + 1];
-        PLP_DCHECK(x0 >= 0 && x1 >= 0 && x0 < kHaloT + ext_cap && x1 < kHaloT + ext_cap && (x0 < nr || x0 >= kHaloT) &&
+        PLP_DCHECK(x0 >= 0 && x1 >= 0 && x0 < kHaloT + a.halo_ext_cap && x1 < kHaloT + a.halo_ext_cap && (x0 < nr || x0 >= kHaloT) &&
                        (x1 < nr || x1 >= kHaloT), "edge's tile-local neighbour index");
         const double w0 = w_s[e], w1 = w_s[e + 1];
         double uj0[CPL], ej0[CPL], uj1[CPL], ej1[CPL];
-        lds_vec<CPL>(tU + x0 * K, uj0);
-        lds_vec<CPL>(tU + x1 * K, uj1);
+        ldU(x0, uj0);
+        ldU(x1, uj1);
         if constexpr (HAS_ETA) {
-          lds_vec<CPL>(tE + x0 * K, ej0);
-          lds_vec<CPL>(tE + x1 * K, ej1);
+          ldE(x0, ej0);
+          ldE(x1, ej1);
         }
         edge_update_mx<CPL, POW, HAS_ETA>(pw, w0, ui, uj0, ei, ej0, L, HA, mx);
         edge_update_mx<CPL, POW, HAS_ETA>(pw, w1, ui, uj1, ei, ej1, L, HA, mx);
@@ -402,8 +438,8 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
         const int x0 = enc_s[e];
         const double w0 = w_s[e];
         double uj0[CPL], ej0[CPL];
-        lds_vec<CPL>(tU + x0 * K, uj0);
-        if constexpr (HAS_ETA) lds_vec<CPL>(tE + x0 * K, ej0);
+        ldU(x0, uj0);
+        if constexpr (HAS_ETA) ldE(x0, ej0);
         edge_update_mx<CPL, POW, HAS_ETA>(pw, w0, ui, uj0, ei, ej0, L, HA, mx);
       }
       // node terms sn = cap(|u|)^{p-2}, tn = |u|^{p-1}, after the edges (fewer live registers in
@@ -443,11 +479,11 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
           for (; ee + 1 < e1; ee += 2) {  // edge pairs: two dependency chains interleave
             const int x0 = enc_s[ee], x1 = enc_s[ee + 1];
             double uj0[CPL], ej0[CPL], uj1[CPL], ej1[CPL];
-            lds_vec<CPL>(tU + x0 * K, uj0);
-            lds_vec<CPL>(tU + x1 * K, uj1);
+            ldU(x0, uj0);
+            ldU(x1, uj1);
             if constexpr (HAS_ETA) {
-              lds_vec<CPL>(tE + x0 * K, ej0);
-              lds_vec<CPL>(tE + x1 * K, ej1);
+              ldE(x0, ej0);
+              ldE(x1, ej1);
             }
             edge_update_capsel<CPL, POW, HAS_ETA>(pw, w_s[ee], ui, uj0, ei, ej0, L, HA, rg);
             edge_update_capsel<CPL, POW, HAS_ETA>(pw, w_s[ee + 1], ui, uj1, ei, ej1, L, HA, rg);
@@ -455,8 +491,8 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
           if (ee < e1) {
             const int x0 = enc_s[ee];
             double uj0[CPL], ej0[CPL];
-            lds_vec<CPL>(tU + x0 * K, uj0);
-            if constexpr (HAS_ETA) lds_vec<CPL>(tE + x0 * K, ej0);
+            ldU(x0, uj0);
+            if constexpr (HAS_ETA) ldE(x0, ej0);
             edge_update_capsel<CPL, POW, HAS_ETA>(pw, w_s[ee], ui, uj0, ei, ej0, L, HA, rg);
           }
           if (rg.bad()) edge_row_exact<CPL, POW, HAS_ETA>(pw, e0, e1, a.col, a.w, a.U, a.eta, K, c0, ui, ei, L, HA);
@@ -516,41 +552,62 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
   }
 }
 
+// Halo rows staged per tile: the whole halo (ext_cap) if the buffers fit, else the largest multiple
+// of 4 that fits (overflow mode); 0 if not even 64 rows fit.
+inline int halo_stage_rows(int k, int ext_cap, int nnz_cap, bool tables, bool obj, bool eta, int nb) {
+  if (halo_smem_bytes(k, ext_cap, nnz_cap, tables, obj, eta, nb) <= kHaloSmemMax) return ext_cap;
+  int lo = 0, hi = ext_cap;
+  while (hi - lo > 4) {
+    const int mid = ((lo + hi) / 2) & ~3;
+    if (halo_smem_bytes(k, mid, nnz_cap, tables, obj, eta, nb) <= kHaloSmemMax) lo = mid; else hi = mid;
+  }
+  return lo >= 64 ? lo : 0;
+}
+
 template <int K, class POW, bool HAS_ETA, bool OBJ>
-plp_status launch_halo_shape(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int* grid_out) {
+plp_status launch_halo_shape(plp_ctx* ctx, const EdgeArgs& a0, const POW& pw, int* grid_out) {
+  EdgeArgs a = a0;
+  const bool T = POW::kNeedsTables;
   // passes without eta stage U rows only: a third buffer fits where the eta pass has two
   constexpr int NB3 = HAS_ETA ? kHaloNBuf : PLP_HALO_NBUF_NOETA;
-  const unsigned smem3 = halo_smem_bytes(K, a.halo_ext_cap, a.halo_nnz_cap, POW::kNeedsTables, OBJ, HAS_ETA, NB3);
-  const bool deep = NB3 != kHaloNBuf && smem3 <= kHaloSmemMax;
+  const bool deep = NB3 != kHaloNBuf &&
+                    halo_smem_bytes(K, a.halo_ext_cap, a.halo_nnz_cap, T, OBJ, HAS_ETA, NB3) <= kHaloSmemMax;
   const int nb = deep ? NB3 : kHaloNBuf;
+  a.halo_stage = halo_stage_rows(K, a.halo_ext_cap, a.halo_nnz_cap, T, OBJ, HAS_ETA, nb);
+  const bool ovf = a.halo_stage < a.halo_ext_cap;
   // the fused F/G/Hv pass (G and eta) keeps the plain loop; every other pass adapts
   const bool adapt = !(HAS_ETA && a.G != nullptr);
   const bool dots = HAS_ETA && a.want_dots;
-  auto kern = deep ? edge_halo_kernel<K, POW, HAS_ETA, OBJ, NB3, true, false>
-                   : (adapt ? (dots ? edge_halo_kernel<K, POW, HAS_ETA, OBJ, kHaloNBuf, true, HAS_ETA>
-                                    : edge_halo_kernel<K, POW, HAS_ETA, OBJ, kHaloNBuf, true, false>)
-                            : (dots ? edge_halo_kernel<K, POW, HAS_ETA, OBJ, kHaloNBuf, false, HAS_ETA>
-                                    : edge_halo_kernel<K, POW, HAS_ETA, OBJ, kHaloNBuf, false, false>));
-  const unsigned smem = halo_smem_bytes(K, a.halo_ext_cap, a.halo_nnz_cap, POW::kNeedsTables, OBJ, HAS_ETA, nb);
+  auto kern = deep ? edge_halo_kernel<K, POW, HAS_ETA, OBJ, NB3, true, false, false>
+            : ovf  ? (adapt ? edge_halo_kernel<K, POW, HAS_ETA, OBJ, kHaloNBuf, true, false, true>
+                            : edge_halo_kernel<K, POW, HAS_ETA, OBJ, kHaloNBuf, false, false, true>)
+                   : (adapt ? (dots ? edge_halo_kernel<K, POW, HAS_ETA, OBJ, kHaloNBuf, true, HAS_ETA, false>
+                                    : edge_halo_kernel<K, POW, HAS_ETA, OBJ, kHaloNBuf, true, false, false>)
+                            : (dots ? edge_halo_kernel<K, POW, HAS_ETA, OBJ, kHaloNBuf, false, HAS_ETA, false>
+                                    : edge_halo_kernel<K, POW, HAS_ETA, OBJ, kHaloNBuf, false, false, false>));
+  const unsigned smem = halo_smem_bytes(K, ovf ? a.halo_stage : a.halo_ext_cap, a.halo_nnz_cap, T, OBJ, HAS_ETA, nb);
   // the dynamic shared-memory opt-in is a per-device function attribute: set it on this ctx's
   // device whenever a launch needs more than the value set so far (per template instance)
-  static unsigned attr_set[64][5] = {};
-  const int vi = deep ? 4 : (adapt ? 1 : 0) + (dots ? 2 : 0);
+  static unsigned attr_set[64][7] = {};
+  const int vi = deep ? 4 : ovf ? 5 + (adapt ? 1 : 0) : (adapt ? 1 : 0) + (dots ? 2 : 0);
   unsigned& set_to = attr_set[ctx->device & 63][vi];
   if (set_to < smem) {
     PLP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     set_to = smem;
   }
-  const int64_t n_tiles = (a.n_rows + kHaloT - 1) / kHaloT;
+  const int64_t n_tiles = a.tile_list ? a.tile_count : (a.n_rows + kHaloT - 1) / kHaloT;
   int64_t grid = (int64_t)ctx->num_sms * PLP_HALO_CTAS;
   if (grid > ctx->max_ctas) grid = ctx->max_ctas;
   if (grid > n_tiles) grid = n_tiles > 0 ? n_tiles : 1;
   kern<<<(int)grid, kHaloThreads, smem, ctx->stream>>>(pw, a);
   PLP_LAUNCH_CHECK("edge_halo_kernel");
-  // [adapt]: the capped-form row recompute (every pass but the fused F/G/Hv benchmark pass)
-  note_edge_kernel(OBJ ? (deep ? "edge_halo_kernel[objective,3buf,adapt]" : "edge_halo_kernel[objective,adapt]")
-                       : (deep ? "edge_halo_kernel[3buf,adapt]" : adapt ? "edge_halo_kernel[adapt]" : "edge_halo_kernel"),
-                   K, halo_cpl<K>(), K / halo_cpl<K>(), 2, POW::kName, HAS_ETA);
+  // [adapt]: the capped-form row recompute (every pass but the fused F/G/Hv benchmark pass);
+  // [ovf]: halo rows beyond what fits in shared memory read from L2
+  char name[96];
+  snprintf(name, sizeof(name), "edge_halo_kernel%s", OBJ ? (deep ? "[objective,3buf,adapt]" : ovf ? "[objective,ovf,adapt]" : "[objective,adapt]")
+                                                         : deep ? "[3buf,adapt]" : ovf ? (adapt ? "[ovf,adapt]" : "[ovf]")
+                                                         : adapt ? "[adapt]" : "");
+  note_edge_kernel(name, K, halo_cpl<K>(), K / halo_cpl<K>(), 2, POW::kName, HAS_ETA);
   *grid_out = (int)grid;
   return PLP_OK;
 }
@@ -565,9 +622,13 @@ plp_status try_launch_halo(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int* 
   if (a.halo_enc == nullptr || (k != 4 && k != 8 && k != 16) || (a.ldx != 0 && a.ldx != k) ||
       !al16(a.U) || (a.eta && !al16(a.eta)) || (a.G && !al16(a.G)) || (a.Hv && !al16(a.Hv)))
     return PLP_OK;
-  if (halo_smem_bytes(k, a.halo_ext_cap, a.halo_nnz_cap, POW::kNeedsTables) > kHaloSmemMax) return PLP_OK;
-  *used = true;
   const bool he = a.eta != nullptr;
+  if (halo_stage_rows(k, a.halo_ext_cap, a.halo_nnz_cap, POW::kNeedsTables, false, true, kHaloNBuf) == 0)
+    return PLP_OK;  // not even 64 halo rows per tile fit: the staged kernel
+  if (he && a.want_dots &&
+      halo_smem_bytes(k, a.halo_ext_cap, a.halo_nnz_cap, POW::kNeedsTables) > kHaloSmemMax)
+    return PLP_OK;  // full-mode dots with an overflowing halo: the staged kernel
+  *used = true;
   const bool obj = !he && a.G == nullptr && a.upper_ok && a.nlow != nullptr && a.sched_up != nullptr;
 #define PLP_HSHAPE(K)                                                                      \
   return he ? launch_halo_shape<K, POW, true, false>(ctx, a, pw, grid)                     \

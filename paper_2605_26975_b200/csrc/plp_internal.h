@@ -42,6 +42,8 @@ struct plp_ctx {
   // single-rank context created without an id)
   int rank = 0, world = 1;
   void* comm = nullptr;
+  cudaStream_t comm_stream = nullptr;       // halo exchanges overlapped with interior tiles
+  cudaEvent_t ev_in = nullptr, ev_halo = nullptr;
 };
 
 // Halo plan of a graph created by plp_create_graph_dist (comm.cu): this rank owns global rows
@@ -53,8 +55,12 @@ struct plp_dist {
   std::vector<int64_t> bounds, send_off, send_cnt, recv_off, recv_cnt;
   int64_t total_send = 0;
   int32_t* send_idx = nullptr;  // device
-  void* sendbuf = nullptr;      // device, grown to total_send x the widest row exchanged
+  void* sendbuf = nullptr;      // device, total_send rows of up to PLP_MAX_K doubles
   size_t sendbuf_bytes = 0;
+  // halo-kernel tiles (PLP_HALO_TILE rows) with no halo column first, then the boundary tiles:
+  // the interior ones run while the halo exchange is in flight
+  int32_t* tile_order = nullptr;  // device, n_interior + n_boundary entries
+  int64_t n_interior = 0, n_boundary = 0;
 };
 
 struct plp_graph {
@@ -106,7 +112,8 @@ plp_status comm_init(plp_ctx* ctx, int rank, int world, const void* nccl_id);
 void comm_destroy(plp_ctx* ctx);
 plp_status comm_allreduce(plp_ctx* ctx, double* buf, size_t count);  // in place, no-op on one rank
 plp_status comm_allreduce_i64(plp_ctx* ctx, int64_t* buf, size_t count);
-plp_status halo_exchange_bytes(plp_ctx* ctx, const plp_graph* g, void* X, int row_bytes);
+plp_status halo_exchange_bytes(plp_ctx* ctx, const plp_graph* g, void* X, int row_bytes,
+                               cudaStream_t stream = nullptr);  // nullptr: ctx->stream
 void dist_destroy(plp_dist* d);
 // records the last launched edge kernel's name (plp_last_edge_kernel)
 void note_edge_kernel(const char* family, int kc, int cpl, int lpr, int unr, const char* pow, int eta);
@@ -136,6 +143,11 @@ struct EdgeArgs {
   const int32_t* halo_enc;
   const int32_t* halo_ext;
   int halo_ext_cap, halo_nnz_cap;
+  int halo_stage;  // halo rows staged per tile (< halo_ext_cap: overflow mode); set by the launcher
+  // optional work list of the halo kernel: tiles tile_list[tile_begin, + tile_count) only (the
+  // interior / boundary launches of a multi-rank call); other kernels refuse a list
+  const int32_t* tile_list;
+  int64_t tile_begin, tile_count;
   const int32_t* nlow;  // objective mode (edge_halo.cuh)
   const int32_t* sched_up;
   int upper_ok;

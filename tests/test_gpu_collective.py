@@ -126,3 +126,56 @@ def test_device_tcg_on_collective_context(plp, ctxs):
         outs.append((U, [r.tcg_iters for r in tr.records]))
     assert outs[0][1] == outs[1][1]
     assert torch.equal(outs[0][0], outs[1][0])
+
+
+_SPLIT_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+from paper_2605_26975_b200 import plp
+from plp_inputs import make_config, draw_U, draw_eta, permute_graph
+g0 = make_config("C5", n=60_000)
+g = permute_graph(g0, plp.tile_order(g0.row_ptr, g0.col))
+plain = plp.Context(0)
+coll = plp.Context(0, rank=0, world=1, nccl_id=plp.get_nccl_unique_id())
+out = {{}}
+for k, p, mode in ((8, 1.2, 0), (4, 1.5, 1)):
+    U = torch.from_numpy(draw_U(g.n, k, 2)).cuda()
+    eta = torch.from_numpy(draw_eta(g.n, k, 2)).cuda()
+    Gp = plp.Graph(plain, g.row_ptr, g.col, g.w)
+    Gc = plp.DistGraph(coll, g.n, 0, g.n, g.row_ptr, g.col, g.w)
+    for name, ctx, G in (("p", plain, Gp), ("c", coll, Gc)):
+        F0, AB, Gr = plp.fgrad(ctx, G, U, p)
+        Hv = plp.hessvec(ctx, G, U, eta, p, AB, mode=mode, G_in=Gr)
+        F, ABo, G2, Hv3 = plp.fgrad_hessvec(ctx, G, U, eta, p, AB_in=AB, mode=mode)
+        torch.cuda.synchronize()
+        kern = plp.last_edge_kernel()
+        for key, v in (("Hv", Hv), ("F", F), ("AB", ABo), ("G", G2), ("Hv3", Hv3)):
+            out[f"{{name}}_{{k}}_{{key}}"] = v.cpu().numpy()
+        out[f"{{name}}_{{k}}_kern"] = np.array(kern)
+np.savez({path!r}, **out)
+"""
+
+
+def test_interior_boundary_split_path(plp, tmp_path):
+    """The overlapped collective pass (interior tiles while the halo exchange is in flight on the
+    comm stream, then the boundary tiles; two launches whose CTA partials are reduced together).
+    PLP_DEBUG_SPLIT=1 marks every third tile a boundary tile so the path runs on one GPU: rows (G,
+    Hv) are bitwise those of the single launch, A, B and F equal up to the partial grouping."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    path = str(tmp_path / "split.npz")
+    script = tmp_path / "split.py"
+    script.write_text(_SPLIT_SCRIPT.format(root=os.path.dirname(here), tests=here, path=path))
+    subprocess.check_call([sys.executable, str(script)], env=dict(os.environ, PLP_DEBUG_SPLIT="1"))
+    z = np.load(path)
+    for k in (8, 4):
+        assert str(z[f"c_{k}_kern"]).startswith("edge_halo_kernel"), str(z[f"c_{k}_kern"])
+        for key in ("Hv", "G", "Hv3"):
+            if k == 8:  # sparse mode: rows bitwise
+                assert np.array_equal(z[f"p_{k}_{key}"], z[f"c_{k}_{key}"]), (k, key)
+            else:  # full mode: the rank-two epilogue uses the reduced dots (partial grouping)
+                assert colwise_relerr(z[f"c_{k}_{key}"], z[f"p_{k}_{key}"]) < 1e-13, (k, key)
+        for key in ("F", "AB"):
+            assert scalar_relerr(z[f"c_{k}_{key}"], z[f"p_{k}_{key}"]) < 1e-14, (k, key)

@@ -63,7 +63,7 @@ def assert_adaptive_path(kern, k, name=""):
     """k = 4, 8: the halo kernel's adaptive variant.  Where a tile's halo does not fit in shared
     memory (k = 16 tiles; C3's 3-D grid with random long-range edges has tiles with ~1000 halo
     rows) the staged kernel (libdevice row recompute) runs instead."""
-    ok = kern.startswith("edge_halo_kernel[adapt]") or \
+    ok = (kern.startswith("edge_halo_kernel[") and "adapt" in kern) or \
         ((k == 16 or name.startswith("C3")) and kern.startswith("edge_staged_kernel"))
     assert ok, kern
 
@@ -131,7 +131,7 @@ def test_hessvec_fully_degenerate_and_exact_ties(plp, ctx, name, k, p):
         eta = draw_eta(g.n, k, 9)
         for mode in (0, 1):
             Hv, AB, kern = gpu_hessvec(plp, ctx, g, U, eta, p, mode, 1e-9)
-            assert kern.startswith("edge_halo_kernel[adapt]"), kern
+            assert kern.startswith("edge_halo_kernel[") and "adapt" in kern, kern
             ref, A, B = oracle_hessvec(g, U, eta, p, mode, 1e-9)
             e = colwise_relerr(Hv, ref)
             assert e < TOL, (noise, mode, e)
@@ -148,7 +148,7 @@ def test_hessvec_out_of_fast_domain_on_halo_path(plp, ctx):
     eta = draw_eta(g.n, k, 21)
     for eps in (1e-300, 1e-9):
         Hv, AB, kern = gpu_hessvec(plp, ctx, g, U, eta, 1.5, 0, eps)
-        assert kern.startswith("edge_halo_kernel[adapt]"), kern
+        assert kern.startswith("edge_halo_kernel[") and "adapt" in kern, kern
         ref, _, _ = oracle_hessvec(g, U, eta, 1.5, 0, eps)
         assert colwise_relerr(Hv, ref) < TOL
 

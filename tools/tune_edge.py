@@ -16,10 +16,13 @@ VDIR = os.path.join(ROOT, "paper_2605_26975_b200", "variants")
 
 VARIANTS = {
     "trace": ["-DPLP_HALO_TRACE"],
+    "prod2": ["-DPLP_HALO_PROD=2"],
+    "prod2trace": ["-DPLP_HALO_PROD=2", "-DPLP_HALO_TRACE"],
     "checked": ["FULL", "-DPLP_DEBUG_CHECKS"],
     "t224b3": ["-DPLP_HALO_TILE_ROWS=224", "-DPLP_HALO_NBUF=3"],
     "t192": ["-DPLP_HALO_TILE_ROWS=192"],
     "t256": ["-DPLP_HALO_TILE_ROWS=256"],
+    "t256trace": ["-DPLP_HALO_TILE_ROWS=256", "-DPLP_HALO_TRACE"],
     "t192trace": ["-DPLP_HALO_TILE_ROWS=192", "-DPLP_HALO_TRACE"],
     "t192b3": ["-DPLP_HALO_TILE_ROWS=192", "-DPLP_HALO_NBUF=3"],
     "t160b3": ["-DPLP_HALO_TILE_ROWS=160", "-DPLP_HALO_NBUF=3"],
