@@ -32,7 +32,7 @@ constexpr int kHaloT = PLP_HALO_TILE;  // rows per tile (plp.h)
 #define PLP_HALO_PROD 1  // producer warps (the halo-row gathers are split between them)
 #endif
 constexpr int kHaloProd = PLP_HALO_PROD;
-constexpr int kHaloCWarps = 2 * (kHaloT / kSchedWindow);  // consumers: a warp pair per window
+constexpr int kHaloCWarps = 2 * (kHaloT / kSchedWindow);  // consumers: a warp pair per 32-row window
 constexpr int kHaloThreads = (kHaloCWarps + kHaloProd) * 32;  // + the producer warp(s)
 static_assert(kHaloT % kSchedWindow == 0 && kHaloThreads <= 1024, "tile map");
 
@@ -83,7 +83,7 @@ constexpr unsigned kHaloSmemMax = 225u * 1024u / PLP_HALO_CTAS;
 #define PLP_HALO_SLEEP_NS 64  // producer back-off between polls of the "empty" barrier
 #endif
 template <int K>
-constexpr int halo_cpl() { return K == 16 ? 4 : 2; }  // columns per lane (k = 8: 4 measured slower)
+constexpr int halo_cpl() { return K == 16 ? 4 : 2; }  // columns per lane (k = 8: 1 and 4 measured slower)
 
 // OBJ: objective-only pass (no eta, no G) on a symmetric graph: A_l = sum over the upper-triangle
 // edges (j > i) of w_ij |u_il - u_jl|^p, i.e. Eq. (1)'s numerator with each undirected edge once

@@ -143,7 +143,9 @@ __device__ __forceinline__ void edge_row_exact(const POW& pw, int e0, int e1, co
   }
 }
 
-template <int CPL, int LPR, class POW, bool HAS_ETA>
+// UNR_T: edges per gather batch (0: the PLP_EDGE_UNR default).  LPR need not divide 32 (k = 20:
+// 10 lanes x 2 columns, 3 rows per warp, 2 idle lanes): lanes past the last row group are idle.
+template <int CPL, int LPR, class POW, bool HAS_ETA, int UNR_T = 0>
 __global__ void __launch_bounds__(kEdgeThreads, PLP_EDGE_MINB) edge_kernel(EdgeArgs a, POW pw) {
   extern __shared__ double4 smem_raw[];
   if constexpr (POW::kNeedsTables) {
@@ -158,7 +160,8 @@ __global__ void __launch_bounds__(kEdgeThreads, PLP_EDGE_MINB) edge_kernel(EdgeA
   const int rows_per_iter = (blockDim.x >> 5) * RPW;
   const int k = a.k;
   const int c0 = li * CPL;
-  const bool active = c0 < k;  // k even when CPL is even, so a lane owns all or none of its columns
+  // k even when CPL is even, so a lane owns all or none of its columns
+  const bool active = c0 < k && grp < RPW;
   const double p = a.p;
   const double pp1 = p * (p - 1.0);
 
@@ -204,7 +207,7 @@ __global__ void __launch_bounds__(kEdgeThreads, PLP_EDGE_MINB) edge_kernel(EdgeA
       for (int c = 0; c < CPL; ++c) L[c] = HA[c] = 0.0;
 
       // edges in batches of UNR; the last batch is padded with weight-0 copies of the first edge
-      constexpr int UNR = (CPL <= 2) ? PLP_EDGE_UNR : (PLP_EDGE_UNR + 1) / 2;
+      constexpr int UNR = UNR_T > 0 ? UNR_T : (CPL <= 2) ? PLP_EDGE_UNR : (PLP_EDGE_UNR + 1) / 2;
       unsigned bad = 0;
       const int jpad = e0 < e1 ? __ldg(col + e0) : row;
       for (int e = e0; e < e1; e += UNR) {
@@ -280,14 +283,14 @@ __global__ void __launch_bounds__(kEdgeThreads, PLP_EDGE_MINB) edge_kernel(EdgeA
     const double* base = red + (q * CPL + c) * nt;
     double s = 0.0;
     for (int w = 0; w < (nt >> 5); ++w)
-      for (int gg = 0; gg < RPW; ++gg) s += base[w * 32 + gg * LPR + l];
+      for (int gg = 0; gg < RPW; ++gg) s += base[w * 32 + gg * LPR + l];  // idle lanes hold zeros
     a.partials[((int64_t)blockIdx.x * 4 + q) * k + cl] = s;
   }
 }
 
-template <int CPL, int LPR, class POW, bool HAS_ETA>
+template <int CPL, int LPR, class POW, bool HAS_ETA, int UNR_T = 0>
 plp_status launch_edge_shape(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int* grid_out) {
-  auto kern = edge_kernel<CPL, LPR, POW, HAS_ETA>;
+  auto kern = edge_kernel<CPL, LPR, POW, HAS_ETA, UNR_T>;
   const size_t red_bytes = (size_t)4 * CPL * kEdgeThreads * sizeof(double);
   const size_t tab_bytes = POW::kNeedsTables ? sizeof(PowTables) : 0;
   const size_t smem = red_bytes > tab_bytes ? red_bytes : tab_bytes;
@@ -306,7 +309,7 @@ plp_status launch_edge_shape(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int
   if (need < grid) grid = (int)(need > 0 ? need : 1);
   kern<<<grid, kEdgeThreads, smem, ctx->stream>>>(a, pw);
   PLP_LAUNCH_CHECK("edge_kernel");
-  note_edge_kernel("edge_kernel", 0, CPL, LPR, (CPL <= 2) ? PLP_EDGE_UNR : (PLP_EDGE_UNR + 1) / 2,
+  note_edge_kernel("edge_kernel", 0, CPL, LPR, UNR_T > 0 ? UNR_T : (CPL <= 2) ? PLP_EDGE_UNR : (PLP_EDGE_UNR + 1) / 2,
                    POW::kName, HAS_ETA);
   *grid_out = grid;
   return PLP_OK;
@@ -331,6 +334,13 @@ plp_status launch_edge_pow(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int* 
       if (quarter <= 4) PLP_SHAPE(4, 4);
       PLP_SHAPE(4, 8);
     }
+  }
+#ifndef PLP_EDGE_K20_UNR
+#define PLP_EDGE_K20_UNR 4  // k = 20 (C4): edges per gather batch (8 and 12 measured slower: registers)
+#endif
+  if (vec_ok && k == 20) {
+    return he ? launch_edge_shape<2, 10, POW, true, PLP_EDGE_K20_UNR>(ctx, a, pw, grid)
+              : launch_edge_shape<2, 10, POW, false, PLP_EDGE_K20_UNR>(ctx, a, pw, grid);
   }
   if (vec_ok) {
     const int half = k / 2;

@@ -19,6 +19,8 @@ VARIANTS = {
     "prod2": ["-DPLP_HALO_PROD=2"],
     "prod2trace": ["-DPLP_HALO_PROD=2", "-DPLP_HALO_TRACE"],
     "checked": ["FULL", "-DPLP_DEBUG_CHECKS"],
+    "k20u4": ["FULL", "-DPLP_EDGE_K20_UNR=4"],
+    "k20u12": ["FULL", "-DPLP_EDGE_K20_UNR=12"],
     "t224b3": ["-DPLP_HALO_TILE_ROWS=224", "-DPLP_HALO_NBUF=3"],
     "t192": ["-DPLP_HALO_TILE_ROWS=192"],
     "t256": ["-DPLP_HALO_TILE_ROWS=256"],
