@@ -107,6 +107,10 @@ __device__ __forceinline__ void cp_async_commit() {
 __device__ __forceinline__ void cp_async_wait_staged() {  // all but the most recent group
   asm volatile("cp.async.wait_group 1;" ::: "memory");
 }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {  // at most N of this thread's groups pending
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }

@@ -28,10 +28,7 @@
 namespace plp {
 
 constexpr int kHaloT = PLP_HALO_TILE;  // rows per tile (plp.h)
-#ifndef PLP_HALO_PROD
-#define PLP_HALO_PROD 1  // producer warps (the halo-row gathers are split between them)
-#endif
-constexpr int kHaloProd = PLP_HALO_PROD;
+constexpr int kHaloProd = 1;  // producer warps (2, splitting the halo gathers, measured slower)
 constexpr int kHaloCWarps = 2 * (kHaloT / kSchedWindow);  // consumers: a warp pair per 32-row window
 constexpr int kHaloThreads = (kHaloCWarps + kHaloProd) * 32;  // + the producer warp(s)
 static_assert(kHaloT % kSchedWindow == 0 && kHaloThreads <= 1024, "tile map");
@@ -232,8 +229,6 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
       if (lane == 0) fence_proxy_async();  // consumers' generic reads before the async refill
       __syncwarp();
       issue_tile(t, b, it % 3, (unsigned)(it / 3) & 1u);
-      // every producer warp is done with list slot it % 3 before producer 0 reuses slot (it + 2) % 3
-      if constexpr (kHaloProd > 1) asm volatile("bar.sync 1, %0;" ::"n"(32 * kHaloProd) : "memory");
       if (lane == 0 && pw_id == 0) PLP_TRACE(it, 1);
       if (lane == 0 && pw_id == 0) issue_list(t + 2 * ts, (it + 2) % 3);
       // warm L2 with the next tile's streamed parts (own rows, enc, w), so that its TMA copies,

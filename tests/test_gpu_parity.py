@@ -107,6 +107,9 @@ CASES = [
     ("C5t", 16, 1.8), ("C3t", 8, 1.5), ("C2t", 2, 1.1), ("iso", 4, 1.2), ("C1", 20, 1.2),
     # the paper's workload shape: Delaunay graph of 2^16 uniform points (NEXT-3), tile order
     ("D16t", 8, 1.2), ("D16t", 4, 1.5), ("D16t", 8, 2.0),
+    # k = 20 (C4's width): the ring-gather kernel -- isolated nodes (degree 0: padded batches),
+    # a 5-node path (one partial pass), generic power
+    ("iso", 20, 1.5), ("P5", 20, 1.2), ("C4s", 20, 1.37), ("C1", 20, 1.8),
 ]
 
 

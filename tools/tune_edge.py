@@ -16,20 +16,12 @@ VDIR = os.path.join(ROOT, "paper_2605_26975_b200", "variants")
 
 VARIANTS = {
     "trace": ["-DPLP_HALO_TRACE"],
-    "prod2": ["-DPLP_HALO_PROD=2"],
-    "prod2trace": ["-DPLP_HALO_PROD=2", "-DPLP_HALO_TRACE"],
+    "nb3": ["-DPLP_HALO_NBUF=3"],
+    "nb3trace": ["-DPLP_HALO_NBUF=3", "-DPLP_HALO_TRACE"],
     "checked": ["FULL", "-DPLP_DEBUG_CHECKS"],
-    "k20u4": ["FULL", "-DPLP_EDGE_K20_UNR=4"],
-    "k20u12": ["FULL", "-DPLP_EDGE_K20_UNR=12"],
-    "t224b3": ["-DPLP_HALO_TILE_ROWS=224", "-DPLP_HALO_NBUF=3"],
-    "t192": ["-DPLP_HALO_TILE_ROWS=192"],
-    "t256": ["-DPLP_HALO_TILE_ROWS=256"],
-    "t256trace": ["-DPLP_HALO_TILE_ROWS=256", "-DPLP_HALO_TRACE"],
-    "t192trace": ["-DPLP_HALO_TILE_ROWS=192", "-DPLP_HALO_TRACE"],
-    "t192b3": ["-DPLP_HALO_TILE_ROWS=192", "-DPLP_HALO_NBUF=3"],
-    "t160b3": ["-DPLP_HALO_TILE_ROWS=160", "-DPLP_HALO_NBUF=3"],
-    "t128b4": ["-DPLP_HALO_TILE_ROWS=128", "-DPLP_HALO_NBUF=4"],
-    "t128c2": ["-DPLP_HALO_TILE_ROWS=128", "-DPLP_HALO_CTAS=2"],
+    "ringS2": ["FULL", "-DPLP_RING_S=2"],
+    "ringE2S4": ["FULL", "-DPLP_RING_E=2", "-DPLP_RING_S=4"],
+    "ringE8S2": ["FULL", "-DPLP_RING_E=8", "-DPLP_RING_S=2"],
     "sleep0": ["-DPLP_HALO_SLEEP_NS=0"],
     "sleep256": ["-DPLP_HALO_SLEEP_NS=256"],
     # full builds (all k): staged-kernel occupancy for the random-graph configs (C4, k = 20)
