@@ -1,7 +1,6 @@
 // Edge-pass dispatcher per power policy (included by the edge_pol_<NAME>.cu instantiation units).
 #pragma once
 #include "edge_halo.cuh"
-#include "edge_ring.cuh"
 
 namespace plp {
 
@@ -36,13 +35,9 @@ plp_status launch_edge_any(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int* 
   if (!staged) {
     st = try_launch_halo(ctx, a, pw, grid, &used);
     if (st || used) return st;
-    // wide rows without a halo tiling (C4: k = 20 on a 10-D kNN graph): latency-bound L2 gathers,
-    // streamed through per-warp shared-memory rings (edge_ring.cuh); other k > 16: the row kernel
-    static const bool no_ring = getenv("PLP_EDGE_NORING") != nullptr;
-    if (!no_ring) {
-      st = try_launch_ring(ctx, a, pw, grid, &used);
-      if (st || used) return st;
-    }
+    // wide rows without a halo tiling (C4: k = 20 on a 10-D kNN graph): latency-bound L2 gathers;
+    // the row kernel (10 lanes x 2 columns at k = 20) keeps the most warps resident (a per-warp
+    // shared-memory ring of cp.async-gathered rows measured slower: 2.3-3.8 against 1.63 ms)
     if (a.k > 16) return launch_edge_pow(ctx, a, pw, grid);
   }
   return launch_staged_pow(ctx, a, pw, grid);

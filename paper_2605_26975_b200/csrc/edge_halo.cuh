@@ -37,18 +37,24 @@ static_assert(kHaloT % kSchedWindow == 0 && kHaloThreads <= 1024, "tile map");
 struct HaloLayout {
   unsigned rp, sched, nl, enc, w, U, E, bytes;
 };
+// Staged halo rows per tile at most (the U / eta row blocks have a fixed size, so the eta rows sit
+// at a compile-time offset from the U rows and the consumers address both with one register);
+// tiles with more halo rows run in overflow mode.
+__host__ __device__ constexpr int halo_rows_cap(int k) { return k <= 4 ? 704 : k == 8 ? 352 : 96; }
+
 __host__ __device__ inline HaloLayout halo_layout(int k, int ext_cap, int nnz_cap, bool obj = false,
                                                   bool eta = true) {
   HaloLayout L;
+  (void)ext_cap;
   unsigned o = 0;
+  L.U = o; o += (unsigned)(kHaloT + halo_rows_cap(k)) * (unsigned)k * 8u;
+  L.E = o; o += eta ? (unsigned)(kHaloT + halo_rows_cap(k)) * (unsigned)k * 8u : 0u;
   L.rp = o; o += (kHaloT + 8) * 4;
   L.sched = o; o += kHaloT * 4;
   L.nl = o; o += obj ? (kHaloT + 8) * 4 : 0u;  // lower-edge counts (objective mode only)
   L.enc = o; o += (unsigned)(nnz_cap + 16) * 4;
   o = (o + 15u) & ~15u;
   L.w = o; o += (unsigned)(nnz_cap + 16) * 8;
-  L.U = o; o += (unsigned)(kHaloT + ext_cap) * (unsigned)k * 8u;
-  L.E = o; o += eta ? (unsigned)(kHaloT + ext_cap) * (unsigned)k * 8u : 0u;
   L.bytes = (o + 127u) & ~127u;
   return L;
 }
@@ -272,8 +278,8 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
     const int eb = rp_s[0];
     const int* enc_s = reinterpret_cast<const int*>(B + Ly.enc) - (eb & ~3);
     const double* w_s = reinterpret_cast<const double*>(B + Ly.w) - (eb & ~1);
-    const double* tU = reinterpret_cast<const double*>(B + Ly.U) + c0;
-    const double* tE = reinterpret_cast<const double*>(B + Ly.E) + c0;
+    const double* tU = reinterpret_cast<const double*>(B) + c0;  // Ly.U == 0
+    const double* tE = tU + (kHaloT + halo_rows_cap(K)) * K;   // Ly.E: a compile-time offset
     // neighbour rows: tile-local index x; OVF: x >= kHaloT + ext_cap is an unstaged halo row, read
     // through its global id in the tile's (global) halo list
     const int* glist = a.halo_ext + tt * LSG + 4 - kHaloT;
@@ -550,6 +556,7 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
 // Halo rows staged per tile: the whole halo (ext_cap) if the buffers fit, else the largest multiple
 // of 4 that fits (overflow mode); 0 if not even 64 rows fit.
 inline int halo_stage_rows(int k, int ext_cap, int nnz_cap, bool tables, bool obj, bool eta, int nb) {
+  ext_cap = ext_cap < halo_rows_cap(k) ? ext_cap : halo_rows_cap(k);
   if (halo_smem_bytes(k, ext_cap, nnz_cap, tables, obj, eta, nb) <= kHaloSmemMax) return ext_cap;
   int lo = 0, hi = ext_cap;
   while (hi - lo > 4) {
@@ -565,7 +572,7 @@ plp_status launch_halo_shape(plp_ctx* ctx, const EdgeArgs& a0, const POW& pw, in
   const bool T = POW::kNeedsTables;
   // passes without eta stage U rows only: a third buffer fits where the eta pass has two
   constexpr int NB3 = HAS_ETA ? kHaloNBuf : PLP_HALO_NBUF_NOETA;
-  const bool deep = NB3 != kHaloNBuf &&
+  const bool deep = NB3 != kHaloNBuf && a.halo_ext_cap <= halo_rows_cap(K) &&
                     halo_smem_bytes(K, a.halo_ext_cap, a.halo_nnz_cap, T, OBJ, HAS_ETA, NB3) <= kHaloSmemMax;
   const int nb = deep ? NB3 : kHaloNBuf;
   a.halo_stage = halo_stage_rows(K, a.halo_ext_cap, a.halo_nnz_cap, T, OBJ, HAS_ETA, nb);
@@ -621,7 +628,8 @@ plp_status try_launch_halo(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int* 
   if (halo_stage_rows(k, a.halo_ext_cap, a.halo_nnz_cap, POW::kNeedsTables, false, true, kHaloNBuf) == 0)
     return PLP_OK;  // not even 64 halo rows per tile fit: the staged kernel
   if (he && a.want_dots &&
-      halo_smem_bytes(k, a.halo_ext_cap, a.halo_nnz_cap, POW::kNeedsTables) > kHaloSmemMax)
+      halo_stage_rows(k, a.halo_ext_cap, a.halo_nnz_cap, POW::kNeedsTables, false, true, kHaloNBuf) <
+          a.halo_ext_cap)
     return PLP_OK;  // full-mode dots with an overflowing halo: the staged kernel
   *used = true;
   const bool obj = !he && a.G == nullptr && a.upper_ok && a.nlow != nullptr && a.sched_up != nullptr;

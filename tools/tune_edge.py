@@ -19,9 +19,6 @@ VARIANTS = {
     "nb3": ["-DPLP_HALO_NBUF=3"],
     "nb3trace": ["-DPLP_HALO_NBUF=3", "-DPLP_HALO_TRACE"],
     "checked": ["FULL", "-DPLP_DEBUG_CHECKS"],
-    "ringS2": ["FULL", "-DPLP_RING_S=2"],
-    "ringE2S4": ["FULL", "-DPLP_RING_E=2", "-DPLP_RING_S=4"],
-    "ringE8S2": ["FULL", "-DPLP_RING_E=8", "-DPLP_RING_S=2"],
     "sleep0": ["-DPLP_HALO_SLEEP_NS=0"],
     "sleep256": ["-DPLP_HALO_SLEEP_NS=256"],
     # full builds (all k): staged-kernel occupancy for the random-graph configs (C4, k = 20)
