@@ -232,6 +232,7 @@ using namespace plp;
 
 static EdgeArgs graph_args(const plp_graph* g) {
   EdgeArgs a{};
+  a.need_ab = 1;
   a.n_rows = g->n_rows;
   a.n_cols = g->n_cols;
   a.rp = g->rp;
@@ -409,15 +410,22 @@ extern "C" plp_status plp_hessvec(plp_ctx* ctx, const plp_graph* g, int k, const
     return set_error(PLP_ERR_ARG, "full mode needs G_in (the Euclidean gradient at U)");
   const bool full = mode == PLP_HESS_FULL;
   const bool coll = collective(ctx, g);
-  if (!coll) {
-    st = plp_edge_pass(ctx, g, k, U, eta, p, eps, AB_in, nullptr, full ? scratch_dots(ctx) : nullptr,
-                       nullptr, Hv);
-    if (st || !full) return st;
+  if (!coll && full) {
+    st = plp_edge_pass(ctx, g, k, U, eta, p, eps, AB_in, nullptr, scratch_dots(ctx), nullptr, Hv);
+    if (st) return st;
+  } else if (!coll) {  // sparse: a Hessian-vector-only pass (no gradient sum, no A, B partials)
+    EdgeArgs a = graph_args(g);
+    a.k = k; a.U = U; a.eta = eta; a.AB = AB_in; a.Hv = Hv; a.p = p; a.eps = eps;
+    a.partials = ctx->partials;
+    a.need_ab = 0;
+    int grid = 0;
+    return launch_edge(ctx, a, &grid);
   } else {
     EdgeArgs a = graph_args(g);
     a.k = k; a.U = U; a.eta = eta; a.AB = AB_in; a.Hv = Hv; a.p = p; a.eps = eps;
     a.partials = ctx->partials;
     a.want_dots = full;
+    a.need_ab = 0;
     int grid = 0;
     if ((st = overlapped_pass(ctx, g, a, u_current ? nullptr : U, eta, &grid))) return st;
     if (!full) return PLP_OK;

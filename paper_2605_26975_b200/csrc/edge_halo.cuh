@@ -116,8 +116,10 @@ static __device__ long long g_halo_trace[160 * kTraceTiles * kTraceSlots];
 // OVF: some tile's halo exceeds what fits in shared memory (a.halo_stage rows are staged, the rest
 // -- the tile's least referenced halo rows, the list being ordered by reference count -- are read
 // from global memory / L2 by the consumers; C3's random long-range edges).
-template <int K, class POW, bool HAS_ETA, bool OBJ, int NB, bool ADAPT, bool DOTS, bool OVF>
+// HVO: Hessian-vector product only (plp_hessvec, sparse mode: no gradient sum L, no A, B partials).
+template <int K, class POW, bool HAS_ETA, bool OBJ, int NB, bool ADAPT, bool DOTS, bool OVF, bool HVO = false>
 __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(POW pw, EdgeArgs a) {
+  constexpr bool WL = !HVO;
   static_assert(!(OBJ && HAS_ETA), "objective mode has no eta");
   constexpr int CPL = halo_cpl<K>(), LPR = K / CPL, RPW = 32 / LPR;  // rows per pass
   extern __shared__ __align__(16) unsigned char smem[];
@@ -432,8 +434,8 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
           ldE(x0, ej0);
           ldE(x1, ej1);
         }
-        edge_update_mx<CPL, POW, HAS_ETA>(pw, w0, ui, uj0, ei, ej0, L, HA, mx);
-        edge_update_mx<CPL, POW, HAS_ETA>(pw, w1, ui, uj1, ei, ej1, L, HA, mx);
+        edge_update_mx<CPL, POW, HAS_ETA, WL>(pw, w0, ui, uj0, ei, ej0, L, HA, mx);
+        edge_update_mx<CPL, POW, HAS_ETA, WL>(pw, w1, ui, uj1, ei, ej1, L, HA, mx);
       }
       if (e < e1) {
         const int x0 = enc_s[e];
@@ -441,7 +443,7 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
         double uj0[CPL], ej0[CPL];
         ldU(x0, uj0);
         if constexpr (HAS_ETA) ldE(x0, ej0);
-        edge_update_mx<CPL, POW, HAS_ETA>(pw, w0, ui, uj0, ei, ej0, L, HA, mx);
+        edge_update_mx<CPL, POW, HAS_ETA, WL>(pw, w0, ui, uj0, ei, ej0, L, HA, mx);
       }
       // node terms sn = cap(|u|)^{p-2}, tn = |u|^{p-1}, after the edges (fewer live registers in
       // the edge loop); same fast-domain test, exact recomputation of the row when it fails
@@ -486,15 +488,15 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
               ldE(x0, ej0);
               ldE(x1, ej1);
             }
-            edge_update_capsel<CPL, POW, HAS_ETA>(pw, w_s[ee], ui, uj0, ei, ej0, L, HA, rg);
-            edge_update_capsel<CPL, POW, HAS_ETA>(pw, w_s[ee + 1], ui, uj1, ei, ej1, L, HA, rg);
+            edge_update_capsel<CPL, POW, HAS_ETA, WL>(pw, w_s[ee], ui, uj0, ei, ej0, L, HA, rg);
+            edge_update_capsel<CPL, POW, HAS_ETA, WL>(pw, w_s[ee + 1], ui, uj1, ei, ej1, L, HA, rg);
           }
           if (ee < e1) {
             const int x0 = enc_s[ee];
             double uj0[CPL], ej0[CPL];
             ldU(x0, uj0);
             if constexpr (HAS_ETA) ldE(x0, ej0);
-            edge_update_capsel<CPL, POW, HAS_ETA>(pw, w_s[ee], ui, uj0, ei, ej0, L, HA, rg);
+            edge_update_capsel<CPL, POW, HAS_ETA, WL>(pw, w_s[ee], ui, uj0, ei, ej0, L, HA, rg);
           }
           if (rg.bad()) edge_row_exact<CPL, POW, HAS_ETA>(pw, e0, e1, a.col, a.w, a.U, a.eta, K, c0, ui, ei, L, HA);
 #pragma unroll
@@ -507,10 +509,12 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
       double g[CPL], hv[CPL];
 #pragma unroll
       for (int cc = 0; cc < CPL; ++cc) {
-        accA[cc] = fma(ui[cc], L[cc], accA[cc]);
-        accB[cc] = fma(tn[cc], fabs(ui[cc]), accB[cc]);
+        if constexpr (!HVO) {
+          accA[cc] = fma(ui[cc], L[cc], accA[cc]);
+          accB[cc] = fma(tn[cc], fabs(ui[cc]), accB[cc]);
+        }
         const double phi = copysign(tn[cc], ui[cc]);
-        g[cc] = cG[cc] * (L[cc] - cAB[cc] * phi);
+        g[cc] = HVO ? 0.0 : cG[cc] * (L[cc] - cAB[cc] * phi);
         if constexpr (HAS_ETA) {
           hv[cc] = cHA[cc] * HA[cc] - cHB[cc] * sn[cc] * ei[cc];
           if constexpr (DOTS) {
@@ -521,7 +525,7 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
           hv[cc] = 0.0;
         }
       }
-      if (a.G != nullptr) st_vec<CPL>(a.G + (int64_t)row * K + c0, g);
+      if (!HVO && a.G != nullptr) st_vec<CPL>(a.G + (int64_t)row * K + c0, g);
       if constexpr (HAS_ETA) {
         if (a.Hv != nullptr) st_vec<CPL>(a.Hv + (int64_t)row * K + c0, hv);
       }
@@ -580,7 +584,9 @@ plp_status launch_halo_shape(plp_ctx* ctx, const EdgeArgs& a0, const POW& pw, in
   // the fused F/G/Hv pass (G and eta) keeps the plain loop; every other pass adapts
   const bool adapt = !(HAS_ETA && a.G != nullptr);
   const bool dots = HAS_ETA && a.want_dots;
+  const bool hvo = HAS_ETA && !OBJ && adapt && !dots && a.G == nullptr && !a.need_ab;
   auto kern = deep ? edge_halo_kernel<K, POW, HAS_ETA, OBJ, NB3, true, false, false>
+            : (hvo && !ovf) ? edge_halo_kernel<K, POW, HAS_ETA, OBJ, kHaloNBuf, true, false, false, HAS_ETA && !OBJ>
             : ovf  ? (adapt ? edge_halo_kernel<K, POW, HAS_ETA, OBJ, kHaloNBuf, true, false, true>
                             : edge_halo_kernel<K, POW, HAS_ETA, OBJ, kHaloNBuf, false, false, true>)
                    : (adapt ? (dots ? edge_halo_kernel<K, POW, HAS_ETA, OBJ, kHaloNBuf, true, HAS_ETA, false>
@@ -590,8 +596,8 @@ plp_status launch_halo_shape(plp_ctx* ctx, const EdgeArgs& a0, const POW& pw, in
   const unsigned smem = halo_smem_bytes(K, ovf ? a.halo_stage : a.halo_ext_cap, a.halo_nnz_cap, T, OBJ, HAS_ETA, nb);
   // the dynamic shared-memory opt-in is a per-device function attribute: set it on this ctx's
   // device whenever a launch needs more than the value set so far (per template instance)
-  static unsigned attr_set[64][7] = {};
-  const int vi = deep ? 4 : ovf ? 5 + (adapt ? 1 : 0) : (adapt ? 1 : 0) + (dots ? 2 : 0);
+  static unsigned attr_set[64][8] = {};
+  const int vi = deep ? 4 : (hvo && !ovf) ? 7 : ovf ? 5 + (adapt ? 1 : 0) : (adapt ? 1 : 0) + (dots ? 2 : 0);
   unsigned& set_to = attr_set[ctx->device & 63][vi];
   if (set_to < smem) {
     PLP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -608,6 +614,7 @@ plp_status launch_halo_shape(plp_ctx* ctx, const EdgeArgs& a0, const POW& pw, in
   char name[96];
   snprintf(name, sizeof(name), "edge_halo_kernel%s", OBJ ? (deep ? "[objective,3buf,adapt]" : ovf ? "[objective,ovf,adapt]" : "[objective,adapt]")
                                                          : deep ? "[3buf,adapt]" : ovf ? (adapt ? "[ovf,adapt]" : "[ovf]")
+                                                         : (hvo && !ovf) ? "[adapt,hv]"
                                                          : adapt ? "[adapt]" : "");
   note_edge_kernel(name, K, halo_cpl<K>(), K / halo_cpl<K>(), 2, POW::kName, HAS_ETA);
   *grid_out = (int)grid;

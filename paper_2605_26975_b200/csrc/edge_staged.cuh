@@ -85,7 +85,7 @@ struct CapRange {
     return (mn * 2u < pw.fast_lo2) | (mx * 2u - pw.fast_lo2 >= pw.fast_span2);
   }
 };
-template <int CPL, class POW, bool HAS_ETA>
+template <int CPL, class POW, bool HAS_ETA, bool WANT_L = true>
 __device__ __forceinline__ void edge_update_capsel(const POW& pw, double wv, const double (&ui)[CPL],
                                                    const double (&uj)[CPL], const double (&ei)[CPL],
                                                    const double (&ej)[CPL], double (&L)[CPL],
@@ -99,7 +99,7 @@ __device__ __forceinline__ void edge_update_capsel(const POW& pw, double wv, con
     rg.mnz = min(rg.mnz, ahi - 1u);
     rg.mx = max(rg.mx, ahi);
     const double wsr = wv * pw.pow_fast(fmax(fabs(d), 0x1p-120));  // w |d|^{p-2}
-    L[c] = fma(wsr, d, L[c]);                                       // w phi_p(d)
+    if constexpr (WANT_L) L[c] = fma(wsr, d, L[c]);                 // w phi_p(d)
     if constexpr (HAS_ETA) HA[c] = fma(fmin(wsr, wcap), ei[c] - ej[c], HA[c]);  // w cap(|d|)^{p-2}
   }
 }
@@ -107,7 +107,8 @@ __device__ __forceinline__ void edge_update_capsel(const POW& pw, double wv, con
 // One stored edge for the lane's CPL columns (branch-free); `mx` collects the fast-domain test
 // (hi word of |d| relative to the lower bound, unsigned max: >= fast_span2 means some |d| left
 // the domain and the row is recomputed exactly).
-template <int CPL, class POW, bool HAS_ETA>
+// WANT_L = false: the Hessian-vector-only passes skip the gradient sum L.
+template <int CPL, class POW, bool HAS_ETA, bool WANT_L = true>
 __device__ __forceinline__ void edge_update_mx(const POW& pw, double wv, const double (&ui)[CPL],
                                                const double (&uj)[CPL], const double (&ei)[CPL],
                                                const double (&ej)[CPL], double (&L)[CPL],
@@ -117,12 +118,12 @@ __device__ __forceinline__ void edge_update_mx(const POW& pw, double wv, const d
   for (int c = 0; c < CPL; ++c) {
     const double d = ui[c] - uj[c];
     if constexpr (POW::kIsP2) {
-      L[c] = fma(wv, d, L[c]);
+      if constexpr (WANT_L) L[c] = fma(wv, d, L[c]);
       if constexpr (HAS_ETA) HA[c] = fma(wv, ei[c] - ej[c], HA[c]);
     } else {
       h2[c] = (unsigned)__double2hiint(d) * 2u - pw.fast_lo2;
       const double wsr = wv * pw.pow_fast(d);  // w |d|^{p-2}
-      L[c] = fma(wsr, d, L[c]);                // w phi_p(d)
+      if constexpr (WANT_L) L[c] = fma(wsr, d, L[c]);  // w phi_p(d)
       if constexpr (HAS_ETA) HA[c] = fma(wsr, ei[c] - ej[c], HA[c]);
     }
   }

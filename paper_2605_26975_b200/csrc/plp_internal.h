@@ -136,6 +136,7 @@ struct EdgeArgs {
   double p, eps;
   double* partials;     // [grid][4][k]: A, B, alpha, gamma partial sums
   int want_dots;
+  int need_ab;   // the caller reduces the A, B partials (0: a Hessian-vector-only pass may skip them)
   // staged kernel (edge_staged.cuh): largest chunk nnz of the graph, ring slot capacity
   int max_chunk_nnz, chunk_cap;
   int ldx;  // row stride (elements) of U and eta in the staged kernel; 0 = k (contiguous)
