@@ -99,8 +99,9 @@ constexpr int halo_cpl() { return K == 16 ? 4 : 2; }  // columns per lane (k = 8
 #ifdef PLP_HALO_TRACE
 // Pipeline trace (tools/trace_halo.py; a build flag, never in the product build): clock64 per tile
 // iteration: [0] producer past the "empty" wait, [1] producer done issuing, [2 + w] consumer warp w
-// past the "full" wait, [16 + w] consumer warp w released the buffer.
-constexpr int kTraceTiles = 320, kTraceSlots = 32;
+// past the "full" wait, [16 + w] consumer warp w released the buffer, [32..34] producer past the
+// list wait / done with the TMA copies / done with the halo gathers.
+constexpr int kTraceTiles = 320, kTraceSlots = 36;
 static __device__ long long g_halo_trace[160 * kTraceTiles * kTraceSlots];
 #define PLP_TRACE(it, slot)                                                                         \
   do {                                                                                              \
@@ -174,6 +175,8 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
     mbar_expect_tx(&lbar[q], (unsigned)LS * 4u);
     tma_bulk_g2s(lists + q * LS, a.halo_ext + tile_of(t) * LSG, (unsigned)LS * 4u, &lbar[q]);
   };
+  int trace_it = 0;  // the producer's iteration (pipeline trace build only)
+  (void)trace_it;
   // (producer warp) stage tile t into buffer b; its halo list is in slot q (use parity lph)
   auto issue_tile = [&](int64_t t, int b, int q, unsigned lph) {
     if (t >= n_tiles) return;
@@ -181,6 +184,7 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
     const int r0 = (int)(tile_of(t) * kHaloT), r1 = min(r0 + kHaloT, n_rows);
     constexpr unsigned RB = K * 8u;  // bytes per row
     mbar_wait(&lbar[q], lph);
+    if (lane == 0 && pw_id == 0) PLP_TRACE(trace_it, 32);
     const int* Lq = lists + q * LS;
     const int nx = OVF ? min(Lq[0], ext_cap) : Lq[0];  // rows staged (OVF: the first ext_cap)
     PLP_DCHECK(nx >= 0 && nx <= ext_cap, "halo count within the tile's list slot");
@@ -203,6 +207,7 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
       }
       tma_bulk_g2s(B + Ly.U, a.U + (int64_t)r0 * K, own_b, &full[b]);
       if constexpr (HAS_ETA) tma_bulk_g2s(B + Ly.E, a.eta + (int64_t)r0 * K, own_b, &full[b]);
+      PLP_TRACE(trace_it, 33);
     }
     // halo rows: PPR lanes per row, 32 / PPR rows per warp instruction
     constexpr int PPR = K / 2, RPI = 32 / PPR;
@@ -215,6 +220,7 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
       cp_async16(B + Ly.U + off, a.U + (int64_t)j * K + 2 * pc);
       if constexpr (HAS_ETA) cp_async16(B + Ly.E + off, a.eta + (int64_t)j * K + 2 * pc);
     }
+    if (lane == 0 && pw_id == 0) PLP_TRACE(trace_it, 34);
     cp_async_mbar_arrive(&full[b]);
   };
 
@@ -236,6 +242,7 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
       if (lane == 0 && pw_id == 0) PLP_TRACE(it, 0);
       if (lane == 0) fence_proxy_async();  // consumers' generic reads before the async refill
       __syncwarp();
+      trace_it = it;
       issue_tile(t, b, it % 3, (unsigned)(it / 3) & 1u);
       if (lane == 0 && pw_id == 0) PLP_TRACE(it, 1);
       if (lane == 0 && pw_id == 0) issue_list(t + 2 * ts, (it + 2) % 3);

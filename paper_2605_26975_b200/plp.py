@@ -403,9 +403,22 @@ def tcg_init(ctx: Context, grad, delta: float, kappa: float, theta: float, eta, 
         "plp_tcg_init")
 
 
+def _tcg_vectors(g: Graph, k: int, eta, Heta, r, dlt, Hd):
+    """The tCG vectors have the graph's owned rows (n_rows x k); the direction dlt, a Hessian-vector
+    input, has n_cols rows (halo slots on a multi-rank graph).  libplp writes n_rows x k doubles to
+    each, so a mis-sized tensor is refused here."""
+    for name, t in (("eta", eta), ("r", r), ("Hd", Hd)):
+        _dev(t, name, shape=(g.n_rows, k))
+    if Heta is not None:
+        _dev(Heta, "Heta", shape=(g.n_rows, k))
+    if tuple(dlt.shape) not in ((g.n_rows, k), (g.n_cols, k)):
+        raise ValueError(f"dlt: shape {tuple(dlt.shape)}, expected ({g.n_rows} or {g.n_cols}, {k})")
+
+
 def tcg_run(ctx: Context, g: Graph, U, AB, G_in, S, p: float, eps: float, mode: int, eta, Heta, r, dlt,
             Hd, scal, status, max_iters: int, iters: int, fused: bool = False):
     k = U.shape[1]
+    _tcg_vectors(g, k, eta, Heta, r, dlt, Hd)
     _ck(_lib.plp_tcg_run(ctx.h, g.h, k, _dev(U, "U", shape=(g.n_cols, k)), _dev(AB, "AB", shape=(2 * k,)),
                          _dev(G_in, "G_in", shape=(g.n_rows, k), nullable=True), _dev(S, "S", shape=(k, k)),
                          C_D(p), C_D(eps), int(mode), _dev(eta, "eta"), _dev(Heta, "Heta", nullable=True), _dev(r, "r"),
@@ -420,6 +433,7 @@ class TcgGraph:
     def __init__(self, ctx: Context, g: Graph, U, AB, G_in, S, p: float, eps: float, mode: int, eta, Heta, r,
                  dlt, Hd, scal, status, max_iters: int, iters: int, fused: bool = False):
         k = U.shape[1]
+        _tcg_vectors(g, k, eta, Heta, r, dlt, Hd)
         h = VP()
         self.ctx = ctx
         self.keep = (U, AB, G_in, S, eta, Heta, r, dlt, Hd, scal, status)  # pointers baked into the graph

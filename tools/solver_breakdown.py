@@ -18,7 +18,7 @@ from bench import get_graph  # noqa: E402
 from paper_2605_26975_b200 import plp, solver  # noqa: E402
 from plp_inputs import draw_U, draw_uniforms  # noqa: E402
 
-FAMILIES = [("edge pass (a3-a7)", ("edge_halo", "edge_staged", "edge_kernel", "edge_tiled", "edge_finalize",
+FAMILIES = [("edge pass (a3-a7)", ("edge_halo", "edge_staged", "edge_kernel", "edge_finalize",
                                    "full_epilogue", "objective_from")),
             ("tCG fused passes (NEXT-2)", ("tcg_gram_a", "tcg_update", "tcg_finish", "tcg_reduce", "tcg_expand")),
             ("tCG scalars / axpby (NEXT-1)", ("tcg_", "axpby_dev")),

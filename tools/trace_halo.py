@@ -20,7 +20,7 @@ from bench import get_graph, CONFIG_KP  # noqa: E402
 from paper_2605_26975_b200 import plp  # noqa: E402
 from plp_inputs import draw_U, draw_eta  # noqa: E402
 
-TT, SL = 320, 32
+TT, SL = 320, 36
 
 
 def main():
@@ -68,6 +68,9 @@ def main():
         "issue_to_ready_p90": float(np.percentile(issue_to_ready, 90)),
         "producer_reaction_median": float(np.median(react)),
         "producer_issue_cycles_median": float(np.median(P1 - P0)),
+        "producer_list_wait_median": float(np.median(T[:, :, 32] - P0)),
+        "producer_tma_issue_median": float(np.median(T[:, :, 33] - T[:, :, 32])),
+        "producer_halo_gather_issue_median": float(np.median(T[:, :, 34] - T[:, :, 33])),
         "warp_compute_by_warp": [float(np.median(comp[:, :, w])) for w in range(NC)],
     }
     print(json.dumps(out, indent=1))
