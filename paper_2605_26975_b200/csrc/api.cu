@@ -175,9 +175,10 @@ static plp_status build_halo_tiles(plp_graph* g, const int64_t* rp, const int32_
     max_nnz = std::max<int64_t>(max_nnz, rp[r1] - rp[r0]);
   }
   // no locality (generator-order graphs, C4's 10-D kNN graph: ~7-10 outside rows per tile row):
-  // halo tiles would mostly overflow to L2, and the staged / ring kernels do better (measured
-  // 3.5 ms against 3.1 ms at C5 in generator order)
-  if ((double)xs.size() > 1.5 * (double)T * (double)nt) return PLP_OK;
+  // halo tiles would mostly overflow to L2, and the staged / row kernels do better (measured
+  // 3.5 ms against 3.1 ms at C5 in generator order); C3's 3-D grid (1.6 halo rows per tile row)
+  // keeps them (overflow mode, 0.24 against 0.34 ms staged)
+  if ((double)xs.size() > 3.0 * (double)T * (double)nt) return PLP_OK;
   const int ext_cap = (max_ext + 3) & ~3, nnz_cap = (max_nnz + 3) & ~3;
 #ifndef PLP_HALO_NBUF
 #define PLP_HALO_NBUF 2

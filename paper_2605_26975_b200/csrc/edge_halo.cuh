@@ -40,7 +40,7 @@ struct HaloLayout {
 // Staged halo rows per tile at most (the U / eta row blocks have a fixed size, so the eta rows sit
 // at a compile-time offset from the U rows and the consumers address both with one register);
 // tiles with more halo rows run in overflow mode.
-__host__ __device__ constexpr int halo_rows_cap(int k) { return k <= 4 ? 704 : k == 8 ? 352 : 96; }
+__host__ __device__ constexpr int halo_rows_cap(int k) { return k <= 4 ? 800 : k == 8 ? 400 : 96; }
 
 __host__ __device__ inline HaloLayout halo_layout(int k, int ext_cap, int nnz_cap, bool obj = false,
                                                   bool eta = true) {
