@@ -11,3 +11,5 @@ done
 timeout 1800 python tools/quality_study.py D16 D20 D21 D22 D23 > gpurun_out/quality_$TAG.jsonl 2> gpurun_out/quality_$TAG.err
 PLP_LIB=paper_2605_26975_b200/variants/trace/libplp.so python tools/trace_halo.py > gpurun_out/trace_$TAG.json 2>&1
 echo DONE > gpurun_out/next4_done_$TAG.txt
+for c in C5 C3 C4 D23; do python bench.py --config $c --steps 10 --warmup 3 --no-cpu --no-e2e --no-variants > gpurun_out/bench_${TAG}_$c.json 2>/dev/null; done
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_hessvec.py -q -x -p no:cacheprovider > gpurun_out/par_$TAG.log 2>&1
