@@ -82,12 +82,6 @@ __host__ __device__ inline unsigned halo_smem_bytes(int k, int ext_cap, int nnz_
 #endif
 constexpr unsigned kHaloSmemMax = 225u * 1024u / PLP_HALO_CTAS;
 
-#ifndef PLP_HALO_GFIRST
-#define PLP_HALO_GFIRST 0
-#endif
-#ifndef PLP_HALO_PFL2
-#define PLP_HALO_PFL2 0  // experiment: L2 prefetch of the next tile's halo rows (prefetch.global.L2)
-#endif
 #ifndef PLP_HALO_SLEEP_NS
 #define PLP_HALO_SLEEP_NS 64  // producer back-off between polls of the "empty" barrier
 #endif
@@ -194,40 +188,6 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
     const int* Lq = lists + q * LS;
     const int nx = OVF ? min(Lq[0], ext_cap) : Lq[0];  // rows staged (OVF: the first ext_cap)
     PLP_DCHECK(nx >= 0 && nx <= ext_cap, "halo count within the tile's list slot");
-#if PLP_HALO_GFIRST  // experiment: the halo gathers (the longer latency) before the TMA copies
-    // halo rows: PPR lanes per row, 32 / PPR rows per warp instruction
-    constexpr int PPR = K / 2, RPI = 32 / PPR;
-    const int rl = lane / PPR + pw_id * RPI, pc = lane % PPR;
-#pragma unroll 4
-    for (int x = rl; x < nx; x += RPI * kHaloProd) {
-      const int j = Lq[4 + x];
-      PLP_DCHECK(j >= 0 && (int64_t)j < a.n_cols && (j < r0 || j >= r1), "halo column outside the tile, inside U");
-      const unsigned off = ((unsigned)(kHaloT + x) * K + 2 * pc) * 8u;
-      cp_async16(B + Ly.U + off, a.U + (int64_t)j * K + 2 * pc);
-      if constexpr (HAS_ETA) cp_async16(B + Ly.E + off, a.eta + (int64_t)j * K + 2 * pc);
-    }
-    if (lane == 0 && pw_id == 0) {
-      const int eb = Lq[1], ee = Lq[2];
-      PLP_DCHECK(ee - eb >= 0 && ee - eb <= a.halo_nnz_cap, "tile nnz within the buffer");
-      PLP_DCHECK(eb == (int)a.rp[r0] && ee == (int)a.rp[r1], "tile CSR bounds match row_ptr");
-      const unsigned rp_b = (unsigned)(((r1 + 1 + 3) & ~3) - r0) * 4u;
-      const unsigned sc_b = (unsigned)(((r1 + 3) & ~3) - r0) * 4u;
-      const int cb = eb & ~3, ce = (ee + 3) & ~3, wb = eb & ~1, we = (ee + 1) & ~1;
-      const unsigned enc_b = (unsigned)(ce - cb) * 4u, w_b = (unsigned)(we - wb) * 8u;
-      const unsigned own_b = (unsigned)(r1 - r0) * RB;
-      mbar_expect_tx(&full[b], rp_b + (OBJ ? 2u : 1u) * sc_b + enc_b + w_b + (HAS_ETA ? 2u : 1u) * own_b);
-      tma_bulk_g2s(B + Ly.rp, a.rp + r0, rp_b, &full[b]);
-      tma_bulk_g2s(B + Ly.sched, (OBJ ? a.sched_up : a.sched) + r0, sc_b, &full[b]);
-      if constexpr (OBJ) tma_bulk_g2s(B + Ly.nl, a.nlow + r0, sc_b, &full[b]);
-      if (enc_b) {
-        tma_bulk_g2s(B + Ly.enc, a.halo_enc + cb, enc_b, &full[b]);
-        tma_bulk_g2s(B + Ly.w, a.w + wb, w_b, &full[b]);
-      }
-      tma_bulk_g2s(B + Ly.U, a.U + (int64_t)r0 * K, own_b, &full[b]);
-      if constexpr (HAS_ETA) tma_bulk_g2s(B + Ly.E, a.eta + (int64_t)r0 * K, own_b, &full[b]);
-      PLP_TRACE(trace_it, 33);
-    }
-#else
     if (lane == 0 && pw_id == 0) {
       const int eb = Lq[1], ee = Lq[2];
       PLP_DCHECK(ee - eb >= 0 && ee - eb <= a.halo_nnz_cap, "tile nnz within the buffer");
@@ -260,7 +220,6 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
       cp_async16(B + Ly.U + off, a.U + (int64_t)j * K + 2 * pc);
       if constexpr (HAS_ETA) cp_async16(B + Ly.E + off, a.eta + (int64_t)j * K + 2 * pc);
     }
-#endif
     if (lane == 0 && pw_id == 0) PLP_TRACE(trace_it, 34);
     cp_async_mbar_arrive(&full[b]);
   };
@@ -290,23 +249,6 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
       // warm L2 with the next tile's streamed parts (own rows, enc, w), so that its TMA copies,
       // issued only once the consumers release a buffer, are L2 hits (per-row bulk prefetches of
       // the halo rows too measured 1.6x slower: tiny bulk operations)
-#if PLP_HALO_PFL2
-      // experiment: warm L2 with the next tile's halo rows by per-line prefetches (LSU, not TMA)
-      {
-        const int64_t tn = t + ts;
-        if (tn < n_tiles) {
-          const int qn = (it + 1) % 3;
-          mbar_wait(&lbar[qn], (unsigned)((it + 1) / 3) & 1u);
-          const int* Ln = lists + qn * LS;
-          const int nxn = OVF ? min(Ln[0], ext_cap) : Ln[0];
-          for (int x = lane; x < nxn; x += 32) {
-            const int64_t j = Ln[4 + x];
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(a.U + j * K));
-            if constexpr (HAS_ETA) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.eta + j * K));
-          }
-        }
-      }
-#endif
       if (lane == 0 && pw_id == 0) {
         const int64_t tn = t + ts;
         if (tn < n_tiles) {

@@ -16,9 +16,6 @@ VDIR = os.path.join(ROOT, "paper_2605_26975_b200", "variants")
 
 VARIANTS = {
     "trace": ["-DPLP_HALO_TRACE"],
-    "pfl2": ["-DPLP_HALO_PFL2=1"],
-    "gfirst": ["-DPLP_HALO_GFIRST=1"],
-    "gfirstpf": ["-DPLP_HALO_GFIRST=1", "-DPLP_HALO_PFL2=1"],
     "nb3": ["-DPLP_HALO_NBUF=3"],
     "nb3trace": ["-DPLP_HALO_NBUF=3", "-DPLP_HALO_TRACE"],
     "checked": ["FULL", "-DPLP_DEBUG_CHECKS"],
