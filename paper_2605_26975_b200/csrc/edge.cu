@@ -435,6 +435,31 @@ extern "C" plp_status plp_hessvec(plp_ctx* ctx, const plp_graph* g, int k, const
   return plp_full_epilogue(ctx, g->n_rows, k, U, p, AB_in, scratch_dots(ctx), G_in, Hv);
 }
 
+namespace plp {
+// The fused tCG's Hessian-vector product with pass A folded in (tcg.cu): a rank-local sparse
+// plp_hessvec whose halo pass also writes pass A's CTA partials when it can (*used; *grid = the
+// number of partial columns), else a plain one (*used = false: the caller runs pass A).
+plp_status hessvec_gram(plp_ctx* ctx, const plp_graph* g, int k, const double* U, const double* eta,
+                        double p, const double* AB_in, double eps, const double* S8, double* Hv,
+                        int* grid, bool* used) {
+  *used = false;
+  plp_status st = check_graph_call(ctx, g, k, U, p, eps);
+  if (st) return st;
+  if (!eta || !AB_in || !Hv || !S8) return set_error(PLP_ERR_ARG, "hessvec_gram: null argument");
+  if (collective(ctx, g)) return set_error(PLP_ERR_ARG, "hessvec_gram is rank-local");
+  EdgeArgs a = graph_args(g);
+  a.k = k; a.U = U; a.eta = eta; a.AB = AB_in; a.Hv = Hv; a.p = p; a.eps = eps;
+  a.partials = ctx->partials;
+  a.need_ab = 0;
+  a.gram_S = S8;
+  int gram_used = 0;
+  a.gram_used = &gram_used;
+  if ((st = launch_edge(ctx, a, grid))) return st;
+  *used = gram_used != 0;
+  return PLP_OK;
+}
+}  // namespace plp
+
 extern "C" plp_status plp_fgrad_hessvec(plp_ctx* ctx, const plp_graph* g, int k, const double* U,
                                         const double* eta, double p, const double* AB_in, int mode,
                                         double eps, double* F, double* AB_out, double* G,

@@ -22,6 +22,7 @@
 // warps of a tile get equal work (rank slices {0, 3} and {1, 2} of each window).
 #pragma once
 #include "async_copy.cuh"
+#include "dense_mma.cuh"
 #include "edge_kernel.cuh"
 #include "edge_staged.cuh"
 
@@ -118,10 +119,20 @@ static __device__ long long g_halo_trace[160 * kTraceTiles * kTraceSlots];
 // -- the tile's least referenced halo rows, the list being ordered by reference count -- are read
 // from global memory / L2 by the consumers; C3's random long-range edges).
 // HVO: Hessian-vector product only (plp_hessvec, sparse mode: no gradient sum L, no A, B partials).
-template <int K, class POW, bool HAS_ETA, bool OBJ, int NB, bool ADAPT, bool DOTS, bool OVF, bool HVO = false>
+// GRAM (HVO at k = 4, 8; the fused tCG, tcg.cu): pass A of the tCG iteration folded into the row
+// epilogue.  A warp's row pass holds an 8 x 8 block X[g][2q + h] (lane 4g + q, column pair h) of
+// U, d = eta and EH = Hv -- k = 8: row g is the pass's g-th row; k = 4: the rows of groups 2g and
+// 2g + 1 side by side (the folded view of tcg.cu) -- which is the accumulator layout of
+// mma.m8n8k4: EH - d S on the fp64 tensor cores, tr += d (EH - d S) element by element, and
+// M1 += X_U^T X_EH, M2 += X_U^T X_D over the block's rows (U, d rows from shared memory, EH
+// transposed by shuffles).  The CTA writes [M1 | M2 | tr | 0] entry-major (partials[e * grid + cta]),
+// what tcg_reduce_kernel<8, 0> reads after pass A.
+template <int K, class POW, bool HAS_ETA, bool OBJ, int NB, bool ADAPT, bool DOTS, bool OVF, bool HVO = false,
+          bool GRAM = false>
 __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(POW pw, EdgeArgs a) {
   constexpr bool WL = !HVO;
   static_assert(!(OBJ && HAS_ETA), "objective mode has no eta");
+  static_assert(!GRAM || (HVO && !OVF && !DOTS && (K == 4 || K == 8)), "pass-A fold: Hv-only pass, k = 4 / 8");
   constexpr int CPL = halo_cpl<K>(), LPR = K / CPL, RPW = 32 / LPR;  // rows per pass
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [2] tile data landed
@@ -167,6 +178,7 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
   double accA[CPL], accB[CPL], accAl[CPL], accGa[CPL];
 #pragma unroll
   for (int c = 0; c < CPL; ++c) accA[c] = accB[c] = accAl[c] = accGa[c] = 0.0;
+  double gm1[2] = {0.0, 0.0}, gm2[2] = {0.0, 0.0}, gtr = 0.0;  // GRAM accumulators (consumers)
   __syncthreads();
 
   // (thread 0) stage the halo list of tile t into list slot q
@@ -271,6 +283,17 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
   // takes slices w, 2C - 1 - w, 2C + w, ...), so every warp gets a heavy and a light slice.
   constexpr int NSL = kHaloT / RPW, C = kHaloCWarps;
   bool capmode = false;  // this warp's previous row needed the capped form
+  // GRAM: B fragments of -S (rows 4s + q, column g), the warp's M1 / M2 accumulators and its share
+  // of sum d (EH - d S)
+  const int g8 = lane >> 2, q4 = lane & 3;
+  double gS[2] = {0.0, 0.0};
+  if constexpr (GRAM) {
+    gS[0] = -a.gram_S[q4 * 8 + g8];
+    gS[1] = -a.gram_S[(4 + q4) * 8 + g8];
+  }
+  (void)gS;
+  (void)g8;
+  (void)q4;
   for (int it = 0;; ++it) {
     const int64_t t = t0 + (int64_t)it * ts;
     if (t >= n_tiles) break;
@@ -316,7 +339,13 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
       const int sl = rd * C + ((rd & 1) ? C - 1 - warp : warp);
       if (sl >= NSL) continue;
       const int lr = sl * RPW + grp;  // position in the tile's schedule
-      if (lr >= nr) continue;
+      int glrow = -1;                 // GRAM: the group's tile row (-1: past the last row)
+      double gH[CPL];                 // GRAM: the group's EH values
+#pragma unroll
+      for (int cc = 0; cc < CPL; ++cc) gH[cc] = 0.0;
+      (void)glrow;
+      do {  // the row (a `continue` below ends it; GRAM then joins the warp's block update)
+      if (lr >= nr) break;
       const int row = sc_s[lr];
       const int lrow = row - r0;
       const int e0 = rp_s[lrow], e1 = rp_s[lrow + 1];
@@ -536,6 +565,48 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
       if constexpr (HAS_ETA) {
         if (a.Hv != nullptr) st_vec<CPL>(a.Hv + (int64_t)row * K + c0, hv);
       }
+      if constexpr (GRAM) {
+        glrow = lrow;
+#pragma unroll
+        for (int cc = 0; cc < CPL; ++cc) gH[cc] = hv[cc];
+      }
+      } while (0);
+      if constexpr (GRAM) {
+        // the warp's 8 x 8 block; X[r][c] lives in group (k = 8) r, (k = 4) 2r + c / 4, column
+        // c % k, i.e. at lane group * LPR; U and d rows come from the tile buffer (own rows)
+        __syncwarp();
+        const double* tUr = tU - c0;
+        const double* tEr = tE - c0;
+        double c0v = gH[0], c1v = gH[1];
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {  // EH - d S: A = X_D[g][4s + q]
+          const int grpA = K == 8 ? g8 : 2 * g8 + s, colA = K == 8 ? 4 * s + q4 : q4;
+          const int lrA = __shfl_sync(0xffffffffu, glrow, grpA * LPR);
+          const double dA = lrA >= 0 ? tEr[lrA * K + colA] : 0.0;
+          dmma884(c0v, c1v, dA, gS[s]);
+        }
+        // tr += d (EH - d S) over the lane's two elements (its own group's row)
+        {
+          double dv[CPL];
+          if (glrow >= 0) lds_vec<CPL>(tE + glrow * K, dv);
+          else dv[0] = dv[1] = 0.0;
+          gtr = fma(dv[0], c0v, gtr);
+          gtr = fma(dv[1], c1v, gtr);
+        }
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {  // rows 4s .. 4s + 3 of the block: A = X_U^T, B = X_EH, X_D
+          const int r = 4 * s + q4;
+          const int grpB = K == 8 ? r : 2 * r + (g8 >> 2), colB = K == 8 ? g8 : (g8 & 3);
+          const int lrB = __shfl_sync(0xffffffffu, glrow, grpB * LPR);
+          const int src = 4 * r + (g8 >> 1);  // C-layout lane of X[r][g]
+          const double h0 = __shfl_sync(0xffffffffu, gH[0], src), h1 = __shfl_sync(0xffffffffu, gH[1], src);
+          const double bh = (g8 & 1) ? h1 : h0;
+          const double au = lrB >= 0 ? tUr[lrB * K + colB] : 0.0;
+          const double bd = lrB >= 0 ? tEr[lrB * K + colB] : 0.0;
+          dmma884(gm1[0], gm1[1], au, bh);
+          dmma884(gm2[0], gm2[1], au, bd);
+        }
+      }
     }
     __syncwarp();
     if (lane == 0) PLP_TRACE(it, 16 + warp);
@@ -546,6 +617,29 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
   // ---- fixed-order CTA reduction (reuses buffer 0: every issued copy has been consumed) ----
   __syncthreads();
   double* red = reinterpret_cast<double*>(buf0);  // [4][CPL][threads]
+  if constexpr (GRAM) {
+    // [M1 | M2 | tr | 0]: fragment element (g, 2q + h) of consumer warp w at red[j][w * 32 + 4g + q]
+    // (j = h for M1, 2 + h for M2, 4 for tr), summed over the warps in order
+    red[0 * kHaloThreads + tid] = gm1[0];
+    red[1 * kHaloThreads + tid] = gm1[1];
+    red[2 * kHaloThreads + tid] = gm2[0];
+    red[3 * kHaloThreads + tid] = gm2[1];
+    red[4 * kHaloThreads + tid] = gtr;
+    __syncthreads();
+    constexpr int E = 2 * 64 + 2;
+    for (int e = tid; e < E; e += kHaloThreads) {
+      double sum = 0.0;
+      if (e < 128) {
+        const int m = e & 63, gg = m >> 3, cc = m & 7;
+        const int j = (e >> 6) * 2 + (cc & 1), ln = 4 * gg + (cc >> 1);
+        for (int w = 0; w < kHaloCWarps; ++w) sum += red[j * kHaloThreads + w * 32 + ln];
+      } else if (e == 128) {
+        for (int th = 0; th < kHaloCWarps * 32; ++th) sum += red[4 * kHaloThreads + th];
+      }
+      a.partials[(int64_t)e * gridDim.x + blockIdx.x] = sum;
+    }
+    return;
+  }
 #pragma unroll
   for (int cc = 0; cc < CPL; ++cc) {
     red[(0 * CPL + cc) * kHaloThreads + tid] = accA[cc];
@@ -592,7 +686,12 @@ plp_status launch_halo_shape(plp_ctx* ctx, const EdgeArgs& a0, const POW& pw, in
   const bool adapt = !(HAS_ETA && a.G != nullptr);
   const bool dots = HAS_ETA && a.want_dots;
   const bool hvo = HAS_ETA && !OBJ && adapt && !dots && a.G == nullptr && !a.need_ab;
+  // the fused tCG's pass A in the Hessian-vector-only pass (k = 4, 8; single launch, no tile list)
+  constexpr bool kGramShape = HAS_ETA && !OBJ && (K == 4 || K == 8);
+  const bool gram = kGramShape && hvo && !ovf && a.gram_S != nullptr && a.tile_list == nullptr;
+  if (a.gram_used) *a.gram_used = gram ? 1 : 0;
   auto kern = deep ? edge_halo_kernel<K, POW, HAS_ETA, OBJ, NB3, true, false, false>
+            : gram ? edge_halo_kernel<K, POW, HAS_ETA, OBJ, kHaloNBuf, true, false, false, kGramShape, kGramShape>
             : (hvo && !ovf) ? edge_halo_kernel<K, POW, HAS_ETA, OBJ, kHaloNBuf, true, false, false, HAS_ETA && !OBJ>
             : ovf  ? (adapt ? edge_halo_kernel<K, POW, HAS_ETA, OBJ, kHaloNBuf, true, false, true>
                             : edge_halo_kernel<K, POW, HAS_ETA, OBJ, kHaloNBuf, false, false, true>)
@@ -603,8 +702,8 @@ plp_status launch_halo_shape(plp_ctx* ctx, const EdgeArgs& a0, const POW& pw, in
   const unsigned smem = halo_smem_bytes(K, ovf ? a.halo_stage : a.halo_ext_cap, a.halo_nnz_cap, T, OBJ, HAS_ETA, nb);
   // the dynamic shared-memory opt-in is a per-device function attribute: set it on this ctx's
   // device whenever a launch needs more than the value set so far (per template instance)
-  static unsigned attr_set[64][8] = {};
-  const int vi = deep ? 4 : (hvo && !ovf) ? 7 : ovf ? 5 + (adapt ? 1 : 0) : (adapt ? 1 : 0) + (dots ? 2 : 0);
+  static unsigned attr_set[64][9] = {};
+  const int vi = deep ? 4 : gram ? 8 : (hvo && !ovf) ? 7 : ovf ? 5 + (adapt ? 1 : 0) : (adapt ? 1 : 0) + (dots ? 2 : 0);
   unsigned& set_to = attr_set[ctx->device & 63][vi];
   if (set_to < smem) {
     PLP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -621,6 +720,7 @@ plp_status launch_halo_shape(plp_ctx* ctx, const EdgeArgs& a0, const POW& pw, in
   char name[96];
   snprintf(name, sizeof(name), "edge_halo_kernel%s", OBJ ? (deep ? "[objective,3buf,adapt]" : ovf ? "[objective,ovf,adapt]" : "[objective,adapt]")
                                                          : deep ? "[3buf,adapt]" : ovf ? (adapt ? "[ovf,adapt]" : "[ovf]")
+                                                         : gram ? "[adapt,hv,gram]"
                                                          : (hvo && !ovf) ? "[adapt,hv]"
                                                          : adapt ? "[adapt]" : "");
   note_edge_kernel(name, K, halo_cpl<K>(), K / halo_cpl<K>(), 2, POW::kName, HAS_ETA);

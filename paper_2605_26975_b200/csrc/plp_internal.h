@@ -152,8 +152,16 @@ struct EdgeArgs {
   const int32_t* nlow;  // objective mode (edge_halo.cuh)
   const int32_t* sched_up;
   int upper_ok;
+  // fused tCG (tcg.cu): a Hessian-vector-only halo pass at k = 4 / 8 may also accumulate pass A's
+  // sums (M1 = U^T EH, M2 = U^T eta, sum eta (EH - eta S)) into `partials`, entry-major per CTA;
+  // gram_S is the 8 x 8 S (k = 4: block-diagonal), *gram_used (host) tells the caller it did
+  const double* gram_S;
+  int* gram_used;
 };
 plp_status launch_edge(plp_ctx* ctx, const EdgeArgs& a, int* grid_out);
+plp_status hessvec_gram(plp_ctx* ctx, const plp_graph* g, int k, const double* U, const double* eta,
+                        double p, const double* AB_in, double eps, const double* S8, double* Hv,
+                        int* grid, bool* used);
 // Fixed-order reduction of edge partials: AB_out (2k), dots_out (2k), F (1); any may be null.
 plp_status launch_edge_finalize(plp_ctx* ctx, int grid, int k, const double* partials,
                                 double* AB_out, double* dots_out, double* F);

@@ -566,7 +566,7 @@ static int fused_grid(plp_ctx* ctx, int64_t row_blocks, int E, int per_sm) {  //
 template <int KT>
 static plp_status fused_iteration(plp_ctx* ctx, int64_t n, const double* U, const double* S, double* eta,
                                   double* Heta, double* r, double* dlt, const double* EH, double* scal,
-                                  int* status, int max_iters, int kr) {
+                                  int* status, int max_iters, int kr, int gram_grid) {
   constexpr int K = 8 * KT, KK = K * K;
   static const int unr_a = env_int("PLP_TCG_UNR_A", 4);
   static const int per_sm_a = env_int("PLP_TCG_GRID_A", unr_a == 4 ? resident_ctas(tcg_gram_a_kernel<KT, 4>, kTcgThreads)
@@ -575,12 +575,15 @@ static plp_status fused_iteration(plp_ctx* ctx, int64_t n, const double* U, cons
   static const int per_sm_c = resident_ctas(tcg_finish_kernel<KT>, kTcgThreads);
   unsigned* counter = reinterpret_cast<unsigned*>(ctx->flag + 4);
   constexpr int EA = 2 * KK + 2, EB = KK + 1;
-  const int ga = fused_grid(ctx, (n + 3) / 4, EA, per_sm_a);
-  if (unr_a == 4)
-    tcg_gram_a_kernel<KT, 4><<<ga, kTcgThreads, 0, ctx->stream>>>(n, U, EH, dlt, S, ctx->partials);
-  else
-    tcg_gram_a_kernel<KT, 2><<<ga, kTcgThreads, 0, ctx->stream>>>(n, U, EH, dlt, S, ctx->partials);
-  PLP_LAUNCH_CHECK("tcg_gram_a_kernel");
+  int ga = gram_grid;  // > 0: the edge pass wrote pass A's partials (edge_halo.cuh, GRAM)
+  if (ga == 0) {
+    ga = fused_grid(ctx, (n + 3) / 4, EA, per_sm_a);
+    if (unr_a == 4)
+      tcg_gram_a_kernel<KT, 4><<<ga, kTcgThreads, 0, ctx->stream>>>(n, U, EH, dlt, S, ctx->partials);
+    else
+      tcg_gram_a_kernel<KT, 2><<<ga, kTcgThreads, 0, ctx->stream>>>(n, U, EH, dlt, S, ctx->partials);
+    PLP_LAUNCH_CHECK("tcg_gram_a_kernel");
+  }
   tcg_reduce_kernel<K, 0><<<EA, 256, 0, ctx->stream>>>(ga, ctx->partials, scal + kTotA, counter, scal, status,
                                                        max_iters, kr);
   PLP_LAUNCH_CHECK("tcg_reduce_kernel");
@@ -668,14 +671,28 @@ extern "C" plp_status plp_tcg_run(plp_ctx* ctx, const plp_graph* g, int k, const
       tcg_expand_s_kernel<<<1, 64, 0, ctx->stream>>>(S, k, scal + kSx);
       PLP_LAUNCH_CHECK("tcg_expand_s_kernel");
     }
+    // pass A folded into the Hessian-vector-only halo pass where it applies (k = 4, 8, sparse
+    // mode, rank-local; PLP_TCG_GRAM_EDGE=0 keeps the separate pass for comparison)
+    static const bool gram_edge = env_int("PLP_TCG_GRAM_EDGE", 1) != 0;
+    const bool try_gram = gram_edge && (k == 8 || k == 4) && mode == PLP_HESS_SPARSE && !(ctx->comm && g->dist);
+    const double* S8 = k == 8 ? S : scal + kSx;
     for (int it = 0; it < iters; ++it) {
-      if ((st = plp_hessvec(ctx, g, k, U, dlt, p, AB, mode, eps, G_in, Hd))) return st;
+      int gram_grid = 0;
+      if (try_gram) {
+        bool used = false;
+        int eg = 0;
+        if ((st = hessvec_gram(ctx, g, k, U, dlt, p, AB, eps, S8, Hd, &eg, &used))) return st;
+        gram_grid = used ? eg : 0;
+      } else if ((st = plp_hessvec(ctx, g, k, U, dlt, p, AB, mode, eps, G_in, Hd))) {
+        return st;
+      }
       if (k == 16)
-        st = fused_iteration<2>(ctx, n, U, S, eta, Heta, r, dlt, Hd, scal, status, max_iters, 16);
+        st = fused_iteration<2>(ctx, n, U, S, eta, Heta, r, dlt, Hd, scal, status, max_iters, 16, 0);
       else if (k == 8)
-        st = fused_iteration<1>(ctx, n, U, S, eta, Heta, r, dlt, Hd, scal, status, max_iters, 8);
+        st = fused_iteration<1>(ctx, n, U, S, eta, Heta, r, dlt, Hd, scal, status, max_iters, 8, gram_grid);
       else  // k = 1, 2, 4: the n x k arrays as n k / 8 rows of 8, S block-diagonal
-        st = fused_iteration<1>(ctx, n * k / 8, U, scal + kSx, eta, Heta, r, dlt, Hd, scal, status, max_iters, k);
+        st = fused_iteration<1>(ctx, n * k / 8, U, scal + kSx, eta, Heta, r, dlt, Hd, scal, status, max_iters, k,
+                                gram_grid);
       if (st) return st;
     }
     return PLP_OK;

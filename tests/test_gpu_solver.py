@@ -328,3 +328,57 @@ def test_fused_tcg_tile_ordered_matches_oracle(mods, cfg, n, k, p, delta):
     assert (it, status) == (it_o, status_o)
     assert np.max(np.abs(eta.cpu().numpy() - eta_o)) <= 1e-9 * np.max(np.abs(eta_o))
     assert np.max(np.abs(Heta.cpu().numpy() - Heta_o)) <= 1e-9 * np.max(np.abs(Heta_o))
+
+
+_GRAM_RUN = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+from paper_2605_26975_b200 import plp, solver
+from plp_inputs import make_config, permute_graph, draw_U
+import oracle
+g0 = make_config({cfg!r}, n={n})
+g = permute_graph(g0, plp.tile_order(g0.row_ptr, g0.col))
+k, p = {k}, {p}
+ctx = plp.Context(0)
+G = plp.Graph(ctx, g.row_ptr, g.col, g.w)
+Uo, _ = oracle.retract(draw_U(g.n, k, 5), np.zeros((g.n, k)))
+cfg = solver.SolverConfig(tcg_fused=True, tcg_graph=False)
+tr = solver.GrassmannTR(ctx, G, k, cfg)
+st = solver._State(tr, torch.from_numpy(Uo).cuda(), p)
+tr.tcg_device(st, p, 1e3)
+eta, Heta, r, dlt, Hd, scal, status = tr._tcg_buf
+plp.tcg_init(ctx, st.grad, 1e3, 0.0, 1.0, eta, None, r, dlt, scal, status)
+plp.tcg_run(ctx, G, st.U, st.AB, None, st.S, p, cfg.eps, plp.HESS_SPARSE, eta, None, r, dlt, Hd, scal, status,
+            1 << 30, {iters}, fused=True)
+torch.cuda.synchronize()
+np.save({out!r}, eta.cpu().numpy())
+print("KERNEL", plp.last_edge_kernel())
+print("STATUS", status.cpu().tolist())
+"""
+
+
+@pytest.mark.parametrize("cfg,n,k,p", [("D16", 8192, 8, 1.2), ("D16", 8192, 4, 1.5), ("C5", 30000, 8, 1.2),
+                                       ("C5", 30002, 4, 1.8)])
+def test_fused_tcg_pass_a_fold_matches_separate_pass(cfg, n, k, p, tmp_path):
+    """NEXT-2: pass A of the fused tCG folded into the Hessian-vector-only halo pass (edge_halo.cuh
+    GRAM; its DMMA Grams and d (EH - d S) sums over the tile's row blocks) against the separate pass A
+    (PLP_TCG_GRAM_EDGE=0): same iteration count and status after 12 iterations, the step equal within
+    1e-10 relative (only the Grams' summation order differs); the fold is what ran."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for fold in (1, 0):
+        out = str(tmp_path / f"eta{fold}.npy")
+        code = _GRAM_RUN.format(root=root, cfg=cfg, n=n, k=k, p=p, iters=12, out=out)
+        env = dict(os.environ, PLP_TCG_GRAM_EDGE=str(fold))
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        lines = dict(ln.split(" ", 1) for ln in r.stdout.splitlines() if ln.startswith(("KERNEL", "STATUS")))
+        res[fold] = (np.load(out), lines["KERNEL"], lines["STATUS"])
+    assert "gram" in res[1][1], res[1][1]
+    assert "gram" not in res[0][1], res[0][1]
+    assert res[1][2] == res[0][2]
+    e1, e0 = res[1][0], res[0][0]
+    assert np.max(np.abs(e1 - e0)) <= 1e-10 * np.max(np.abs(e0))
