@@ -339,11 +339,33 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
       const int sl = rd * C + ((rd & 1) ? C - 1 - warp : warp);
       if (sl >= NSL) continue;
       const int lr = sl * RPW + grp;  // position in the tile's schedule
-      int glrow = -1;                 // GRAM: the group's tile row (-1: past the last row)
       double gH[CPL];                 // GRAM: the group's EH values
 #pragma unroll
       for (int cc = 0; cc < CPL; ++cc) gH[cc] = 0.0;
-      (void)glrow;
+      // GRAM, before the rows (their latency hides behind the edge loop): the block's U and d
+      // operands from the tile buffer, M2 += X_U^T X_D and P = X_D S on the tensor cores; the
+      // EH-dependent part (M1, d (EH - P)) follows the rows.  X[r][c] lives in group (k = 8) r,
+      // (k = 4) 2r + c / 4, column c % k, i.e. at lane group * LPR.
+      const int glrow = GRAM ? (lr < nr ? sc_s[lr] - r0 : -1) : -1;  // the group's tile row
+      double gAU[2] = {0.0, 0.0}, gP0 = 0.0, gP1 = 0.0;
+      if constexpr (GRAM) {
+        const double* tUr = tU - c0;
+        const double* tEr = tE - c0;
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          const int grpA = K == 8 ? g8 : 2 * g8 + s, colA = K == 8 ? 4 * s + q4 : q4;
+          const int lrA = __shfl_sync(0xffffffffu, glrow, grpA * LPR);
+          const int r = 4 * s + q4;
+          const int grpB = K == 8 ? r : 2 * r + (g8 >> 2), colB = K == 8 ? g8 : (g8 & 3);
+          const int lrB = __shfl_sync(0xffffffffu, glrow, grpB * LPR);
+          const double dA = lrA >= 0 ? tEr[lrA * K + colA] : 0.0;   // X_D[g][4s + q]
+          gAU[s] = lrB >= 0 ? tUr[lrB * K + colB] : 0.0;          // X_U[4s + q][g]
+          const double bd = lrB >= 0 ? tEr[lrB * K + colB] : 0.0;  // X_D[4s + q][g]
+          dmma884(gP0, gP1, dA, gS[s]);
+          dmma884(gm2[0], gm2[1], gAU[s], bd);
+        }
+      }
+      (void)gAU;
       do {  // the row (a `continue` below ends it; GRAM then joins the warp's block update)
       if (lr >= nr) break;
       const int row = sc_s[lr];
@@ -566,45 +588,19 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
         if (a.Hv != nullptr) st_vec<CPL>(a.Hv + (int64_t)row * K + c0, hv);
       }
       if constexpr (GRAM) {
-        glrow = lrow;
 #pragma unroll
-        for (int cc = 0; cc < CPL; ++cc) gH[cc] = hv[cc];
+        for (int cc = 0; cc < CPL; ++cc) {
+          gH[cc] = hv[cc];
+          gtr = fma(ei[cc], hv[cc] + (cc == 0 ? gP0 : gP1), gtr);  // d (EH - d S): gP = X_D (-S)
+        }
       }
       } while (0);
       if constexpr (GRAM) {
-        // the warp's 8 x 8 block; X[r][c] lives in group (k = 8) r, (k = 4) 2r + c / 4, column
-        // c % k, i.e. at lane group * LPR; U and d rows come from the tile buffer (own rows)
-        __syncwarp();
-        const double* tUr = tU - c0;
-        const double* tEr = tE - c0;
-        double c0v = gH[0], c1v = gH[1];
 #pragma unroll
-        for (int s = 0; s < 2; ++s) {  // EH - d S: A = X_D[g][4s + q]
-          const int grpA = K == 8 ? g8 : 2 * g8 + s, colA = K == 8 ? 4 * s + q4 : q4;
-          const int lrA = __shfl_sync(0xffffffffu, glrow, grpA * LPR);
-          const double dA = lrA >= 0 ? tEr[lrA * K + colA] : 0.0;
-          dmma884(c0v, c1v, dA, gS[s]);
-        }
-        // tr += d (EH - d S) over the lane's two elements (its own group's row)
-        {
-          double dv[CPL];
-          if (glrow >= 0) lds_vec<CPL>(tE + glrow * K, dv);
-          else dv[0] = dv[1] = 0.0;
-          gtr = fma(dv[0], c0v, gtr);
-          gtr = fma(dv[1], c1v, gtr);
-        }
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {  // rows 4s .. 4s + 3 of the block: A = X_U^T, B = X_EH, X_D
-          const int r = 4 * s + q4;
-          const int grpB = K == 8 ? r : 2 * r + (g8 >> 2), colB = K == 8 ? g8 : (g8 & 3);
-          const int lrB = __shfl_sync(0xffffffffu, glrow, grpB * LPR);
-          const int src = 4 * r + (g8 >> 1);  // C-layout lane of X[r][g]
+        for (int s = 0; s < 2; ++s) {  // M1 += X_U^T X_EH over rows 4s .. 4s + 3 of the block
+          const int src = 4 * (4 * s + q4) + (g8 >> 1);  // C-layout lane of X[4s + q][g]
           const double h0 = __shfl_sync(0xffffffffu, gH[0], src), h1 = __shfl_sync(0xffffffffu, gH[1], src);
-          const double bh = (g8 & 1) ? h1 : h0;
-          const double au = lrB >= 0 ? tUr[lrB * K + colB] : 0.0;
-          const double bd = lrB >= 0 ? tEr[lrB * K + colB] : 0.0;
-          dmma884(gm1[0], gm1[1], au, bh);
-          dmma884(gm2[0], gm2[1], au, bd);
+          dmma884(gm1[0], gm1[1], gAU[s], (g8 & 1) ? h1 : h0);
         }
       }
     }
