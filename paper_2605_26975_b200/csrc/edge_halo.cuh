@@ -34,6 +34,18 @@ constexpr int kHaloCWarps = 2 * (kHaloT / kSchedWindow);  // consumers: a warp p
 constexpr int kHaloThreads = (kHaloCWarps + kHaloProd) * 32;  // + the producer warp(s)
 static_assert(kHaloT % kSchedWindow == 0 && kHaloThreads <= 1024, "tile map");
 
+// CPL doubles at shared-window address addr + OFF (16-byte aligned for even CPL)
+template <unsigned OFF>
+__device__ __forceinline__ void lds_pair(unsigned addr, double& a, double& b) {
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2+%3];" : "=d"(a), "=d"(b) : "r"(addr), "n"(OFF));
+}
+template <int CPL, unsigned OFF>
+__device__ __forceinline__ void lds_row(unsigned addr, double (&v)[CPL]) {
+  static_assert(CPL == 2 || CPL == 4, "halo kernel: 2 or 4 columns per lane");
+  lds_pair<OFF>(addr, v[0], v[1]);
+  if constexpr (CPL == 4) lds_pair<OFF + 16u>(addr, v[2], v[3]);
+}
+
 // Per-buffer shared-memory layout (bytes), identical on host and device.
 struct HaloLayout {
   unsigned rp, sched, nl, enc, w, U, E, bytes;
@@ -86,8 +98,16 @@ constexpr unsigned kHaloSmemMax = 225u * 1024u / PLP_HALO_CTAS;
 #ifndef PLP_HALO_SLEEP_NS
 #define PLP_HALO_SLEEP_NS 64  // producer back-off between polls of the "empty" barrier
 #endif
-template <int K>
-constexpr int halo_cpl() { return K == 16 ? 4 : 2; }  // columns per lane (k = 8: 1 and 4 measured slower)
+#ifndef PLP_HALO_CPL8
+#define PLP_HALO_CPL8 2  // k = 8 columns per lane outside the Hessian-vector-only passes (2 or 4)
+#endif
+// columns per lane: 4 at k = 16, 2 at k = 4, 8.  PLP_HALO_CPL8=4 (k = 8 passes with a gradient or
+// objective: 2 lanes per row, one edge per iteration, four independent power chains per lane,
+// 7 % fewer instructions) measured slower on C5: 0.928 against 0.823 ms (16 rows per warp pass
+// and one slice per warp per tile); the Hessian-vector-only passes (and their pass-A fold, which
+// needs the 2-column accumulator layout) always take 2 (k = 8: 1 column per lane measured slower)
+template <int K, bool HVO = false>
+constexpr int halo_cpl() { return K == 16 ? 4 : (K == 8 && !HVO) ? PLP_HALO_CPL8 : 2; }
 
 // OBJ: objective-only pass (no eta, no G) on a symmetric graph: A_l = sum over the upper-triangle
 // edges (j > i) of w_ij |u_il - u_jl|^p, i.e. Eq. (1)'s numerator with each undirected edge once
@@ -133,7 +153,9 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
   constexpr bool WL = !HVO;
   static_assert(!(OBJ && HAS_ETA), "objective mode has no eta");
   static_assert(!GRAM || (HVO && !OVF && !DOTS && (K == 4 || K == 8)), "pass-A fold: Hv-only pass, k = 4 / 8");
-  constexpr int CPL = halo_cpl<K>(), LPR = K / CPL, RPW = 32 / LPR;  // rows per pass
+  constexpr int CPL = halo_cpl<K, HVO>(), LPR = K / CPL, RPW = 32 / LPR;  // rows per pass
+  constexpr int EB = (CPL == 4 && K == 8) ? 1 : 2;  // edges per loop iteration (independent chains: EB x CPL)
+  static_assert(!GRAM || CPL == 2, "pass-A fold: the 2-column accumulator layout");
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [2] tile data landed
   uint64_t* lbar = full + NB;                   // [3] halo list landed
@@ -315,6 +337,10 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
     // neighbour rows: tile-local index x; OVF: x >= kHaloT + ext_cap is an unstaged halo row, read
     // through its global id in the tile's (global) halo list
     const int* glist = a.halo_ext + tt * LSG + 4 - kHaloT;
+    // staged rows by 32-bit shared-window address: one IMAD per neighbour row serves U and eta
+    // (eta at a compile-time offset)
+    const unsigned sU = smem_u32(tU);
+    constexpr unsigned kEOff = (unsigned)(kHaloT + halo_rows_cap(K)) * K * 8u;
     auto ldU = [&](int x, double (&v)[CPL]) {
       if constexpr (OVF) {
         if (x >= kHaloT + ext_cap) {
@@ -322,7 +348,7 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
           return;
         }
       }
-      lds_vec<CPL>(tU + x * K, v);
+      lds_row<CPL, 0>(sU + (unsigned)x * (K * 8u), v);
     };
     auto ldE = [&](int x, double (&v)[CPL]) {
       if constexpr (OVF) {
@@ -331,12 +357,14 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
           return;
         }
       }
-      lds_vec<CPL>(tE + x * K, v);
+      lds_row<CPL, kEOff>(sU + (unsigned)x * (K * 8u), v);
     };
 
 #pragma unroll 1
     for (int rd = 0; rd * C < NSL; ++rd) {
-      const int sl = rd * C + ((rd & 1) ? C - 1 - warp : warp);
+      // snake order alternating with the tile parity: over any two consecutive tiles (one is
+      // resident while the other is computed) every warp takes a heavy and a light slice
+      const int sl = rd * C + (((rd + it) & 1) ? C - 1 - warp : warp);
       if (sl >= NSL) continue;
       const int lr = sl * RPW + grp;  // position in the tile's schedule
       double gH[CPL];                 // GRAM: the group's EH values
@@ -396,17 +424,20 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
           }
         };
         int e = eu;
+        if constexpr (EB == 2) {
 #pragma unroll 1
-        for (; e + 1 < e1; e += 2) {
-          const int x0 = enc_s[e], x1 = enc_s[e + 1];
-          const double w0 = w_s[e], w1 = w_s[e + 1];
-          double uj0[CPL], uj1[CPL];
-          ldU(x0, uj0);
-          ldU(x1, uj1);
-          obj_edge(w0, uj0);
-          obj_edge(w1, uj1);
+          for (; e + 1 < e1; e += 2) {
+            const int x0 = enc_s[e], x1 = enc_s[e + 1];
+            const double w0 = w_s[e], w1 = w_s[e + 1];
+            double uj0[CPL], uj1[CPL];
+            ldU(x0, uj0);
+            ldU(x1, uj1);
+            obj_edge(w0, uj0);
+            obj_edge(w1, uj1);
+          }
         }
-        if (e < e1) {
+#pragma unroll 1
+        for (; e < e1; ++e) {  // EB = 1: every edge; EB = 2: the odd last one
           double uj0[CPL];
           ldU(enc_s[e], uj0);
           obj_edge(w_s[e], uj0);
@@ -479,12 +510,26 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
       // edge pairs as straight-line code (their dependency chains interleave), then the
       // remaining edge; summation order stays the CSR order
       int e = (ADAPT && capmode) ? e1 : e0;  // capmode: the capped form below recomputes the row
+      const int* ep = enc_s + e;  // running pointers: immediate-offset loads, no per-pair index math
+      const double* wp = w_s + e;
+      const int* const ep_last = enc_s + (e1 - 1);
+      if constexpr (EB == 1) {
 #pragma unroll 1
-      for (; e + 1 < e1; e += 2) {
-        const int x0 = enc_s[e], x1 = enc_s[e + 1];
+        for (; ep <= ep_last; ++ep, ++wp) {
+          const int x0 = *ep;
+          const double w0 = *wp;
+          double uj0[CPL], ej0[CPL];
+          ldU(x0, uj0);
+          if constexpr (HAS_ETA) ldE(x0, ej0);
+          edge_update_mx<CPL, POW, HAS_ETA, WL>(pw, w0, ui, uj0, ei, ej0, L, HA, mx);
+        }
+      }
+#pragma unroll 1
+      for (; EB == 2 && ep < ep_last; ep += 2, wp += 2) {
+        const int x0 = ep[0], x1 = ep[1];
         PLP_DCHECK(x0 >= 0 && x1 >= 0 && x0 < kHaloT + a.halo_ext_cap && x1 < kHaloT + a.halo_ext_cap && (x0 < nr || x0 >= kHaloT) &&
                        (x1 < nr || x1 >= kHaloT), "edge's tile-local neighbour index");
-        const double w0 = w_s[e], w1 = w_s[e + 1];
+        const double w0 = wp[0], w1 = wp[1];
         double uj0[CPL], ej0[CPL], uj1[CPL], ej1[CPL];
         ldU(x0, uj0);
         ldU(x1, uj1);
@@ -495,9 +540,9 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
         edge_update_mx<CPL, POW, HAS_ETA, WL>(pw, w0, ui, uj0, ei, ej0, L, HA, mx);
         edge_update_mx<CPL, POW, HAS_ETA, WL>(pw, w1, ui, uj1, ei, ej1, L, HA, mx);
       }
-      if (e < e1) {
-        const int x0 = enc_s[e];
-        const double w0 = w_s[e];
+      if (EB == 2 && ep == ep_last) {  // the odd last edge
+        const int x0 = *ep;
+        const double w0 = *wp;
         double uj0[CPL], ej0[CPL];
         ldU(x0, uj0);
         if constexpr (HAS_ETA) ldE(x0, ej0);
@@ -537,7 +582,7 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
           for (int cc = 0; cc < CPL; ++cc) L[cc] = HA[cc] = 0.0;
           int ee = e0;
 #pragma unroll 1
-          for (; ee + 1 < e1; ee += 2) {  // edge pairs: two dependency chains interleave
+          for (; EB == 2 && ee + 1 < e1; ee += 2) {  // edge pairs: two dependency chains interleave
             const int x0 = enc_s[ee], x1 = enc_s[ee + 1];
             double uj0[CPL], ej0[CPL], uj1[CPL], ej1[CPL];
             ldU(x0, uj0);
@@ -549,7 +594,8 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
             edge_update_capsel<CPL, POW, HAS_ETA, WL>(pw, w_s[ee], ui, uj0, ei, ej0, L, HA, rg);
             edge_update_capsel<CPL, POW, HAS_ETA, WL>(pw, w_s[ee + 1], ui, uj1, ei, ej1, L, HA, rg);
           }
-          if (ee < e1) {
+#pragma unroll 1
+          for (; ee < e1; ++ee) {  // EB = 1: every edge; EB = 2: the odd last one
             const int x0 = enc_s[ee];
             double uj0[CPL], ej0[CPL];
             ldU(x0, uj0);
@@ -719,7 +765,9 @@ plp_status launch_halo_shape(plp_ctx* ctx, const EdgeArgs& a0, const POW& pw, in
                                                          : gram ? "[adapt,hv,gram]"
                                                          : (hvo && !ovf) ? "[adapt,hv]"
                                                          : adapt ? "[adapt]" : "");
-  note_edge_kernel(name, K, halo_cpl<K>(), K / halo_cpl<K>(), 2, POW::kName, HAS_ETA);
+  constexpr int kCplN = halo_cpl<K>();  // the name reports the non-Hessian-vector shape
+  note_edge_kernel(name, K, (hvo && !ovf) ? halo_cpl<K, true>() : kCplN, K / ((hvo && !ovf) ? halo_cpl<K, true>() : kCplN),
+                   (hvo && !ovf) || kCplN == 2 ? 2 : 1, POW::kName, HAS_ETA);
   *grid_out = (int)grid;
   return PLP_OK;
 }

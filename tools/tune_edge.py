@@ -21,6 +21,7 @@ VARIANTS = {
     "checked": ["FULL", "-DPLP_DEBUG_CHECKS"],
     "sleep0": ["-DPLP_HALO_SLEEP_NS=0"],
     "sleep256": ["-DPLP_HALO_SLEEP_NS=256"],
+    "cpl4": ["-DPLP_HALO_CPL8=4"],
     # full builds (all k): staged-kernel occupancy for the random-graph configs (C4, k = 20)
     "full_minb3": ["FULL", "-DPLP_EDGE_MINB=3"],
 }
