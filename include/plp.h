@@ -277,6 +277,20 @@ plp_status plp_gather_rows(plp_ctx* ctx, int64_t m, int k, const int64_t* idx, c
 plp_status plp_kmeans(plp_ctx* ctx, int64_t n, int dim, int clusters, const double* X,
                       const double* uniforms, int restarts, int max_iters, double rel_tol,
                       int32_t* labels, double* centroids, double* sse, int* iters);
+/* Collective k-means (k x k / k x dim reductions all-reduced): the rows are the
+ * ranks' X blocks (n_local x dim each, device) concatenated in rank order, n_local >= 0 with the
+ * global n >= clusters.  The same algorithm and uniforms as plp_kmeans on the concatenated rows:
+ * seeding picks use the global D^2 sum (each rank's sum all-reduced; the rank whose running sum
+ * crosses u sum D^2 picks inside its block and broadcasts the point), Lloyd's per-cluster sums,
+ * counts and sse are all-reduced, an empty cluster takes the globally farthest point (largest
+ * distance, lowest global index).  Outputs: labels of this rank's rows (device int32 n_local);
+ * centroids, *sse, *iters identical on every rank.  On one rank (a context without a
+ * communicator, or world = 1) bitwise equal to plp_kmeans; across ranks equal up to the rounding
+ * order of the all-reduced sums.  Collective: every rank calls it with the same arguments except
+ * n_local, X and labels.  Synchronises. */
+plp_status plp_kmeans_dist(plp_ctx* ctx, int64_t n_local, int dim, int clusters, const double* X,
+                           const double* uniforms, int restarts, int max_iters, double rel_tol,
+                           int32_t* labels, double* centroids, double* sse, int* iters);
 /* RCut = sum_c cut(C_c, ~C_c) / |C_c| over the graph's rows; labels (device
  * int32, n_cols entries so halo labels resolve).  Outputs (device, nullable): cut[clusters],
  * sizes[clusters] (int64), rcut[1].  Empty cluster -> rcut = NaN (device; the binding raises). */

@@ -103,11 +103,15 @@ __device__ void block_find(int cnt, double base, double target, const double* pr
 // (in slices of 1024), then the D^2 values of the chosen chunk.  The running sums differ from the
 // oracle's sequential sum only in rounding order (reading #13); where rounding leaves no crossing
 // inside the chosen range, its last positive entry is taken.
+// Multi-rank seeding (plp_kmeans_dist) splits the pick: S_out != nullptr writes this rank's sum S
+// and returns; target_in >= 0 replaces u * S by a given threshold (the global u * S less the
+// lower ranks' sums) on the rank that owns the crossing.
 __global__ void __launch_bounds__(1024) km_pick_kernel(int64_t n, int dim, const double* __restrict__ X,
                                                        const double* __restrict__ D2,
                                                        const double* __restrict__ cs, double u,
                                                        double* __restrict__ cent_row,
-                                                       int64_t* pick_out) {
+                                                       int64_t* pick_out, double target_in = -1.0,
+                                                       double* S_out = nullptr) {
   __shared__ double wsum[32];
   __shared__ double pre[1024];
   __shared__ int s_hit, s_last;
@@ -118,12 +122,16 @@ __global__ void __launch_bounds__(1024) km_pick_kernel(int64_t n, int dim, const
   for (int64_t c = t * per; c < (t + 1) * per && c < nch; ++c) v += cs[c];
   block_scan_to(v, 0.0, wsum, pre);
   const double S = pre[T - 1];
+  if (S_out) {
+    if (t == 0) *S_out = S;
+    return;
+  }
   int64_t pick;
   if (!(S > 0.0)) {
     pick = (int64_t)floor(u * (double)n);
     if (pick >= n) pick = n - 1;
   } else {
-    const double target = u * S;
+    const double target = target_in >= 0.0 ? target_in : u * S;
     // level 1: thread range q
     block_find(T, 0.0, target, pre, &s_hit, &s_last);
     const int q = s_hit >= 0 ? s_hit : s_last;
@@ -428,6 +436,18 @@ __global__ void km_reseed_kernel(int grid, int dim, int c, const double* pv, con
   if (threadIdx.x == 0) best_d[far] = -1.0;
 }
 
+// (value, index) of the argmax partials of km_argmax_kernel (largest value, lowest index)
+__global__ void km_argmax_final_kernel(int grid, const double* pv, const int64_t* pi, double* out) {
+  if (threadIdx.x == 0) {
+    double bv = -INFINITY;
+    int64_t bi = 0;
+    for (int b = 0; b < grid; ++b)
+      if (pv[b] > bv || (pv[b] == bv && pi[b] < bi)) { bv = pv[b]; bi = pi[b]; }
+    out[0] = bv;
+    out[1] = (double)bi;
+  }
+}
+
 // out[e] = sum_b part[b][e]: one CTA per entry (thread-strided, warp xor trees, warps in order)
 __global__ void __launch_bounds__(256) km_sum_kernel(int grid, int E, const double* part, double* out) {
   __shared__ double ws[8];
@@ -449,20 +469,51 @@ __global__ void __launch_bounds__(256) km_sum_kernel(int grid, int E, const doub
 
 using namespace plp;
 
-extern "C" plp_status plp_kmeans(plp_ctx* ctx, int64_t n, int dim, int K, const double* X,
-                                 const double* uniforms, int restarts, int max_iters,
-                                 double rel_tol, int32_t* labels, double* centroids, double* sse,
-                                 int* iters) {
-  if (!ctx || !X || !uniforms || !labels || !centroids || !sse)
+namespace plp {
+// k-means over this rank's n rows; coll: the rows of all ranks of ctx in rank order (every
+// reduction all-reduced, every pick made by the rank owning the point and broadcast), the
+// single-rank computation when coll is false.
+static plp_status kmeans_impl(plp_ctx* ctx, int64_t n, int dim, int K, const double* X,
+                              const double* uniforms, int restarts, int max_iters, double rel_tol,
+                              int32_t* labels, double* centroids, double* sse, int* iters, bool coll) {
+  if (!ctx || (!X && n > 0) || !uniforms || (!labels && n > 0) || !centroids || !sse)
     return set_error(PLP_ERR_ARG, "null argument");
   if (dim < 1 || dim > PLP_MAX_K || K < 1 || K > PLP_MAX_K)
     return set_error(PLP_ERR_DOMAIN, "dim and clusters must be in [1, 32]");
-  if (n < K) return set_error(PLP_ERR_SHAPE, "need n >= clusters");
   if (restarts < 1 || max_iters < 0) return set_error(PLP_ERR_ARG, "restarts >= 1, max_iters >= 0");
+  if (n < 0) return set_error(PLP_ERR_SHAPE, "n >= 0");
   cudaStream_t st = ctx->stream;
+  const int world = coll ? ctx->world : 1, rank = coll ? ctx->rank : 0;
+  if (world > 512) return set_error(PLP_ERR_ARG, "plp_kmeans_dist: at most 512 ranks");
+  // rank row offsets (all-reduce of a one-hot count vector: exact)
+  std::vector<int64_t> cnt(world, 0), off(world + 1, 0);
+  double* cscr = ctx->scratch + 4096;  // collective scratch: 2 x world doubles
+  std::vector<double> hsc(2 * (size_t)world);
+  if (coll) {
+    double* dcnt = cscr + 1024;
+    PLP_CUDA(cudaMemsetAsync(dcnt, 0, sizeof(double) * world, st));
+    const double nd = (double)n;
+    PLP_CUDA(cudaMemcpyAsync(dcnt + rank, &nd, sizeof(double), cudaMemcpyHostToDevice, st));
+    plp_status s0 = comm_allreduce(ctx, dcnt, world);
+    if (s0) return s0;
+    PLP_CUDA(cudaMemcpyAsync(hsc.data(), dcnt, sizeof(double) * world, cudaMemcpyDeviceToHost, st));
+    PLP_CUDA(cudaStreamSynchronize(st));
+    for (int r = 0; r < world; ++r) cnt[r] = (int64_t)hsc[r];
+  } else {
+    cnt[0] = n;
+  }
+  for (int r = 0; r < world; ++r) off[r + 1] = off[r] + cnt[r];
+  const int64_t N = off[world], my0 = off[rank];
+  if (N < K) return set_error(PLP_ERR_SHAPE, "need n >= clusters");
+  auto owner_of = [&](int64_t gi) {
+    int r = 0;
+    while (r + 1 < world && gi >= off[r + 1]) ++r;
+    return r;
+  };
   // workspace: best_d (n), D2 (n), chunk sums, labels + centroids of the running restart
   const int64_t nch = (n + kChunk - 1) / kChunk;
   const size_t need = (size_t)(2 * n + nch + K * dim + (n + 1) / 2 + 64);
+  // a point of this rank -> cent row (dev), and its all-reduce broadcast (others contribute 0)
   if (ctx->km_cap < need) {
     cudaFree(ctx->km_best);
     ctx->km_best = nullptr;
@@ -490,17 +541,69 @@ extern "C" plp_status plp_kmeans(plp_ctx* ctx, int64_t n, int dim, int K, const 
   std::vector<double> host(E);
   double best = INFINITY;
   int best_iters = 0;
+  // broadcast of centre row c from the rank that wrote it (the others zero it): exact
+  auto bcast_row = [&](int c) -> plp_status { return comm_allreduce(ctx, cent + (int64_t)c * dim, dim); };
+  auto zero_row = [&](int c) -> plp_status {
+    PLP_CUDA(cudaMemsetAsync(cent + (int64_t)c * dim, 0, sizeof(double) * dim, st));
+    return PLP_OK;
+  };
   for (int r = 0; r < restarts; ++r) {
     const double* u = uniforms + (int64_t)r * K;
+    plp_status s;
     // ---- k-means++ seeding ----
-    int64_t c0 = (int64_t)floor(u[0] * (double)n);
-    if (c0 >= n) c0 = n - 1;
-    PLP_CUDA(cudaMemcpyAsync(cent, X + c0 * dim, sizeof(double) * dim, cudaMemcpyDeviceToDevice, st));
+    int64_t c0 = (int64_t)floor(u[0] * (double)N);
+    if (c0 >= N) c0 = N - 1;
+    if (coll && (s = zero_row(0))) return s;
+    if (c0 >= my0 && c0 < my0 + n)
+      PLP_CUDA(cudaMemcpyAsync(cent, X + (c0 - my0) * dim, sizeof(double) * dim, cudaMemcpyDeviceToDevice, st));
+    if (coll && (s = bcast_row(0))) return s;
     for (int m = 1; m < K; ++m) {
-      km_d2_kernel<<<gridd, kChunk, 0, st>>>(n, dim, X, cent + (int64_t)(m - 1) * dim, D2, csum, m == 1);
-      PLP_LAUNCH_CHECK("km_d2_kernel");
-      km_pick_kernel<<<1, 1024, 0, st>>>(n, dim, X, D2, csum, u[m], cent + (int64_t)m * dim, nullptr);
-      PLP_LAUNCH_CHECK("km_pick_kernel");
+      if (n > 0) {
+        km_d2_kernel<<<gridd, kChunk, 0, st>>>(n, dim, X, cent + (int64_t)(m - 1) * dim, D2, csum, m == 1);
+        PLP_LAUNCH_CHECK("km_d2_kernel");
+      }
+      if (!coll) {
+        km_pick_kernel<<<1, 1024, 0, st>>>(n, dim, X, D2, csum, u[m], cent + (int64_t)m * dim, nullptr);
+        PLP_LAUNCH_CHECK("km_pick_kernel");
+        continue;
+      }
+      // every rank's sum of D^2, the global threshold u * sum, and the rank whose running sum
+      // crosses it (where rounding leaves no crossing: the last rank with a positive sum)
+      PLP_CUDA(cudaMemsetAsync(cscr, 0, sizeof(double) * world, st));
+      if (n > 0) {
+        km_pick_kernel<<<1, 1024, 0, st>>>(n, dim, X, D2, csum, u[m], nullptr, nullptr, -1.0, cscr + rank);
+        PLP_LAUNCH_CHECK("km_pick_kernel");
+      }
+      if ((s = comm_allreduce(ctx, cscr, world))) return s;
+      PLP_CUDA(cudaMemcpyAsync(hsc.data(), cscr, sizeof(double) * world, cudaMemcpyDeviceToHost, st));
+      PLP_CUDA(cudaStreamSynchronize(st));
+      double S = 0.0;
+      for (int q = 0; q < world; ++q) S += hsc[q];
+      if ((s = zero_row(m))) return s;
+      if (!(S > 0.0)) {
+        int64_t pk = (int64_t)floor(u[m] * (double)N);
+        if (pk >= N) pk = N - 1;
+        if (pk >= my0 && pk < my0 + n)
+          PLP_CUDA(cudaMemcpyAsync(cent + (int64_t)m * dim, X + (pk - my0) * dim, sizeof(double) * dim,
+                                   cudaMemcpyDeviceToDevice, st));
+      } else {
+        const double target = u[m] * S;
+        int own = -1, lastpos = -1;
+        double pre = 0.0, pre_own = 0.0, pre_last = 0.0;
+        for (int q = 0; q < world; ++q) {
+          const double nx = pre + hsc[q];
+          if (hsc[q] > 0.0) { lastpos = q; pre_last = pre; }
+          if (own < 0 && pre <= target && target < nx) { own = q; pre_own = pre; }
+          pre = nx;
+        }
+        if (own < 0) { own = lastpos; pre_own = pre_last; }
+        if (own == rank) {
+          km_pick_kernel<<<1, 1024, 0, st>>>(n, dim, X, D2, csum, u[m], cent + (int64_t)m * dim, nullptr,
+                                             target - pre_own, nullptr);
+          PLP_LAUNCH_CHECK("km_pick_kernel");
+        }
+      }
+      if ((s = bcast_row(m))) return s;
     }
     // ---- Lloyd ----
     const bool mma = K <= 8 && dim <= 8;
@@ -511,27 +614,35 @@ extern "C" plp_status plp_kmeans(plp_ctx* ctx, int64_t n, int dim, int K, const 
     const int64_t groups = (n + 63) / 64;
     if (groups < (int64_t)grid_mma * 8) grid_mma = (int)std::max<int64_t>(1, (groups + 7) / 8);
     auto assign = [&](double* sse_out, std::vector<double>& h) -> plp_status {
-      if (mma) {
-        if (dim == 8 && K == 8 && ((uintptr_t)X & 15u) == 0)
-          km_assign_mma_kernel<8, 8><<<grid_mma, 256, 0, st>>>(n, dim, K, X, cent, lab, best_d, ctx->partials);
-        else if (dim == 8 && ((uintptr_t)X & 15u) == 0)
-          km_assign_mma_kernel<8, 0><<<grid_mma, 256, 0, st>>>(n, dim, K, X, cent, lab, best_d, ctx->partials);
-        else
-          km_assign_mma_kernel<0, 0><<<grid_mma, 256, 0, st>>>(n, dim, K, X, cent, lab, best_d, ctx->partials);
-        PLP_LAUNCH_CHECK("km_assign_mma_kernel");
+      if (n == 0) {
+        PLP_CUDA(cudaMemsetAsync(red, 0, sizeof(double) * E, st));
       } else {
-        km_assign_kernel<<<grid, kKmThreads, 0, st>>>(n, dim, K, X, cent, lab, best_d, ctx->partials);
-        PLP_LAUNCH_CHECK("km_assign_kernel");
+        if (mma) {
+          if (dim == 8 && K == 8 && ((uintptr_t)X & 15u) == 0)
+            km_assign_mma_kernel<8, 8><<<grid_mma, 256, 0, st>>>(n, dim, K, X, cent, lab, best_d, ctx->partials);
+          else if (dim == 8 && ((uintptr_t)X & 15u) == 0)
+            km_assign_mma_kernel<8, 0><<<grid_mma, 256, 0, st>>>(n, dim, K, X, cent, lab, best_d, ctx->partials);
+          else
+            km_assign_mma_kernel<0, 0><<<grid_mma, 256, 0, st>>>(n, dim, K, X, cent, lab, best_d, ctx->partials);
+          PLP_LAUNCH_CHECK("km_assign_mma_kernel");
+        } else {
+          km_assign_kernel<<<grid, kKmThreads, 0, st>>>(n, dim, K, X, cent, lab, best_d, ctx->partials);
+          PLP_LAUNCH_CHECK("km_assign_kernel");
+        }
+        km_sum_kernel<<<E, 256, 0, st>>>(mma ? grid_mma : grid, E, ctx->partials, red);
+        PLP_LAUNCH_CHECK("km_sum_kernel");
       }
-      km_sum_kernel<<<E, 256, 0, st>>>(mma ? grid_mma : grid, E, ctx->partials, red);
-      PLP_LAUNCH_CHECK("km_sum_kernel");
+      if (coll) {  // sums, counts and sse over the ranks
+        plp_status s2 = comm_allreduce(ctx, red, E);
+        if (s2) return s2;
+      }
       PLP_CUDA(cudaMemcpyAsync(h.data(), red, sizeof(double) * E, cudaMemcpyDeviceToHost, st));
       PLP_CUDA(cudaStreamSynchronize(st));
       *sse_out = h[E - 1];
       return PLP_OK;
     };
     double cur = 0.0;
-    plp_status s = assign(&cur, host);
+    s = assign(&cur, host);
     if (s) return s;
     int it = 0;
     while (it < max_iters) {
@@ -539,10 +650,34 @@ extern "C" plp_status plp_kmeans(plp_ctx* ctx, int64_t n, int dim, int K, const 
       PLP_LAUNCH_CHECK("km_update_kernel");
       for (int c = 0; c < K; ++c) {
         if (host[K * dim + c] > 0.0) continue;  // empty cluster -> farthest point
-        km_argmax_kernel<<<gridn, 256, 0, st>>>(n, best_d, pv, pi);
-        PLP_LAUNCH_CHECK("km_argmax_kernel");
-        km_reseed_kernel<<<1, 32, 0, st>>>(gridn, dim, c, pv, pi, X, cent, best_d);
-        PLP_LAUNCH_CHECK("km_reseed_kernel");
+        if (!coll) {
+          km_argmax_kernel<<<gridn, 256, 0, st>>>(n, best_d, pv, pi);
+          PLP_LAUNCH_CHECK("km_argmax_kernel");
+          km_reseed_kernel<<<1, 32, 0, st>>>(gridn, dim, c, pv, pi, X, cent, best_d);
+          PLP_LAUNCH_CHECK("km_reseed_kernel");
+          continue;
+        }
+        // every rank's farthest point (value, global index); largest value, lowest index wins
+        std::vector<double> vi(2 * (size_t)world);
+        PLP_CUDA(cudaMemsetAsync(cscr, 0, sizeof(double) * 2 * world, st));
+        if (n > 0) {
+          km_argmax_kernel<<<gridn, 256, 0, st>>>(n, best_d, pv, pi);
+          PLP_LAUNCH_CHECK("km_argmax_kernel");
+          km_argmax_final_kernel<<<1, 32, 0, st>>>(gridn, pv, pi, cscr + 2 * rank);
+          PLP_LAUNCH_CHECK("km_argmax_final_kernel");
+        }
+        if ((s = comm_allreduce(ctx, cscr, 2 * (size_t)world))) return s;
+        PLP_CUDA(cudaMemcpyAsync(vi.data(), cscr, sizeof(double) * 2 * world, cudaMemcpyDeviceToHost, st));
+        PLP_CUDA(cudaStreamSynchronize(st));
+        int own = -1;
+        for (int q = 0; q < world; ++q)
+          if (cnt[q] > 0 && (own < 0 || vi[2 * q] > vi[2 * own])) own = q;
+        if ((s = zero_row(c))) return s;
+        if (own == rank) {
+          km_reseed_kernel<<<1, 32, 0, st>>>(gridn, dim, c, pv, pi, X, cent, best_d);
+          PLP_LAUNCH_CHECK("km_reseed_kernel");
+        }
+        if ((s = bcast_row(c))) return s;
       }
       double nxt = 0.0;
       if ((s = assign(&nxt, host))) return s;
@@ -554,7 +689,7 @@ extern "C" plp_status plp_kmeans(plp_ctx* ctx, int64_t n, int dim, int K, const 
     if (cur < best) {
       best = cur;
       best_iters = it;
-      PLP_CUDA(cudaMemcpyAsync(labels, lab, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st));
+      if (n > 0) PLP_CUDA(cudaMemcpyAsync(labels, lab, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st));
       PLP_CUDA(cudaMemcpyAsync(centroids, cent, sizeof(double) * K * dim, cudaMemcpyDeviceToDevice, st));
     }
   }
@@ -562,4 +697,22 @@ extern "C" plp_status plp_kmeans(plp_ctx* ctx, int64_t n, int dim, int K, const 
   *sse = best;
   if (iters) *iters = best_iters;
   return PLP_OK;
+}
+}  // namespace plp
+
+extern "C" plp_status plp_kmeans(plp_ctx* ctx, int64_t n, int dim, int K, const double* X,
+                                 const double* uniforms, int restarts, int max_iters,
+                                 double rel_tol, int32_t* labels, double* centroids, double* sse,
+                                 int* iters) {
+  if (n < 1) return set_error(PLP_ERR_SHAPE, "need n >= clusters");
+  return kmeans_impl(ctx, n, dim, K, X, uniforms, restarts, max_iters, rel_tol, labels, centroids, sse, iters,
+                     false);
+}
+
+extern "C" plp_status plp_kmeans_dist(plp_ctx* ctx, int64_t n_local, int dim, int K, const double* X,
+                                      const double* uniforms, int restarts, int max_iters, double rel_tol,
+                                      int32_t* labels, double* centroids, double* sse, int* iters) {
+  if (!ctx) return set_error(PLP_ERR_ARG, "null argument");
+  return kmeans_impl(ctx, n_local, dim, K, X, uniforms, restarts, max_iters, rel_tol, labels, centroids, sse,
+                     iters, ctx->comm != nullptr);
 }

@@ -43,7 +43,7 @@ SYMBOLS = [
     "plp_halo_plan", "plp_create_graph", "plp_graph_info", "plp_destroy_graph", "plp_fgrad",
     "plp_hessvec", "plp_fgrad_hessvec", "plp_edge_pass", "plp_full_epilogue",
     "plp_objective_from_ab", "plp_gram", "plp_project", "plp_apply_sub", "plp_retract",
-    "plp_cholesky", "plp_apply_rinv", "plp_dot", "plp_axpby", "plp_gather_rows", "plp_kmeans",
+    "plp_cholesky", "plp_apply_rinv", "plp_dot", "plp_axpby", "plp_gather_rows", "plp_kmeans", "plp_kmeans_dist",
     "plp_rcut", "plp_debug_pow", "plp_tile_order", "plp_last_edge_kernel", "plp_halo_tile_rows", "plp_tcg_init",
     "plp_tcg_run", "plp_tcg_graph_create", "plp_tcg_graph_launch", "plp_tcg_graph_nodes",
     "plp_tcg_graph_destroy", "plp_get_nccl_unique_id", "plp_ctx_comm_info", "plp_allreduce_sum",
@@ -490,6 +490,25 @@ def kmeans(ctx: Context, X, clusters: int, uniforms, restarts: int = 10, max_ite
     _ck(_lib.plp_kmeans(ctx.h, C_I64(n), dim, clusters, _dev(X, "X"), up, restarts, max_iters,
                         C_D(rel_tol), _dev(labels, "labels", dtype=torch.int32), _dev(cent, "centroids"),
                         ctypes.byref(sse), ctypes.byref(it)), "plp_kmeans")
+    return labels, cent, sse.value, it.value
+
+
+def kmeans_dist(ctx: Context, X, clusters: int, uniforms, restarts: int = 10, max_iters: int = 300,
+                rel_tol: float = 1e-9):
+    """Collective k-means over the ranks' row blocks X (plp_kmeans_dist): labels of this rank's
+    rows; centroids, sse and iterations identical on every rank."""
+    n, dim = X.shape
+    u, up = _host(uniforms, np.float64)
+    if u.size < restarts * clusters:
+        raise ValueError("uniforms must hold restarts x clusters values")
+    labels = torch.empty(n, dtype=torch.int32, device=X.device)
+    cent = _empty(ctx, clusters, dim)
+    sse = ctypes.c_double()
+    it = ctypes.c_int()
+    xp = _dev(X, "X") if n > 0 else None
+    lp = _dev(labels, "labels", dtype=torch.int32) if n > 0 else None
+    _ck(_lib.plp_kmeans_dist(ctx.h, C_I64(n), dim, clusters, xp, up, restarts, max_iters, C_D(rel_tol), lp,
+                             _dev(cent, "centroids"), ctypes.byref(sse), ctypes.byref(it)), "plp_kmeans_dist")
     return labels, cent, sse.value, it.value
 
 

@@ -343,18 +343,24 @@ def _allgather_rows(X, group=None):
     return torch.cat([pt[:int(v.item())] for pt, v in zip(parts, ns)])
 
 
-def cluster(ctx: plp.Context, g: plp.Graph, U, k: int, uniforms, restarts: int = 10):
+def cluster(ctx: plp.Context, g: plp.Graph, U, k: int, uniforms, restarts: int = 10, kmeans: str = "sharded"):
     """Discretisation: k-means on the rows of U, then RCut of the labels.
 
-    Multi-rank: the n x k embedding is gathered on every rank (NCCL all-gather; 0.5 GB at C5, a
-    millisecond over NVLink) and k-means runs on the whole embedding on each GPU (identical input,
-    identical labels: the same seeding uniforms and deterministic kernels); each rank keeps its
-    own rows' labels (+ halo slots) and RCut is collective (plp_rcut)."""
-    if isinstance(g, plp.DistGraph) and ctx.world > 1:
-        Ua = _allgather_rows(U[:g.n_rows].contiguous())
-        lab_all, centroids, sse, _ = plp.kmeans(ctx, Ua, k, uniforms, restarts=restarts)
+    Multi-rank (a DistGraph): kmeans="sharded" (default) runs the collective k-means on each
+    rank's own rows (plp_kmeans_dist: D^2 sums, per-cluster sums / counts / sse and the farthest
+    point all-reduced; bitwise plp_kmeans on one rank); kmeans="gathered" all-gathers the n x k
+    embedding and runs plp_kmeans on the whole of it on every GPU (identical labels everywhere,
+    0.5 GB over NVLink at C5).  Each rank keeps its own rows' labels (+ halo slots) and RCut is
+    collective (plp_rcut)."""
+    if isinstance(g, plp.DistGraph):
         labels = torch.zeros(g.n_cols, dtype=torch.int32, device=U.device)
-        labels[:g.n_rows] = lab_all[g.row_begin:g.row_end]
+        if kmeans == "gathered" and ctx.world > 1:
+            Ua = _allgather_rows(U[:g.n_rows].contiguous())
+            lab_all, centroids, sse, _ = plp.kmeans(ctx, Ua, k, uniforms, restarts=restarts)
+            labels[:g.n_rows] = lab_all[g.row_begin:g.row_end]
+        else:
+            lab, centroids, sse, _ = plp.kmeans_dist(ctx, U[:g.n_rows].contiguous(), k, uniforms, restarts=restarts)
+            labels[:g.n_rows] = lab
         rc, cut, sizes = plp.rcut(ctx, g, k, labels)
         return labels[:g.n_rows], float(rc.item()), sse
     labels, centroids, sse, _ = plp.kmeans(ctx, U, k, uniforms, restarts=restarts)

@@ -102,3 +102,150 @@ def test_sharded_oracle_matches_single(name, n, k, p, world):
         assert eA < 1e-13 and eB < 1e-13, (eA, eB)
         assert eG < 1e-12 and eH < 1e-12, (eG, eH)
         assert n_halo > 0 and n_recv >= 1 and n_send >= 1
+
+
+# ---- the collective k-means protocol (plp_kmeans_dist, csrc/kmeans.cu) on CPU ranks --------------
+# Each rank holds a contiguous block of the points; the local steps are plain numpy (a stand-in for
+# the kernels), the cross-rank steps are the protocol's all-reduces: row counts, per-rank D^2 sums
+# (the rank whose running sum crosses u * sum picks inside its block and broadcasts the point),
+# per-cluster sums / counts / sse, and the farthest point (value, global index) for an empty
+# cluster.  The result must be the sequential k-means of the oracle on the concatenated points.
+def _kmeans_protocol(X, K, u_all, restarts, max_iters=300, rel_tol=1e-9):
+    rank, world = dist.get_rank(), dist.get_world_size()
+    n, dim = X.shape
+    cnt = torch.zeros(world, dtype=torch.float64)
+    cnt[rank] = n
+    dist.all_reduce(cnt)
+    off = np.concatenate([[0], np.cumsum(cnt.numpy().astype(np.int64))])
+    N, my0 = int(off[-1]), int(off[rank])
+
+    def bcast(row_or_none):
+        v = torch.zeros(dim, dtype=torch.float64)
+        if row_or_none is not None:
+            v += torch.from_numpy(row_or_none)
+        dist.all_reduce(v)
+        return v.numpy()
+
+    def mine(gi):
+        return X[gi - my0] if my0 <= gi < my0 + n else None
+
+    best = (np.inf, None, None, 0)
+    u_all = np.asarray(u_all, dtype=np.float64).reshape(-1)
+    for r in range(restarts):
+        u = u_all[r * K:(r + 1) * K]
+        C = np.zeros((K, dim))
+        c0 = min(int(np.floor(u[0] * N)), N - 1)
+        C[0] = bcast(mine(c0))
+        D2 = None
+        for m in range(1, K):
+            d = ((X - C[m - 1]) ** 2).sum(axis=1)
+            D2 = d if D2 is None else np.minimum(D2, d)
+            S_r = torch.zeros(world, dtype=torch.float64)
+            S_r[rank] = D2.sum()
+            dist.all_reduce(S_r)
+            S_r = S_r.numpy()
+            S = float(S_r.sum())
+            row = None
+            if not S > 0.0:
+                row = mine(min(int(np.floor(u[m] * N)), N - 1))
+            else:
+                t = u[m] * S
+                pre = np.concatenate([[0.0], np.cumsum(S_r)])
+                own = next((q for q in range(world) if pre[q] <= t < pre[q + 1]),
+                           max(q for q in range(world) if S_r[q] > 0))
+                if own == rank:
+                    cs = np.cumsum(D2)
+                    hit = np.nonzero(cs > t - pre[own])[0]
+                    row = X[hit[0] if hit.size else int(np.max(np.nonzero(D2 > 0)[0]))]
+            C[m] = bcast(row)
+
+        def assign(C):
+            dd = ((X[:, None, :] - C[None, :, :]) ** 2).sum(axis=2)
+            lab = np.argmin(dd, axis=1)
+            bd = dd[np.arange(n), lab]
+            red = np.zeros(K * dim + K + 1)
+            for c in range(K):
+                red[c * dim:(c + 1) * dim] = X[lab == c].sum(axis=0)
+                red[K * dim + c] = np.sum(lab == c)
+            red[-1] = bd.sum()
+            red = torch.from_numpy(red)
+            dist.all_reduce(red)
+            return lab, bd, red.numpy()
+
+        lab, bd, red = assign(C)
+        cur, it = red[-1], 0
+        while it < max_iters:
+            for c in range(K):
+                if red[K * dim + c] > 0:
+                    C[c] = red[c * dim:(c + 1) * dim] / red[K * dim + c]
+            for c in range(K):
+                if red[K * dim + c] > 0:
+                    continue
+                vi = torch.zeros(2 * world, dtype=torch.float64)
+                if n:
+                    j = int(np.argmax(bd))
+                    vi[2 * rank], vi[2 * rank + 1] = bd[j], my0 + j
+                dist.all_reduce(vi)
+                vi = vi.numpy()
+                own = max(range(world), key=lambda q: (vi[2 * q], -q))
+                row = None
+                if own == rank:
+                    j = int(vi[2 * own + 1]) - my0
+                    row, bd[j] = X[j].copy(), -1.0
+                C[c] = bcast(row)
+            lab, bd, red = assign(C)
+            it += 1
+            nxt = red[-1]
+            conv = cur == 0.0 or abs(cur - nxt) < rel_tol * cur
+            cur = nxt
+            if conv:
+                break
+        if cur < best[0]:
+            best = (cur, lab.copy(), C.copy(), it)
+    return best
+
+
+def _km_worker(rank, world, port, n, dim, K, seed, q):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        from plp_inputs import draw_uniforms
+        rng = np.random.default_rng(seed)
+        X = rng.uniform(-8, 8, size=(K, dim))[rng.integers(0, K, n)] + rng.standard_normal((n, dim))
+        if seed % 2:  # duplicates: empty clusters and the farthest-point reseed
+            X[: n // 2] = X[0]
+        u = draw_uniforms(3, K)
+        b = np.linspace(0, n, world + 1).astype(int)
+        b[1] = b[1] // 3  # unequal blocks
+        sse, lab, C, it = _kmeans_protocol(X[b[rank]:b[rank + 1]], K, u, restarts=3)
+        lab_o, C_o, sse_o, it_o = oracle.kmeans(X, K, u, restarts=3)
+        q.put((rank, bool(np.array_equal(lab, lab_o[b[rank]:b[rank + 1]])),
+               float(np.max(np.abs(C - C_o)) / np.max(np.abs(C_o))), abs(sse - sse_o) / sse_o, it == it_o))
+    except Exception as e:
+        q.put((rank, "error", repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n,dim,K,seed,world", [(3000, 4, 5, 0, 2), (2500, 8, 8, 1, 3), (4001, 3, 3, 2, 3)])
+def test_kmeans_collective_protocol_matches_oracle(n, dim, K, seed, world):
+    """The protocol of plp_kmeans_dist on 2 and 3 gloo ranks (unequal row blocks, empty clusters)
+    gives the oracle's sequential k-means: labels equal, centroids and sse within 1e-12."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_km_worker, args=(r, world, port, n, dim, K, seed, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+    errs = [r for r in res if r[1] == "error"]
+    assert not errs, errs
+    for rank, same_lab, eC, eS, same_it in res:
+        assert same_lab, f"rank {rank}: labels differ"
+        assert eC < 1e-12 and eS < 1e-12, (eC, eS)
+        assert same_it

@@ -179,3 +179,39 @@ def test_interior_boundary_split_path(plp, tmp_path):
                 assert colwise_relerr(z[f"c_{k}_{key}"], z[f"p_{k}_{key}"]) < 1e-13, (k, key)
         for key in ("F", "AB"):
             assert scalar_relerr(z[f"c_{k}_{key}"], z[f"p_{k}_{key}"]) < 1e-14, (k, key)
+
+
+@pytest.mark.parametrize("n,dim,K,seed", [(30_000, 8, 8, 0), (20_011, 4, 5, 1), (5_000, 3, 3, 2),
+                                          (40_000, 12, 10, 3)])
+def test_kmeans_dist_one_rank_bitwise_equal_to_kmeans(plp, ctxs, n, dim, K, seed):
+    """plp_kmeans_dist on a one-rank communicator (the collective seeding / Lloyd / reseed code
+    path: sums all-reduced, picks by the owning rank and broadcast) is bitwise plp_kmeans, and
+    plp_kmeans_dist on a context without a communicator is too; labels equal the oracle's."""
+    plain, coll = ctxs
+    rng = np.random.default_rng(seed)
+    C = rng.uniform(-6, 6, size=(K, dim))
+    X = C[rng.integers(0, K, n)] + rng.standard_normal((n, dim))
+    Xt = torch.from_numpy(X).cuda()
+    u = draw_uniforms(4, K)
+    ref = plp.kmeans(plain, Xt, K, u, restarts=4)
+    for ctx in (coll, plain):
+        got = plp.kmeans_dist(ctx, Xt, K, u, restarts=4)
+        assert torch.equal(got[0], ref[0])
+        assert torch.equal(got[1], ref[1])
+        assert got[2] == ref[2] and got[3] == ref[3]
+    lab_o, _, sse_o, _ = oracle.kmeans(X, K, u, restarts=4)
+    assert np.array_equal(ref[0].cpu().numpy(), lab_o)
+
+
+def test_kmeans_dist_empty_cluster_reseed_one_rank(plp, ctxs):
+    """Duplicate points force empty clusters: the farthest-point reseed through the collective
+    path equals plp_kmeans bitwise."""
+    plain, coll = ctxs
+    rng = np.random.default_rng(7)
+    X = np.repeat(rng.standard_normal((6, 4)), 500, axis=0)
+    X[:10] += 1e-3 * rng.standard_normal((10, 4))
+    Xt = torch.from_numpy(X).cuda()
+    u = draw_uniforms(3, 8)
+    ref = plp.kmeans(plain, Xt, 8, u, restarts=3)
+    got = plp.kmeans_dist(coll, Xt, 8, u, restarts=3)
+    assert torch.equal(got[0], ref[0]) and torch.equal(got[1], ref[1]) and got[2] == ref[2]
