@@ -1,25 +1,27 @@
 // Halo-tile edge kernel: the fused F / EucGrad / EucHessianEta pass (
 // DESIGN.md §5) with every neighbour row served from shared memory.
 //
-// The rows are cut into tiles of kHaloT = 256 consecutive rows.  plp_create_graph lists, per tile,
-// the distinct columns outside it (the tile's halo, at most halo_ext_cap of them) and re-encodes
-// every stored edge as a tile-local index: j - r0 for an internal neighbour, kHaloT + x for the
-// x-th halo row.  One persistent CTA of 512 threads per SM walks the tiles (interleaved across
-// CTAs, so neighbouring tiles are in flight together and the halo rows hit L2), double-buffered:
-//   * a dedicated producer warp (warp specialisation: 16 consumer warps + 1) stages each tile: lane 0
-//     issues TMA bulk copies (cp.async.bulk + mbarrier) of the tile's own U / eta rows, row_ptr and
-//     schedule slices, (enc, w) ranges, and two tiles ahead the tile's halo list (count, CSR
-//     bounds, columns); the 32 lanes gather the halo rows U_j, eta_j with cp.async (16-byte pieces,
-//     8 rows per instruction at k = 8) whose cp.async.mbarrier.arrive joins the TMA bytes on the
-//     buffer's "full" mbarrier;
+// The rows are cut into tiles of kHaloT = PLP_HALO_TILE (224) consecutive rows.  plp_create_graph
+// lists, per tile, the distinct columns outside it (the tile's halo, ordered by decreasing number
+// of references) and re-encodes every stored edge as a tile-local index: j - r0 for an internal
+// neighbour, kHaloT + x for the x-th halo row.  One persistent CTA of 15 warps per SM walks the
+// tiles (interleaved across CTAs, so neighbouring tiles are in flight together and the halo rows
+// hit L2), double-buffered:
+//   * a producer warp (warp specialisation: 14 consumer warps + 1) stages each tile: lane 0 issues
+//     TMA bulk copies (cp.async.bulk + mbarrier) of the tile's own U / eta rows, row_ptr and
+//     schedule slices, (enc, w) ranges, and two tiles ahead the tile's halo list; the 32 lanes
+//     gather the halo rows U_j, eta_j with cp.async (16-byte pieces, 8 rows per instruction at
+//     k = 8) whose cp.async.mbarrier.arrive joins the TMA bytes on the buffer's "full" mbarrier;
+//     a tile whose halo exceeds the staged rows (overflow mode) leaves its least referenced halo
+//     rows in L2, where the consumers read them;
 //   * consumers release a buffer with one arrival per warp on its "empty" mbarrier; there is no
 //     CTA-wide barrier per tile, so a warp that finishes early goes on with the next (resident)
 //     tile; while tile i is computed, tile i + 1 is resident and tile i + 2 is in flight.
 // Rows are processed as in the row kernels (one group of LPR lanes per row, CPL = 2 columns per
-// lane, CSR order per row, one power per stored edge-column), reading U_j / eta_j with LDS.128, so
-// the only global traffic is the streaming of the tile data and the G / Hv stores: the L2 no longer
-// serves ~128 bytes per edge.  Degree-sorted 32-row windows are split between warp pairs so the
-// warps of a tile get equal work (rank slices {0, 3} and {1, 2} of each window).
+// lane at k = 4, 8, 4 at k = 16; CSR order per row, one power per stored edge-column, edges in
+// pairs), reading U_j / eta_j with 32-bit shared-window loads, so the only global traffic is the
+// streaming of the tile data and the G / Hv stores.  The tile's degree-sorted rows form slices of
+// 32 / LPR rows dealt to the warps in snake order (a heavy and a light slice per warp).
 #pragma once
 #include "async_copy.cuh"
 #include "dense_mma.cuh"
