@@ -479,33 +479,14 @@ __device__ void expand_blocks(const double* f, int K, int kr, double* out) {
   }
 }
 
+// The scalar step on the reduced totals (one CTA of 256 threads): fold / expand, <d, Hd> or
+// ||P r||^2, tcg_scalar_a / _b, and the matrix the next pass applies.
 template <int K, int MODE>
-__global__ void __launch_bounds__(256) tcg_reduce_kernel(int P, const double* __restrict__ part, double* tot,
-                                                         unsigned* counter, double* sc, int* st, int max_iters,
-                                                         int kr) {
+__device__ void tcg_reduce_tail(double* tot, double* sc, int* st, int max_iters, int kr) {
   constexpr int KK = K * K, E = MODE == 0 ? 2 * KK + 2 : KK + 1;
-  __shared__ double ws[8];
   __shared__ double t[E];
   __shared__ double f1[KK], f2[KK];
-  __shared__ unsigned ticket;
   __shared__ int go;
-  const int e = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double v = 0.0;
-  for (int b = threadIdx.x; b < P; b += 256) v += __ldcg(part + (int64_t)e * P + b);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if (lane == 0) ws[warp] = v;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int w = 0; w < 8; ++w) s += ws[w];
-    tot[e] = s;
-    __threadfence();
-    ticket = atomicAdd(counter, 1u);
-  }
-  __syncthreads();
-  if (ticket != (unsigned)E - 1) return;
-  __threadfence();
   for (int i = threadIdx.x; i < E; i += 256) t[i] = __ldcg(tot + i);
   __syncthreads();
   const bool fold = kr < K;
@@ -521,7 +502,6 @@ __global__ void __launch_bounds__(256) tcg_reduce_kernel(int P, const double* __
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    *counter = 0u;
     if (MODE == 0) {
       double c1 = 0.0;
       for (int i = 0; i < kk; ++i) c1 = fma(f2[i], f1[i], c1);
@@ -545,6 +525,43 @@ __global__ void __launch_bounds__(256) tcg_reduce_kernel(int P, const double* __
   }
 }
 
+// Multi-rank fused tCG: the scalar step after the totals were all-reduced over the ranks.
+template <int K, int MODE>
+__global__ void __launch_bounds__(256) tcg_step_kernel(double* tot, double* sc, int* st, int max_iters, int kr) {
+  tcg_reduce_tail<K, MODE>(tot, sc, st, max_iters, kr);
+}
+
+// defer = 1 (multi-rank): the last CTA only resets the ticket; the caller all-reduces tot and
+// launches tcg_step_kernel.
+template <int K, int MODE>
+__global__ void __launch_bounds__(256) tcg_reduce_kernel(int P, const double* __restrict__ part, double* tot,
+                                                         unsigned* counter, double* sc, int* st, int max_iters,
+                                                         int kr, int defer = 0) {
+  constexpr int KK = K * K, E = MODE == 0 ? 2 * KK + 2 : KK + 1;
+  __shared__ double ws[8];
+  __shared__ unsigned ticket;
+  const int e = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double v = 0.0;
+  for (int b = threadIdx.x; b < P; b += 256) v += __ldcg(part + (int64_t)e * P + b);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) ws[warp] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < 8; ++w) s += ws[w];
+    tot[e] = s;
+    __threadfence();
+    ticket = atomicAdd(counter, 1u);
+  }
+  __syncthreads();
+  if (ticket != (unsigned)E - 1) return;
+  __threadfence();
+  if (threadIdx.x == 0) *counter = 0u;
+  if (defer) return;
+  tcg_reduce_tail<K, MODE>(tot, sc, st, max_iters, kr);
+}
+
 __global__ void tcg_expand_s_kernel(const double* __restrict__ S, int kr, double* __restrict__ out) {
   expand_blocks(S, 8, kr, out);
 }
@@ -566,7 +583,7 @@ static int fused_grid(plp_ctx* ctx, int64_t row_blocks, int E, int per_sm) {  //
 template <int KT>
 static plp_status fused_iteration(plp_ctx* ctx, int64_t n, const double* U, const double* S, double* eta,
                                   double* Heta, double* r, double* dlt, const double* EH, double* scal,
-                                  int* status, int max_iters, int kr, int gram_grid) {
+                                  int* status, int max_iters, int kr, int gram_grid, bool coll = false) {
   constexpr int K = 8 * KT, KK = K * K;
   static const int unr_a = env_int("PLP_TCG_UNR_A", 4);
   static const int per_sm_a = env_int("PLP_TCG_GRID_A", unr_a == 4 ? resident_ctas(tcg_gram_a_kernel<KT, 4>, kTcgThreads)
@@ -585,16 +602,28 @@ static plp_status fused_iteration(plp_ctx* ctx, int64_t n, const double* U, cons
     PLP_LAUNCH_CHECK("tcg_gram_a_kernel");
   }
   tcg_reduce_kernel<K, 0><<<EA, 256, 0, ctx->stream>>>(ga, ctx->partials, scal + kTotA, counter, scal, status,
-                                                       max_iters, kr);
+                                                       max_iters, kr, coll ? 1 : 0);
   PLP_LAUNCH_CHECK("tcg_reduce_kernel");
+  if (coll) {  // multi-rank: the totals over all ranks, then the scalar step
+    plp_status s = comm_allreduce(ctx, scal + kTotA, EA);
+    if (s) return s;
+    tcg_step_kernel<K, 0><<<1, 256, 0, ctx->stream>>>(scal + kTotA, scal, status, max_iters, kr);
+    PLP_LAUNCH_CHECK("tcg_step_kernel");
+  }
   const int gb = fused_grid(ctx, (n + 7) / 8, EB, per_sm_b);
   auto upd = Heta ? tcg_update_kernel<KT, true> : tcg_update_kernel<KT, false>;
   upd<<<gb, kTcgThreads, 0, ctx->stream>>>(n, U, EH, dlt, S, scal, eta, Heta, r,
                                                              ctx->partials);
   PLP_LAUNCH_CHECK("tcg_update_kernel");
   tcg_reduce_kernel<K, 1><<<EB, 256, 0, ctx->stream>>>(gb, ctx->partials, scal + kTotB, counter + 1, scal, status,
-                                                       max_iters, kr);
+                                                       max_iters, kr, coll ? 1 : 0);
   PLP_LAUNCH_CHECK("tcg_reduce_kernel");
+  if (coll) {
+    plp_status s = comm_allreduce(ctx, scal + kTotB, EB);
+    if (s) return s;
+    tcg_step_kernel<K, 1><<<1, 256, 0, ctx->stream>>>(scal + kTotB, scal, status, max_iters, kr);
+    PLP_LAUNCH_CHECK("tcg_step_kernel");
+  }
   int64_t gc = (int64_t)ctx->num_sms * per_sm_c;
   const int64_t bc = (n + 7) / 8;
   if (bc < gc * kTcgWarps) gc = std::max<int64_t>(1, (bc + kTcgWarps - 1) / kTcgWarps);
@@ -659,8 +688,10 @@ extern "C" plp_status plp_tcg_run(plp_ctx* ctx, const plp_graph* g, int k, const
   if (!fused && !Heta) return set_error(PLP_ERR_ARG, "Heta may be NULL only with fused = 1");
   if (fused && !(al16(U) && al16(eta) && (!Heta || al16(Heta)) && al16(r) && al16(dlt) && al16(Hd)))
     return set_error(PLP_ERR_ARG, "fused tCG needs 16-byte aligned vectors");
-  if (fused && ctx->comm && g->dist && ctx->world > 1)
-    return set_error(PLP_ERR_ARG, "fused tCG is single-rank (its reductions are CTA tickets): use fused = 0");
+  // multi-rank graph: the fused passes run on the owned rows, their k x k / scalar totals are
+  // all-reduced before each scalar step (tcg_step_kernel), the direction's halo is exchanged by
+  // the collective Hessian-vector product
+  const bool coll = ctx->comm && g->dist;
   // on a multi-rank graph U's halo rows are current (the plp_fgrad at this iterate exchanged them):
   // each Hessian-vector product exchanges only the direction's halo
   if (ctx->comm && g->dist) mode |= PLP_U_HALO_CURRENT;
@@ -674,7 +705,7 @@ extern "C" plp_status plp_tcg_run(plp_ctx* ctx, const plp_graph* g, int k, const
     // pass A folded into the Hessian-vector-only halo pass where it applies (k = 4, 8, sparse
     // mode, rank-local; PLP_TCG_GRAM_EDGE=0 keeps the separate pass for comparison)
     static const bool gram_edge = env_int("PLP_TCG_GRAM_EDGE", 1) != 0;
-    const bool try_gram = gram_edge && (k == 8 || k == 4) && mode == PLP_HESS_SPARSE && !(ctx->comm && g->dist);
+    const bool try_gram = gram_edge && (k == 8 || k == 4) && mode == PLP_HESS_SPARSE && !coll;
     const double* S8 = k == 8 ? S : scal + kSx;
     for (int it = 0; it < iters; ++it) {
       int gram_grid = 0;
@@ -687,12 +718,12 @@ extern "C" plp_status plp_tcg_run(plp_ctx* ctx, const plp_graph* g, int k, const
         return st;
       }
       if (k == 16)
-        st = fused_iteration<2>(ctx, n, U, S, eta, Heta, r, dlt, Hd, scal, status, max_iters, 16, 0);
+        st = fused_iteration<2>(ctx, n, U, S, eta, Heta, r, dlt, Hd, scal, status, max_iters, 16, 0, coll);
       else if (k == 8)
-        st = fused_iteration<1>(ctx, n, U, S, eta, Heta, r, dlt, Hd, scal, status, max_iters, 8, gram_grid);
+        st = fused_iteration<1>(ctx, n, U, S, eta, Heta, r, dlt, Hd, scal, status, max_iters, 8, gram_grid, coll);
       else  // k = 1, 2, 4: the n x k arrays as n k / 8 rows of 8, S block-diagonal
         st = fused_iteration<1>(ctx, n * k / 8, U, scal + kSx, eta, Heta, r, dlt, Hd, scal, status, max_iters, k,
-                                gram_grid);
+                                gram_grid, coll);
       if (st) return st;
     }
     return PLP_OK;

@@ -110,15 +110,17 @@ class GrassmannTR:
 
     def __init__(self, ctx: plp.Context, g: plp.Graph, k: int, cfg: SolverConfig | None = None):
         self.ctx, self.g, self.k = ctx, g, k
-        # multi-rank (a DistGraph on a context with peers): global sizes for the defaults, the
-        # unfused device tCG (its reductions go through the collective plp_dot / plp_project),
-        # no CUDA-graph capture of the NCCL calls
+        # multi-rank (a DistGraph on a context with peers): global sizes for the defaults, no
+        # CUDA-graph capture of the NCCL calls; the fused device tCG at k = 8, 16 (its k x k and
+        # scalar totals all-reduced before each scalar step, tcg.cu), the unfused one otherwise (the
+        # folded k = 1, 2, 4 view needs n_own k % 8 == 0 on every rank)
         self.n_own, self.n_cols = g.n_rows, g.n_cols
         self.multi = isinstance(g, plp.DistGraph) and ctx.world > 1
         n_glob = g.n_global if isinstance(g, plp.DistGraph) else g.n_rows
         cfg = cfg or SolverConfig()
         if self.multi:
-            cfg = SolverConfig(**{**cfg.__dict__, "tcg_fused": False, "tcg_graph": False})
+            fused = cfg.tcg_fused if k in (8, 16) else False
+            cfg = SolverConfig(**{**cfg.__dict__, "tcg_fused": fused, "tcg_graph": False})
         self.cfg = cfg.resolved(n_glob, k)
         self.hmode = self.cfg.hessian_mode | (plp.U_HALO_CURRENT if isinstance(g, plp.DistGraph) else 0)
 

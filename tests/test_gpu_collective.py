@@ -215,3 +215,42 @@ def test_kmeans_dist_empty_cluster_reseed_one_rank(plp, ctxs):
     ref = plp.kmeans(plain, Xt, 8, u, restarts=3)
     got = plp.kmeans_dist(coll, Xt, 8, u, restarts=3)
     assert torch.equal(got[0], ref[0]) and torch.equal(got[1], ref[1]) and got[2] == ref[2]
+
+
+@pytest.mark.parametrize("cfg,n,k,p,delta", [("C2", 4003, 16, 1.5, 0.3), ("C2", 4000, 2, 1.2, 50.0),
+                                              ("C5", 30000, 8, 1.2, 1e3)])
+def test_fused_tcg_on_collective_context(plp, ctxs, cfg, n, k, p, delta):
+    """The fused device tCG on a collective context (k x k and scalar totals all-reduced, then the
+    scalar step in tcg_step_kernel): on the one-rank communicator bitwise the plain context's tCG
+    where neither folds pass A into the edge pass (k = 16; k = 2 on a graph without halo tiles),
+    and at k = 8 on a tile-ordered graph (plain: pass A folded) the same iteration count and status
+    with the step within 1e-10; the oracle's tCG agrees within 1e-9."""
+    from oracle import solver as osol
+    from paper_2605_26975_b200 import solver
+    plain, coll = ctxs
+    g = make_config(cfg, n=n)
+    if cfg == "C5":
+        g = permute_graph(g, plp.tile_order(g.row_ptr, g.col))
+    Uo, _ = oracle.retract(draw_U(g.n, k, 5), np.zeros((g.n, k)))
+    res = []
+    for ctx, mk in ((plain, lambda c: plp.Graph(c, g.row_ptr, g.col, g.w)),
+                    (coll, lambda c: plp.DistGraph(c, g.n, 0, g.n, g.row_ptr, g.col, g.w))):
+        G = mk(ctx)
+        with torch.cuda.stream(ctx.stream):
+            tr = solver.GrassmannTR(ctx, G, k, solver.SolverConfig(tcg_fused=True, tcg_graph=False))
+            st = solver._State(tr, torch.from_numpy(Uo).cuda(), p)
+            eta, Heta, it, status = tr.tcg_device(st, p, delta)
+        torch.cuda.synchronize()
+        res.append((eta.cpu().numpy(), it, status))
+    (e0, it0, s0), (e1, it1, s1) = res
+    assert (it0, s0) == (it1, s1)
+    if k == 8:
+        assert np.max(np.abs(e0 - e1)) <= 1e-10 * np.max(np.abs(e0))
+    else:
+        assert np.array_equal(e0, e1)
+    ocfg = osol.default_cfg(g.n, k)
+    sto = osol._state(g, Uo, p, osol.oracle_fns())
+    eta_o, _, it_o, status_o = osol.tcg(
+        lambda xi: osol._hess(g, sto, p, xi, ocfg["eps"], "sparse", osol.oracle_fns()), sto["grad"], Uo, delta, ocfg)
+    assert (it1, s1) == (it_o, status_o)
+    assert np.max(np.abs(e1 - eta_o)) <= 1e-9 * np.max(np.abs(eta_o))
