@@ -294,8 +294,8 @@ extern "C" plp_status plp_create_graph(plp_ctx* ctx, int64_t n_rows, int64_t n_c
   // the window keeps the U_j gathers L2-local.  Row results do not depend on it.
   // (+16 entries: the staged kernel's bulk copies round the schedule slice up to 16 bytes)
   std::vector<int32_t> sched((size_t)n_rows + 16, 0);
-  for (int64_t c0 = 0; c0 < n_rows; c0 += kSchedWindow) {
-    const int64_t c1 = std::min<int64_t>(n_rows, c0 + kSchedWindow);
+  for (int64_t c0 = 0; c0 < n_rows; c0 += kStagedChunk) {
+    const int64_t c1 = std::min<int64_t>(n_rows, c0 + kStagedChunk);
     g->max_chunk_nnz = std::max<int>(g->max_chunk_nnz, rp32[c1] - rp32[c0]);
   }
   for (int64_t w0 = 0; w0 < n_rows; w0 += kSchedWindow) {

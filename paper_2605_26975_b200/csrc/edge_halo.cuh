@@ -32,7 +32,7 @@ namespace plp {
 
 constexpr int kHaloT = PLP_HALO_TILE;  // rows per tile (plp.h)
 constexpr int kHaloProd = 1;  // producer warps (2, splitting the halo gathers, measured slower)
-constexpr int kHaloCWarps = 2 * (kHaloT / kSchedWindow);  // consumers: a warp pair per 32-row window
+constexpr int kHaloCWarps = kHaloT / 16;  // consumers: two slices of 8 rows each per tile
 constexpr int kHaloThreads = (kHaloCWarps + kHaloProd) * 32;  // + the producer warp(s)
 static_assert(kHaloT % kSchedWindow == 0 && kHaloThreads <= 1024, "tile map");
 
@@ -55,7 +55,13 @@ struct HaloLayout {
 // Staged halo rows per tile at most (the U / eta row blocks have a fixed size, so the eta rows sit
 // at a compile-time offset from the U rows and the consumers address both with one register);
 // tiles with more halo rows run in overflow mode.
-__host__ __device__ constexpr int halo_rows_cap(int k) { return k <= 4 ? 800 : k == 8 ? 400 : 96; }
+#ifndef PLP_HALO_CAP8
+#define PLP_HALO_CAP8 380
+#endif
+#ifndef PLP_HALO_CAP16
+#define PLP_HALO_CAP16 64
+#endif
+__host__ __device__ constexpr int halo_rows_cap(int k) { return k <= 4 ? 800 : k == 8 ? PLP_HALO_CAP8 : PLP_HALO_CAP16; }
 
 __host__ __device__ inline HaloLayout halo_layout(int k, int ext_cap, int nnz_cap, bool obj = false,
                                                   bool eta = true) {
@@ -80,7 +86,12 @@ __host__ __device__ inline HaloLayout halo_layout(int k, int ext_cap, int nnz_ca
 #define PLP_HALO_NBUF_NOETA 3  // passes without eta (objective, gradient) stage half the rows: 3 buffers
 #endif
 constexpr int kHaloNBuf = PLP_HALO_NBUF;
-constexpr unsigned kHaloHead = 256;  // mbarriers (full[NBUF], list[3], empty[NBUF]); tables follow
+#ifndef PLP_HALO_COEF_SMEM
+#define PLP_HALO_COEF_SMEM 0  // 1: the row epilogue's A, B coefficients in shared memory (16 registers)
+#endif
+// mbarriers (full[NBUF], list[3], empty[NBUF]) in the first 256 bytes, the epilogue coefficients
+// (PLP_HALO_COEF_SMEM: [4][k <= 16] doubles) after them; tables follow
+constexpr unsigned kHaloHead = PLP_HALO_COEF_SMEM ? 256 + 4 * 16 * 8 : 256;
 __host__ __device__ inline unsigned halo_tab_bytes(bool tables) {
   return tables ? (unsigned)((sizeof(PowTables) + 127) & ~(size_t)127) : 0u;
 }
@@ -187,16 +198,34 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
   const int64_t n_tiles = a.tile_list ? a.tile_count : (a.n_rows + kHaloT - 1) / kHaloT;
   auto tile_of = [&](int64_t li) -> int64_t { return a.tile_list ? (int64_t)a.tile_list[a.tile_begin + li] : li; };
   const double p = a.p, pp1 = p * (p - 1.0);
+  double* coef = reinterpret_cast<double*>(smem + 256);  // PLP_HALO_COEF_SMEM: [cG | cAB | cHA | cHB][K]
   double cG[CPL], cAB[CPL], cHA[CPL], cHB[CPL];
+  if constexpr (PLP_HALO_COEF_SMEM) {
+    if (tid < K) {
+      double g0 = 0.0, g1 = 0.0, g2 = 0.0, g3 = 0.0;
+      if (a.AB != nullptr) {
+        const double A = a.AB[tid], B = a.AB[K + tid];
+        g0 = p / B;
+        g1 = A / B;
+        g2 = pp1 / B;
+        g3 = pp1 * A / (B * B);
+      }
+      coef[tid] = g0;
+      coef[K + tid] = g1;
+      coef[2 * K + tid] = g2;
+      coef[3 * K + tid] = g3;
+    }
+  } else {
 #pragma unroll
-  for (int c = 0; c < CPL; ++c) {
-    cG[c] = cAB[c] = cHA[c] = cHB[c] = 0.0;
-    if (a.AB != nullptr) {
-      const double A = a.AB[c0 + c], B = a.AB[K + c0 + c];
-      cG[c] = p / B;
-      cAB[c] = A / B;
-      cHA[c] = pp1 / B;
-      cHB[c] = pp1 * A / (B * B);
+    for (int c = 0; c < CPL; ++c) {
+      cG[c] = cAB[c] = cHA[c] = cHB[c] = 0.0;
+      if (a.AB != nullptr) {
+        const double A = a.AB[c0 + c], B = a.AB[K + c0 + c];
+        cG[c] = p / B;
+        cAB[c] = A / B;
+        cHA[c] = pp1 / B;
+        cHB[c] = pp1 * A / (B * B);
+      }
     }
   }
   double accA[CPL], accB[CPL], accAl[CPL], accGa[CPL];
@@ -613,6 +642,12 @@ __global__ void __launch_bounds__(kHaloThreads, PLP_HALO_CTAS) edge_halo_kernel(
         capmode = __any_sync(__activemask(), fast_fails);
       }
       double g[CPL], hv[CPL];
+      if constexpr (PLP_HALO_COEF_SMEM) {
+        lds_vec<CPL>(coef + c0, cG);
+        lds_vec<CPL>(coef + K + c0, cAB);
+        lds_vec<CPL>(coef + 2 * K + c0, cHA);
+        lds_vec<CPL>(coef + 3 * K + c0, cHB);
+      }
 #pragma unroll
       for (int cc = 0; cc < CPL; ++cc) {
         if constexpr (!HVO) {

@@ -22,7 +22,7 @@
 
 namespace plp {
 
-constexpr int kChunkRows = kSchedWindow;  // rows per staged chunk (== the degree-sorting window)
+constexpr int kChunkRows = kStagedChunk;  // rows per staged chunk (whole degree-sorting windows)
 #ifndef PLP_STAGES
 #define PLP_STAGES 2
 #endif

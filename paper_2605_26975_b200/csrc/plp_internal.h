@@ -70,7 +70,7 @@ struct plp_graph {
   int32_t* col = nullptr;    // device int32 col[nnz]
   double* w = nullptr;       // device fp64 w[nnz]
   int32_t* sched = nullptr;  // device row schedule: rows sorted by degree within windows
-  int max_chunk_nnz = 0;  // max nnz over chunks of kSchedWindow rows (staged kernel ring slots)
+  int max_chunk_nnz = 0;  // max nnz over chunks of kStagedChunk rows (staged kernel ring slots)
   // Halo tiles (edge_halo.cuh): tiles of PLP_HALO_TILE rows; per stored edge the tile-local index
   // (j - r0 inside the tile, PLP_HALO_TILE + x for the x-th halo row); per tile a slot of
   // halo_ext_cap + 4 ints at halo_ext[t * (halo_ext_cap + 4)]: n_ext, rp[r0], rp[r1], 0, then the
@@ -88,7 +88,13 @@ struct plp_graph {
 };
 // rows per degree-sorting window: small enough that a CTA's rows per iteration stay contiguous
 // (neighbour rows of a tile-ordered graph then hit L1)
-constexpr int kSchedWindow = 32;
+#ifndef PLP_SCHED_WINDOW
+#define PLP_SCHED_WINDOW 16  // degree-sorting window (the halo kernel's tiles are whole windows)
+#endif
+constexpr int kSchedWindow = PLP_SCHED_WINDOW;
+// rows per chunk of the staged kernel (a union of whole degree-sorting windows)
+constexpr int kStagedChunk = 32;
+static_assert(kStagedChunk % kSchedWindow == 0, "staged chunks hold whole schedule windows");
 namespace plp {
 
 plp_status set_error(plp_status st, const char* fmt, ...);

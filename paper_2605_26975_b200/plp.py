@@ -543,8 +543,8 @@ def rcm_order(row_ptr, col):
 
 def tile_order(row_ptr, col, tile: int = TILE_ROWS):
     """RCM sweep + BFS-grown tiles of `tile` nodes (perm[new] = old), rows of a tile by decreasing
-    degree.  Default 120: cut into the halo kernel's 224-row tiles, a C5 kernel tile has ~181 halo
-    rows; BFS tiles aligned with the kernel's (tile = HALO_TILE) have only ~71, but measured slower
+    degree.  Default 120: two BFS tiles per 240-row halo-kernel tile.  BFS tiles as large as the
+    kernel's (round-1 measurement at 224 rows) have a third of the halo rows but measured slower
     (0.90 vs 0.86 ms per fused pass): their halo rows come from BFS tiles further along the sweep,
     not yet in L2, and the longer tile loads starve the consumer warps."""
     rp, rpp = _host(row_ptr, np.int64)

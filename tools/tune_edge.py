@@ -22,6 +22,14 @@ VARIANTS = {
     "sleep0": ["-DPLP_HALO_SLEEP_NS=0"],
     "sleep256": ["-DPLP_HALO_SLEEP_NS=256"],
     "cpl4": ["-DPLP_HALO_CPL8=4"],
+    # epilogue coefficients in shared memory (16 registers freed); with 256-row tiles, 16 consumer
+    # warps + 1 producer (17 warps per SM, <= 120 registers), halo stage cap 352 rows
+    "coef": ["-DPLP_HALO_COEF_SMEM=1"],
+    "t256coef": ["-DPLP_HALO_COEF_SMEM=1", "-DPLP_HALO_TILE_ROWS=256", "-DPLP_HALO_CAP8=352"],
+    # 240-row tiles: 15 consumer warps + 1 producer = 16 warps, 4 per SM sub-partition (each
+    # sub-partition's register file holds 4 warps x 128 registers); 16-row degree-sorting windows
+    "t224": ["FULL", "-DPLP_HALO_TILE_ROWS=224", "-DPLP_SCHED_WINDOW=32", "-DPLP_HALO_CAP8=400", "-DPLP_HALO_CAP16=96"],  # the earlier default
+    "w8": ["FULL", "-DPLP_SCHED_WINDOW=8"],  # degree sort within 8-row windows (row kernel: C4)
     # full builds (all k): staged-kernel occupancy for the random-graph configs (C4, k = 20)
     "full_minb3": ["FULL", "-DPLP_EDGE_MINB=3"],
 }
