@@ -60,7 +60,7 @@ enum { PLP_HESS_SPARSE = 0, PLP_HESS_FULL = 1 };          /* reading #5 */
  * single-rank graph. */
 enum { PLP_U_HALO_CURRENT = 16 };
 enum { PLP_VALIDATE = 1u, PLP_VALIDATE_SYMMETRIC = 2u };  /* plp_create_graph flags */
-enum { PLP_TILE_ROWS = 120 };  /* default BFS tile of plp_tile_order */
+enum { PLP_TILE_ROWS = 80 };  /* default BFS tile of plp_tile_order (three per halo-kernel tile) */
 #ifndef PLP_HALO_TILE_ROWS
 #define PLP_HALO_TILE_ROWS 240  /* 15 consumer warps x 2 slices of 8 rows: 16 warps per SM with the producer */
 #endif
@@ -117,7 +117,7 @@ plp_status plp_validate_csr(int64_t n_rows, int64_t n_cols, const int64_t* row_p
  * reversed.  Deterministic.  Used so that U_j gathers hit L2. */
 plp_status plp_rcm_order(int64_t n, const int64_t* row_ptr, const int32_t* col, int64_t* perm);
 /* Tile ordering for the halo-tile edge kernel: RCM sweep, then tiles of `tile`
- * nodes (PLP_TILE_ROWS = 120: two per 240-row halo-kernel tile) grown by BFS along
+ * nodes (PLP_TILE_ROWS = 80: three per 240-row halo-kernel tile) grown by BFS along
  * the sweep, the nodes of a tile sorted by decreasing degree.
  * perm[new] = old.  Relabel with plp_permute_csr; U and eta must then use the new order. */
 plp_status plp_tile_order(int64_t n, const int64_t* row_ptr, const int32_t* col, int tile,

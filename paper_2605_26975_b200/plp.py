@@ -51,7 +51,7 @@ SYMBOLS = [
 ]
 TCG_STATUS = {0: "running", 1: "boundary", 2: "negative_curvature", 3: "converged", 4: "maxiter",
               5: "interior"}
-TILE_ROWS = 120  # PLP_TILE_ROWS in include/plp.h (tiled kernel)
+TILE_ROWS = 80  # PLP_TILE_ROWS in include/plp.h: plp_tile_order's default BFS tile
 HALO_TILE = int(_lib.plp_halo_tile_rows())  # PLP_HALO_TILE: tile_order's default tile size
 TCG_SCAL_LEN = 4160  # PLP_TCG_SCAL_LEN in include/plp.h
 
@@ -543,10 +543,9 @@ def rcm_order(row_ptr, col):
 
 def tile_order(row_ptr, col, tile: int = TILE_ROWS):
     """RCM sweep + BFS-grown tiles of `tile` nodes (perm[new] = old), rows of a tile by decreasing
-    degree.  Default 120: two BFS tiles per 240-row halo-kernel tile.  BFS tiles as large as the
-    kernel's (round-1 measurement at 224 rows) have a third of the halo rows but measured slower
-    (0.90 vs 0.86 ms per fused pass): their halo rows come from BFS tiles further along the sweep,
-    not yet in L2, and the longer tile loads starve the consumer warps."""
+    degree.  Default 80: three BFS tiles per 240-row halo-kernel tile.  Measured on the fused pass
+    with 240-row kernel tiles (ms, C5 / D23): 60 -> 0.822 / 0.776, 80 -> 0.789 / 0.725,
+    120 -> 0.812 / 0.748, 240 -> 0.798 / 0.712 (`profiles/r02l_order_tile.txt`)."""
     rp, rpp = _host(row_ptr, np.int64)
     c, cp = _host(col, np.int32)
     perm = np.empty(rp.size - 1, dtype=np.int64)
