@@ -94,12 +94,6 @@ constexpr int kEdgeThreads = 256;
 #ifndef PLP_EDGE_CPL4
 #define PLP_EDGE_CPL4 0
 #endif
-#ifndef PLP_EDGE_CHUNK
-#define PLP_EDGE_CHUNK 1  // consecutive row groups per CTA per window (1: grid stride)
-#endif
-#ifndef PLP_EDGE_K20_CPL4
-#define PLP_EDGE_K20_CPL4 0  // k = 20: 5 lanes x 4 columns (256-bit gathers), 6 rows per warp
-#endif
 
 // One stored edge (weight wv) for the lane's CPL columns; branch-free.
 template <int CPL, class POW, bool HAS_ETA>
@@ -196,19 +190,14 @@ __global__ void __launch_bounds__(kEdgeThreads, PLP_EDGE_MINB) edge_kernel(EdgeA
   const double* __restrict__ eta = a.eta;
 
   if (active) {
-    // Row order: windows of gridDim.x * CHUNK * rows_per_iter rows; inside a window CTA b takes the
-    // b-th run of CHUNK * rows_per_iter consecutive rows (CHUNK = 1: plain grid stride).
-    constexpr int CHUNK = PLP_EDGE_CHUNK;
-    const int64_t win = (int64_t)gridDim.x * CHUNK * rows_per_iter;
-    const int64_t off = (int64_t)blockIdx.x * CHUNK * rows_per_iter + warp * RPW + grp;
-    auto row_at = [&](int64_t t) { return (t / CHUNK) * win + off + (t % CHUNK) * rows_per_iter; };
-    int64_t t = 0, idx = row_at(0);
+    const int64_t stride = (int64_t)gridDim.x * rows_per_iter;
+    int64_t idx = (int64_t)blockIdx.x * rows_per_iter + warp * RPW + grp;
     // software pipeline: the next row's schedule entry and row bounds are loaded one iteration
     // ahead, so each row starts with its edge metadata already in flight
     int row = idx < a.n_rows ? __ldg(sched + idx) : 0;
     int e0 = idx < a.n_rows ? __ldg(rp + row) : 0, e1 = idx < a.n_rows ? __ldg(rp + row + 1) : 0;
-    for (; idx < a.n_rows;) {
-      const int64_t idxn = row_at(++t);  // increasing in t: past n_rows, the CTA is done
+    for (; idx < a.n_rows; idx += stride) {
+      const int64_t idxn = idx + stride;
       const int rown = idxn < a.n_rows ? __ldg(sched + idxn) : row;
       double ui[CPL], ei[CPL];
       ld_vec<CPL>(U + (int64_t)row * k + c0, ui);
@@ -273,7 +262,6 @@ __global__ void __launch_bounds__(kEdgeThreads, PLP_EDGE_MINB) edge_kernel(EdgeA
       row = rown;
       e0 = e0n;
       e1 = e1n;
-      idx = idxn;
     }
   }
 
@@ -350,14 +338,6 @@ plp_status launch_edge_pow(plp_ctx* ctx, const EdgeArgs& a, const POW& pw, int* 
 #ifndef PLP_EDGE_K20_UNR
 #define PLP_EDGE_K20_UNR 4  // k = 20 (C4): edges per gather batch (8 and 12 measured slower: registers)
 #endif
-  if constexpr (PLP_EDGE_K20_CPL4 != 0) {
-    auto al32 = [](const void* ptr) { return ((uintptr_t)ptr & 31u) == 0; };
-    if (vec_ok && k == 20 && al32(a.U) && (a.eta == nullptr || al32(a.eta)) && (a.G == nullptr || al32(a.G)) &&
-        (a.Hv == nullptr || al32(a.Hv))) {
-      return he ? launch_edge_shape<4, 5, POW, true, PLP_EDGE_K20_CPL4>(ctx, a, pw, grid)
-                : launch_edge_shape<4, 5, POW, false, PLP_EDGE_K20_CPL4>(ctx, a, pw, grid);
-    }
-  }
   if (vec_ok && k == 20) {
     return he ? launch_edge_shape<2, 10, POW, true, PLP_EDGE_K20_UNR>(ctx, a, pw, grid)
               : launch_edge_shape<2, 10, POW, false, PLP_EDGE_K20_UNR>(ctx, a, pw, grid);
