@@ -268,6 +268,7 @@ static plp_status build_halo_tiles(plp_graph* g, const int64_t* rp, const int32_
 extern "C" plp_status plp_create_graph(plp_ctx* ctx, int64_t n_rows, int64_t n_cols,
                                        const int64_t* row_ptr, const int32_t* col, const double* w,
                                        uint32_t flags, plp_graph** out) {
+  PLP_NVTX("plp_create_graph");
   if (!ctx || !out || !row_ptr || (!col && row_ptr[n_rows] > 0) || (!w && row_ptr[n_rows] > 0))
     return set_error(PLP_ERR_ARG, "null argument");
   *out = nullptr;

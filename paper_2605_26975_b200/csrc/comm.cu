@@ -204,11 +204,13 @@ extern "C" plp_status plp_ctx_comm_info(const plp_ctx* ctx, int* rank, int* worl
 }
 
 extern "C" plp_status plp_allreduce_sum(plp_ctx* ctx, double* buf, int64_t count) {
+  PLP_NVTX("plp_allreduce_sum");
   if (!ctx || (!buf && count > 0) || count < 0) return set_error(PLP_ERR_ARG, "bad argument");
   return comm_allreduce(ctx, buf, (size_t)count);
 }
 
 extern "C" plp_status plp_halo_exchange(plp_ctx* ctx, const plp_graph* g, int row_bytes, void* X) {
+  PLP_NVTX("plp_halo_exchange");
   if (!ctx || !g || !X || row_bytes <= 0) return set_error(PLP_ERR_ARG, "bad argument");
   if (g->ctx != ctx) return set_error(PLP_ERR_ARG, "graph belongs to another ctx");
   return halo_exchange_bytes(ctx, g, X, row_bytes);
@@ -236,6 +238,7 @@ extern "C" plp_status plp_dist_recv_plan(int world, const int64_t* bounds, int64
 extern "C" plp_status plp_create_graph_dist(plp_ctx* ctx, int64_t n_global, int64_t row_begin,
                                             int64_t row_end, const int64_t* row_ptr, const int32_t* col,
                                             const double* w, uint32_t flags, plp_graph** out) {
+  PLP_NVTX("plp_create_graph_dist");
   if (!ctx || !row_ptr || !out || row_begin < 0 || row_end < row_begin || row_end > n_global)
     return set_error(PLP_ERR_ARG, "bad argument");
   *out = nullptr;

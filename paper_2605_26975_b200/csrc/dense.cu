@@ -304,6 +304,7 @@ using namespace plp;
 
 extern "C" plp_status plp_gram(plp_ctx* ctx, int64_t n, int k, const double* X, const double* Y,
                                double* out) {
+  PLP_NVTX("plp_gram");
   PLP_REQ(ctx && X && Y && out && n >= 0, "bad argument");
   plp_status st = check_k(k);
   if (st) return st;
@@ -322,6 +323,7 @@ extern "C" plp_status plp_apply_sub(plp_ctx* ctx, int64_t n, int k, const double
 
 extern "C" plp_status plp_project(plp_ctx* ctx, int64_t n, int k, const double* U, const double* G,
                                   double* out) {
+  PLP_NVTX("plp_project");
   PLP_REQ(ctx && U && G && out && n >= 0, "bad argument");
   plp_status st = check_k(k);
   if (st) return st;
@@ -354,6 +356,7 @@ extern "C" plp_status plp_apply_rinv(plp_ctx* ctx, int64_t n, int k, const doubl
 
 extern "C" plp_status plp_retract(plp_ctx* ctx, int64_t n, int k, const double* U, const double* xi,
                                   double* Q, double* R_out) {
+  PLP_NVTX("plp_retract");
   PLP_REQ(ctx && U && xi && Q && n >= 0, "bad argument");
   plp_status st = check_k(k);
   if (st) return st;
@@ -386,6 +389,7 @@ extern "C" plp_status plp_retract(plp_ctx* ctx, int64_t n, int k, const double* 
 
 extern "C" plp_status plp_dot(plp_ctx* ctx, int64_t n, int k, const double* x, const double* y,
                               double* out) {
+  PLP_NVTX("plp_dot");
   PLP_REQ(ctx && x && y && out && n >= 0 && k >= 1, "bad argument");
   const int64_t total = n * k;
   const int grid = grid_for(ctx, total, 256 * 8);
@@ -398,6 +402,7 @@ extern "C" plp_status plp_dot(plp_ctx* ctx, int64_t n, int k, const double* x, c
 
 extern "C" plp_status plp_axpby(plp_ctx* ctx, int64_t n, int k, double a, const double* x, double b,
                                 double* y) {
+  PLP_NVTX("plp_axpby");
   PLP_REQ(ctx && x && y && n >= 0 && k >= 1, "bad argument");
   const int64_t total = n * k;
   const int grid = grid_for(ctx, total, 256 * 4);

@@ -315,6 +315,7 @@ static plp_status overlapped_pass(plp_ctx* ctx, const plp_graph* g, const EdgeAr
 extern "C" plp_status plp_edge_pass(plp_ctx* ctx, const plp_graph* g, int k, const double* U,
                                     const double* eta, double p, double eps, const double* AB_in,
                                     double* AB_out, double* dots_out, double* G, double* Hv) {
+  PLP_NVTX("plp_edge_pass");
   plp_status st = check_graph_call(ctx, g, k, U, p, eps);
   if (st) return st;
   if (!AB_in && (G || Hv || dots_out))
@@ -369,6 +370,7 @@ static double* scratch_ab2(plp_ctx* ctx) { return ctx->scratch + 4 * PLP_MAX_K; 
 
 extern "C" plp_status plp_fgrad(plp_ctx* ctx, const plp_graph* g, int k, const double* U, double p,
                                 double* F, double* AB_out, double* G) {
+  PLP_NVTX("plp_fgrad");
   plp_status st = check_graph_call(ctx, g, k, U, p, 1.0);
   if (st) return st;
   const bool coll = collective(ctx, g);
@@ -400,6 +402,7 @@ extern "C" plp_status plp_fgrad(plp_ctx* ctx, const plp_graph* g, int k, const d
 extern "C" plp_status plp_hessvec(plp_ctx* ctx, const plp_graph* g, int k, const double* U,
                                   const double* eta, double p, const double* AB_in, int mode,
                                   double eps, const double* G_in, double* Hv) {
+  PLP_NVTX("plp_hessvec");
   plp_status st = check_graph_call(ctx, g, k, U, p, eps);
   if (st) return st;
   const bool u_current = (mode & PLP_U_HALO_CURRENT) != 0;
@@ -464,6 +467,7 @@ extern "C" plp_status plp_fgrad_hessvec(plp_ctx* ctx, const plp_graph* g, int k,
                                         const double* eta, double p, const double* AB_in, int mode,
                                         double eps, double* F, double* AB_out, double* G,
                                         double* Hv) {
+  PLP_NVTX("plp_fgrad_hessvec");
   plp_status st = check_graph_call(ctx, g, k, U, p, eps);
   if (st) return st;
   const bool u_current = (mode & PLP_U_HALO_CURRENT) != 0;
@@ -530,6 +534,7 @@ __global__ void rcut_ratio_kernel(int K, const double* cut, const int64_t* sizes
 
 extern "C" plp_status plp_rcut(plp_ctx* ctx, const plp_graph* g, int clusters,
                                const int32_t* labels, double* cut, int64_t* sizes, double* rcut) {
+  PLP_NVTX("plp_rcut");
   if (!ctx || !g || !labels) return set_error(PLP_ERR_ARG, "null argument");
   if (clusters < 1 || clusters > PLP_MAX_K) return set_error(PLP_ERR_DOMAIN, "clusters must be in [1, 32]");
   const bool coll = collective(ctx, g);

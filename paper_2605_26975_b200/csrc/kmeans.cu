@@ -704,6 +704,7 @@ extern "C" plp_status plp_kmeans(plp_ctx* ctx, int64_t n, int dim, int K, const 
                                  const double* uniforms, int restarts, int max_iters,
                                  double rel_tol, int32_t* labels, double* centroids, double* sse,
                                  int* iters) {
+  PLP_NVTX("plp_kmeans");
   if (n < 1) return set_error(PLP_ERR_SHAPE, "need n >= clusters");
   return kmeans_impl(ctx, n, dim, K, X, uniforms, restarts, max_iters, rel_tol, labels, centroids, sse, iters,
                      false);
@@ -712,6 +713,7 @@ extern "C" plp_status plp_kmeans(plp_ctx* ctx, int64_t n, int dim, int K, const 
 extern "C" plp_status plp_kmeans_dist(plp_ctx* ctx, int64_t n_local, int dim, int K, const double* X,
                                       const double* uniforms, int restarts, int max_iters, double rel_tol,
                                       int32_t* labels, double* centroids, double* sse, int* iters) {
+  PLP_NVTX("plp_kmeans_dist");
   if (!ctx) return set_error(PLP_ERR_ARG, "null argument");
   return kmeans_impl(ctx, n_local, dim, K, X, uniforms, restarts, max_iters, rel_tol, labels, centroids, sse,
                      iters, ctx->comm != nullptr);

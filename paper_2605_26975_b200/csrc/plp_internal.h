@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "plp.h"
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: a no-op unless a profiler injects itself
 
 #define PLP_MAX_K 32
 // Cap used by passes that need no curvature (objective, gradient, full-mode epilogue): s is then
@@ -96,6 +97,16 @@ constexpr int kSchedWindow = PLP_SCHED_WINDOW;
 constexpr int kStagedChunk = 32;
 static_assert(kStagedChunk % kSchedWindow == 0, "staged chunks hold whole schedule windows");
 namespace plp {
+
+// NVTX range over one C-ABI call (named after it), for nsys / ncu --nvtx timelines of the solver
+// (SURVEY.md §5 tracing).  Host-side push / pop only: nothing is enqueued on the stream.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define PLP_NVTX(name) ::plp::NvtxRange plp_nvtx_range_(name)
 
 plp_status set_error(plp_status st, const char* fmt, ...);
 plp_status cuda_check(cudaError_t e, const char* what);
