@@ -107,9 +107,17 @@ __global__ void tcg_scalar_b_kernel(double* sc, int* st, int max_iters) { tcg_sc
 //   eta += c d, Heta += c Hd, r += c' Hd, MR = U^T r, ||r||^2                (pass B: Hd never stored)
 //   r <- r - U MR (the residual's re-projection), ||P r||^2 = ||r||^2 - ||MR||_F^2,
 //   d <- -r + beta d                                                          (pass C)
+// Pass C writes only d: the stored r keeps the un-projected residual and the next pass B applies
+// -U MR (MR still in scal[kMR]) to it before adding cr Hd -- the same operations in the same
+// order, so the iterates are bitwise those of writing r in pass C, and each iteration moves 8 n k
+// bytes less.  The last iteration of a tcg_run batch writes r (projected) and zeroes scal[kMR], so
+// r is the projected residual between calls.
 // All Grams and the k x k applies run on the fp64 tensor cores (dmma884, as dense_mma.cuh).
 // ---------------------------------------------------------------------------------------------
 constexpr int kTcgThreads = 256, kTcgWarps = kTcgThreads / 32;
+#ifndef PLP_TCG_R_EVERY_ITER
+#define PLP_TCG_R_EVERY_ITER 0  // 1: every pass C writes r (the round-2 traffic, for A/B timing)
+#endif
 
 // Grid reductions: each pass CTA writes its E block totals entry-major (part[e * P + cta]); then
 // tcg_reduce_kernel runs one CTA per entry (coalesced fixed-order sum: thread-strided, warp xor
@@ -298,6 +306,15 @@ __global__ void __launch_bounds__(kTcgThreads, KT == 1 ? PLP_TCG_MINB_B : 1) tcg
         bm[ta][ks][tb] = -sc[kM1 + e];
         bs[ta][ks][tb] = -S[e];
       }
+  // B fragments of -MR of the previous iteration (zero after tcg_init and after a batch's last
+  // pass C, which left r projected)
+  double bp[KT][2][KT];
+#pragma unroll
+  for (int ta = 0; ta < KT; ++ta)
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+      for (int tb = 0; tb < KT; ++tb) bp[ta][ks][tb] = -sc[kMR + (8 * ta + 4 * ks + q) * K + 8 * tb + g];
   const double ce = sc[kCEta], cr = sc[kCR];
   double mr[KT][KT][2], zz = 0.0;
 #pragma unroll
@@ -342,6 +359,7 @@ __global__ void __launch_bounds__(kTcgThreads, KT == 1 ? PLP_TCG_MINB_B : 1) tcg
         for (int ks = 0; ks < 2; ++ks) {
           dmma884(hd[tb][0], hd[tb][1], au[ta][ks], bm[ta][ks][tb]);
           dmma884(hd[tb][0], hd[tb][1], ad[ta][ks], bs[ta][ks][tb]);
+          dmma884(r2[tb].x, r2[tb].y, au[ta][ks], bp[ta][ks][tb]);  // r - U MR (deferred pass C)
         }
 #pragma unroll
     for (int tb = 0; tb < KT; ++tb) {
@@ -397,11 +415,11 @@ __global__ void __launch_bounds__(kTcgThreads, KT == 1 ? PLP_TCG_MINB_B : 1) tcg
   for (int e = threadIdx.x; e < E; e += kTcgThreads) part[(int64_t)e * gridDim.x + blockIdx.x] = red[e];
 }
 
-// pass C over 8-row blocks: r <- r - U MR, d <- ca r + cb d
+// pass C over 8-row blocks: d <- ca (r - U MR) + cb d; r <- r - U MR stored only when WRITE_R
 #ifndef PLP_TCG_MINB_C
 #define PLP_TCG_MINB_C 5
 #endif
-template <int KT>
+template <int KT, bool WRITE_R>
 __global__ void __launch_bounds__(kTcgThreads, KT == 1 ? PLP_TCG_MINB_C : 1) tcg_finish_kernel(int64_t n, const double* __restrict__ U,
                                                                  const double* __restrict__ sc,
                                                                  double* __restrict__ r,
@@ -449,7 +467,7 @@ __global__ void __launch_bounds__(kTcgThreads, KT == 1 ? PLP_TCG_MINB_C : 1) tcg
 #pragma unroll
       for (int tb = 0; tb < KT; ++tb) {
         const int64_t o = row * K + 8 * tb + 2 * q;
-        *reinterpret_cast<double2*>(r + o) = make_double2(rv[tb][0], rv[tb][1]);
+        if constexpr (WRITE_R) *reinterpret_cast<double2*>(r + o) = make_double2(rv[tb][0], rv[tb][1]);
         *reinterpret_cast<double2*>(D + o) =
             make_double2(fma(ca, rv[tb][0], cb * d2[tb].x), fma(ca, rv[tb][1], cb * d2[tb].y));
       }
@@ -583,13 +601,13 @@ static int fused_grid(plp_ctx* ctx, int64_t row_blocks, int E, int per_sm) {  //
 template <int KT>
 static plp_status fused_iteration(plp_ctx* ctx, int64_t n, const double* U, const double* S, double* eta,
                                   double* Heta, double* r, double* dlt, const double* EH, double* scal,
-                                  int* status, int max_iters, int kr, int gram_grid, bool coll = false) {
+                                  int* status, int max_iters, int kr, int gram_grid, bool coll, bool last) {
   constexpr int K = 8 * KT, KK = K * K;
   static const int unr_a = env_int("PLP_TCG_UNR_A", 4);
   static const int per_sm_a = env_int("PLP_TCG_GRID_A", unr_a == 4 ? resident_ctas(tcg_gram_a_kernel<KT, 4>, kTcgThreads)
                                                                     : resident_ctas(tcg_gram_a_kernel<KT, 2>, kTcgThreads));
   static const int per_sm_b = env_int("PLP_TCG_GRID_B", resident_ctas(tcg_update_kernel<KT, true>, kTcgThreads));
-  static const int per_sm_c = resident_ctas(tcg_finish_kernel<KT>, kTcgThreads);
+  static const int per_sm_c = resident_ctas(tcg_finish_kernel<KT, true>, kTcgThreads);
   unsigned* counter = reinterpret_cast<unsigned*>(ctx->flag + 4);
   constexpr int EA = 2 * KK + 2, EB = KK + 1;
   int ga = gram_grid;  // > 0: the edge pass wrote pass A's partials (edge_halo.cuh, GRAM)
@@ -627,8 +645,14 @@ static plp_status fused_iteration(plp_ctx* ctx, int64_t n, const double* U, cons
   int64_t gc = (int64_t)ctx->num_sms * per_sm_c;
   const int64_t bc = (n + 7) / 8;
   if (bc < gc * kTcgWarps) gc = std::max<int64_t>(1, (bc + kTcgWarps - 1) / kTcgWarps);
-  tcg_finish_kernel<KT><<<(int)gc, kTcgThreads, 0, ctx->stream>>>(n, U, scal, r, dlt);
-  PLP_LAUNCH_CHECK("tcg_finish_kernel");
+  if (last) {  // r projected for the caller; the next pass B must not apply MR again
+    tcg_finish_kernel<KT, true><<<(int)gc, kTcgThreads, 0, ctx->stream>>>(n, U, scal, r, dlt);
+    PLP_LAUNCH_CHECK("tcg_finish_kernel");
+    PLP_CUDA(cudaMemsetAsync(scal + kMR, 0, sizeof(double) * KK, ctx->stream));
+  } else {
+    tcg_finish_kernel<KT, false><<<(int)gc, kTcgThreads, 0, ctx->stream>>>(n, U, scal, r, dlt);
+    PLP_LAUNCH_CHECK("tcg_finish_kernel");
+  }
   return PLP_OK;
 }
 
@@ -654,6 +678,7 @@ using namespace plp;
 extern "C" plp_status plp_tcg_init(plp_ctx* ctx, int64_t n, int k, const double* grad, double delta,
                                    double kappa, double theta, double* eta, double* Heta, double* r,
                                    double* dlt, double* scal, int* status) {
+  PLP_NVTX("plp_tcg_init");
   if (!ctx || !grad || !eta || !r || !dlt || !scal || !status || n < 0)
     return set_error(PLP_ERR_ARG, "null argument");
   plp_status st = check_k(k);
@@ -666,6 +691,7 @@ extern "C" plp_status plp_tcg_init(plp_ctx* ctx, int64_t n, int k, const double*
   PLP_CUDA(cudaMemsetAsync(dlt, 0, bytes, ctx->stream));
   if ((st = plp_axpby(ctx, n, k, -1.0, r, 0.0, dlt))) return st;  // delta = -r
   if ((st = plp_dot(ctx, n, k, r, r, scal + kZr))) return st;
+  PLP_CUDA(cudaMemsetAsync(scal + kMR, 0, sizeof(double) * PLP_MAX_K * PLP_MAX_K, ctx->stream));  // no MR to defer
   tcg_init_kernel<<<1, 1, 0, ctx->stream>>>(scal, status, delta, kappa, theta);
   PLP_LAUNCH_CHECK("tcg_init_kernel");
   return PLP_OK;
@@ -676,6 +702,7 @@ extern "C" plp_status plp_tcg_run(plp_ctx* ctx, const plp_graph* g, int k, const
                                   double eps, int mode, double* eta, double* Heta, double* r,
                                   double* dlt, double* Hd, double* scal, int* status, int max_iters,
                                   int iters, int fused) {
+  PLP_NVTX("plp_tcg_run");
   if (!ctx || !g || !U || !AB || !S || !eta || !r || !dlt || !Hd || !scal || !status)
     return set_error(PLP_ERR_ARG, "null argument");
   if (iters < 0 || max_iters < 1) return set_error(PLP_ERR_ARG, "iters >= 0, max_iters >= 1");
@@ -708,6 +735,7 @@ extern "C" plp_status plp_tcg_run(plp_ctx* ctx, const plp_graph* g, int k, const
     const bool try_gram = gram_edge && (k == 8 || k == 4) && mode == PLP_HESS_SPARSE && !coll;
     const double* S8 = k == 8 ? S : scal + kSx;
     for (int it = 0; it < iters; ++it) {
+      const bool last = PLP_TCG_R_EVERY_ITER || it == iters - 1;
       int gram_grid = 0;
       if (try_gram) {
         bool used = false;
@@ -718,12 +746,12 @@ extern "C" plp_status plp_tcg_run(plp_ctx* ctx, const plp_graph* g, int k, const
         return st;
       }
       if (k == 16)
-        st = fused_iteration<2>(ctx, n, U, S, eta, Heta, r, dlt, Hd, scal, status, max_iters, 16, 0, coll);
+        st = fused_iteration<2>(ctx, n, U, S, eta, Heta, r, dlt, Hd, scal, status, max_iters, 16, 0, coll, last);
       else if (k == 8)
-        st = fused_iteration<1>(ctx, n, U, S, eta, Heta, r, dlt, Hd, scal, status, max_iters, 8, gram_grid, coll);
+        st = fused_iteration<1>(ctx, n, U, S, eta, Heta, r, dlt, Hd, scal, status, max_iters, 8, gram_grid, coll, last);
       else  // k = 1, 2, 4: the n x k arrays as n k / 8 rows of 8, S block-diagonal
         st = fused_iteration<1>(ctx, n * k / 8, U, scal + kSx, eta, Heta, r, dlt, Hd, scal, status, max_iters, k,
-                                gram_grid, coll);
+                                gram_grid, coll, last);
       if (st) return st;
     }
     return PLP_OK;
@@ -765,6 +793,7 @@ extern "C" plp_status plp_tcg_graph_create(plp_ctx* ctx, const plp_graph* g, int
                                            double eps, int mode, double* eta, double* Heta, double* r,
                                            double* dlt, double* Hd, double* scal, int* status, int max_iters,
                                            int iters, int fused, plp_tcg_graph** out) {
+  PLP_NVTX("plp_tcg_graph_create");
   if (!ctx || !out) return set_error(PLP_ERR_ARG, "null argument");
   *out = nullptr;
   if (ctx->stream == nullptr || ctx->stream == cudaStreamLegacy || ctx->stream == cudaStreamPerThread)
@@ -799,6 +828,7 @@ extern "C" plp_status plp_tcg_graph_create(plp_ctx* ctx, const plp_graph* g, int
 }
 
 extern "C" plp_status plp_tcg_graph_launch(plp_tcg_graph* gr) {
+  PLP_NVTX("plp_tcg_graph_launch");
   if (!gr) return set_error(PLP_ERR_ARG, "graph is null");
   PLP_CUDA(cudaGraphLaunch(gr->exec, gr->ctx->stream));
   return PLP_OK;

@@ -32,13 +32,8 @@ VARIANTS = {
     "w8": ["FULL", "-DPLP_SCHED_WINDOW=8"],  # degree sort within 8-row windows (row kernel: C4)
     # full builds (all k): staged-kernel occupancy for the random-graph configs (C4, k = 20)
     "full_minb3": ["FULL", "-DPLP_EDGE_MINB=3"],
-    # C4 (k = 20) row kernel: runs of CHUNK row groups per CTA inside a window (L1 reuse of the
-    # gathered rows between consecutive rows of a CTA), and 5 lanes x 4 columns (256-bit gathers)
-    "c4_chunk4": ["FULL", "-DPLP_EDGE_CHUNK=4"],
-    "c4_chunk16": ["FULL", "-DPLP_EDGE_CHUNK=16"],
-    "c4_cpl4u2": ["FULL", "-DPLP_EDGE_K20_CPL4=2"],
-    "c4_cpl4u3": ["FULL", "-DPLP_EDGE_K20_CPL4=3"],
-    "c4_cpl4u2_chunk4": ["FULL", "-DPLP_EDGE_K20_CPL4=2", "-DPLP_EDGE_CHUNK=4"],
+    # fused tCG: every pass C writes the projected r (no deferred re-projection; A/B timing)
+    "tcg_r_every": ["FULL", "-DPLP_TCG_R_EVERY_ITER=1"],
 }
 
 
