@@ -115,9 +115,6 @@ __global__ void tcg_scalar_b_kernel(double* sc, int* st, int max_iters) { tcg_sc
 // All Grams and the k x k applies run on the fp64 tensor cores (dmma884, as dense_mma.cuh).
 // ---------------------------------------------------------------------------------------------
 constexpr int kTcgThreads = 256, kTcgWarps = kTcgThreads / 32;
-#ifndef PLP_TCG_R_EVERY_ITER
-#define PLP_TCG_R_EVERY_ITER 0  // 1: every pass C writes r (the round-2 traffic, for A/B timing)
-#endif
 
 // Grid reductions: each pass CTA writes its E block totals entry-major (part[e * P + cta]); then
 // tcg_reduce_kernel runs one CTA per entry (coalesced fixed-order sum: thread-strided, warp xor
@@ -735,7 +732,7 @@ extern "C" plp_status plp_tcg_run(plp_ctx* ctx, const plp_graph* g, int k, const
     const bool try_gram = gram_edge && (k == 8 || k == 4) && mode == PLP_HESS_SPARSE && !coll;
     const double* S8 = k == 8 ? S : scal + kSx;
     for (int it = 0; it < iters; ++it) {
-      const bool last = PLP_TCG_R_EVERY_ITER || it == iters - 1;
+      const bool last = it == iters - 1;
       int gram_grid = 0;
       if (try_gram) {
         bool used = false;

@@ -394,3 +394,38 @@ def test_fused_tcg_pass_a_fold_matches_separate_pass(cfg, n, k, p, tmp_path):
     assert res[1][2] == res[0][2]
     e1, e0 = res[1][0], res[0][0]
     assert np.max(np.abs(e1 - e0)) <= 1e-10 * np.max(np.abs(e0))
+
+
+@pytest.mark.parametrize("k", [8, 4, 16])
+def test_fused_tcg_deferred_reprojection_is_bitwise(mods, k):
+    """Fused tCG with the residual's re-projection deferred into the next pass B (tcg.cu: pass C
+    writes only d; the last pass C of a plp_tcg_run batch writes the projected r and zeroes MR):
+    one batch of N iterations against N batches of one iteration (each of which writes r, so no
+    re-projection is deferred) -- step, residual, direction, iteration count and status bitwise
+    equal (the same operations in the same order), the projected residual of the batch
+    horizontal (U^T r ~ 0)."""
+    plp, solver, ctx = mods
+    g = make_config("C2", n=3000)
+    G = plp.Graph(ctx, g.row_ptr, g.col, g.w)
+    # near a p = 2 minimiser the Hessian is positive definite: tCG runs many iterations
+    Z = torch.from_numpy(draw_U(g.n, k, 6)).cuda()
+    U, _ = solver.continuation_solve(ctx, G, Z, [2.0], solver.SolverConfig(grad_tol=1e-2, tcg_graph=False))
+    cfg = solver.SolverConfig(tcg_fused=True, tcg_graph=False)
+    tr = solver.GrassmannTR(ctx, G, k, cfg)
+    st = solver._State(tr, U, 1.8)
+    tr.tcg_device(st, 1.8, 10.0)
+    n_it = 7
+    out = []
+    for batches in ((n_it,), (1,) * n_it):
+        eta, Heta, r, dlt, Hd, scal, status = (t.clone() for t in tr._tcg_buf)
+        plp.tcg_init(ctx, st.grad, 10.0, 0.0, 1.0, eta, None, r, dlt, scal, status)
+        for b in batches:
+            plp.tcg_run(ctx, G, st.U, st.AB, None, st.S, 1.8, cfg.eps, plp.HESS_SPARSE, eta, None, r, dlt, Hd,
+                        scal, status, 1 << 30, b, fused=True)
+        torch.cuda.synchronize()
+        out.append((eta, r, dlt, status.cpu().tolist()))
+    (e1, r1, d1, s1), (e2, r2, d2, s2) = out
+    assert s1 == s2 and s1[1] >= 3, (s1, s2)
+    assert torch.equal(e1, e2) and torch.equal(r1, r2) and torch.equal(d1, d2)
+    utr = (st.U[: g.n].T @ r1).abs().max().item()
+    assert utr <= 1e-10 * max(1.0, r1.abs().max().item()), utr

@@ -32,8 +32,6 @@ VARIANTS = {
     "w8": ["FULL", "-DPLP_SCHED_WINDOW=8"],  # degree sort within 8-row windows (row kernel: C4)
     # full builds (all k): staged-kernel occupancy for the random-graph configs (C4, k = 20)
     "full_minb3": ["FULL", "-DPLP_EDGE_MINB=3"],
-    # fused tCG: every pass C writes the projected r (no deferred re-projection; A/B timing)
-    "tcg_r_every": ["FULL", "-DPLP_TCG_R_EVERY_ITER=1"],
 }
 
 
