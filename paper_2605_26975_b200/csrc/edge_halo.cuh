@@ -1,13 +1,13 @@
 // Halo-tile edge kernel: the fused F / EucGrad / EucHessianEta pass (
 // DESIGN.md §5) with every neighbour row served from shared memory.
 //
-// The rows are cut into tiles of kHaloT = PLP_HALO_TILE (224) consecutive rows.  plp_create_graph
+// The rows are cut into tiles of kHaloT = PLP_HALO_TILE (240) consecutive rows.  plp_create_graph
 // lists, per tile, the distinct columns outside it (the tile's halo, ordered by decreasing number
 // of references) and re-encodes every stored edge as a tile-local index: j - r0 for an internal
-// neighbour, kHaloT + x for the x-th halo row.  One persistent CTA of 15 warps per SM walks the
+// neighbour, kHaloT + x for the x-th halo row.  One persistent CTA of 16 warps per SM walks the
 // tiles (interleaved across CTAs, so neighbouring tiles are in flight together and the halo rows
 // hit L2), double-buffered:
-//   * a producer warp (warp specialisation: 14 consumer warps + 1) stages each tile: lane 0 issues
+//   * a producer warp (warp specialisation: 15 consumer warps + 1) stages each tile: lane 0 issues
 //     TMA bulk copies (cp.async.bulk + mbarrier) of the tile's own U / eta rows, row_ptr and
 //     schedule slices, (enc, w) ranges, and two tiles ahead the tile's halo list; the 32 lanes
 //     gather the halo rows U_j, eta_j with cp.async (16-byte pieces, 8 rows per instruction at
