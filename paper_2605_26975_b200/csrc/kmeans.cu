@@ -35,11 +35,25 @@ __global__ void __launch_bounds__(kChunk) km_d2_kernel(int64_t n, int dim, const
   __syncthreads();
   const int64_t nch = (n + kChunk - 1) / kChunk;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool vec8 = dim == 8 && (reinterpret_cast<uintptr_t>(X) & 15u) == 0;
   for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
     const int64_t i = ch * kChunk + threadIdx.x;
     double v = 0.0;
     if (i < n) {
-      const double d = km_dist2(X + i * dim, 1, cs, dim);
+      double d;
+      if (vec8) {  // the row as four 16-byte loads (half the L1 wavefronts of eight 8-byte ones); same order
+        const double2* xr = reinterpret_cast<const double2*>(X + i * 8);
+        d = 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double2 t = __ldg(xr + q);
+          const double t0 = __dsub_rn(t.x, cs[2 * q]), t1 = __dsub_rn(t.y, cs[2 * q + 1]);
+          d = __dadd_rn(d, __dmul_rn(t0, t0));
+          d = __dadd_rn(d, __dmul_rn(t1, t1));
+        }
+      } else {
+        d = km_dist2(X + i * dim, 1, cs, dim);
+      }
       v = first ? d : (d < D2[i] ? d : D2[i]);
       D2[i] = v;
     }
@@ -239,8 +253,12 @@ __global__ void __launch_bounds__(kKmThreads) km_assign_kernel(int64_t n, int di
 // m8n8k4: A[c][q] = [label of point q == c], B[q][d] = X[q][d] or 1), 4 points per instruction.
 // Each warp owns a contiguous range of 32-point groups; per-CTA partials in a fixed order, layout
 // [sums K*dim | counts K | sse] like km_assign_kernel.
+#ifndef PLP_KM_PREFETCH
+#define PLP_KM_PREFETCH 1  // next group's point loads issued before the current group's DMMA phase
+#endif
 #ifndef PLP_KM_MINB
-#define PLP_KM_MINB 1  // 3 (80 registers, small spill) measured slower: Lloyd 0.223 vs 0.211 ms
+#define PLP_KM_MINB 2  // 128 registers with the prefetch (146 unbounded: one CTA per SM); 3 (80 registers,
+                       // spills) measured slower before the prefetch: Lloyd 0.223 vs 0.211 ms
 #endif
 template <int DIM, int KC>  // DIM = 8: vectorised point loads; DIM = 0: runtime dim <= 8;
                            // KC = 8: K = 8 at compile time (unrolled); KC = 0: runtime K <= 8
@@ -264,13 +282,13 @@ __global__ void __launch_bounds__(256, KC == 8 ? PLP_KM_MINB : 1) km_assign_mma_
   const int64_t g0 = groups * wid / tw, g1 = groups * (wid + 1) / tw;
   double s0 = 0.0, s1 = 0.0, sse = 0.0;
   int cnt = 0;  // lane c < K counts cluster c
-  for (int64_t gr = g0; gr < g1; ++gr) {
-    const int64_t p0 = gr * 32 * PPL;
-    double x[PPL][8];
-    bool ok[PPL];
+  // the lane's PPL points of group gr (rows past n read as zeros)
+  double x[PPL][8];
+  bool ok[PPL];
+  auto load_group = [&](int64_t gr) {
 #pragma unroll
     for (int h = 0; h < PPL; ++h) {
-      const int64_t i = p0 + 32 * h + lane;
+      const int64_t i = gr * 32 * PPL + 32 * h + lane;
       ok[h] = i < n;
       if constexpr (DIM == 8) {
         if (ok[h]) {
@@ -289,6 +307,13 @@ __global__ void __launch_bounds__(256, KC == 8 ? PLP_KM_MINB : 1) km_assign_mma_
         for (int d = 0; d < 8; ++d) x[h][d] = (ok[h] && d < dim) ? __ldg(X + i * dim + d) : 0.0;
       }
     }
+  };
+  // Software pipeline: the next group's point loads are issued as soon as the distances of the
+  // current one are done (x is dead from there on), so their latency runs behind the label
+  // stores, ballots and DMMAs of the current group.
+  if (g0 < g1) load_group(g0);
+  for (int64_t gr = g0; gr < g1; ++gr) {
+    const int64_t p0 = gr * 32 * PPL;
     int bc[PPL];
     double bd[PPL];
 #pragma unroll
@@ -335,10 +360,16 @@ __global__ void __launch_bounds__(256, KC == 8 ? PLP_KM_MINB : 1) km_assign_mma_
           bc[h] = c;
         }
     }
+    bool okc[PPL];
+#pragma unroll
+    for (int h = 0; h < PPL; ++h) okc[h] = ok[h];
+#if PLP_KM_PREFETCH
+    if (gr + 1 < g1) load_group(gr + 1);
+#endif
 #pragma unroll
     for (int h = 0; h < PPL; ++h) {
       const int64_t i = p0 + 32 * h + lane;
-      if (ok[h]) {
+      if (okc[h]) {
         lab[i] = bc[h];
         best_d[i] = bd[h];
         sse += bd[h];
@@ -362,6 +393,9 @@ __global__ void __launch_bounds__(256, KC == 8 ? PLP_KM_MINB : 1) km_assign_mma_
         dmma884(s0, s1, a, b);
       }
     }
+#if !PLP_KM_PREFETCH
+    if (gr + 1 < g1) load_group(gr + 1);
+#endif
   }
   // per-warp results -> shared, then a fixed-order sum over warps
   const int E = K * dim + K + 1;
