@@ -253,6 +253,10 @@ __global__ void __launch_bounds__(kKmThreads) km_assign_kernel(int64_t n, int di
 // m8n8k4: A[c][q] = [label of point q == c], B[q][d] = X[q][d] or 1), 4 points per instruction.
 // Each warp owns a contiguous range of 32-point groups; per-CTA partials in a fixed order, layout
 // [sums K*dim | counts K | sse] like km_assign_kernel.
+#ifndef PLP_KM_PPL
+#define PLP_KM_PPL 2  // points per lane and loop iteration (1: 78 / 64 registers at 3 / 4 CTAs per SM, but twice the
+                     // centroid reads per point: 0.221 / 0.225 vs 0.208 ms per Lloyd iteration, r02t)
+#endif
 #ifndef PLP_KM_PREFETCH
 #define PLP_KM_PREFETCH 1  // next group's point loads issued before the current group's DMMA phase
 #endif
@@ -268,7 +272,7 @@ __global__ void __launch_bounds__(256, KC == 8 ? PLP_KM_MINB : 1) km_assign_mma_
                                                             int32_t* __restrict__ lab,
                                                             double* __restrict__ best_d,
                                                             double* __restrict__ part) {
-  constexpr int NW = 8, PPL = 2;  // two points per lane: each centroid load serves both
+  constexpr int NW = 8, PPL = PLP_KM_PPL;  // two points per lane: each centroid load serves both
   const int dim = DIM > 0 ? DIM : dim_rt;
   const int K = KC > 0 ? KC : K_rt;
   __shared__ __align__(16) double cs[8 * 8];
@@ -641,9 +645,11 @@ static plp_status kmeans_impl(plp_ctx* ctx, int64_t n, int dim, int K, const dou
     }
     // ---- Lloyd ----
     const bool mma = K <= 8 && dim <= 8;
-    static const int res_mma = std::min(resident_ctas(km_assign_mma_kernel<8, 8>, 256),
-                                        resident_ctas(km_assign_mma_kernel<0, 0>, 256));
-    int grid_mma = ctx->num_sms * res_mma;  // one full wave
+    static const int res_mma88 = resident_ctas(km_assign_mma_kernel<8, 8>, 256);
+    static const int res_mma0 = std::min(resident_ctas(km_assign_mma_kernel<8, 0>, 256),
+                                         resident_ctas(km_assign_mma_kernel<0, 0>, 256));
+    const bool mma88 = dim == 8 && K == 8 && ((uintptr_t)X & 15u) == 0;
+    int grid_mma = ctx->num_sms * (mma88 ? res_mma88 : res_mma0);  // one full wave
     if ((int64_t)grid_mma * E > part_cap) grid_mma = (int)(part_cap / E);
     const int64_t groups = (n + 63) / 64;
     if (groups < (int64_t)grid_mma * 8) grid_mma = (int)std::max<int64_t>(1, (groups + 7) / 8);
@@ -652,7 +658,7 @@ static plp_status kmeans_impl(plp_ctx* ctx, int64_t n, int dim, int K, const dou
         PLP_CUDA(cudaMemsetAsync(red, 0, sizeof(double) * E, st));
       } else {
         if (mma) {
-          if (dim == 8 && K == 8 && ((uintptr_t)X & 15u) == 0)
+          if (mma88)
             km_assign_mma_kernel<8, 8><<<grid_mma, 256, 0, st>>>(n, dim, K, X, cent, lab, best_d, ctx->partials);
           else if (dim == 8 && ((uintptr_t)X & 15u) == 0)
             km_assign_mma_kernel<8, 0><<<grid_mma, 256, 0, st>>>(n, dim, K, X, cent, lab, best_d, ctx->partials);
