@@ -1,6 +1,6 @@
 #!/bin/bash
 # k-means variants on one box: Lloyd / seeding times of the built library and of variant libraries
-# (PLP_LIB), then the k-means GPU tests under each variant.
+# (PLP_LIB), then the k-means, clustering and end-to-end GPU tests under each variant.
 #   /usr/local/graft/bin/gpurun --timeout 1500 -- 'bash tools/kmeans_var.sh TAG variant.so ...'
 set -u
 TAG=$1; shift
@@ -14,9 +14,9 @@ for rep in 1 2; do
   done
 done
 for lib in "$@"; do
-  PLP_LIB=$PWD/paper_2605_26975_b200/$lib timeout 600 python -m pytest tests/test_gpu_dense.py tests/test_gpu_collective.py -m gpu -q -p no:cacheprovider -k "kmeans" > $OUT/kmeans_tests_${TAG}_$lib.log 2>&1
+  PLP_LIB=$PWD/paper_2605_26975_b200/$lib timeout 600 python -m pytest tests -m gpu -q -p no:cacheprovider -k "kmeans or cluster or end_to_end" > $OUT/kmeans_tests_${TAG}_$lib.log 2>&1
   echo "TESTS_RC=$?" >> $OUT/kmeans_tests_${TAG}_$lib.log
 done
-timeout 600 python -m pytest tests/test_gpu_dense.py tests/test_gpu_collective.py -m gpu -q -p no:cacheprovider -k "kmeans" > $OUT/kmeans_tests_${TAG}_default.log 2>&1
+timeout 600 python -m pytest tests -m gpu -q -p no:cacheprovider -k "kmeans or cluster or end_to_end" > $OUT/kmeans_tests_${TAG}_default.log 2>&1
 echo "TESTS_RC=$?" >> $OUT/kmeans_tests_${TAG}_default.log
 echo DONE > $OUT/kmeans_var_done_$TAG.txt
